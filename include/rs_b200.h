@@ -1,0 +1,140 @@
+/*
+ * rs_b200.h -- C ABI of the B200 range-separated (RS) tensor assembly path.
+ *
+ * The reference (rstensor 0.1.0, pure numpy/scipy) has no FFI layer: its
+ * boundary is the public Python API in pkg/src/rstensor/__init__.py:4-94.
+ * Every entry point below replaces the numerical core of one reference
+ * function; the Python package paper_1606_09218_b200 binds them with ctypes
+ * (paper_1606_09218_b200/_native.py) and keeps the reference's names,
+ * argument meanings and exception classes on top.
+ *
+ * Conventions
+ *   - All arrays are device pointers (cudaMalloc / torch CUDA storage),
+ *     row-major, fp64 unless the name says i64/i32.  "ld" = leading dimension
+ *     in elements.  No pointer is retained after a call returns.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call
+ *     only enqueues work; nothing synchronises the host.
+ *   - Return value: RS_OK or one of the RS_ERR_* codes; rs_last_error()
+ *     returns the message of the last failure on the calling thread.
+ *   - Results are deterministic: no floating-point atomics, fixed-order
+ *     split-K reductions.
+ */
+#ifndef RS_B200_H
+#define RS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_OK 0
+#define RS_ERR_DOMAIN 1      /* -> DomainError      */
+#define RS_ERR_CAPACITY 2    /* -> CapacityError    */
+#define RS_ERR_NUMERICAL 3   /* -> NumericalError   */
+#define RS_ERR_CUDA 4        /* -> RsTensorError    */
+#define RS_ERR_UNSUPPORTED 5 /* -> CapabilityError  */
+
+int rs_abi_version(void);
+const char *rs_last_error(void);
+
+/* (a2) snap_to_grid, particles.py:302-329.
+ * idx[3p+l] = clip(ceil(pos[3p+l]/h + n/2 - 0.5), 1, n-1);
+ * disp[p] = |pos_p - (idx_p - n/2) h|_2 (IEEE-exact, no FMA contraction). */
+int rs_snap(const double *pos, int64_t count, double h, int64_t n,
+            int64_t *idx, double *disp, void *stream);
+
+/* (a7) window gather, assembly.py:111-136 (assemble_long) and the
+ * shift-merged Gram operand of rankred.py:90-96.
+ * out[i*ld_out + g*n_terms + k] = gscale[g] * tscale[k] *
+ *                                 table[(starts[g]+i)*ld_table + term0 + k]
+ * for i < n_rows, g < n_groups, k < n_terms.  gscale/tscale may be NULL (=1). */
+int rs_gather_windows(const double *table, int64_t ld_table, int64_t n_rows,
+                      const int64_t *starts, int64_t n_groups, int64_t n_terms,
+                      int64_t term0, const double *gscale, const double *tscale,
+                      double *out, int64_t ld_out, void *stream);
+
+/* (a8) Gram of a side matrix, rankred.py:91 (gram = a @ a.T).
+ * G (n x n, ld n) = A A^T with A n x K (ld lda, lda even, A 16-byte aligned).
+ * FP64 tensor cores (DMMA), lower-triangle tiles, fixed-order split-K into
+ * `work` (rs_syrk_workspace_bytes), mirrored to a full symmetric matrix. */
+int64_t rs_syrk_workspace_bytes(int64_t n, int64_t K);
+int rs_syrk(const double *A, int64_t lda, int64_t n, int64_t K, double *G,
+            void *work, int64_t work_bytes, void *stream);
+
+/* Plain NT GEMM on DMMA: C (M x N, ldc) = A (M x K, lda) * B^T (B: N x K, ldb).
+ * Used for projections Z^T U (rankred.py:175) on explicit side matrices. */
+int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb,
+               double *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);
+
+/* (a10) shift projection: for the doubled table T (ld_table) and an orthonormal
+ * basis Z (n x r, ld ldz): TT[(a*n_shift + s)*R + k] = sum_i Z[i*ldz+a] *
+ * T[(s+i)*ld_table + k], s < n_shift, k < R.  This is Z^T U restricted to one
+ * particle shift -- rankred.py:175 without materialising U. */
+int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r,
+                     const double *table, int64_t ld_table, int64_t R,
+                     int64_t n_shift, double *TT, void *stream);
+
+/* (a10) RHOSVD core, rankred.py:151-161 (_core_from_projections) on the
+ * particle-major term order of assembly.py:127-135:
+ * core[(a*r2+b)*r3+c] = sum_p z[p] sum_k w[k] P1(a,p,k) P2(b,p,k) P3(c,p,k)
+ * with Pl(a,p,k) = TTl[(a*n_shift + shift[3p+l])*R + k].
+ * `work` holds fixed-order split partials (rs_core_workspace_bytes). */
+int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count);
+int rs_core(const double *TT1, const double *TT2, const double *TT3,
+            int64_t r1, int64_t r2, int64_t r3, int64_t n_shift, int64_t R,
+            const int64_t *shift, const double *z, const double *w, int64_t count,
+            double *core, void *work, int64_t work_bytes, void *stream);
+
+/* (a12-a14) fused RS grid assembly of x1-planes [x1_lo, x1_hi):
+ * out[((x1-x1_lo)*n + x2)*n + x3] = Tucker(core,V1,V2,V3)[x1,x2,x3]
+ *                                  + sum_p z_p L0[x - c_p + gamma]
+ * with L0 = sum_k wl[k] ul[.,k] (x) ul[.,k] (x) ul[.,k] (the normalised CCT
+ * local tensor, formats.py:103-118, 432-445) and windows clipped to the grid.
+ * Particles must be given bucketed by their x3 index: bucket b holds sorted
+ * entries [bstart[b], bstart[b+1]) with x3 index bc3[b] (ascending), x1/x2
+ * indices c1/c2 and charges zq.  Workspace: rs_assemble_workspace_bytes. */
+int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax,
+                                    int64_t n_buckets, int64_t Rs); /* rmax = max(r1,r2,r3) */
+int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3,
+                       const double *V1, const double *V2, const double *V3,
+                       int64_t n, const double *ul, const double *wl, int64_t Rs,
+                       int64_t gamma, const int32_t *c1, const int32_t *c2,
+                       const double *zq, const int32_t *bstart, const int32_t *bc3,
+                       int64_t n_buckets, int64_t x1_lo, int64_t x1_hi,
+                       double *out, void *work, int64_t work_bytes, void *stream);
+
+/* (a15) Tucker point values, formats.py:347-352 (eval_tucker_many). */
+int rs_eval_tucker(const double *core, int64_t r1, int64_t r2, int64_t r3,
+                   const double *V1, const double *V2, const double *V3,
+                   const int64_t *idx, int64_t m, double *out, void *stream);
+
+/* (a15) CCT point values, formats.py:380-398 (eval_cct) for m points; also
+ * returns the number of covering copies per point (hits) so the caller can
+ * apply the soft-overlap cap (CapacityError).  centers i64 (count x 3). */
+int rs_eval_cct(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
+                const int64_t *centers, const double *zq, int64_t count,
+                const int64_t *idx, int64_t m, double *out, int32_t *hits,
+                void *stream);
+
+/* (a16-a18) windowed long-range pair sums, observables.py:175-259.
+ * For every target j in [0, m): with offsets o = idx[tgt[j]] - idx[p] (+ shift):
+ *   base[j]      = sum_{p != excl} z[p] * pl(o)            (double-double)
+ *   dshift[3j+a] = sum_{p != tgt} z[p] * (pl(o - e_a) - pl(o))
+ * where pl(o) = sum_{k<R_l} w[k] T[n0+o0,k] T[n0+o1,k] T[n0+o2,k] / h3.
+ * mode 0: energy terms (all p, incl. self), mode 1: forces (p != j). */
+int rs_pair_sums(const double *table, int64_t ld_table, int64_t n0,
+                 const double *w, int64_t Rl, double h3,
+                 const int64_t *idx, const double *z, int64_t count,
+                 const int64_t *tgt, int64_t m, int mode,
+                 double *base, double *dshift, void *stream);
+
+/* Compensated (double-double, fixed order) sum of v[0..m), result in out[0]. */
+int rs_sum_dd(const double *v, int64_t m, double *out, void *work,
+              int64_t work_bytes, void *stream);
+int64_t rs_sum_workspace_bytes(int64_t m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_B200_H */

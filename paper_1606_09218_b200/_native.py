@@ -1,0 +1,124 @@
+"""ctypes binding of ``librsb200.so`` (the C ABI in ``include/rs_b200.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no CPU fallback: if the
+library or a CUDA device is missing every compute entry point raises
+:class:`CapabilityError` -- the product path never silently degrades.
+
+Wrappers take torch CUDA tensors, pass raw pointers plus the current torch
+stream, and map a non-zero status to the reference exception classes
+(``errors.STATUS_TO_ERROR``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import STATUS_TO_ERROR, CapabilityError, RsTensorError
+
+LIB_NAME = "librsb200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_dbl = ctypes.c_double
+_ptr = ctypes.c_void_p
+
+# name -> (restype, argtypes); must match include/rs_b200.h exactly
+SIGNATURES = {
+    "rs_abi_version": (_i32, []),
+    "rs_last_error": (ctypes.c_char_p, []),
+    "rs_snap": (_i32, [_ptr, _i64, _dbl, _i64, _ptr, _ptr, _ptr]),
+    "rs_gather_windows": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64,
+                                 _ptr]),
+    "rs_syrk_workspace_bytes": (_i64, [_i64, _i64]),
+    "rs_syrk": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr]),
+    "rs_gemm_nt": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
+    "rs_shift_project": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr]),
+    "rs_core_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64]),
+    "rs_core": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr,
+                       _ptr, _i64, _ptr]),
+    "rs_assemble_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
+    "rs_assemble_planes": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _i64,
+                                  _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _i64, _ptr, _ptr,
+                                  _i64, _ptr]),
+    "rs_eval_tucker": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
+    "rs_eval_cct": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64, _ptr, _ptr, _ptr]),
+    "rs_pair_sums": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _dbl, _ptr, _ptr, _i64, _ptr, _i64, _i32,
+                            _ptr, _ptr, _ptr]),
+    "rs_sum_workspace_bytes": (_i64, [_i64]),
+    "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise CapabilityError(
+                f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise CapabilityError("the RS assembly path needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().rs_last_error().decode(errors="replace")
+        raise STATUS_TO_ERROR.get(status, RsTensorError)(f"{what}: {msg}")
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr() -> int:
+    torch = _torch()
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """Grow-only device scratch buffer (one per device), reused across calls so
+    the steady state allocates nothing."""
+
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, slot: str = "main"):
+        torch = _torch()
+        dev = torch.cuda.current_device()
+        key = (dev, slot)
+        buf = cls._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            cls._bufs.pop(key, None)
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=f"cuda:{dev}")
+            cls._bufs[key] = buf
+        return buf
+
+    @classmethod
+    def release(cls):
+        cls._bufs.clear()

@@ -1,0 +1,420 @@
+"""RS tensor construction: the reference's ``build_rs`` pipeline on the device.
+
+Reference: ``assembly.py:39-279``.  Per grid configuration the host prologue
+(quadrature, ``(2n, R)`` table, split, gamma, normalised short window) is
+computed once and cached in an :class:`RSPlan` (it never depends on the
+particles).  Per particle system everything runs on the device:
+
+1. snap (``rs_snap``) and the duplicate-node check,
+2. per-mode shift histograms and the shift-merged Gram (``rs_gather_windows``
+   + ``rs_syrk`` on DMMA), cuSOLVER ``eigh``,
+3. ONE host synchronisation: spectra (for the eps-rank rule), collision flag,
+   max displacement,
+4. shift projection + RHOSVD core (``rs_shift_project`` + ``rs_core``),
+5. the CCT short part (centres/charges stay on the device).
+
+The long side matrices of ``assemble_long`` are never materialised on this
+path; ``assemble_long`` itself (public API) materialises them on the device
+with ``rs_gather_windows`` for callers that want them.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConfigError, DomainError, ResolutionError
+from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, is_device, storage_report, \
+    to_device, to_host
+from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
+    snap_to_grid
+from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
+    project_kernel, split_rank, split_tensor
+from .rankred import ReductionConfig, SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, \
+    rhosvd_error_bound, select_ranks, shift_histograms, shifted_core, shifted_gram, side_svd, \
+    tucker_to_canonical
+
+
+@dataclass(frozen=True)
+class AssemblyConfig:
+    """Pipeline configuration, same fields/defaults as ``assembly.py:39-69``."""
+
+    grid: Grid3
+    kernel: RadialKernel = field(default_factory=lambda: RadialKernel("newton"))
+    M: int = 25
+    C0: float = 3.0
+    split_index: Optional[int] = None
+    sigma: Optional[float] = None
+    delta: float = 1e-4
+    criterion: str = "max_norm"
+    overlap_policy: str = "soft"
+    max_overlap: Optional[int] = 8
+    reduction: ReductionConfig = field(default_factory=lambda: ReductionConfig(eps=1e-5))
+    long_format: str = "canonical"
+    entry_rule: str = "integral"
+    reduce_long: Optional[bool] = None
+    reduce_threshold: int = 2000
+
+    def __post_init__(self):
+        if self.long_format not in ("canonical", "tucker"):
+            raise ConfigError(f"unknown long format {self.long_format!r}")
+        if not (0 < self.delta < 1):
+            raise ConfigError(f"delta must lie in (0,1), got {self.delta}")
+
+
+def reference_for(cfg: AssemblyConfig) -> ReferenceCanonical:
+    """Doubled-grid reference calibrated on ``[h/2, 2 sqrt(3) b]`` (``assembly.py:72-82``)."""
+    b = cfg.grid.box.half_width
+    rule = build_quadrature(cfg.kernel, cfg.M, cfg.C0,
+                            r_range=(0.5 * cfg.grid.h, 2.0 * math.sqrt(3.0) * b))
+    return project_kernel(rule, cfg.grid, doubled=True, entry_rule=cfg.entry_rule)
+
+
+def window_slice(ref2n: ReferenceCanonical, j, k: int):
+    """Mode vectors of one windowed term: slices of the table (``assembly.py:85-98``)."""
+    if not ref2n.doubled:
+        raise ConfigError("windowing requires the doubled-grid reference")
+    n = ref2n.grid.n // 2
+    j = tuple(int(v) for v in j)
+    if len(j) != 3 or any(v < 0 or v >= n for v in j):
+        raise DomainError(f"particle index {j} outside the n-grid")
+    return tuple(ref2n.tensor.factors[l][n - j[l]:2 * n - j[l], k] for l in range(3))
+
+
+# ----------------------------------------------------------------- the plan
+@dataclass
+class RSPlan:
+    """Per-configuration device state: everything ``build_rs`` needs that does
+    not depend on the particle set.  Cached by :func:`plan_for`."""
+
+    ref2n: ReferenceCanonical
+    split_index: int
+    gamma: int
+    local: CanonicalTensor          # normalised short window (host)
+    table_dev: object               # (2n, R) float64 CUDA
+    w_long: object                  # (R_l,) weights
+    w_long_abs: object
+
+    @property
+    def n(self) -> int:
+        return self.ref2n.grid.n // 2
+
+
+_QUAD_CACHE: dict = {}
+_PLAN_CACHE: dict = {}
+
+
+def _reference_cached(cfg: AssemblyConfig) -> ReferenceCanonical:
+    key = (cfg.grid, cfg.kernel, cfg.M, cfg.C0, cfg.entry_rule)
+    ref = _QUAD_CACHE.get(key)
+    if ref is None:
+        ref = reference_for(cfg)
+        _QUAD_CACHE[key] = ref
+    return ref
+
+
+def _short_window(ref2n: ReferenceCanonical, split_index: int, delta: float, gamma=None):
+    """(gamma, normalised local tensor) exactly as ``assembly.py:139-184``."""
+    n = ref2n.grid.n // 2
+    short, _ = split_tensor(ref2n, split_index)
+    if short.rank == 0:
+        return 0, CanonicalTensor.empty((1, 1, 1))
+    if gamma is None:
+        gamma = effective_support(short, delta, ref2n.grid.h)
+    gamma = int(min(max(gamma, 0), n - 1))
+    n0 = ref2n.origin_index
+    local = CanonicalTensor(short.weights, tuple(f[n0 - gamma:n0 + gamma + 1, :]
+                                                 for f in short.factors)).normalize()
+    return gamma, local
+
+
+def plan_for(cfg: AssemblyConfig, split_index: int) -> RSPlan:
+    key = (cfg.grid, cfg.kernel, cfg.M, cfg.C0, cfg.entry_rule, int(split_index), cfg.delta)
+    plan = _PLAN_CACHE.get(key)
+    if plan is not None:
+        return plan
+    ref = dataclasses.replace(_reference_cached(cfg), split_index=int(split_index))
+    gamma, local = _short_window(ref, split_index, cfg.delta)
+    torch = nat._torch()
+    table = to_device(ref.table)
+    w = to_device(ref.tensor.weights[: split_index + 1])
+    plan = RSPlan(ref2n=ref, split_index=int(split_index), gamma=gamma, local=local,
+                  table_dev=table, w_long=w, w_long_abs=w.abs().contiguous())
+    _PLAN_CACHE[key] = plan
+    return plan
+
+
+# ---------------------------------------------------------- particle input
+@dataclass(frozen=True)
+class DeviceParticles:
+    """Device-resident particle system (positions ``(N,3)``, charges ``(N,)``,
+    CUDA float64) -- the zero-copy input of :func:`build_rs`."""
+
+    positions: object
+    charges: object
+    box: object
+
+    @property
+    def count(self) -> int:
+        return int(self.positions.shape[0])
+
+
+@dataclass(frozen=True)
+class DeviceIndexedSystem:
+    """Snapped device particle system; host views are materialised lazily."""
+
+    positions: object     # snapped positions (device)
+    charges: object       # (device)
+    grid: Grid3
+    indices: object       # (N, 3) int64 (device)
+    box: object
+    _disp: object = None  # (N,) displacement (device)
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def count(self) -> int:
+        return int(self.indices.shape[0])
+
+    @property
+    def max_displacement(self) -> float:
+        v = self._cache.get("maxdisp")
+        if v is None:
+            v = float(self._disp.max())
+            self._cache["maxdisp"] = v
+        return v
+
+    @property
+    def base(self) -> ParticleSystem:
+        b = self._cache.get("base")
+        if b is None:
+            b = ParticleSystem(to_host(self.positions), to_host(self.charges), self.box)
+            self._cache["base"] = b
+        return b
+
+    def to_indexed(self) -> IndexedParticleSystem:
+        return IndexedParticleSystem(base=self.base, grid=self.grid, indices=to_host(self.indices),
+                                     max_displacement=self.max_displacement)
+
+
+def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
+    """``rs_snap`` on device data; the collision check is deferred to the
+    caller's next synchronisation (see :func:`_collision_flag`)."""
+    torch = nat._torch()
+    pos = to_device(positions)
+    z = to_device(charges)
+    count = int(pos.shape[0])
+    idx = torch.empty((count, 3), dtype=torch.int64, device="cuda")
+    disp = torch.empty(count, dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().rs_snap(pos.data_ptr(), count, grid.h, grid.n, idx.data_ptr(),
+                                disp.data_ptr(), nat.stream_ptr()), "rs_snap")
+    snapped = (idx.to(torch.float64) - grid.n // 2) * grid.h
+    return DeviceIndexedSystem(positions=snapped, charges=z, grid=grid, indices=idx, box=box,
+                               _disp=disp)
+
+
+def _collision_flag(idx, n: int):
+    """Device int64: index of the first duplicated node key, or -1."""
+    torch = nat._torch()
+    keys = (idx[:, 0] * n + idx[:, 1]) * n + idx[:, 2]
+    ks, _ = torch.sort(keys)
+    dup = ks[1:] == ks[:-1]
+    first = torch.where(dup.any(), ks[:-1][dup.to(torch.int64).argmax()], ks.new_tensor(-1))
+    return first.reshape(1)
+
+
+def _as_device_system(system, grid: Grid3):
+    """Accept the reference's types or :class:`DeviceParticles`."""
+    if isinstance(system, DeviceIndexedSystem):
+        if system.grid != grid:
+            raise ConfigError("particle system snapped to a different grid")
+        return system, None
+    if isinstance(system, DeviceParticles):
+        ds = snap_device(system.positions, system.charges, system.box, grid)
+        return ds, _collision_flag(ds.indices, grid.n)
+    if isinstance(system, IndexedParticleSystem):
+        if system.grid != grid:
+            raise ConfigError("particle system snapped to a different grid")
+        torch = nat._torch()
+        ds = DeviceIndexedSystem(positions=to_device(system.base.positions),
+                                 charges=to_device(system.charges), grid=grid,
+                                 indices=to_device(system.indices, torch.int64),
+                                 box=system.base.box,
+                                 _disp=torch.full((1,), system.max_displacement,
+                                                  dtype=torch.float64, device="cuda"))
+        ds._cache["host"] = system
+        return ds, None
+    if isinstance(system, ParticleSystem):
+        ds = snap_device(system.positions, system.charges, system.box, grid)
+        return ds, _collision_flag(ds.indices, grid.n)
+    raise ConfigError(f"expected a particle system, got {type(system).__name__}")
+
+
+def _host_system(ds: DeviceIndexedSystem):
+    h = ds._cache.get("host")
+    return h if h is not None else ds
+
+
+# ----------------------------------------------------- public assembly API
+def assemble_long(ref2n: ReferenceCanonical, system, split_index: int) -> CanonicalTensor:
+    """Rank ``(R_l+1) N`` long part, particle-major term order, side matrices
+    materialised on the device by ``rs_gather_windows`` (``assembly.py:111-136``)."""
+    if not (0 <= split_index < ref2n.R):
+        raise DomainError(f"split index {split_index} out of range")
+    torch = nat._torch()
+    n = ref2n.grid.n // 2
+    nt = split_index + 1
+    ds, flag = _as_device_system(system, Grid3(n, Box3_half(ref2n)))
+    z = ds.charges
+    table = to_device(ref2n.table)
+    w = to_device(ref2n.tensor.weights[:nt])
+    weights = (z[:, None] * w[None, :]).reshape(-1)
+    count = ds.count
+    facs = []
+    for l in range(3):
+        starts = (n - ds.indices[:, l]).contiguous()
+        out = torch.empty((n, count * nt), dtype=torch.float64, device="cuda")
+        nat.check(nat.lib().rs_gather_windows(table.data_ptr(), table.shape[1], n, starts.data_ptr(),
+                                              count, nt, 0, None, None, out.data_ptr(), count * nt,
+                                              nat.stream_ptr()), "rs_gather_windows")
+        facs.append(out)
+    return CanonicalTensor(weights, tuple(facs))
+
+
+def Box3_half(ref2n: ReferenceCanonical):
+    from .particles import Box3
+
+    return Box3(ref2n.grid.box.half_width / 2.0)
+
+
+def assemble_short(ref2n: ReferenceCanonical, system, split_index: int, delta: float,
+                   overlap_policy: str = "soft", max_overlap: Optional[int] = 8,
+                   gamma: Optional[int] = None) -> CCT:
+    """Short part as a uniform CCT (``assembly.py:139-184``)."""
+    n = ref2n.grid.n // 2
+    g, local = _short_window(ref2n, split_index, delta, gamma)
+    centers = system.indices
+    weights = system.charges
+    return CCT(local=local, gamma=g, centers=centers, weights=weights, mode_sizes=(n, n, n),
+               overlap_policy=overlap_policy, max_overlap=max_overlap)
+
+
+@dataclass(frozen=True)
+class AssemblyResult:
+    rs: Union[RSCanonical, RSTucker]
+    reference: ReferenceCanonical
+    system: object
+    split_index: int
+    sigma: float
+    gamma: int
+    report: dict
+
+
+def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
+    """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
+
+    ``system`` may be a reference-style :class:`ParticleSystem` /
+    :class:`IndexedParticleSystem` (host arrays) or :class:`DeviceParticles`.
+    """
+    torch = nat._torch()
+    grid = cfg.grid
+    n = grid.n
+    ds, collision = _as_device_system(system, grid)
+    if cfg.sigma is not None:
+        sigma = float(cfg.sigma)
+    elif ds.count >= 2:
+        sigma = separation_distance(ParticleSystem(to_host(ds.positions), to_host(ds.charges),
+                                                   ds.box))
+    else:
+        sigma = grid.h
+    if cfg.split_index is not None:
+        split_index = int(cfg.split_index)
+    else:
+        split_index = split_rank(_reference_cached(cfg), sigma, cfg.delta, cfg.criterion)
+    plan = plan_for(cfg, split_index)
+    ref2n = plan.ref2n
+    nt = split_index + 1
+    raw_rank = ds.count * nt
+    reduce_long = cfg.reduce_long
+    if reduce_long is None:
+        reduce_long = cfg.long_format == "tucker" or raw_rank > cfg.reduce_threshold
+    if cfg.long_format == "tucker":
+        reduce_long = True
+
+    idx = ds.indices
+    z = ds.charges
+    starts = (n - idx).contiguous()
+    report = {"n": n, "b": grid.box.half_width, "particles": ds.count}
+
+    if reduce_long and cfg.reduction.max_sweeps == 0:
+        # shift-merged Gram per mode, eigh, one synchronisation
+        hists = shift_histograms(starts, z, n)
+        eig = [eig_desc(shifted_gram(plan.table_dev, n, plan.w_long_abs, h)) for h in hists]
+        k = min(n, raw_rank)
+        parts = [s[:k] for s, _ in eig] + [ds._disp.max().reshape(1)]
+        if collision is not None:
+            parts.append(collision.to(torch.float64))
+        packed = to_host(torch.cat(parts))
+        if collision is not None and packed[-1] >= 0:
+            key = int(packed[-1])
+            node = (key // (n * n), (key // n) % n, key % n)
+            raise ResolutionError(f"grid n={n} cannot resolve the system: several particles "
+                                  f"snap to node {node}; use a larger n")
+        values = tuple(packed[i * k:(i + 1) * k] for i in range(3))
+        ds._cache["maxdisp"] = float(packed[3 * k])
+        spectrum = SvdSpectrum(values=values, vectors=tuple(zz for _, zz in eig))
+        ranks = select_ranks((n, n, n), raw_rank, values, cfg.reduction)
+        zs = [eig[l][1][:, :ranks[l]].contiguous() for l in range(3)]
+        core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
+        tucker = _trusted_tucker(core, zs)
+        long_raw = None
+    else:
+        if collision is not None and int(collision[0]) >= 0:
+            key = int(collision[0])
+            raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "
+                                  f"to node {(key // (n * n), (key // n) % n, key % n)}; use a "
+                                  f"larger n")
+        long_raw = assemble_long(ref2n, ds, split_index)
+        if reduce_long:
+            spectrum = side_svd(long_raw)
+            tucker = c2t_als(long_raw, cfg.reduction, spectrum=spectrum)
+            ranks = tucker.ranks
+    report.update({
+        "max_snap_displacement": ds.max_displacement,
+        "quadrature_rank": ref2n.R,
+        "split_index": split_index,
+        "short_terms": ref2n.R - split_index - 1,
+        "sigma": sigma,
+        "raw_long_rank": raw_rank,
+        "reduced": bool(reduce_long),
+    })
+    if reduce_long:
+        report["tucker_ranks"] = list(ranks)
+        report["reduction_tail_bracket"] = rhosvd_error_bound(None, spectrum, ranks)
+        totals = [float(np.sqrt(np.sum(s * s))) for s in spectrum.values]
+        report["reduction_tail_fraction"] = [
+            float(np.sqrt(np.sum(s[r:] ** 2)) / t) if t > 0 else 0.0
+            for s, r, t in zip(spectrum.values, ranks, totals)]
+        if cfg.long_format == "tucker":
+            long_part = tucker
+        else:
+            long_part = tucker_to_canonical(tucker, cfg.reduction.eps_t2c)
+            report["reduced_canonical_rank"] = long_part.rank
+    else:
+        long_part = long_raw
+
+    short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z, mode_sizes=(n, n, n),
+                overlap_policy=cfg.overlap_policy, max_overlap=cfg.max_overlap)
+    report["gamma"] = plan.gamma
+    report["gamma_h"] = plan.gamma * grid.h
+    rs = RSTucker(long=long_part, short=short, grid=grid) if cfg.long_format == "tucker" else \
+        RSCanonical(long=long_part, short=short, grid=grid)
+    sto = storage_report(rs)
+    report["storage_floats"] = sto.total
+    report["storage_bound"] = sto.bound
+    return AssemblyResult(rs=rs, reference=ref2n, system=_host_system(ds),
+                          split_index=split_index, sigma=sigma, gamma=plan.gamma, report=report)

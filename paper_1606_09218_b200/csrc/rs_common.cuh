@@ -1,0 +1,62 @@
+// Shared plumbing for the sm_100a RS kernels: status codes, the per-thread
+// error message behind rs_last_error(), launch checks, double-double helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/rs_b200.h"
+
+namespace rsb {
+
+extern thread_local char g_err[512];
+
+inline int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+inline int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return RS_OK;
+  if (e == cudaErrorMemoryAllocation)
+    return fail(RS_ERR_CAPACITY, "%s: %s", what, cudaGetErrorString(e));
+  return fail(RS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define RS_REQUIRE(cond, ...)                         \
+  do {                                                \
+    if (!(cond)) return ::rsb::fail(RS_ERR_DOMAIN, __VA_ARGS__); \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---- double-double accumulation (Knuth TwoSum; no FMA contraction) -------
+struct dd {
+  double hi, lo;
+};
+
+__device__ __forceinline__ dd dd_add_d(dd a, double b) {
+  double s = __dadd_rn(a.hi, b);
+  double bb = __dsub_rn(s, a.hi);
+  double err = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  double lo = __dadd_rn(a.lo, err);
+  double hi = __dadd_rn(s, lo);
+  lo = __dsub_rn(lo, __dsub_rn(hi, s));
+  return dd{hi, lo};
+}
+
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd r = dd_add_d(a, b.hi);
+  return dd_add_d(r, b.lo);
+}
+
+}  // namespace rsb

@@ -1,0 +1,796 @@
+// sm_100a kernels + C ABI for the range-separated tensor assembly path.
+// Declarations and the mapping to the reference functions: include/rs_b200.h.
+#include <math.h>
+
+#include <algorithm>
+
+#include "rs_common.cuh"
+#include "rs_dmma.cuh"
+
+namespace rsb {
+thread_local char g_err[512] = "";
+
+// ===================================================================== snap
+__global__ void k_snap(const double *__restrict__ pos, int64_t count, double h, int64_t n,
+                       int64_t *__restrict__ idx, double *__restrict__ disp) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= count) return;
+  const double half = (double)(n / 2);
+  double sq[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    double x = pos[3 * p + l];
+    double f = __dsub_rn(__dadd_rn(__ddiv_rn(x, h), half), 0.5);
+    int64_t i = (int64_t)ceil(f);
+    i = i < 1 ? 1 : (i > n - 1 ? n - 1 : i);
+    idx[3 * p + l] = i;
+    double snapped = __dmul_rn(__dsub_rn((double)i, half), h);
+    double d = __dsub_rn(x, snapped);
+    sq[l] = __dmul_rn(d, d);
+  }
+  disp[p] = __dsqrt_rn(__dadd_rn(__dadd_rn(sq[0], sq[1]), sq[2]));
+}
+
+// ======================================================== window gather (K1)
+__global__ void k_gather(const double *__restrict__ table, int64_t ld_table, int64_t n_rows,
+                         const int64_t *__restrict__ starts, int64_t n_groups, int64_t n_terms,
+                         int64_t term0, const double *__restrict__ gscale,
+                         const double *__restrict__ tscale, double *__restrict__ out,
+                         int64_t ld_out) {
+  const int64_t cols = n_groups * n_terms;
+  const int64_t total = n_rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, col = e - i * cols;
+    int64_t g = col / n_terms, k = col - g * n_terms;
+    double v = table[(starts[g] + i) * ld_table + term0 + k];
+    if (gscale) v *= gscale[g];
+    if (tscale) v *= tscale[k];
+    out[i * ld_out + col] = v;
+  }
+}
+
+// ============================================================ GEMM kernels
+using TilePlane = Tile<128, 64, 32, 32, 3>;  // plane GEMM / generic NT GEMM
+using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
+
+// C[m0.., n0..] = sum over the K ranges of this column tile of A B^T.
+// ranges: per column tile, nr (lo, hi) pairs; NULL => single range [0, K).
+template <class T>
+__global__ void __launch_bounds__(T::THREADS)
+    k_gemm_nt(const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
+              double *__restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+              const int64_t *__restrict__ ranges, int nr) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t n0 = (int64_t)blockIdx.x * T::BN;  // x: column tile (adjacent CTAs share A rows)
+  const int64_t m0 = (int64_t)blockIdx.y * T::BM;
+  Acc<T> acc;
+  acc.zero();
+  if (ranges) {
+    for (int r = 0; r < nr; ++r) {
+      int64_t lo = ranges[(blockIdx.x * nr + r) * 2], hi = ranges[(blockIdx.x * nr + r) * 2 + 1];
+      mainloop<T>(smem, acc, A, lda, m0, M, B, ldb, n0, N, lo, hi);
+    }
+  } else {
+    mainloop<T>(smem, acc, A, lda, m0, M, B, ldb, n0, N, 0, K);
+  }
+  store_tile<T>(acc, C, ldc, m0, M, n0, N);
+}
+
+__device__ __forceinline__ void tri_decode(int64_t t, int64_t &bi, int64_t &bj) {
+  int64_t i = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while (i * (i + 1) / 2 > t) --i;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  bi = i;
+  bj = t - i * (i + 1) / 2;
+}
+
+// Lower-triangle Gram tiles, one K slice per blockIdx.y, partials to `part`.
+__global__ void __launch_bounds__(TileSyrk::THREADS)
+    k_syrk_part(const double *__restrict__ A, int64_t lda, int64_t n, int64_t K, int64_t kslice,
+                double *__restrict__ part) {
+  using T = TileSyrk;
+  extern __shared__ __align__(16) double smem[];
+  int64_t bi, bj;
+  tri_decode(blockIdx.x, bi, bj);
+  const int64_t k_lo = (int64_t)blockIdx.y * kslice;
+  const int64_t k_hi = k_lo + kslice < K ? k_lo + kslice : K;
+  Acc<T> acc;
+  acc.zero();
+  mainloop<T>(smem, acc, A, lda, bi * T::BM, n, A, lda, bj * T::BN, n, k_lo, k_hi);
+  double *dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (T::BM * T::BN);
+  store_tile<T>(acc, dst, T::BN, 0, T::BM, 0, T::BN);
+}
+
+__global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, int64_t ntiles,
+                              int64_t n, double *__restrict__ G) {
+  using T = TileSyrk;
+  const int64_t per = T::BM * T::BN;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntiles * per;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = e / per, loc = e - t * per;
+    int64_t bi, bj;
+    tri_decode(t, bi, bj);
+    int64_t r = bi * T::BM + loc / T::BN, c = bj * T::BN + loc % T::BN;
+    if (r >= n || c >= n || c > r) continue;
+    double s = 0.0;
+    for (int64_t sp = 0; sp < splits; ++sp) s += part[(sp * ntiles + t) * per + loc];
+    G[r * n + c] = s;
+    G[c * n + r] = s;
+  }
+}
+
+// ===================================================== shift projection (K4a)
+__global__ void k_shift_project(const double *__restrict__ Z, int64_t ldz, int64_t n, int64_t r,
+                                const double *__restrict__ T, int64_t ld_table, int64_t R,
+                                int64_t n_shift, double *__restrict__ TT) {
+  const int64_t total = r * n_shift * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = e % R, s = (e / R) % n_shift, a = e / (R * n_shift);
+    const double *col = T + s * ld_table + k;
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc = fma(Z[i * ldz + a], col[i * ld_table], acc);
+    TT[e] = acc;
+  }
+}
+
+// ============================================================ RHOSVD core (K4b)
+constexpr int CORE_THREADS = 256;
+constexpr int CORE_EPT = 24;  // core entries per thread
+constexpr int CORE_COLS = 32; // (particle, term) columns staged per round
+
+__global__ void __launch_bounds__(CORE_THREADS)
+    k_core_part(const double *__restrict__ TT1, const double *__restrict__ TT2,
+                const double *__restrict__ TT3, int r1, int r2, int r3, int64_t n_shift, int R,
+                const int64_t *__restrict__ shift, const double *__restrict__ z,
+                const double *__restrict__ w, int64_t count, int64_t per_split, int a_tile,
+                double *__restrict__ part) {
+  extern __shared__ __align__(16) double sm[];
+  const int a0 = blockIdx.y * a_tile;
+  const int na = min(a_tile, r1 - a0);
+  const int rs = na + r2 + r3;  // staged values per column
+  double *col = sm;             // CORE_COLS x rs
+  const int64_t p_lo = blockIdx.x * per_split;
+  const int64_t p_hi = min(count, p_lo + per_split);
+  const int entries = na * r2 * r3;
+  double acc[CORE_EPT];
+  int ia[CORE_EPT], ib[CORE_EPT], ic[CORE_EPT];
+#pragma unroll
+  for (int j = 0; j < CORE_EPT; ++j) {
+    int e = threadIdx.x + j * CORE_THREADS;
+    acc[j] = 0.0;
+    int ee = e < entries ? e : 0;
+    ia[j] = ee / (r2 * r3);
+    ib[j] = na + (ee / r3) % r2;
+    ic[j] = na + r2 + ee % r3;
+  }
+  const int64_t ncols = (p_hi - p_lo) * R;
+  for (int64_t c0 = 0; c0 < ncols; c0 += CORE_COLS) {
+    __syncthreads();
+    const int nc = (int)(ncols - c0 < CORE_COLS ? ncols - c0 : CORE_COLS);
+    for (int e = threadIdx.x; e < nc * rs; e += CORE_THREADS) {
+      int cc = e / rs, v = e - cc * rs;
+      int64_t gc = c0 + cc;
+      int64_t p = p_lo + gc / R;
+      int k = (int)(gc % R);
+      double val;
+      if (v < na) {
+        int64_t s = shift[3 * p + 0];
+        val = z[p] * w[k] * TT1[((int64_t)(a0 + v) * n_shift + s) * R + k];
+      } else if (v < na + r2) {
+        int64_t s = shift[3 * p + 1];
+        val = TT2[((int64_t)(v - na) * n_shift + s) * R + k];
+      } else {
+        int64_t s = shift[3 * p + 2];
+        val = TT3[((int64_t)(v - na - r2) * n_shift + s) * R + k];
+      }
+      col[cc * rs + v] = val;
+    }
+    __syncthreads();
+    for (int cc = 0; cc < nc; ++cc) {
+      const double *cv = col + cc * rs;
+#pragma unroll
+      for (int j = 0; j < CORE_EPT; ++j) acc[j] = fma(cv[ia[j]] * cv[ib[j]], cv[ic[j]], acc[j]);
+    }
+  }
+  const int64_t r123 = (int64_t)r1 * r2 * r3;
+#pragma unroll
+  for (int j = 0; j < CORE_EPT; ++j) {
+    int e = threadIdx.x + j * CORE_THREADS;
+    if (e < entries) part[blockIdx.x * r123 + (int64_t)a0 * r2 * r3 + e] = acc[j];
+  }
+}
+
+__global__ void k_split_reduce(const double *__restrict__ part, int64_t splits, int64_t len,
+                               double *__restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t sp = 0; sp < splits; ++sp) s += part[sp * len + e];
+    out[e] = s;
+  }
+}
+
+// ===================================================== grid assembly (K5)
+// Y[x1l, b, c] = sum_a V1[x1, a] core[a, b, c]
+__global__ void k_tucker_y(const double *__restrict__ core, int r1, int r2, int r3,
+                           const double *__restrict__ V1, int64_t x1_lo, int64_t planes,
+                           double *__restrict__ Y) {
+  const int64_t total = planes * r2 * r3;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t bc = e % ((int64_t)r2 * r3), x1l = e / ((int64_t)r2 * r3);
+    const double *v = V1 + (x1_lo + x1l) * r1;
+    double acc = 0.0;
+    for (int a = 0; a < r1; ++a) acc = fma(v[a], core[(int64_t)a * r2 * r3 + bc], acc);
+    Y[e] = acc;
+  }
+}
+
+// A[(x1l*n + x2), c] = sum_b V2[x2, b] Y[x1l, b, c] for c < r3, 0 for r3 <= c < r3p
+__global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p,
+                           const double *__restrict__ V2, int64_t n, int64_t planes,
+                           double *__restrict__ A, int64_t lda) {
+  const int64_t total = planes * n * r3p;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = e % r3p, row = e / r3p;
+    int64_t x2 = row % n, x1l = row / n;
+    double acc = 0.0;
+    if (c < r3) {
+      const double *y = Y + x1l * r2 * r3 + c;
+      const double *v = V2 + x2 * r2;
+      for (int b = 0; b < r2; ++b) acc = fma(v[b], y[(int64_t)b * r3], acc);
+    }
+    A[row * lda + c] = acc;
+  }
+}
+
+// Short-range rows, x3-merged: for plane x1 and x3-bucket b,
+// A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
+//                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
+constexpr int SD_THREADS = 256;
+constexpr int SD_MAXR = 24;
+constexpr int SD_PCHUNK = 64;
+
+__global__ void __launch_bounds__(SD_THREADS)
+    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
+                 int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+                 const double *__restrict__ zq, const int32_t *__restrict__ bstart, int64_t n,
+                 int64_t x1_lo, double *__restrict__ A, int64_t lda, int64_t col0) {
+  __shared__ double alpha[SD_PCHUNK][SD_MAXR];
+  __shared__ int pc2[SD_PCHUNK];
+  const int64_t x1l = blockIdx.x;
+  const int64_t x1 = x1_lo + x1l;
+  const int b = blockIdx.y;
+  const int p_lo = bstart[b], p_hi = bstart[b + 1];
+  // each thread owns rows x2 = threadIdx.x + j * SD_THREADS
+  const int rows_per = (int)((n + SD_THREADS - 1) / SD_THREADS);
+  for (int j = 0; j < rows_per; ++j) {
+    int64_t x2 = threadIdx.x + (int64_t)j * SD_THREADS;
+    double acc[SD_MAXR];
+#pragma unroll
+    for (int k = 0; k < SD_MAXR; ++k) acc[k] = 0.0;
+    for (int q0 = p_lo; q0 < p_hi; q0 += SD_PCHUNK) {
+      const int nq = min(SD_PCHUNK, p_hi - q0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nq * Rs; e += SD_THREADS) {
+        int q = e / Rs, k = e - q * Rs;
+        int d1 = (int)(x1 - c1[q0 + q]);
+        double v = 0.0;
+        if (d1 >= -gamma && d1 <= gamma) v = zq[q0 + q] * wl[k] * ul[(d1 + gamma) * Rs + k];
+        alpha[q][k] = v;
+        if (k == 0) pc2[q] = (d1 >= -gamma && d1 <= gamma) ? c2[q0 + q] : INT32_MIN / 2;
+      }
+      __syncthreads();
+      if (x2 < n) {
+        for (int q = 0; q < nq; ++q) {
+          int d2 = (int)(x2 - pc2[q]);
+          if (d2 < -gamma || d2 > gamma) continue;
+          const double *u = ul + (int64_t)(d2 + gamma) * Rs;
+#pragma unroll
+          for (int k = 0; k < SD_MAXR; ++k)
+            if (k < Rs) acc[k] = fma(alpha[q][k], u[k], acc[k]);
+        }
+      }
+    }
+    if (x2 < n) {
+      double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)b * G;
+#pragma unroll
+      for (int k = 0; k < SD_MAXR; ++k)
+        if (k < G) dst[k] = k < Rs ? acc[k] : 0.0;
+    }
+  }
+}
+
+// Bt[x3, :] = [V3[x3, :r3], 0.., E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in the band.
+__global__ void k_build_bt(const double *__restrict__ V3, int r3, int r3p,
+                           const double *__restrict__ ul, int Rs, int G, int gamma,
+                           const int32_t *__restrict__ bc3, int64_t n_buckets, int64_t n,
+                           double *__restrict__ Bt, int64_t ldb) {
+  const int64_t total = n * ldb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x3 = e / ldb, col = e - x3 * ldb;
+    double v = 0.0;
+    if (col < r3) {
+      v = V3[x3 * r3 + col];
+    } else if (col >= r3p) {
+      int64_t q = col - r3p, b = q / G;
+      int k = (int)(q - b * G);
+      if (b < n_buckets && k < Rs) {
+        int64_t d = x3 - bc3[b];
+        if (d >= -gamma && d <= gamma) v = ul[(d + gamma) * Rs + k];
+      }
+    }
+    Bt[e] = v;
+  }
+}
+
+// Per column tile t: range 0 = Tucker columns [0, r3p), range 1 = the buckets
+// whose x3 index lies within gamma of the tile's x3 span.
+__global__ void k_band_ranges(const int32_t *__restrict__ bc3, int64_t n_buckets, int64_t n,
+                              int gamma, int BN, int64_t r3p, int G, int64_t ntiles,
+                              int64_t *__restrict__ ranges) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  int64_t top = t * BN + BN - 1 < n - 1 ? t * BN + BN - 1 : n - 1;
+  int64_t lo_x = t * BN - gamma, hi_x = top + gamma;
+  // first bucket with bc3 >= lo_x, first bucket with bc3 > hi_x (bc3 ascending)
+  int64_t a = 0, b = n_buckets;
+  while (a < b) {
+    int64_t m = (a + b) / 2;
+    if (bc3[m] < lo_x) a = m + 1; else b = m;
+  }
+  int64_t blo = a;
+  a = blo;
+  b = n_buckets;
+  while (a < b) {
+    int64_t m = (a + b) / 2;
+    if (bc3[m] <= hi_x) a = m + 1; else b = m;
+  }
+  int64_t bhi = a;
+  ranges[t * 4 + 0] = 0;
+  ranges[t * 4 + 1] = r3p;
+  ranges[t * 4 + 2] = r3p + blo * G;
+  ranges[t * 4 + 3] = r3p + bhi * G;
+}
+
+// ======================================================== point evaluation
+// warp per point: Tucker value sum_abc core V1[i,a] V2[j,b] V3[l,c]
+__global__ void k_eval_tucker(const double *__restrict__ core, int r1, int r2, int r3,
+                              const double *__restrict__ V1, const double *__restrict__ V2,
+                              const double *__restrict__ V3, const int64_t *__restrict__ idx,
+                              int64_t m, double *__restrict__ out) {
+  const int64_t pt = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (pt >= m) return;
+  const double *v1 = V1 + idx[3 * pt] * r1;
+  const double *v2 = V2 + idx[3 * pt + 1] * r2;
+  const double *v3 = V3 + idx[3 * pt + 2] * r3;
+  double acc = 0.0;
+  for (int ab = lane; ab < r1 * r2; ab += 32) {
+    int a = ab / r2, b = ab - a * r2;
+    const double *cr = core + (int64_t)ab * r3;
+    double t = 0.0;
+    for (int c = 0; c < r3; ++c) t = fma(cr[c], v3[c], t);
+    acc = fma(v1[a] * v2[b], t, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[pt] = acc;
+}
+
+// warp per point: short-range value and hit count (brute force over copies)
+__global__ void k_eval_cct(const double *__restrict__ ul, const double *__restrict__ wl, int Rs,
+                           int gamma, const int64_t *__restrict__ centers,
+                           const double *__restrict__ zq, int64_t count,
+                           const int64_t *__restrict__ idx, int64_t m, double *__restrict__ out,
+                           int32_t *__restrict__ hits) {
+  const int64_t pt = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (pt >= m) return;
+  const int64_t i0 = idx[3 * pt], i1 = idx[3 * pt + 1], i2 = idx[3 * pt + 2];
+  dd acc{0.0, 0.0};
+  int h = 0;
+  for (int64_t p = lane; p < count; p += 32) {
+    int64_t o0 = i0 - centers[3 * p], o1 = i1 - centers[3 * p + 1], o2 = i2 - centers[3 * p + 2];
+    if (o0 < -gamma || o0 > gamma || o1 < -gamma || o1 > gamma || o2 < -gamma || o2 > gamma)
+      continue;
+    ++h;
+    const double *u0 = ul + (o0 + gamma) * Rs, *u1 = ul + (o1 + gamma) * Rs,
+                 *u2 = ul + (o2 + gamma) * Rs;
+    double s = 0.0;
+    for (int k = 0; k < Rs; ++k) s = fma(wl[k], u0[k] * u1[k] * u2[k], s);
+    acc = dd_add_d(acc, zq[p] * s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+    acc = dd_add(acc, other);
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+  }
+  if (lane == 0) {
+    out[pt] = acc.hi + acc.lo;
+    hits[pt] = h;
+  }
+}
+
+// ============================================ windowed pair sums (K6: energy/forces)
+constexpr int PS_THREADS = 256;
+
+__device__ __forceinline__ double window_value(const double *__restrict__ T, int64_t ldt,
+                                               int64_t n0, const double *__restrict__ w, int Rl,
+                                               double h3, int64_t o0, int64_t o1, int64_t o2) {
+  const double *r0 = T + (n0 + o0) * ldt, *r1 = T + (n0 + o1) * ldt, *r2 = T + (n0 + o2) * ldt;
+  double s = 0.0;
+  for (int k = 0; k < Rl; ++k) s = fma(__dmul_rn(__dmul_rn(r0[k], r1[k]), r2[k]), w[k], s);
+  return s / h3;
+}
+
+__device__ dd block_reduce_dd(dd v, dd *scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd other{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+    v = dd_add(v, other);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  dd r{0.0, 0.0};
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = dd_add(r, scratch[i]);
+  return r;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(PS_THREADS)
+    k_pair_sums(const double *__restrict__ T, int64_t ldt, int64_t n0, const double *__restrict__ w,
+                int Rl, double h3, const int64_t *__restrict__ idx, const double *__restrict__ z,
+                int64_t count, const int64_t *__restrict__ tgt, int mode,
+                double *__restrict__ base, double *__restrict__ dshift) {
+  __shared__ dd scratch[PS_THREADS / 32];
+  const int64_t j = tgt[blockIdx.x];
+  const int64_t j0 = idx[3 * j], j1 = idx[3 * j + 1], j2 = idx[3 * j + 2];
+  if (mode == 0) {
+    dd acc{0.0, 0.0};
+    for (int64_t p = threadIdx.x; p < count; p += PS_THREADS) {
+      double v = window_value(T, ldt, n0, w, Rl, h3, j0 - idx[3 * p], j1 - idx[3 * p + 1],
+                              j2 - idx[3 * p + 2]);
+      acc = dd_add_d(acc, __dmul_rn(z[p], v));
+    }
+    dd r = block_reduce_dd(acc, scratch);
+    if (threadIdx.x == 0) base[blockIdx.x] = r.hi + r.lo;
+  } else {
+    dd acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t p = threadIdx.x; p < count; p += PS_THREADS) {
+      if (p == j) continue;
+      int64_t o0 = j0 - idx[3 * p], o1 = j1 - idx[3 * p + 1], o2 = j2 - idx[3 * p + 2];
+      double b0 = window_value(T, ldt, n0, w, Rl, h3, o0, o1, o2);
+      double s0 = window_value(T, ldt, n0, w, Rl, h3, o0 - 1, o1, o2);
+      double s1 = window_value(T, ldt, n0, w, Rl, h3, o0, o1 - 1, o2);
+      double s2 = window_value(T, ldt, n0, w, Rl, h3, o0, o1, o2 - 1);
+      acc[0] = dd_add_d(acc[0], __dmul_rn(z[p], __dsub_rn(s0, b0)));
+      acc[1] = dd_add_d(acc[1], __dmul_rn(z[p], __dsub_rn(s1, b0)));
+      acc[2] = dd_add_d(acc[2], __dmul_rn(z[p], __dsub_rn(s2, b0)));
+    }
+    for (int a = 0; a < 3; ++a) {
+      dd r = block_reduce_dd(acc[a], scratch);
+      if (threadIdx.x == 0) dshift[3 * blockIdx.x + a] = r.hi + r.lo;
+    }
+  }
+}
+
+// ================================================= compensated vector sum
+constexpr int SUM_THREADS = 256;
+__global__ void __launch_bounds__(SUM_THREADS)
+    k_sum_dd_part(const double *__restrict__ v, int64_t m, int64_t per, double *__restrict__ part) {
+  __shared__ dd scratch[SUM_THREADS / 32];
+  int64_t lo = blockIdx.x * per, hi = min(m, lo + per);
+  dd acc{0.0, 0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += SUM_THREADS) acc = dd_add_d(acc, v[i]);
+  dd r = block_reduce_dd(acc, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r.hi;
+    part[2 * blockIdx.x + 1] = r.lo;
+  }
+}
+
+__global__ void k_sum_dd_final(const double *__restrict__ part, int64_t np, double *__restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  dd acc{0.0, 0.0};
+  for (int64_t i = 0; i < np; ++i) acc = dd_add(acc, dd{part[2 * i], part[2 * i + 1]});
+  out[0] = acc.hi + acc.lo;
+}
+
+inline int grid_for(int64_t total, int threads) {
+  int64_t g = ceil_div(total, threads);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64));
+}
+
+template <class T>
+int set_smem(const void *fn) {
+  cudaError_t e =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  return RS_OK;
+}
+
+}  // namespace rsb
+
+using namespace rsb;
+
+// ============================================================== C ABI
+extern "C" {
+
+int rs_abi_version(void) { return 1; }
+const char *rs_last_error(void) { return g_err; }
+
+int rs_snap(const double *pos, int64_t count, double h, int64_t n, int64_t *idx, double *disp,
+            void *stream) {
+  RS_REQUIRE(count >= 0 && n >= 2 && h > 0, "rs_snap: bad arguments");
+  if (count == 0) return RS_OK;
+  RS_REQUIRE(pos && idx && disp, "rs_snap: null pointer");
+  k_snap<<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(pos, count, h, n, idx, disp);
+  return check_launch("rs_snap");
+}
+
+int rs_gather_windows(const double *table, int64_t ld_table, int64_t n_rows, const int64_t *starts,
+                      int64_t n_groups, int64_t n_terms, int64_t term0, const double *gscale,
+                      const double *tscale, double *out, int64_t ld_out, void *stream) {
+  RS_REQUIRE(n_rows >= 0 && n_groups >= 0 && n_terms >= 0 && term0 >= 0,
+             "rs_gather_windows: negative size");
+  RS_REQUIRE(ld_out >= n_groups * n_terms && ld_table >= term0 + n_terms,
+             "rs_gather_windows: leading dimension too small");
+  int64_t total = n_rows * n_groups * n_terms;
+  if (total == 0) return RS_OK;
+  k_gather<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+      table, ld_table, n_rows, starts, n_groups, n_terms, term0, gscale, tscale, out, ld_out);
+  return check_launch("rs_gather_windows");
+}
+
+static int64_t syrk_splits(int64_t n, int64_t K, int64_t *kslice) {
+  const int64_t nt = ceil_div(n, TileSyrk::BM);
+  const int64_t ntp = nt * (nt + 1) / 2;
+  int64_t want = std::max<int64_t>(1, ceil_div(148 * 3, ntp));
+  int64_t ks = round_up(std::max<int64_t>(ceil_div(K, want), 1), TileSyrk::BK);
+  ks = std::max<int64_t>(ks, 64);
+  *kslice = ks;
+  return std::max<int64_t>(1, ceil_div(K, ks));
+}
+
+int64_t rs_syrk_workspace_bytes(int64_t n, int64_t K) {
+  int64_t ks;
+  int64_t sp = syrk_splits(n, K, &ks);
+  int64_t nt = ceil_div(n, TileSyrk::BM);
+  return sp * (nt * (nt + 1) / 2) * TileSyrk::BM * TileSyrk::BN * 8;
+}
+
+int rs_syrk(const double *A, int64_t lda, int64_t n, int64_t K, double *G, void *work,
+            int64_t work_bytes, void *stream) {
+  RS_REQUIRE(n >= 1 && K >= 0 && lda >= K, "rs_syrk: bad shape");
+  RS_REQUIRE(lda % 2 == 0 && K % 2 == 0, "rs_syrk: lda and K must be even (pad with zeros)");
+  RS_REQUIRE(((uintptr_t)A & 15) == 0, "rs_syrk: A must be 16-byte aligned");
+  int64_t ks;
+  int64_t sp = syrk_splits(n, K, &ks);
+  int64_t nt = ceil_div(n, TileSyrk::BM), ntp = nt * (nt + 1) / 2;
+  int64_t need = sp * ntp * TileSyrk::BM * TileSyrk::BN * 8;
+  if (work_bytes < need) return fail(RS_ERR_CAPACITY, "rs_syrk: workspace %lld < %lld",
+                                     (long long)work_bytes, (long long)need);
+  int st = set_smem<TileSyrk>((const void *)k_syrk_part);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  double *part = (double *)work;
+  k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
+      A, lda, n, K, ks, part);
+  if ((st = check_launch("rs_syrk part"))) return st;
+  int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
+  k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G);
+  return check_launch("rs_syrk reduce");
+}
+
+int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+               int64_t M, int64_t N, int64_t K, void *stream) {
+  RS_REQUIRE(M >= 0 && N >= 0 && K >= 0 && lda >= K && ldb >= K && ldc >= N, "rs_gemm_nt: bad shape");
+  RS_REQUIRE(lda % 2 == 0 && ldb % 2 == 0 && K % 2 == 0, "rs_gemm_nt: lda, ldb, K must be even");
+  RS_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0, "rs_gemm_nt: operands must be 16-byte aligned");
+  if (M == 0 || N == 0) return RS_OK;
+  int st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane>);
+  if (st) return st;
+  dim3 grid((unsigned)ceil_div(N, TilePlane::BN), (unsigned)ceil_div(M, TilePlane::BM));
+  k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, as_stream(stream)>>>(
+      A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
+  return check_launch("rs_gemm_nt");
+}
+
+int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const double *table,
+                     int64_t ld_table, int64_t R, int64_t n_shift, double *TT, void *stream) {
+  RS_REQUIRE(n >= 1 && r >= 1 && R >= 1 && n_shift >= 1 && ldz >= r && ld_table >= R,
+             "rs_shift_project: bad shape");
+  int64_t total = r * n_shift * R;
+  k_shift_project<<<grid_for(total, 128), 128, 0, as_stream(stream)>>>(Z, ldz, n, r, table,
+                                                                         ld_table, R, n_shift, TT);
+  return check_launch("rs_shift_project");
+}
+
+static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t *splits,
+                      int64_t *per, int *a_tile, int64_t *a_tiles) {
+  int64_t cap = (int64_t)CORE_THREADS * CORE_EPT;
+  int64_t at = std::max<int64_t>(1, std::min<int64_t>(r1, cap / std::max<int64_t>(1, r2 * r3)));
+  *a_tile = (int)at;
+  *a_tiles = ceil_div(r1, at);
+  int64_t r123 = r1 * r2 * r3;
+  int64_t by_mem = std::max<int64_t>(1, ((int64_t)1 << 27) / std::max<int64_t>(1, r123));
+  int64_t want = std::max<int64_t>(1, ceil_div(148 * 4, *a_tiles));
+  int64_t sp = std::min<int64_t>({want, by_mem, std::max<int64_t>(1, count)});
+  *per = ceil_div(count, sp);
+  *splits = ceil_div(count, *per);
+}
+
+int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count) {
+  int64_t sp, per, at_n;
+  int at;
+  core_plan(r1, r2, r3, count, &sp, &per, &at, &at_n);
+  return sp * r1 * r2 * r3 * 8;
+}
+
+int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1, int64_t r2,
+            int64_t r3, int64_t n_shift, int64_t R, const int64_t *shift, const double *z,
+            const double *w, int64_t count, double *core, void *work, int64_t work_bytes,
+            void *stream) {
+  RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && R >= 1 && count >= 1, "rs_core: bad shape");
+  RS_REQUIRE(r2 * r3 <= (int64_t)CORE_THREADS * CORE_EPT,
+             "rs_core: r2*r3 = %lld exceeds %d", (long long)(r2 * r3), CORE_THREADS * CORE_EPT);
+  int64_t sp, per, at_n;
+  int at;
+  core_plan(r1, r2, r3, count, &sp, &per, &at, &at_n);
+  int64_t need = sp * r1 * r2 * r3 * 8;
+  if (work_bytes < need) return fail(RS_ERR_CAPACITY, "rs_core: workspace too small");
+  size_t smem = (size_t)CORE_COLS * (at + r2 + r3) * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_core_part,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "rs_core smem: %s", cudaGetErrorString(e));
+  }
+  cudaStream_t s = as_stream(stream);
+  double *part = (double *)work;
+  k_core_part<<<dim3((unsigned)sp, (unsigned)at_n), CORE_THREADS, smem, s>>>(
+      TT1, TT2, TT3, (int)r1, (int)r2, (int)r3, n_shift, (int)R, shift, z, w, count, per, at, part);
+  int st = check_launch("rs_core part");
+  if (st) return st;
+  int64_t len = r1 * r2 * r3;
+  k_split_reduce<<<grid_for(len, 256), 256, 0, s>>>(part, sp, len, core);
+  return check_launch("rs_core reduce");
+}
+
+// workspace: A (planes*n x lda) | Bt (n x lda) | Y (planes x r2 r3) | ranges
+static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int64_t n_buckets,
+                       int64_t Rs, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
+                       int64_t *offY, int64_t *offR, int64_t *total) {
+  *r3p = round_up(std::max<int64_t>(r3, 1), 2);
+  *G = round_up(std::max<int64_t>(Rs, 1), 2);
+  *lda = *r3p + n_buckets * *G;
+  int64_t a = round_up(planes * n * *lda * 8, 256);
+  int64_t b = round_up(n * *lda * 8, 256);
+  int64_t y = round_up(planes * r2r3 * 8, 256);
+  int64_t ntiles = ceil_div(n, TilePlane::BN);
+  int64_t rr = round_up(ntiles * 4 * 8, 256);
+  *offB = a;
+  *offY = a + b;
+  *offR = a + b + y;
+  *total = a + b + y + rr;
+}
+
+int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t n_buckets,
+                                    int64_t Rs) {
+  int64_t lda, r3p, G, oB, oY, oR, tot;
+  asm_layout(n, planes, rmax * rmax, rmax, Rs > 0 ? n_buckets : 0, Rs, &lda, &r3p, &G, &oB, &oY,
+             &oR, &tot);
+  return tot;
+}
+
+int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, const double *V1,
+                       const double *V2, const double *V3, int64_t n, const double *ul,
+                       const double *wl, int64_t Rs, int64_t gamma, const int32_t *c1,
+                       const int32_t *c2, const double *zq, const int32_t *bstart,
+                       const int32_t *bc3, int64_t n_buckets, int64_t x1_lo, int64_t x1_hi,
+                       double *out, void *work, int64_t work_bytes, void *stream) {
+  RS_REQUIRE(n >= 2 && r1 >= 1 && r2 >= 1 && r3 >= 1, "rs_assemble_planes: bad ranks");
+  RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
+  RS_REQUIRE(Rs >= 0 && Rs <= SD_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs, SD_MAXR);
+  RS_REQUIRE(gamma >= 0 && 2 * gamma + 1 <= 2 * n, "rs_assemble_planes: bad gamma");
+  const int64_t planes = x1_hi - x1_lo;
+  const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
+  int64_t lda, r3p, G, oB, oY, oR, tot;
+  asm_layout(n, planes, rmax * rmax, r3, Rs > 0 ? n_buckets : 0, Rs, &lda, &r3p, &G, &oB, &oY,
+             &oR, &tot);
+  if (work_bytes < tot)
+    return fail(RS_ERR_CAPACITY, "rs_assemble_planes: workspace %lld < %lld",
+                (long long)work_bytes, (long long)tot);
+  char *wb = (char *)work;
+  double *A = (double *)wb;
+  double *Bt = (double *)(wb + oB);
+  double *Y = (double *)(wb + oY);
+  int64_t *ranges = (int64_t *)(wb + oR);
+  cudaStream_t s = as_stream(stream);
+  int st;
+  const int64_t nb = Rs > 0 ? n_buckets : 0;
+  k_tucker_y<<<grid_for(planes * r2 * r3, 128), 128, 0, s>>>(core, (int)r1, (int)r2, (int)r3, V1,
+                                                             x1_lo, planes, Y);
+  if ((st = check_launch("tucker_y"))) return st;
+  k_tucker_f<<<grid_for(planes * n * r3p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r3p, V2, n,
+                                                             planes, A, lda);
+  if ((st = check_launch("tucker_f"))) return st;
+  if (nb > 0) {
+    k_short_rows<<<dim3((unsigned)planes, (unsigned)nb), SD_THREADS, 0, s>>>(
+        ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, n, x1_lo, A, lda, r3p);
+    if ((st = check_launch("short_rows"))) return st;
+  }
+  k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(V3, (int)r3, (int)r3p, ul, (int)Rs, (int)G,
+                                                     (int)gamma, bc3, nb, n, Bt, lda);
+  if ((st = check_launch("build_bt"))) return st;
+  const int64_t ntiles = ceil_div(n, TilePlane::BN);
+  if (nb > 0) {
+    k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
+        bc3, nb, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles, ranges);
+    if ((st = check_launch("band_ranges"))) return st;
+  }
+  if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane>))) return st;
+  dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
+  k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+      A, lda, Bt, lda, out, n, planes * n, n, r3p, nb > 0 ? ranges : nullptr, 2);
+  return check_launch("plane_gemm");
+}
+
+int rs_eval_tucker(const double *core, int64_t r1, int64_t r2, int64_t r3, const double *V1,
+                   const double *V2, const double *V3, const int64_t *idx, int64_t m, double *out,
+                   void *stream) {
+  RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && m >= 0, "rs_eval_tucker: bad shape");
+  if (m == 0) return RS_OK;
+  k_eval_tucker<<<(unsigned)ceil_div(m * 32, 256), 256, 0, as_stream(stream)>>>(
+      core, (int)r1, (int)r2, (int)r3, V1, V2, V3, idx, m, out);
+  return check_launch("rs_eval_tucker");
+}
+
+int rs_eval_cct(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
+                const int64_t *centers, const double *zq, int64_t count, const int64_t *idx,
+                int64_t m, double *out, int32_t *hits, void *stream) {
+  RS_REQUIRE(Rs >= 1 && gamma >= 0 && count >= 0 && m >= 0, "rs_eval_cct: bad shape");
+  if (m == 0) return RS_OK;
+  k_eval_cct<<<(unsigned)ceil_div(m * 32, 256), 256, 0, as_stream(stream)>>>(
+      ul, wl, (int)Rs, (int)gamma, centers, zq, count, idx, m, out, hits);
+  return check_launch("rs_eval_cct");
+}
+
+int rs_pair_sums(const double *table, int64_t ld_table, int64_t n0, const double *w, int64_t Rl,
+                 double h3, const int64_t *idx, const double *z, int64_t count, const int64_t *tgt,
+                 int64_t m, int mode, double *base, double *dshift, void *stream) {
+  RS_REQUIRE(Rl >= 1 && count >= 1 && m >= 0 && (mode == 0 || mode == 1) && h3 > 0,
+             "rs_pair_sums: bad arguments");
+  if (m == 0) return RS_OK;
+  k_pair_sums<<<(unsigned)m, PS_THREADS, 0, as_stream(stream)>>>(
+      table, ld_table, n0, w, (int)Rl, h3, idx, z, count, tgt, mode, base, dshift);
+  return check_launch("rs_pair_sums");
+}
+
+int64_t rs_sum_workspace_bytes(int64_t m) {
+  int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(1024, ceil_div(m, 4096)));
+  return blocks * 16;
+}
+
+int rs_sum_dd(const double *v, int64_t m, double *out, void *work, int64_t work_bytes,
+              void *stream) {
+  RS_REQUIRE(m >= 0, "rs_sum_dd: bad size");
+  int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(1024, ceil_div(m, 4096)));
+  if (work_bytes < blocks * 16) return fail(RS_ERR_CAPACITY, "rs_sum_dd: workspace too small");
+  int64_t per = std::max<int64_t>(1, ceil_div(m, blocks));
+  cudaStream_t s = as_stream(stream);
+  k_sum_dd_part<<<(unsigned)blocks, SUM_THREADS, 0, s>>>(v, m, per, (double *)work);
+  int st = check_launch("rs_sum_dd part");
+  if (st) return st;
+  k_sum_dd_final<<<1, 32, 0, s>>>((double *)work, blocks, out);
+  return check_launch("rs_sum_dd final");
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""Kernel-level checks of librsb200.so against numpy references (float64)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nat(cuda):
+    from paper_1606_09218_b200 import _native
+    _native.load_library()
+    return _native
+
+
+@pytest.mark.parametrize("n,K", [(8, 2), (37, 130), (64, 64), (256, 700), (130, 4000), (300, 18)])
+def test_syrk_matches_numpy(nat, cuda, n, K):
+    from paper_1606_09218_b200.rankred import gram
+    rng = np.random.default_rng(n + K)
+    a = rng.normal(size=(n, K))
+    g = gram(cuda.from_numpy(a).cuda()).cpu().numpy()
+    ref = a @ a.T
+    assert np.allclose(g, ref, rtol=0, atol=1e-13 * np.abs(ref).max() * math.sqrt(K))
+    assert np.array_equal(g, g.T)
+
+
+def test_syrk_deterministic(nat, cuda):
+    from paper_1606_09218_b200.rankred import gram
+    a = cuda.randn(200, 5000, dtype=cuda.float64, device="cuda")
+    g1, g2 = gram(a), gram(a)
+    assert cuda.equal(g1, g2)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 2), (129, 65, 30), (1000, 256, 712), (77, 300, 8)])
+def test_gemm_nt(nat, cuda, M, N, K):
+    rng = np.random.default_rng(M * N)
+    a = rng.normal(size=(M, K))
+    b = rng.normal(size=(N, K))
+    A = cuda.from_numpy(a).cuda()
+    B = cuda.from_numpy(b).cuda()
+    C = cuda.empty((M, N), dtype=cuda.float64, device="cuda")
+    nat.check(nat.lib().rs_gemm_nt(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K,
+                                   nat.stream_ptr()), "gemm")
+    ref = a @ b.T
+    assert np.allclose(C.cpu().numpy(), ref, rtol=0, atol=1e-13 * np.abs(ref).max() * math.sqrt(K))
+
+
+def test_gather_windows(nat, cuda):
+    rng = np.random.default_rng(3)
+    n, R = 40, 9
+    table = rng.normal(size=(2 * n, R))
+    starts = np.array([1, 5, 40, 17], dtype=np.int64)
+    gs = rng.uniform(1, 2, size=4)
+    ts = rng.uniform(1, 2, size=5)
+    T = cuda.from_numpy(table).cuda()
+    S = cuda.from_numpy(starts).cuda()
+    out = cuda.empty((n, 20), dtype=cuda.float64, device="cuda")
+    nat.check(nat.lib().rs_gather_windows(T.data_ptr(), R, n, S.data_ptr(), 4, 5, 2,
+                                          cuda.from_numpy(gs).cuda().data_ptr(),
+                                          cuda.from_numpy(ts).cuda().data_ptr(), out.data_ptr(), 20,
+                                          nat.stream_ptr()), "gather")
+    ref = np.concatenate([table[s:s + n, 2:7] * g * ts for s, g in zip(starts, gs)], axis=1)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_snap_bit_exact(nat, cuda):
+    import paper_1606_09218_b200 as rt
+    from paper_1606_09218_b200 import configs
+    for name in ("C2", "C3"):
+        s = configs.system(name)
+        m = configs.MANIFEST[name]
+        grid = rt.Grid3(m["n"], rt.Box3(m["b"]))
+        host = rt.snap_to_grid(s, grid)
+        dev = rt.snap_device(s.positions, s.charges, s.box, grid)
+        assert np.array_equal(dev.indices.cpu().numpy(), host.indices)
+        assert np.array_equal(dev.positions.cpu().numpy(), host.base.positions)
+        assert dev.max_displacement == host.max_displacement
+
+
+def test_sum_dd_matches_fsum(nat, cuda):
+    from paper_1606_09218_b200.observables import dd_sum
+    rng = np.random.default_rng(7)
+    v = np.concatenate([rng.normal(size=100000) * 1e8, rng.normal(size=1000), [1e16, -1e16]])
+    got = float(dd_sum(cuda.from_numpy(v).cuda()))
+    assert got == math.fsum(v)

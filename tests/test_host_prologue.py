@@ -1,0 +1,119 @@
+"""Host prologue of the package vs the reference's own outputs (golden), bit-exact.
+
+Golden hashes were produced by running the reference (tests/golden/make_golden.py);
+equality of sha256 over the raw float64 bytes means bit-identical arrays.
+"""
+import dataclasses
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1606_09218_b200 as rt
+from paper_1606_09218_b200 import configs
+from conftest import load_npz
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+PROLOGUES = {
+    **{k: (m["kernel"], m["lam"], m["b"], m["n"], m["M"], m["split_index"], configs.DELTA)
+       for k, m in configs.MANIFEST.items()},
+    "tiny_newton": ("newton", 1.0, 8.0, 32, 15, 7, 1e-6),
+    "tiny_yukawa": ("yukawa", 0.5, 8.0, 32, 15, 7, 1e-6),
+    "slater48": ("slater", 1.5, 10.0, 48, 17, 8, 1e-6),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PROLOGUES))
+def test_prologue_bit_exact(name, golden):
+    kind, lam, b, n, M, split, delta = PROLOGUES[name]
+    cfg = rt.AssemblyConfig(grid=rt.Grid3(n, rt.Box3(b)), kernel=rt.RadialKernel(kind, lam), M=M,
+                            split_index=split, delta=delta)
+    ref = rt.reference_for(cfg)
+    g = golden[f"prologue_{name}"]
+    assert sha(ref.rule.nodes) == g["nodes_sha"]
+    assert sha(ref.rule.weights) == g["qweights_sha"]
+    assert sha(ref.tensor.weights) == g["weights_sha"]
+    assert sha(ref.table) == g["table_sha"]
+    assert ref.R == g["R"] and ref.rule.h_M == g["h_M"]
+    short, _ = rt.split_tensor(ref, split)
+    assert rt.effective_support(short, delta, ref.grid.h) == g["gamma"]
+    assert dataclasses.replace(ref, split_index=split).self_value() == g["self_value"]
+
+
+def test_generators_match_reference(golden):
+    g = golden["generators"]
+    c1 = rt.generate_random_cluster(64, rt.Box3(6.0), min_sep=1e-9, seed=0, charge_law="uniform")
+    assert sha(c1.positions) == g["c1_pos"] and sha(c1.charges) == g["c1_q"]
+    c4 = rt.generate_random_cluster(3000, rt.Box3(56.0), 0.8, seed=0, charge_law="uniform")
+    assert sha(c4.positions) == g["c4_3000_pos"] and sha(c4.charges) == g["c4_3000_q"]
+    lat = rt.generate_lattice((7, 5, 3), 1.25, charge_law="random_sign", seed=3)
+    assert sha(lat.positions) == g["lattice_pos"] and sha(lat.charges) == g["lattice_q"]
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_config_systems_and_snap(name, golden):
+    g = golden[f"snap_{name}"]
+    s = configs.system(name)
+    assert sha(s.positions) == g["pos_sha"] and sha(s.charges) == g["q_sha"]
+    m = configs.MANIFEST[name]
+    snapped = rt.snap_to_grid(s, rt.Grid3(m["n"], rt.Box3(m["b"])))
+    assert snapped.count == g["count"] == m["N"]
+    assert sha(snapped.indices) == g["indices"]
+    assert sha(snapped.base.positions) == g["positions"]
+    assert snapped.max_displacement == g["max_disp"]
+
+
+def test_snap_collision_raises():
+    grid = rt.Grid3(8, rt.Box3(1.0))
+    sys2 = rt.ParticleSystem(np.array([[0.01, 0.0, 0.0], [-0.01, 0.0, 0.0]]), np.ones(2), rt.Box3(1.0))
+    with pytest.raises(rt.ResolutionError):
+        rt.snap_to_grid(sys2, grid)
+
+
+def test_snap_ties_low_and_clip():
+    grid = rt.Grid3(8, rt.Box3(1.0))   # h = 0.25
+    pos = np.array([[0.125, -0.999, 0.999], [0.0, 0.0, 0.0]])
+    s = rt.snap_to_grid(rt.ParticleSystem(pos, np.ones(2), rt.Box3(1.0)), grid)
+    assert s.indices[0].tolist() == [4, 1, 7]
+    assert s.indices[1].tolist() == [4, 4, 4]
+
+
+def test_config_validation():
+    with pytest.raises(rt.ConfigError):
+        rt.ReductionConfig()
+    with pytest.raises(rt.ConfigError):
+        rt.ReductionConfig(eps=1e-3, ranks=(1, 1, 1))
+    with pytest.raises(rt.ConfigError):
+        rt.ReductionConfig(ranks=(1, 0, 1))
+    with pytest.raises(rt.ConfigError):
+        rt.AssemblyConfig(grid=rt.Grid3(8, rt.Box3(1.0)), long_format="dense")
+    with pytest.raises(rt.ConfigError):
+        rt.AssemblyConfig(grid=rt.Grid3(8, rt.Box3(1.0)), delta=2.0)
+    with pytest.raises(rt.DomainError):
+        rt.Grid3(7, rt.Box3(1.0))
+    with pytest.raises(rt.DomainError):
+        rt.ParticleSystem(np.array([[2.0, 0, 0]]), np.ones(1), rt.Box3(1.0))
+    with pytest.raises(rt.CapabilityError):
+        rt.RadialKernel("coulomb")
+
+
+def test_particle_file_roundtrip(tmp_path):
+    s = configs.system("C1")
+    p = tmp_path / "c1.txt"
+    rt.save_particles(s, p)
+    back = rt.load_particles(p)
+    assert np.array_equal(back.positions, s.positions) and np.array_equal(back.charges, s.charges)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("# rs-particles v1 b=2.0\n0 0 0 1\nnot a number here\n")
+    with pytest.raises(rt.ParseError, match="line 3"):
+        rt.load_particles(bad)
+
+
+def test_separation_distance_matches_bruteforce():
+    s = rt.generate_random_cluster(5000, rt.Box3(20.0), 0.3, seed=4)
+    from scipy.spatial.distance import pdist
+    assert rt.separation_distance(s) == float(pdist(s.positions).min())
