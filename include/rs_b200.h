@@ -38,6 +38,13 @@ extern "C" {
 int rs_abi_version(void);
 const char *rs_last_error(void);
 
+/* Instrumentation: number of kernels this library has launched, and optional
+ * CUDA-event timing of the hot launches ("gemm_plane", "short_rows", "syrk",
+ * "core", "shift_project").  rs_prof_query synchronises on the recorded events. */
+int64_t rs_launch_count(void);
+int rs_prof_enable(int on);
+int rs_prof_query(const char *name, double *total_ms, int64_t *count);
+
 /* (a2) snap_to_grid, particles.py:302-329.
  * idx[3p+l] = clip(ceil(pos[3p+l]/h + n/2 - 0.5), 1, n-1);
  * disp[p] = |pos_p - (idx_p - n/2) h|_2 (IEEE-exact, no FMA contraction). */

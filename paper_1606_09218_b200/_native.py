@@ -30,6 +30,9 @@ _ptr = ctypes.c_void_p
 SIGNATURES = {
     "rs_abi_version": (_i32, []),
     "rs_last_error": (ctypes.c_char_p, []),
+    "rs_launch_count": (_i64, []),
+    "rs_prof_enable": (_i32, [_i32]),
+    "rs_prof_query": (_i32, [ctypes.c_char_p, ctypes.POINTER(_dbl), ctypes.POINTER(_i64)]),
     "rs_snap": (_i32, [_ptr, _i64, _dbl, _i64, _ptr, _ptr, _ptr]),
     "rs_gather_windows": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64,
                                  _ptr]),
@@ -99,6 +102,14 @@ def ptr(t) -> int | None:
 def stream_ptr() -> int:
     torch = _torch()
     return torch.cuda.current_stream().cuda_stream
+
+
+def prof_query(name: str):
+    """(total_ms, launches) recorded for ``name`` since rs_prof_enable(1)."""
+    ms = _dbl(0.0)
+    cnt = _i64(0)
+    check(lib().rs_prof_query(name.encode(), ctypes.byref(ms), ctypes.byref(cnt)), "rs_prof_query")
+    return ms.value, cnt.value
 
 
 class Workspace:

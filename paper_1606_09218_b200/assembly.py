@@ -220,6 +220,8 @@ def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
 def _collision_flag(idx, n: int):
     """Device int64: index of the first duplicated node key, or -1."""
     torch = nat._torch()
+    if idx.shape[0] < 2:
+        return torch.full((1,), -1, dtype=torch.int64, device=idx.device)
     keys = (idx[:, 0] * n + idx[:, 1]) * n + idx[:, 2]
     ks, _ = torch.sort(keys)
     dup = ks[1:] == ks[:-1]

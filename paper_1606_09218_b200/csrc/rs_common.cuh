@@ -9,9 +9,42 @@
 
 #include "../../include/rs_b200.h"
 
+#include <atomic>
+#include <mutex>
+#include <string.h>
+#include <vector>
+
 namespace rsb {
 
 extern thread_local char g_err[512];
+extern std::atomic<int64_t> g_launches;
+
+// Optional per-kernel CUDA-event timing (rs_prof_enable); off by default.
+struct ProfRec {
+  const char *name;
+  cudaEvent_t a, b;
+};
+extern std::vector<ProfRec> g_prof;
+extern std::mutex g_prof_mu;
+extern bool g_prof_on;
+
+struct ProfScope {
+  cudaStream_t s;
+  const char *name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(cudaStream_t s_, const char *n_) : s(s_), name(n_) {
+    if (!g_prof_on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(ProfRec{name, a, b});
+  }
+};
 
 inline int fail(int code, const char *fmt, ...) {
   va_list ap;
@@ -22,6 +55,7 @@ inline int fail(int code, const char *fmt, ...) {
 }
 
 inline int check_launch(const char *what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) return RS_OK;
   if (e == cudaErrorMemoryAllocation)

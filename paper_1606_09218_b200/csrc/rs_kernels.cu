@@ -9,6 +9,10 @@
 
 namespace rsb {
 thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
+std::vector<ProfRec> g_prof;
+std::mutex g_prof_mu;
+bool g_prof_on = false;
 
 // ===================================================================== snap
 __global__ void k_snap(const double *__restrict__ pos, int64_t count, double h, int64_t n,
@@ -527,6 +531,40 @@ extern "C" {
 int rs_abi_version(void) { return 1; }
 const char *rs_last_error(void) { return g_err; }
 
+int64_t rs_launch_count(void) { return g_launches.load(); }
+
+int rs_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (on) {
+    for (auto &r : g_prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+  }
+  g_prof_on = on != 0;
+  return RS_OK;
+}
+
+int rs_prof_query(const char *name, double *total_ms, int64_t *count) {
+  RS_REQUIRE(name && total_ms && count, "rs_prof_query: null pointer");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double tot = 0.0;
+  int64_t c = 0;
+  for (auto &r : g_prof) {
+    if (strcmp(r.name, name) != 0) continue;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "rs_prof_query: %s", cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    tot += ms;
+    ++c;
+  }
+  *total_ms = tot;
+  *count = c;
+  return RS_OK;
+}
+
 int rs_snap(const double *pos, int64_t count, double h, int64_t n, int64_t *idx, double *disp,
             void *stream) {
   RS_REQUIRE(count >= 0 && n >= 2 && h > 0, "rs_snap: bad arguments");
@@ -582,8 +620,11 @@ int rs_syrk(const double *A, int64_t lda, int64_t n, int64_t K, double *G, void 
   if (st) return st;
   cudaStream_t s = as_stream(stream);
   double *part = (double *)work;
-  k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
-      A, lda, n, K, ks, part);
+  {
+    ProfScope ps(s, "syrk");
+    k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
+        A, lda, n, K, ks, part);
+  }
   if ((st = check_launch("rs_syrk part"))) return st;
   int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
   k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G);
@@ -609,8 +650,11 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const d
   RS_REQUIRE(n >= 1 && r >= 1 && R >= 1 && n_shift >= 1 && ldz >= r && ld_table >= R,
              "rs_shift_project: bad shape");
   int64_t total = r * n_shift * R;
-  k_shift_project<<<grid_for(total, 128), 128, 0, as_stream(stream)>>>(Z, ldz, n, r, table,
-                                                                         ld_table, R, n_shift, TT);
+  {
+    ProfScope ps(as_stream(stream), "shift_project");
+    k_shift_project<<<grid_for(total, 128), 128, 0, as_stream(stream)>>>(Z, ldz, n, r, table,
+                                                                           ld_table, R, n_shift, TT);
+  }
   return check_launch("rs_shift_project");
 }
 
@@ -655,8 +699,12 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
   }
   cudaStream_t s = as_stream(stream);
   double *part = (double *)work;
-  k_core_part<<<dim3((unsigned)sp, (unsigned)at_n), CORE_THREADS, smem, s>>>(
-      TT1, TT2, TT3, (int)r1, (int)r2, (int)r3, n_shift, (int)R, shift, z, w, count, per, at, part);
+  {
+    ProfScope ps(s, "core");
+    k_core_part<<<dim3((unsigned)sp, (unsigned)at_n), CORE_THREADS, smem, s>>>(
+        TT1, TT2, TT3, (int)r1, (int)r2, (int)r3, n_shift, (int)R, shift, z, w, count, per, at,
+        part);
+  }
   int st = check_launch("rs_core part");
   if (st) return st;
   int64_t len = r1 * r2 * r3;
@@ -723,6 +771,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                                                              planes, A, lda);
   if ((st = check_launch("tucker_f"))) return st;
   if (nb > 0) {
+    ProfScope ps(s, "short_rows");
     k_short_rows<<<dim3((unsigned)planes, (unsigned)nb), SD_THREADS, 0, s>>>(
         ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, n, x1_lo, A, lda, r3p);
     if ((st = check_launch("short_rows"))) return st;
@@ -738,8 +787,11 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane>))) return st;
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
-  k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-      A, lda, Bt, lda, out, n, planes * n, n, r3p, nb > 0 ? ranges : nullptr, 2);
+  {
+    ProfScope ps(s, "gemm_plane");
+    k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+        A, lda, Bt, lda, out, n, planes * n, n, r3p, nb > 0 ? ranges : nullptr, 2);
+  }
   return check_launch("plane_gemm");
 }
 

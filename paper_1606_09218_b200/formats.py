@@ -52,7 +52,7 @@ def to_device(x, dtype=None):
     if isinstance(x, torch.Tensor):
         t = x if x.is_cuda else x.cuda()
         return t.to(dt).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x))).to(device="cuda", dtype=dt)
+    return torch.from_numpy(np.array(x, copy=True, order="C")).to(device="cuda", dtype=dt)
 
 
 def to_host(x) -> np.ndarray:

@@ -56,10 +56,10 @@ def test_gather_windows(nat, cuda):
     T = cuda.from_numpy(table).cuda()
     S = cuda.from_numpy(starts).cuda()
     out = cuda.empty((n, 20), dtype=cuda.float64, device="cuda")
-    nat.check(nat.lib().rs_gather_windows(T.data_ptr(), R, n, S.data_ptr(), 4, 5, 2,
-                                          cuda.from_numpy(gs).cuda().data_ptr(),
-                                          cuda.from_numpy(ts).cuda().data_ptr(), out.data_ptr(), 20,
-                                          nat.stream_ptr()), "gather")
+    G, Ts = cuda.from_numpy(gs).cuda(), cuda.from_numpy(ts).cuda()  # keep alive across the launch
+    nat.check(nat.lib().rs_gather_windows(T.data_ptr(), R, n, S.data_ptr(), 4, 5, 2, G.data_ptr(),
+                                          Ts.data_ptr(), out.data_ptr(), 20, nat.stream_ptr()),
+              "gather")
     ref = np.concatenate([table[s:s + n, 2:7] * g * ts for s, g in zip(starts, gs)], axis=1)
     assert np.array_equal(out.cpu().numpy(), ref)
 
