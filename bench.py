@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""RS potential-sum assembly benchmark (driver contract: one JSON line on rank 0).
+
+Workload (default ``--config C2`` = BASELINE.json configs[1]): Newton kernel,
+N = 1000 particles on a jittered 10^3 lattice, n = 256, R = 28 (R_l = R_s = 14),
+eps = 1e-6, delta = 1e-8.  One *step* = one full RS assembly of the particle
+system into the dense fp64 grid through the package API:
+``build_rs`` (snap, shift-merged Gram on DMMA, eigh, rank selection, RHOSVD
+core) + ``assemble_grid`` (fused Tucker + short-range plane GEMM).  The host
+prologue (quadrature calibration, (2n,R) table: depends only on the grid
+configuration) is planned once before timing, like an FFT plan.
+
+* ``value``  -- grid points per second, inputs resident in HBM, device time
+  (CUDA events), L2 flushed (256 MiB write) before every timed step.
+* ``e2e``    -- same metric through the public API from pinned HOST buffers:
+  H2D of positions/charges + assembly + D2H of the whole grid, every step.
+* ``roofline`` -- the dominant kernel (plane GEMM, ``gemm_plane``) timed live
+  with CUDA events around its launches; algorithmic flops per SURVEY 8(d):
+  2 P (short-range pairs) + 2 r3 n^3 (last Tucker mode); peak = a cuBLAS
+  DGEMM 8192^3 measured live in this process (MEASURED_PEAKS.json has no FP64).
+* ``cpu_baseline`` -- the reference algorithm (oracle port, numpy + OpenBLAS
+  on all host cores; the reference's dense_cct loop is single-threaded) on
+  the same workload, dense_cct on a deterministic particle subsample and
+  extrapolated by exact pair counts.
+
+``--impl reference`` runs only that CPU path (rank 0; other ranks exit 0).
+Multi-GPU (torchrun): each rank assembles a work-balanced x1 slab of the same
+grid (strong scaling); build_rs is replicated (deterministic, bitwise equal).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-stride", type=int, default=0,
+                    help="reference arm: time dense_cct on every k-th particle (0 = auto)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def workload_desc(name):
+    from paper_1606_09218_b200 import configs
+    m = configs.MANIFEST[name]
+    return {"workload": f"{name}: {m['kernel']} kernel, N={m['N']}, n={m['n']}, b={m['b']}, "
+                        f"R={m['M'] + 1} (R_l={m['split_index'] + 1}, "
+                        f"R_s={m['M'] - m['split_index']}), eps={m['eps']}, delta={configs.DELTA}",
+            "N": m["N"], "n": m["n"], "kernel": m["kernel"],
+            "step": "build_rs + dense grid assembly (plan = host quadrature/table, built once)"}
+
+
+def pair_counts(idx, gamma, n):
+    lo = np.maximum(idx - gamma, 0)
+    hi = np.minimum(idx + gamma, n - 1)
+    return np.prod(hi - lo + 1, axis=1).astype(np.float64)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------- CPU reference (oracle)
+def reference_assembly_time(name, stride, repeats=1):
+    """Reference algorithm (oracle port) on host cores: full pipeline except
+    that dense_cct runs on every ``stride``-th particle and is extrapolated by
+    exact pair counts.  Returns (seconds per assembly, details)."""
+    from oracle import rs_oracle as orc
+    from paper_1606_09218_b200 import configs
+
+    case = configs.oracle_case(name)
+    p = orc.prologue(case["kind"], case["lam"], case["b"], case["n"], case["M"],
+                     case["split_index"], case["delta"])  # plan (not timed; see docstring)
+    n = case["n"]
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        idx, _, _ = orc.snap(case["positions"], case["b"], n)
+        z = case["charges"]
+        weights, facs = orc.long_side_matrices(p["table"], p["w"], idx, z, case["split_index"])
+        core, zs, _, ranks = orc.rhosvd(weights, facs, eps=case["eps"])
+        ul, wl = orc.local_window(p["table"], p["w"], case["split_index"], p["gamma"])
+        t_long = orc.tucker_dense(core, zs)
+        L0 = orc.local_dense(ul, wl)
+        t1 = time.perf_counter()
+        sub = np.arange(0, idx.shape[0], stride)
+        orc.dense_cct_numpy(L0, p["gamma"], idx[sub], z[sub], n)
+        t2 = time.perf_counter()
+        pc = pair_counts(idx, p["gamma"], n)
+        frac = pc[sub].sum() / pc.sum()
+        total = (t1 - t0) + (t2 - t1) / frac
+        del t_long
+        if best is None or total < best[0]:
+            best = (total, dict(setup_s=t1 - t0, cct_sample_s=t2 - t1, pair_fraction=float(frac),
+                                ranks=list(ranks)))
+    return best
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    name = args.config
+    from paper_1606_09218_b200 import configs
+    m = configs.MANIFEST[name]
+    stride = args.ref_stride or max(1, m["N"] // 64)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, det = reference_assembly_time(name, stride)
+        if i >= args.warmup:
+            times.append(t)
+    t = float(np.mean(times))
+    value = m["n"] ** 3 / t
+    sample = (f"oracle port of the reference pipeline (numpy/OpenBLAS, {threads_used()} BLAS "
+              f"threads; dense_cct single-threaded numpy loop on every {stride}-th particle = "
+              f"{det['pair_fraction']:.4f} of the pairs, extrapolated by pair count)")
+    line = {"impl": "reference", "metric": "rs_assembly_grid_pts_per_s", "value": value,
+            "unit": "grid-pts/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded recipe, paper_1606_09218_b200/configs.py)",
+            "config": workload_desc(name),
+            "cpu_baseline": {"value": value, "unit": "grid-pts/s", "cores": threads_used(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "grid-pts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm
+def measure_dgemm_peak(torch):
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        a @ b
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 3 / 1e3
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * n ** 3 / t / 1e12
+
+
+def slab_bounds(weights, world):
+    """Contiguous x1 slabs with ~equal work (prefix sums of per-plane cost)."""
+    c = np.concatenate([[0.0], np.cumsum(weights)])
+    total = c[-1]
+    bounds = [0]
+    for r in range(1, world):
+        bounds.append(int(np.searchsorted(c, total * r / world)))
+    bounds.append(len(weights))
+    for i in range(1, len(bounds)):
+        bounds[i] = max(bounds[i], bounds[i - 1] + (1 if i < len(bounds) - 1 else 0))
+    bounds[-1] = len(weights)
+    return bounds
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1606_09218_b200 as rt
+    from paper_1606_09218_b200 import _native as nat
+    from paper_1606_09218_b200 import configs
+    from paper_1606_09218_b200.formats import assemble_grid
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    name = args.config
+    m = configs.MANIFEST[name]
+    n = m["n"]
+    system = configs.system(name)
+    cfg = configs.assembly_config(name)
+    grid = rt.Grid3(n, rt.Box3(m["b"]))
+    host_idx = rt.snap_to_grid(system, grid).indices
+
+    # plan (host prologue) once, outside timing
+    plan = rt.plan_for(cfg, cfg.split_index)
+    gamma = plan.gamma
+    # work-balanced x1 slab of this rank: per-plane pair count + n^2 store
+    per_plane = np.full(n, float(n * n))
+    lo = np.maximum(host_idx[:, 0] - gamma, 0)
+    hi = np.minimum(host_idx[:, 0] + gamma, n - 1)
+    w23 = pair_counts(host_idx, gamma, n) / (hi - lo + 1)
+    np.add.at(per_plane, np.concatenate([np.arange(a, b + 1) for a, b in zip(lo, hi)]),
+              np.repeat(w23, hi - lo + 1))
+    bounds = slab_bounds(per_plane, world)
+    x1_lo, x1_hi = bounds[rank], bounds[rank + 1]
+
+    pos_d = torch.tensor(system.positions, device="cuda")
+    q_d = torch.tensor(system.charges, device="cuda")
+    dp = rt.DeviceParticles(pos_d, q_d, system.box)
+    out = torch.empty((max(x1_hi - x1_lo, 1), n, n), dtype=torch.float64, device="cuda")
+
+    def step(particles):
+        res = rt.build_rs(particles, cfg)
+        if x1_hi > x1_lo:
+            assemble_grid(res.rs.long, res.rs.short, x1_lo, x1_hi, out=out)
+        return res
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        res = step(dp)
+    torch.cuda.synchronize()
+    ranks_used = res.report["tucker_ranks"]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    L = nat.lib()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier()
+    launches0 = L.rs_launch_count()
+    L.rs_prof_enable(1)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record()
+            step(dp)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    L.rs_prof_enable(0)
+    launches = L.rs_launch_count() - launches0
+    barrier()
+    t_steps = [a.elapsed_time(b) for a, b in ev]
+    t_mean = float(np.mean(t_steps)) / 1e3
+    gemm_ms, gemm_n = nat.prof_query("gemm_plane")
+    prof = {k: nat.prof_query(k) for k in ("gemm_plane", "short_rows", "syrk", "core",
+                                          "shift_project")}
+    tt = torch.tensor([t_mean], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+
+    # ---- end to end through the public API from pinned host buffers
+    pos_h = torch.tensor(system.positions).pin_memory()
+    q_h = torch.tensor(system.charges).pin_memory()
+    out_h = torch.empty(out.shape, dtype=torch.float64).pin_memory()
+    pos_e = torch.empty_like(pos_d)
+    q_e = torch.empty_like(q_d)
+
+    def e2e_step():
+        pos_e.copy_(pos_h, non_blocking=True)
+        q_e.copy_(q_h, non_blocking=True)
+        step(rt.DeviceParticles(pos_e, q_e, system.box))
+        out_h.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+
+    if rank == 0:
+        peak = measure_dgemm_peak(torch)
+        P = float(pair_counts(host_idx, gamma, n).sum())
+        r3 = ranks_used[2]
+        alg_flops = 2.0 * P + 2.0 * r3 * n ** 3
+        slab_frac = (x1_hi - x1_lo) / n
+        gemm_avg_s = gemm_ms / max(gemm_n, 1) / 1e3
+        launches_per_step = max(gemm_n, 1) / args.steps
+        achieved = alg_flops * slab_frac / launches_per_step / gemm_avg_s / 1e12 if gemm_n else None
+        # executed flops of the banded GEMM (K per column tile)
+        bc3 = np.unique(host_idx[:, 2])
+        G = m["M"] - m["split_index"] + (m["M"] - m["split_index"]) % 2
+        r3p = r3 + r3 % 2
+        keff = []
+        for t0 in range(0, n, 64):
+            lo_x, hi_x = t0 - gamma, min(n - 1, t0 + 63) + gamma
+            nb = np.count_nonzero((bc3 >= lo_x) & (bc3 <= hi_x))
+            keff.append(r3p + nb * G)
+        exec_flops = 2.0 * n * n * 64 * float(np.sum(keff))
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            stride = max(1, m["N"] // 8)
+            tc, det = reference_assembly_time(name, stride)
+            cpu = {"value": n ** 3 / tc, "unit": "grid-pts/s", "cores": threads_used(),
+                   "kind": "port",
+                   "sample": (f"{name} reference pipeline (oracle numpy port; BLAS on "
+                              f"{threads_used()} threads, dense_cct single-threaded) with "
+                              f"dense_cct on every {stride}-th particle = "
+                              f"{det['pair_fraction']:.4f} of the pairs, extrapolated by pair "
+                              f"count: {tc:.2f} s per assembly")}
+        clocks = clk.summary()
+        line = {
+            "metric": "rs_assembly_grid_pts_per_s",
+            "value": n ** 3 / t_max,
+            "unit": "grid-pts/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_max * 1e3,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded recipe, paper_1606_09218_b200/configs.py)",
+            "config": {**workload_desc(name), "parallelism": f"x1-slabs x{world}",
+                       "l2": "flushed (256 MiB write) before each timed step",
+                       "tucker_ranks": ranks_used, "gamma": gamma},
+            "gbs": 8.0 * n ** 3 / t_max / 1e9,
+            "clocks": clocks,
+            "e2e": {"value": n ** 3 / t_e2e, "unit": "grid-pts/s",
+                    "h2d_bytes_per_step": int(pos_h.numel() * 8 + q_h.numel() * 8),
+                    "d2h_bytes_per_step": int(out_h.numel() * 8), "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": "k_gemm_nt<TilePlane> (gemm_plane)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured live (fp64; "
+                                        "MEASURED_PEAKS.json has no FP64 entry)",
+                         "algorithmic_flops_per_step": alg_flops,
+                         "executed_flops_per_step": exec_flops,
+                         "executed_tflops": exec_flops * slab_frac / launches_per_step /
+                         gemm_avg_s / 1e12 if gemm_n else None,
+                         "avg_launch_ms": gemm_avg_s * 1e3},
+            "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
