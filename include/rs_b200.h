@@ -82,6 +82,24 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r,
                      const double *table, int64_t ld_table, int64_t R,
                      int64_t n_shift, double *TT, void *stream);
 
+/* (a8) shift histograms of the long side matrices: c[l*n + s] = sum of z_p^2
+ * over particles p whose mode-l window starts at s = n - idx[3p+l] (l = 0,1,2),
+ * summed in particle order; cnt3[x] = number of particles with idx[3p+2] == x.
+ * With them G_l = sum_s c[l][s] sum_k w_k^2 u_k[s:s+n] u_k[s:s+n]^T equals
+ * the reference Gram A A^T of rankred.py:91 (A = side matrix * |weights|). */
+int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n,
+                  double *c, int32_t *cnt3, void *stream);
+
+/* Top-b eigenpairs of nmat symmetric PSD n x n matrices G (contiguous), for
+ * the eigen-truncation of rankred.py:90-96/129-148: block subspace iteration
+ * (iters steps, CGS2), Rayleigh-Ritz, cyclic Jacobi.  evals (nmat x b,
+ * descending), U (nmat x b x n, rows = Ritz vectors, largest-|entry|
+ * positive), trace (nmat).  b even, b <= min(n, 96). */
+int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b);
+int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters,
+              double *evals, double *U, double *trace, void *work, int64_t work_bytes,
+              void *stream);
+
 /* (a10) RHOSVD core, rankred.py:151-161 (_core_from_projections) on the
  * particle-major term order of assembly.py:127-135:
  * core[(a*r2+b)*r3+c] = sum_p z[p] sum_k w[k] P1(a,p,k) P2(b,p,k) P3(c,p,k)

@@ -35,9 +35,9 @@ from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
     project_kernel, split_rank, split_tensor
-from .rankred import ReductionConfig, SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, \
-    rhosvd_error_bound, select_ranks, shift_histograms, shifted_core, shifted_gram, side_svd, \
-    tucker_to_canonical
+from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, \
+    SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eps_rank, rhosvd_error_bound, shift_histograms, \
+    shifted_core, shifted_grams, side_svd, top_eig, truncated_spectrum, tucker_to_canonical
 
 
 @dataclass(frozen=True)
@@ -99,6 +99,8 @@ class RSPlan:
     table_dev: object               # (2n, R) float64 CUDA
     w_long: object                  # (R_l,) weights
     w_long_abs: object
+    local_ul: object = None         # (W, R_s) device copy of the local factor
+    local_wl: object = None
 
     @property
     def n(self) -> int:
@@ -144,7 +146,8 @@ def plan_for(cfg: AssemblyConfig, split_index: int) -> RSPlan:
     table = to_device(ref.table)
     w = to_device(ref.tensor.weights[: split_index + 1])
     plan = RSPlan(ref2n=ref, split_index=int(split_index), gamma=gamma, local=local,
-                  table_dev=table, w_long=w, w_long_abs=w.abs().contiguous())
+                  table_dev=table, w_long=w, w_long_abs=w.abs().contiguous(),
+                  local_ul=to_device(local.factors[0]), local_wl=to_device(local.weights))
     _PLAN_CACHE[key] = plan
     return plan
 
@@ -352,29 +355,80 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
     starts = (n - idx).contiguous()
     report = {"n": n, "b": grid.box.half_width, "particles": ds.count}
 
+    tails = None
     if reduce_long and cfg.reduction.max_sweeps == 0:
-        # shift-merged Gram per mode, eigh, one synchronisation
-        hists = shift_histograms(starts, z, n)
-        eig = [eig_desc(shifted_gram(plan.table_dev, n, plan.w_long_abs, h)) for h in hists]
-        k = min(n, raw_rank)
-        parts = [s[:k] for s, _ in eig] + [ds._disp.max().reshape(1)]
-        if collision is not None:
-            parts.append(collision.to(torch.float64))
+        # shift histograms -> per-mode Grams on DMMA -> top-b eigenpairs, then
+        # ONE synchronisation for everything the host must decide on
+        hist, cnt3 = shift_histograms(idx, z, n)
+        G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
+        b = min(n - n % 2, TOPEIG_BLOCK)
+        evals, U, trace = top_eig(G, b)
+        order3 = torch.argsort(idx[:, 2], stable=True)
+        parts = [evals.reshape(-1), trace, ds._disp.max().reshape(1),
+                 collision.to(torch.float64) if collision is not None else
+                 torch.full((1,), -1.0, dtype=torch.float64, device="cuda"),
+                 cnt3.to(torch.float64)]
         packed = to_host(torch.cat(parts))
-        if collision is not None and packed[-1] >= 0:
-            key = int(packed[-1])
+        if packed[3 * b + 4] >= 0:
+            key = int(packed[3 * b + 4])
             node = (key // (n * n), (key // n) % n, key % n)
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles "
                                   f"snap to node {node}; use a larger n")
-        values = tuple(packed[i * k:(i + 1) * k] for i in range(3))
-        ds._cache["maxdisp"] = float(packed[3 * k])
-        spectrum = SvdSpectrum(values=values, vectors=tuple(zz for _, zz in eig))
-        ranks = select_ranks((n, n, n), raw_rank, values, cfg.reduction)
-        zs = [eig[l][1][:, :ranks[l]].contiguous() for l in range(3)]
+        ds._cache["maxdisp"] = float(packed[3 * b + 3])
+        counts3 = packed[3 * b + 5:].astype(np.int64)
+        limit = min(n, raw_rank)
+        forced = cfg.reduction.ranks
+        if forced is not None:
+            for r in forced:
+                if r > limit:
+                    raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
+        ranks, values, tails, zs = [], [], [], []
+        for l in range(3):
+            theta = packed[l * b:(l + 1) * b]
+            fr = forced[l] if forced is not None else None
+            r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n, cfg.reduction.eps,
+                                                    fr, limit)
+            if r is None or (fr is not None and fr > b):
+                # block too small or not converged: wider block, then full eigh
+                bb = min(n - n % 2, TOPEIG_MAX_BLOCK)
+                if bb > b:
+                    ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb)
+                    theta2 = to_host(ev2[0])
+                    r, sv, tail, total = truncated_spectrum(theta2, float(tr2[0]), n,
+                                                            cfg.reduction.eps, fr, limit)
+                    if r is not None and (fr is None or fr <= bb):
+                        Ul = U2[0]
+                if r is None or (fr is not None and fr > bb):
+                    s_full, z_full = eig_desc(G[l])     # full cuSOLVER spectrum
+                    sh = to_host(s_full)
+                    r = fr if fr is not None else min(eps_rank(sh, cfg.reduction.eps), limit)
+                    sv, total = sh, float(np.sum(sh * sh))
+                    tail = np.cumsum((sh * sh)[::-1])[::-1]
+                    Ul = z_full.T
+            else:
+                Ul = U[l]
+            ranks.append(int(r))
+            values.append(sv)
+            tails.append((float(tail[r]) if r < len(tail) else 0.0, total))
+            zs.append(Ul[:r].T.contiguous())
+        ranks = tuple(ranks)
+        spectrum = SvdSpectrum(values=tuple(values), vectors=tuple(zs))
         core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
         tucker = _trusted_tucker(core, zs)
         long_raw = None
+        # CCT device layout from the stable x3 order and the host bucket counts
+        occ = np.flatnonzero(counts3)
+        bstart = np.zeros(occ.size + 1, dtype=np.int32)
+        bstart[1:] = np.cumsum(counts3[occ])
+        cs = idx[order3]
+        short_layout = dict(c1=cs[:, 0].to(torch.int32).contiguous(),
+                            c2=cs[:, 1].to(torch.int32).contiguous(),
+                            zq=z[order3].contiguous(),
+                            bstart=torch.from_numpy(bstart).to("cuda", non_blocking=True),
+                            bc3=torch.from_numpy(occ.astype(np.int32)).to("cuda", non_blocking=True),
+                            n_buckets=int(occ.size), centers=idx, z=z)
     else:
+        short_layout = None
         if collision is not None and int(collision[0]) >= 0:
             key = int(collision[0])
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "
@@ -396,11 +450,17 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
     })
     if reduce_long:
         report["tucker_ranks"] = list(ranks)
-        report["reduction_tail_bracket"] = rhosvd_error_bound(None, spectrum, ranks)
-        totals = [float(np.sqrt(np.sum(s * s))) for s in spectrum.values]
-        report["reduction_tail_fraction"] = [
-            float(np.sqrt(np.sum(s[r:] ** 2)) / t) if t > 0 else 0.0
-            for s, r, t in zip(spectrum.values, ranks, totals)]
+        if tails is not None:
+            # tail energies include the part of the spectrum beyond the Ritz block
+            report["reduction_tail_bracket"] = float(sum(np.sqrt(t) for t, _ in tails))
+            report["reduction_tail_fraction"] = [float(np.sqrt(t) / np.sqrt(tot)) if tot > 0 else 0.0
+                                                 for t, tot in tails]
+        else:
+            report["reduction_tail_bracket"] = rhosvd_error_bound(None, spectrum, ranks)
+            totals = [float(np.sqrt(np.sum(s * s))) for s in spectrum.values]
+            report["reduction_tail_fraction"] = [
+                float(np.sqrt(np.sum(s[r:] ** 2)) / t) if t > 0 else 0.0
+                for s, r, t in zip(spectrum.values, ranks, totals)]
         if cfg.long_format == "tucker":
             long_part = tucker
         else:
@@ -411,6 +471,8 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
 
     short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z, mode_sizes=(n, n, n),
                 overlap_policy=cfg.overlap_policy, max_overlap=cfg.max_overlap)
+    if short_layout is not None and plan.local.rank > 0:
+        short._cache["dev"] = dict(short_layout, ul=plan.local_ul, wl=plan.local_wl)
     report["gamma"] = plan.gamma
     report["gamma_h"] = plan.gamma * grid.h
     rs = RSTucker(long=long_part, short=short, grid=grid) if cfg.long_format == "tucker" else \

@@ -73,6 +73,14 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
+// grid size for a grid-stride loop over `total` items with 256-thread blocks
+inline unsigned grid_blocks(int64_t total, int threads = 256) {
+  int64_t g = ceil_div(total, threads);
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return (unsigned)g;
+}
+
 // ---- double-double accumulation (Knuth TwoSum; no FMA contraction) -------
 struct dd {
   double hi, lo;

@@ -1,0 +1,360 @@
+// Top-b eigenpairs of small symmetric PSD Gram matrices (the per-mode
+// eigen-truncation of rankred.py:90-96, 129-148) without cuSOLVER's
+// latency-bound full syevd.
+//
+// The side-matrix Grams of the RS long part have exponentially decaying
+// spectra (lambda_i / lambda_0 reaches the 1e-16 noise floor after a few
+// dozen indices), so a block of b basis vectors captures everything above
+// rounding: block subspace iteration Q <- orth(Q G) (q steps, CGS2
+// orthonormalisation in one CTA per matrix), Rayleigh-Ritz T = Q G Q^T,
+// parallel cyclic Jacobi on T in shared memory, Ritz vectors U = V^T Q,
+// largest-|entry|-positive signs.  The host checks convergence with the
+// returned Ritz values (and escalates b, see rankred.top_eig).
+#include <math.h>
+
+#include <algorithm>
+
+#include "rs_common.cuh"
+#include "rs_dmma.cuh"
+
+namespace rsb {
+
+__device__ __forceinline__ double hash_unit(uint64_t a, uint64_t b) {
+  uint64_t x = a * 0x9E3779B97F4A7C15ull ^ (b + 0x632BE59BD9B4E019ull);
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+}
+
+// Qt[m][j][i] = pseudo-random start block (deterministic)
+__global__ void k_eig_start(double *__restrict__ Qt, int nmat, int b, int64_t n, uint64_t seed) {
+  const int64_t total = (int64_t)nmat * b * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    Qt[e] = hash_unit(seed, (uint64_t)e);
+}
+
+constexpr int ORTH_THREADS = 1024;
+
+__device__ double block_sum(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;  // identical in every thread (fixed order)
+}
+
+// Orthonormalise the b rows of Q (n each) in place: classical Gram-Schmidt
+// applied twice per vector ("twice is enough"); a vector that collapses is
+// replaced by a fresh pseudo-random one.  One CTA per matrix.
+__global__ void __launch_bounds__(ORTH_THREADS)
+    k_orth_rows(double *__restrict__ Qall, int b, int64_t n, int64_t stride, uint64_t seed) {
+  extern __shared__ double sm[];
+  double *v = sm;           // n
+  double *coef = sm + n;    // b
+  double *red = coef + b;   // 32
+  double *Q = Qall + blockIdx.x * stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int i = 0; i < b; ++i) {
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Q[i * n + e];
+    __syncthreads();
+    double ss = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+    double nrm0 = sqrt(block_sum(ss, red));
+    double nrm = 0.0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = warp; j < i; j += nwarps) {
+          const double *qj = Q + (int64_t)j * n;
+          double d = 0.0;
+          for (int64_t e = lane; e < n; e += 32) d += qj[e] * v[e];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (lane == 0) coef[j] = d;
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+          double acc = v[e];
+          for (int j = 0; j < i; ++j) acc -= coef[j] * Q[(int64_t)j * n + e];
+          v[e] = acc;
+        }
+        __syncthreads();
+      }
+      ss = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+      nrm = sqrt(block_sum(ss, red));
+      if (nrm > 1e-13 * nrm0 && nrm > 0.0) break;
+      // breakdown: restart this vector from a fresh deterministic direction
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x)
+        v[e] = hash_unit(seed + 7919 * (attempt + 1), (uint64_t)(i * n + e));
+      __syncthreads();
+      ss = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+      nrm0 = sqrt(block_sum(ss, red));
+    }
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) Q[i * n + e] = v[e] * inv;
+    __syncthreads();
+  }
+}
+
+// Parallel cyclic Jacobi on the b x b symmetric T (shared memory), one CTA per
+// matrix.  Outputs eigenvalues sorted descending and the matching
+// eigenvectors as rows of Vt.
+constexpr int JAC_THREADS = 512;
+
+__global__ void __launch_bounds__(JAC_THREADS)
+    k_jacobi(const double *__restrict__ Tall, int b, double *__restrict__ evals,
+             double *__restrict__ Vtall, int max_sweeps) {
+  extern __shared__ double sm[];
+  const int ld = b + 1;
+  double *T = sm;                 // b x ld
+  double *V = T + b * ld;         // b x ld
+  double *rc = V + b * ld;        // b/2 x 2 (c, s)
+  int *rp = (int *)(rc + b);      // b/2 x 2 (p, q)
+  int *flag = rp + b;
+  const double *Tg = Tall + (int64_t)blockIdx.x * b * b;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    int r = e / b, c = e % b;
+    // symmetrise (T = W Q^T is symmetric only up to rounding)
+    T[r * ld + c] = 0.5 * (Tg[r * b + c] + Tg[c * b + r]);
+    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int half = b / 2;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int round = 0; round < b - 1; ++round) {
+      for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        int a0 = i, a1 = b - 1 - i;
+        int p = a0 == 0 ? 0 : 1 + (a0 - 1 + round) % (b - 1);
+        int q = a1 == 0 ? 0 : 1 + (a1 - 1 + round) % (b - 1);
+        if (p > q) {
+          int t = p;
+          p = q;
+          q = t;
+        }
+        double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
+        double c = 1.0, s = 0.0;
+        if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq)) && apq != 0.0) {
+          double tau = (aqq - app) / (2.0 * apq);
+          double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          *flag = 1;
+        }
+        rp[2 * i] = p;
+        rp[2 * i + 1] = q;
+        rc[2 * i] = c;
+        rc[2 * i + 1] = s;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // rows: J^T T
+        int i = e / b, k = e % b;
+        double c = rc[2 * i], s = rc[2 * i + 1];
+        if (s == 0.0) continue;
+        int p = rp[2 * i], q = rp[2 * i + 1];
+        double tp = T[p * ld + k], tq = T[q * ld + k];
+        T[p * ld + k] = c * tp - s * tq;
+        T[q * ld + k] = s * tp + c * tq;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // columns: (.) J, V J
+        int i = e / b, k = e % b;
+        double c = rc[2 * i], s = rc[2 * i + 1];
+        if (s == 0.0) continue;
+        int p = rp[2 * i], q = rp[2 * i + 1];
+        double tp = T[k * ld + p], tq = T[k * ld + q];
+        T[k * ld + p] = c * tp - s * tq;
+        T[k * ld + q] = s * tp + c * tq;
+        double vp = V[k * ld + p], vq = V[k * ld + q];
+        V[k * ld + p] = c * vp - s * vq;
+        V[k * ld + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  // sort descending (stable by index) and emit
+  double *ev = evals + (int64_t)blockIdx.x * b;
+  double *Vt = Vtall + (int64_t)blockIdx.x * b * b;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    double ei = T[i * ld + i];
+    int pos = 0;
+    for (int j = 0; j < b; ++j) {
+      double ej = T[j * ld + j];
+      pos += (ej > ei) || (ej == ei && j < i);
+    }
+    ev[pos] = ei;
+    for (int k = 0; k < b; ++k) Vt[(int64_t)pos * b + k] = V[k * ld + i];
+  }
+}
+
+// U[m][j][i] = sum_k Vt[m][j][k] Q[m][k][i]   (b x b times b x n, per matrix)
+__global__ void k_ritz(const double *__restrict__ Vt, const double *__restrict__ Q, int b, int64_t n,
+                       int nmat, double *__restrict__ U) {
+  const int64_t total = (int64_t)nmat * b * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e % n, j = (e / n) % b, m = e / (n * b);
+    const double *v = Vt + (m * b + j) * b;
+    const double *q = Q + m * b * n + i;
+    double acc = 0.0;
+    for (int k = 0; k < b; ++k) acc = fma(v[k], q[(int64_t)k * n], acc);
+    U[e] = acc;
+  }
+}
+
+// Largest-|entry| (first occurrence) of each row made positive; row per block.
+__global__ void k_sign_rows(double *__restrict__ U, int64_t n) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  double *row = U + (int64_t)blockIdx.x * n;
+  double best = -1.0;
+  int64_t arg = 0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    double a = fabs(row[e]);
+    if (a > best) {
+      best = a;
+      arg = e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int64_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oa < arg)) {
+      best = ob;
+      arg = oa;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    bv[warp] = best;
+    bi[warp] = arg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) {
+        bv[0] = bv[w];
+        bi[0] = bi[w];
+      }
+  }
+  __syncthreads();
+  const double sgn = row[bi[0]] < 0.0 ? -1.0 : 1.0;
+  if (sgn < 0.0)
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) row[e] = -row[e];
+}
+
+// trace of each matrix (fixed order)
+__global__ void k_trace(const double *__restrict__ G, int64_t n, double *__restrict__ tr) {
+  if (threadIdx.x != 0) return;
+  const double *g = G + (int64_t)blockIdx.x * n * n;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += g[i * n + i];
+  tr[blockIdx.x] = s;
+}
+
+template <class T>
+__global__ void __launch_bounds__(T::THREADS)
+    k_gemm_nt_batched(const double *__restrict__ A, int64_t lda, int64_t sA,
+                      const double *__restrict__ B, int64_t ldb, int64_t sB, double *__restrict__ C,
+                      int64_t ldc, int64_t sC, int64_t M, int64_t N, int64_t K) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t n0 = (int64_t)blockIdx.x * T::BN;
+  const int64_t m0 = (int64_t)blockIdx.y * T::BM;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  Acc<T> acc;
+  acc.zero();
+  mainloop<T>(smem, acc, A, lda, m0, M, B, ldb, n0, N, 0, K);
+  store_tile<T>(acc, C, ldc, m0, M, n0, N);
+}
+
+using TileEig = Tile<64, 64, 32, 32, 3>;
+
+static int gemm_batched(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
+                        int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
+                        int64_t K, int nb, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute((const void *)k_gemm_nt_batched<TileEig>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TileEig::SMEM_BYTES);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+  dim3 grid((unsigned)ceil_div(N, TileEig::BN), (unsigned)ceil_div(M, TileEig::BM), (unsigned)nb);
+  k_gemm_nt_batched<TileEig><<<grid, TileEig::THREADS, TileEig::SMEM_BYTES, s>>>(
+      A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
+  return check_launch("eig gemm");
+}
+
+}  // namespace rsb
+
+using namespace rsb;
+
+extern "C" {
+
+int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b) {
+  // Q, Y (nmat*b*n each), T (nmat*b*b), Vt (nmat*b*b)
+  return (2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024;
+}
+
+int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters, double *evals,
+              double *U, double *trace, void *work, int64_t work_bytes, void *stream) {
+  RS_REQUIRE(nmat >= 1 && n >= 2 && b >= 2 && b <= n && b % 2 == 0 && b <= 96 && iters >= 1,
+             "rs_topeig: bad sizes (need 2 <= b <= min(n, 96), b even)");
+  RS_REQUIRE(n % 2 == 0, "rs_topeig: n must be even");
+  if (work_bytes < rs_topeig_workspace_bytes(nmat, n, b))
+    return fail(RS_ERR_CAPACITY, "rs_topeig: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  double *Q = (double *)work;
+  double *Y = Q + nmat * b * n;
+  double *T = Y + nmat * b * n;
+  double *Vt = T + nmat * b * b;
+  int st;
+  ProfScope ps(s, "topeig");
+  k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Q, (int)nmat, (int)b, n, 12345);
+  if ((st = check_launch("eig start"))) return st;
+  size_t orth_smem = (size_t)(n + b + 32) * 8;
+  if (orth_smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_orth_rows,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)orth_smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth smem: %s", cudaGetErrorString(e));
+  }
+  // Y = Q G (rows), orth
+  for (int64_t it = 0; it < iters; ++it) {
+    if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
+    k_orth_rows<<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
+    if ((st = check_launch("orth"))) return st;
+    std::swap(Q, Y);
+  }
+  // Rayleigh-Ritz: W = Q G (into Y), T = W Q^T
+  if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
+  if ((st = gemm_batched(Y, n, b * n, Q, n, b * n, T, b, b * b, b, b, n, (int)nmat, s))) return st;
+  size_t jac_smem = (size_t)(2 * b * (b + 1) + b) * 8 + (size_t)(b + 1) * 4;
+  {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_jacobi,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
+  }
+  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 30);
+  if ((st = check_launch("jacobi"))) return st;
+  k_ritz<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Vt, Q, (int)b, n, (int)nmat, U);
+  if ((st = check_launch("ritz"))) return st;
+  k_sign_rows<<<(unsigned)(nmat * b), 256, 0, s>>>(U, n);
+  if ((st = check_launch("sign"))) return st;
+  k_trace<<<(unsigned)nmat, 32, 0, s>>>(G, n, trace);
+  return check_launch("trace");
+}
+
+}  // extern "C"

@@ -125,17 +125,75 @@ __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, i
 }
 
 // ===================================================== shift projection (K4a)
-__global__ void k_shift_project(const double *__restrict__ Z, int64_t ldz, int64_t n, int64_t r,
-                                const double *__restrict__ T, int64_t ld_table, int64_t R,
-                                int64_t n_shift, double *__restrict__ TT) {
-  const int64_t total = r * n_shift * R;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t k = e % R, s = (e / R) % n_shift, a = e / (R * n_shift);
-    const double *col = T + s * ld_table + k;
+// Block = (32 consecutive shifts, one term k); the table window T[s0 : s0+32+n, k]
+// is staged in shared memory and every thread (a, s) streams Z[:, a].
+constexpr int SP_SHIFTS = 32;
+
+__global__ void __launch_bounds__(256)
+    k_shift_project(const double *__restrict__ Z, int64_t ldz, int64_t n, int64_t r,
+                    const double *__restrict__ T, int64_t ld_table, int64_t R, int64_t n_shift,
+                    double *__restrict__ TT) {
+  extern __shared__ double win[];  // n + SP_SHIFTS
+  const int64_t s0 = (int64_t)blockIdx.x * SP_SHIFTS;
+  const int64_t k = blockIdx.y;
+  const int64_t len = n + SP_SHIFTS;
+  const int64_t rows = 2 * n;  // doubled table height... bounded by caller
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+    int64_t row = s0 + e;
+    win[e] = row < rows ? T[row * ld_table + k] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < r * SP_SHIFTS; t += blockDim.x) {
+    int64_t a = t / SP_SHIFTS, sl = t % SP_SHIFTS;
+    int64_t s = s0 + sl;
+    if (s >= n_shift) continue;
+    const double *w = win + sl;
     double acc = 0.0;
-    for (int64_t i = 0; i < n; ++i) acc = fma(Z[i * ldz + a], col[i * ld_table], acc);
-    TT[e] = acc;
+    for (int64_t i = 0; i < n; ++i) acc = fma(Z[i * ldz + a], w[i], acc);
+    TT[(a * n_shift + s) * R + k] = acc;
+  }
+}
+
+// Per-mode shift histograms c[l][s] = sum_{p: n - idx[p][l] == s} z_p^2 and
+// the x3 occupancy counts cnt[x] = #{p: idx[p][2] == x}; thread per (l, s),
+// particles streamed through shared memory in index order (deterministic).
+constexpr int SH_CHUNK = 1024;
+
+__global__ void __launch_bounds__(256)
+    k_shift_hist(const int64_t *__restrict__ idx, const double *__restrict__ z, int64_t count,
+                 int64_t n, double *__restrict__ c, int32_t *__restrict__ cnt3) {
+  __shared__ int32_t key[SH_CHUNK][3];
+  __shared__ double zz[SH_CHUNK];
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // shift / x3 value
+  double acc[3] = {0.0, 0.0, 0.0};
+  int32_t occ = 0;
+  for (int64_t p0 = 0; p0 < count; p0 += SH_CHUNK) {
+    const int m = (int)(count - p0 < SH_CHUNK ? count - p0 : SH_CHUNK);
+    __syncthreads();
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+      const int64_t *ip = idx + 3 * (p0 + e);
+      key[e][0] = (int32_t)(n - ip[0]);
+      key[e][1] = (int32_t)(n - ip[1]);
+      key[e][2] = (int32_t)ip[2];
+      double q = z[p0 + e];
+      zz[e] = q * q;
+    }
+    __syncthreads();
+    if (s < n) {
+      for (int e = 0; e < m; ++e) {
+        const double q2 = zz[e];
+        if (key[e][0] == s) acc[0] += q2;
+        if (key[e][1] == s) acc[1] += q2;
+        if ((int32_t)n - key[e][2] == s) acc[2] += q2;
+        occ += key[e][2] == s;
+      }
+    }
+  }
+  if (s < n) {
+    c[s] = acc[0];
+    c[n + s] = acc[1];
+    c[2 * n + s] = acc[2];
+    cnt3[s] = occ;
   }
 }
 
@@ -508,10 +566,7 @@ __global__ void k_sum_dd_final(const double *__restrict__ part, int64_t np, doub
   out[0] = acc.hi + acc.lo;
 }
 
-inline int grid_for(int64_t total, int threads) {
-  int64_t g = ceil_div(total, threads);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64));
-}
+inline int grid_for(int64_t total, int threads) { return (int)grid_blocks(total, threads); }
 
 template <class T>
 int set_smem(const void *fn) {
@@ -647,15 +702,29 @@ int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb, doubl
 
 int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const double *table,
                      int64_t ld_table, int64_t R, int64_t n_shift, double *TT, void *stream) {
-  RS_REQUIRE(n >= 1 && r >= 1 && R >= 1 && n_shift >= 1 && ldz >= r && ld_table >= R,
-             "rs_shift_project: bad shape");
-  int64_t total = r * n_shift * R;
+  RS_REQUIRE(n >= 1 && r >= 1 && R >= 1 && n_shift >= 1 && n_shift <= n && ldz >= r &&
+                 ld_table >= R,
+             "rs_shift_project: bad shape (table must have 2n rows, n_shift <= n)");
+  size_t smem = (size_t)(n + SP_SHIFTS) * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_shift_project,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
+  }
   {
     ProfScope ps(as_stream(stream), "shift_project");
-    k_shift_project<<<grid_for(total, 128), 128, 0, as_stream(stream)>>>(Z, ldz, n, r, table,
-                                                                           ld_table, R, n_shift, TT);
+    dim3 grid((unsigned)ceil_div(n_shift, SP_SHIFTS), (unsigned)R);
+    k_shift_project<<<grid, 256, smem, as_stream(stream)>>>(Z, ldz, n, r, table, ld_table, R,
+                                                             n_shift, TT);
   }
   return check_launch("rs_shift_project");
+}
+
+int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n, double *c,
+                  int32_t *cnt3, void *stream) {
+  RS_REQUIRE(count >= 1 && n >= 2, "rs_shift_hist: bad sizes");
+  k_shift_hist<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(idx, z, count, n, c, cnt3);
+  return check_launch("rs_shift_hist");
 }
 
 static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t *splits,

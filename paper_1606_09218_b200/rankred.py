@@ -301,38 +301,99 @@ def tucker_to_canonical(t: TuckerTensor, eps_t2c: float = 1e-6) -> CanonicalTens
 
 
 # ---------------------------------------------- shift-structured long part
-def shift_histograms(starts, z, n: int):
-    """Per mode: distinct window starts (ascending) and c_s = sum z^2 over the
-    particles with that start, summed in particle order (deterministic)."""
+def shift_histograms(idx, z, n: int):
+    """(c, cnt3): per-mode shift histograms ``c`` (3, n) -- ``c[l, s] = sum z^2``
+    over particles whose mode-l window starts at ``s = n - idx[:, l]`` -- and
+    the x3 occupancy counts (n,), one deterministic kernel (``rs_shift_hist``)."""
     torch = nat._torch()
-    out = []
-    zz = z * z
-    for l in range(3):
-        s = starts[:, l]
-        order = torch.argsort(s, stable=True)
-        uniq, counts = torch.unique_consecutive(s[order], return_counts=True)
-        c = torch.segment_reduce(zz[order], "sum", lengths=counts)
-        out.append((uniq.contiguous(), c.contiguous()))
-    return out
+    c = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    cnt3 = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib().rs_shift_hist(idx.data_ptr(), z.data_ptr(), int(z.shape[0]), n,
+                                      c.data_ptr(), cnt3.data_ptr(), nat.stream_ptr()),
+              "rs_shift_hist")
+    return c, cnt3
 
 
-def shifted_gram(table_dev, n: int, w_long_abs, hist):
-    """Gram of the |z w|-weighted long side matrix of one mode from its shift
-    histogram: K_merged = #shifts * R_l columns, built by ``rs_gather_windows``."""
+def shifted_grams(table_dev, n: int, w_long_abs, c):
+    """Per-mode Grams of the |z w|-weighted long side matrices from the shift
+    histograms: ``X_l[:, s R_l + k] = sqrt(c_ls) |w_k| T[s:s+n, k]`` for every
+    start s in [0, n) (empty shifts give zero columns), ``G_l = X_l X_l^T`` on
+    DMMA.  Returns (3, n, n)."""
     torch = nat._torch()
-    uniq, c = hist
     R_l = int(w_long_abs.shape[0])
-    ng = int(uniq.shape[0])
-    k = ng * R_l
+    k = n * R_l
     kp = k + (k % 2)
+    starts = torch.arange(n, dtype=torch.int64, device="cuda")
+    gs = torch.sqrt(c)
+    G = torch.empty((3, n, n), dtype=torch.float64, device="cuda")
     x = torch.zeros((n, kp), dtype=torch.float64, device="cuda") if kp != k else \
         torch.empty((n, kp), dtype=torch.float64, device="cuda")
-    gs = torch.sqrt(c)
-    nat.check(nat.lib().rs_gather_windows(table_dev.data_ptr(), table_dev.shape[1], n,
-                                          uniq.data_ptr(), ng, R_l, 0, gs.data_ptr(),
-                                          w_long_abs.data_ptr(), x.data_ptr(), kp,
-                                          nat.stream_ptr()), "rs_gather_windows")
-    return gram(x)
+    L = nat.lib()
+    ws = nat.Workspace.get(L.rs_syrk_workspace_bytes(n, kp), "syrk")
+    for l in range(3):
+        nat.check(L.rs_gather_windows(table_dev.data_ptr(), table_dev.shape[1], n, starts.data_ptr(),
+                                      n, R_l, 0, gs[l].data_ptr(), w_long_abs.data_ptr(),
+                                      x.data_ptr(), kp, nat.stream_ptr()), "rs_gather_windows")
+        nat.check(L.rs_syrk(x.data_ptr(), kp, n, kp, G[l].data_ptr(), ws.data_ptr(), ws.numel(),
+                            nat.stream_ptr()), "rs_syrk")
+    return G
+
+
+TOPEIG_BLOCK = 64
+TOPEIG_MAX_BLOCK = 96
+TOPEIG_ITERS = 3
+
+
+def top_eig(G, b: int, iters: int = TOPEIG_ITERS):
+    """Top-``b`` eigenpairs of a (m, n, n) stack of PSD Grams (``rs_topeig``).
+    Returns device (evals (m, b) descending, U (m, b, n) Ritz rows, trace (m,))."""
+    torch = nat._torch()
+    m, n, _ = G.shape
+    evals = torch.empty((m, b), dtype=torch.float64, device="cuda")
+    U = torch.empty((m, b, n), dtype=torch.float64, device="cuda")
+    tr = torch.empty(m, dtype=torch.float64, device="cuda")
+    L = nat.lib()
+    ws = nat.Workspace.get(L.rs_topeig_workspace_bytes(m, n, b), "topeig")
+    nat.check(L.rs_topeig(G.data_ptr(), m, n, b, iters, evals.data_ptr(), U.data_ptr(),
+                          tr.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr()), "rs_topeig")
+    return evals, U, tr
+
+
+def truncated_spectrum(theta: np.ndarray, trace: float, n: int, eps, forced_rank=None,
+                       limit=None, iters: int = TOPEIG_ITERS):
+    """Rank rule of ``_eps_rank`` on a top-b spectrum.
+
+    ``theta`` are the b leading Ritz values (clipped at 0); the uncaptured
+    remainder ``max(trace - sum theta, 0)`` (rounding noise once b covers the
+    numerical rank) joins every tail sum.  Returns (rank or None if b is too
+    small to decide / not converged, s values padded to n, tail(r), total).
+    """
+    theta = np.clip(theta, 0.0, None)
+    b = theta.size
+    rem = max(float(trace) - float(np.sum(theta)), 0.0) if b < n else 0.0
+    total = float(np.sum(theta)) + rem
+    tail = np.cumsum(theta[::-1])[::-1] + rem  # tail[r] = sum_{k>=r} lambda_k
+    s = np.zeros(n)
+    s[:b] = np.sqrt(theta)
+    if forced_rank is not None:
+        r = int(forced_rank)
+    elif total == 0.0:
+        r = 1
+    else:
+        ok = np.flatnonzero(tail <= eps * total)
+        if ok.size == 0:
+            return None, s, tail, total          # rank >= b: block too small
+        r = max(int(ok[0]), 1)
+    if limit is not None:
+        r = min(r, limit)
+    if b < n:
+        # subspace-iteration convergence of the kept vectors
+        if r >= b:
+            return None, s, tail, total
+        lam_r = theta[r - 1]
+        if lam_r <= 0.0 or (theta[b - 1] / lam_r) ** iters > 1e-13:
+            return None, s, tail, total
+    return r, s, tail, total
 
 
 def shifted_core(table_dev, n: int, zs, starts, z, w_long):

@@ -84,3 +84,40 @@ def test_sum_dd_matches_fsum(nat, cuda):
     v = np.concatenate([rng.normal(size=100000) * 1e8, rng.normal(size=1000), [1e16, -1e16]])
     got = float(dd_sum(cuda.from_numpy(v).cuda()))
     assert got == math.fsum(v)
+
+
+@pytest.mark.parametrize("n,b", [(256, 64), (96, 32), (512, 96), (32, 32)])
+def test_topeig_graded_spectrum(nat, cuda, n, b):
+    """Block subspace iteration + Jacobi vs the known eigensystem of a graded
+    PSD matrix (the spectral shape of the RS side-matrix Grams)."""
+    from paper_1606_09218_b200.rankred import top_eig
+    rng = np.random.default_rng(n + b)
+    q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    lam = 10.0 ** (-np.arange(n) / 2.5)
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    ev, U, tr = top_eig(cuda.from_numpy(np.stack([g, 2 * g])).cuda(), b)
+    ev, U = ev.cpu().numpy(), U.cpu().numpy()
+    keep = int(np.count_nonzero(lam >= 1e-8))
+    for m, scale in ((0, 1.0), (1, 2.0)):
+        assert np.allclose(ev[m, :keep], scale * lam[:keep], rtol=0, atol=1e-14 * scale)
+        proj = np.abs(U[m, :keep] @ q[:, :keep])
+        assert np.allclose(np.diag(proj), 1.0, atol=1e-9)
+        lead = np.abs(U[m]).argmax(axis=1)
+        assert np.all(U[m][np.arange(b), lead] > 0)
+    assert np.allclose(tr.cpu().numpy(), [np.trace(g), 2 * np.trace(g)], rtol=1e-14)
+
+
+def test_shift_hist_deterministic(nat, cuda):
+    from paper_1606_09218_b200.rankred import shift_histograms
+    rng = np.random.default_rng(1)
+    n = 64
+    idx = rng.integers(1, n, size=(3000, 3))
+    z = rng.normal(size=3000)
+    c, cnt = shift_histograms(cuda.from_numpy(idx).cuda(), cuda.from_numpy(z).cuda(), n)
+    c = c.cpu().numpy()
+    for l in range(3):
+        ref = np.zeros(n)
+        np.add.at(ref, n - idx[:, l], z * z)
+        assert np.allclose(c[l], ref, rtol=1e-14, atol=0)
+    assert np.array_equal(cnt.cpu().numpy(), np.bincount(idx[:, 2], minlength=n))
