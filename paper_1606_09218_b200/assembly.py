@@ -361,7 +361,12 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
         # ONE synchronisation for everything the host must decide on
         hist, cnt3 = shift_histograms(idx, z, n)
         G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
-        b = min(n - n % 2, TOPEIG_BLOCK)
+        # block size: the numerical rank of the long-part Grams grows as eps shrinks
+        eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
+        b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 2 * TOPEIG_BLOCK)
+        if forced_b := (max(cfg.reduction.ranks) if cfg.reduction.ranks else 0):
+            b = min(n - n % 2, max(b, forced_b + 16 + (forced_b % 2)))
+            b = min(b, TOPEIG_MAX_BLOCK)
         evals, U, trace = top_eig(G, b)
         order3 = torch.argsort(idx[:, 2], stable=True)
         parts = [evals.reshape(-1), trace, ds._disp.max().reshape(1),
@@ -390,7 +395,7 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
                                                     fr, limit)
             if r is None or (fr is not None and fr > b):
                 # block too small or not converged: wider block, then full eigh
-                bb = min(n - n % 2, TOPEIG_MAX_BLOCK)
+                bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 2 * TOPEIG_BLOCK else 2 * b)
                 if bb > b:
                     ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb)
                     theta2 = to_host(ev2[0])

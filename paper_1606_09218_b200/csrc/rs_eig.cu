@@ -37,7 +37,7 @@ __global__ void k_eig_start(double *__restrict__ Qt, int nmat, int b, int64_t n,
     Qt[e] = hash_unit(seed, (uint64_t)e);
 }
 
-constexpr int ORTH_THREADS = 1024;
+constexpr int ORTH_THREADS = 256;
 
 __device__ double block_sum(double v, double *red) {
 #pragma unroll
@@ -53,18 +53,23 @@ __device__ double block_sum(double v, double *red) {
 
 // Orthonormalise the b rows of Q (n each) in place: classical Gram-Schmidt
 // applied twice per vector ("twice is enough"); a vector that collapses is
-// replaced by a fresh pseudo-random one.  One CTA per matrix.
+// replaced by a fresh pseudo-random one.  One CTA per matrix.  With
+// IN_SMEM the finished rows live in shared memory (n*b*8 bytes) and are
+// written back at the end; otherwise they are read from global/L2.
+template <bool IN_SMEM>
 __global__ void __launch_bounds__(ORTH_THREADS)
     k_orth_rows(double *__restrict__ Qall, int b, int64_t n, int64_t stride, uint64_t seed) {
   extern __shared__ double sm[];
   double *v = sm;           // n
   double *coef = sm + n;    // b
   double *red = coef + b;   // 32
-  double *Q = Qall + blockIdx.x * stride;
+  double *Qs = red + 32;    // b*n when IN_SMEM
+  double *Qg = Qall + blockIdx.x * stride;
+  double *Q = IN_SMEM ? Qs : Qg;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   for (int i = 0; i < b; ++i) {
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Q[i * n + e];
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Qg[i * n + e];
     __syncthreads();
     double ss = 0.0;
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
@@ -75,16 +80,23 @@ __global__ void __launch_bounds__(ORTH_THREADS)
         for (int j = warp; j < i; j += nwarps) {
           const double *qj = Q + (int64_t)j * n;
           double d = 0.0;
-          for (int64_t e = lane; e < n; e += 32) d += qj[e] * v[e];
+          for (int64_t e = lane; e < n; e += 32) d = fma(qj[e], v[e], d);
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
           if (lane == 0) coef[j] = d;
         }
         __syncthreads();
         for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-          double acc = v[e];
-          for (int j = 0; j < i; ++j) acc -= coef[j] * Q[(int64_t)j * n + e];
-          v[e] = acc;
+          double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int j = 0;
+          for (; j + 4 <= i; j += 4) {
+            a0 -= coef[j] * Q[(int64_t)j * n + e];
+            a1 -= coef[j + 1] * Q[(int64_t)(j + 1) * n + e];
+            a2 -= coef[j + 2] * Q[(int64_t)(j + 2) * n + e];
+            a3 -= coef[j + 3] * Q[(int64_t)(j + 3) * n + e];
+          }
+          for (; j < i; ++j) a0 -= coef[j] * Q[(int64_t)j * n + e];
+          v[e] = (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
       }
@@ -104,12 +116,14 @@ __global__ void __launch_bounds__(ORTH_THREADS)
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) Q[i * n + e] = v[e] * inv;
     __syncthreads();
   }
+  if (IN_SMEM)
+    for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
 }
 
 // Parallel cyclic Jacobi on the b x b symmetric T (shared memory), one CTA per
 // matrix.  Outputs eigenvalues sorted descending and the matching
 // eigenvectors as rows of Vt.
-constexpr int JAC_THREADS = 512;
+constexpr int JAC_THREADS = 128;
 
 __global__ void __launch_bounds__(JAC_THREADS)
     k_jacobi(const double *__restrict__ Tall, int b, double *__restrict__ evals,
@@ -129,6 +143,11 @@ __global__ void __launch_bounds__(JAC_THREADS)
     V[r * ld + c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  // absolute threshold: off-diagonals below 1e-18 max|diag| are already
+  // rounding-level for every eigenvector that matters
+  double dmax = 0.0;
+  for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * ld + i]));
+  const double tol = 1e-18 * dmax;
   const int half = b / 2;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
@@ -145,7 +164,7 @@ __global__ void __launch_bounds__(JAC_THREADS)
         }
         double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > 1e-18 * sqrt(fabs(app * aqq)) && apq != 0.0) {
+        if (fabs(apq) > tol) {
           double tau = (aqq - app) / (2.0 * apq);
           double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -325,16 +344,21 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   ProfScope ps(s, "topeig");
   k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Q, (int)nmat, (int)b, n, 12345);
   if ((st = check_launch("eig start"))) return st;
-  size_t orth_smem = (size_t)(n + b + 32) * 8;
+  const bool q_smem = (size_t)(n + b + 32 + b * n) * 8 <= 200 * 1024;
+  size_t orth_smem = (size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8;
+  const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
   if (orth_smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_orth_rows,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)orth_smem);
+    cudaError_t e = cudaFuncSetAttribute(orth_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)orth_smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth smem: %s", cudaGetErrorString(e));
   }
   // Y = Q G (rows), orth
   for (int64_t it = 0; it < iters; ++it) {
     if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
-    k_orth_rows<<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
+    if (q_smem)
+      k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
+    else
+      k_orth_rows<false><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
     if ((st = check_launch("orth"))) return st;
     std::swap(Q, Y);
   }
@@ -347,7 +371,7 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
   }
-  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 30);
+  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 16);
   if ((st = check_launch("jacobi"))) return st;
   k_ritz<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Vt, Q, (int)b, n, (int)nmat, U);
   if ((st = check_launch("ritz"))) return st;

@@ -312,58 +312,103 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-constexpr int SD_THREADS = 256;
-constexpr int SD_MAXR = 24;
-constexpr int SD_PCHUNK = 64;
+// Block = (plane x1, group of BG buckets) -> a (n x BG*G) column panel of A.
+// The group's particles whose window covers x1 are compacted into shared
+// memory (alpha = z w ul[x1 - c1 + g]); each thread then owns one column and
+// 8 consecutive rows, so every row segment is stored coalesced and written once.
+constexpr int SR_THREADS = 256;
+constexpr int SR_COLS = 64;
+constexpr int SR_ROWS = 8;
+constexpr int SR_Q = 256;
 
-__global__ void __launch_bounds__(SD_THREADS)
-    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
+__global__ void __launch_bounds__(SR_THREADS)
+    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
-                 const double *__restrict__ zq, const int32_t *__restrict__ bstart, int64_t n,
-                 int64_t x1_lo, double *__restrict__ A, int64_t lda, int64_t col0) {
-  __shared__ double alpha[SD_PCHUNK][SD_MAXR];
-  __shared__ int pc2[SD_PCHUNK];
-  const int64_t x1l = blockIdx.x;
-  const int64_t x1 = x1_lo + x1l;
-  const int b = blockIdx.y;
-  const int p_lo = bstart[b], p_hi = bstart[b + 1];
-  // each thread owns rows x2 = threadIdx.x + j * SD_THREADS
-  const int rows_per = (int)((n + SD_THREADS - 1) / SD_THREADS);
-  for (int j = 0; j < rows_per; ++j) {
-    int64_t x2 = threadIdx.x + (int64_t)j * SD_THREADS;
-    double acc[SD_MAXR];
+                 const double *__restrict__ zq, const int32_t *__restrict__ bstart, int n_buckets,
+                 int64_t n, int64_t x1_lo, double *__restrict__ A, int64_t lda, int64_t col0) {
+  extern __shared__ double sm[];
+  double *alpha = sm;                            // SR_Q * Rs
+  int *qc2 = (int *)(alpha + SR_Q * Rs);         // SR_Q
+  int *scan = qc2 + SR_Q;                        // SR_Q + 1
+  int *cst = scan + SR_Q + 1;                    // BG + 1
+  int *wsum = cst + BG + 1;                      // SR_THREADS / 32
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
+  const int b0 = blockIdx.y * BG;
+  const int nbg = min(BG, n_buckets - b0);
+  const int p_lo = bstart[b0], p_hi = bstart[b0 + nbg];
+  const int ncols = nbg * G;
+  const int col = tid % SR_COLS, rsub = tid / SR_COLS;
+  const int j = col / G, k = col - (col / G) * G;
+  const bool active = col < ncols;
+  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G + col;
+  bool first = true;
+  int chunk_lo = p_lo;
+  do {
+    const int m = min(SR_Q, p_hi - chunk_lo);
+    __syncthreads();
+    // covering flags + block exclusive scan (order preserving compaction)
+    int d1 = 0;
+    bool cov = false;
+    if (tid < m) {
+      d1 = (int)(x1 - c1[chunk_lo + tid]);
+      cov = d1 >= -gamma && d1 <= gamma;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, cov);
+    int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 31) wsum[warp] = pre + (cov ? 1 : 0);
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    const int pos = base + pre;
+    scan[tid] = pos;
+    if (tid == SR_THREADS - 1) scan[SR_THREADS] = pos + (cov ? 1 : 0);
+    if (cov) {
+      const int p = chunk_lo + tid;
+      qc2[pos] = c2[p];
+      const double zp = zq[p];
+      const double *u1 = ul + (int64_t)(d1 + gamma) * Rs;
+      for (int kk = 0; kk < Rs; ++kk) alpha[pos * Rs + kk] = zp * wl[kk] * u1[kk];
+    }
+    __syncthreads();
+    if (tid <= nbg) {
+      int e = bstart[b0 + tid] - chunk_lo;
+      e = e < 0 ? 0 : (e > m ? m : e);
+      cst[tid] = scan[e];
+    }
+    __syncthreads();
+    const int qs = active ? cst[j] : 0, qe = active ? cst[j + 1] : 0;
+    for (int64_t rb = 0; rb < n; rb += SR_ROWS * (SR_THREADS / SR_COLS)) {
+      const int64_t r0 = rb + rsub * SR_ROWS;
+      double acc[SR_ROWS];
 #pragma unroll
-    for (int k = 0; k < SD_MAXR; ++k) acc[k] = 0.0;
-    for (int q0 = p_lo; q0 < p_hi; q0 += SD_PCHUNK) {
-      const int nq = min(SD_PCHUNK, p_hi - q0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < nq * Rs; e += SD_THREADS) {
-        int q = e / Rs, k = e - q * Rs;
-        int d1 = (int)(x1 - c1[q0 + q]);
-        double v = 0.0;
-        if (d1 >= -gamma && d1 <= gamma) v = zq[q0 + q] * wl[k] * ul[(d1 + gamma) * Rs + k];
-        alpha[q][k] = v;
-        if (k == 0) pc2[q] = (d1 >= -gamma && d1 <= gamma) ? c2[q0 + q] : INT32_MIN / 2;
+      for (int u = 0; u < SR_ROWS; ++u) acc[u] = 0.0;
+      if (active && k < Rs) {
+        for (int q = qs; q < qe; ++q) {
+          const int c2q = qc2[q];
+          if (c2q + gamma < r0 || c2q - gamma > r0 + SR_ROWS - 1) continue;
+          const double a = alpha[q * Rs + k];
+          const double *uk = ul + k;
+#pragma unroll
+          for (int u = 0; u < SR_ROWS; ++u) {
+            const int64_t d = r0 + u - c2q;
+            if (d >= -gamma && d <= gamma) acc[u] = fma(a, uk[(d + gamma) * Rs], acc[u]);
+          }
+        }
       }
-      __syncthreads();
-      if (x2 < n) {
-        for (int q = 0; q < nq; ++q) {
-          int d2 = (int)(x2 - pc2[q]);
-          if (d2 < -gamma || d2 > gamma) continue;
-          const double *u = ul + (int64_t)(d2 + gamma) * Rs;
+      if (active) {
 #pragma unroll
-          for (int k = 0; k < SD_MAXR; ++k)
-            if (k < Rs) acc[k] = fma(alpha[q][k], u[k], acc[k]);
+        for (int u = 0; u < SR_ROWS; ++u) {
+          if (r0 + u >= n) break;
+          double *dst = Ab + (r0 + u) * lda;
+          if (first) *dst = acc[u];
+          else *dst += acc[u];
         }
       }
     }
-    if (x2 < n) {
-      double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)b * G;
-#pragma unroll
-      for (int k = 0; k < SD_MAXR; ++k)
-        if (k < G) dst[k] = k < Rs ? acc[k] : 0.0;
-    }
-  }
+    first = false;
+    chunk_lo += SR_Q;
+  } while (chunk_lo < p_hi);
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0.., E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in the band.
@@ -815,7 +860,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                        double *out, void *work, int64_t work_bytes, void *stream) {
   RS_REQUIRE(n >= 2 && r1 >= 1 && r2 >= 1 && r3 >= 1, "rs_assemble_planes: bad ranks");
   RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
-  RS_REQUIRE(Rs >= 0 && Rs <= SD_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs, SD_MAXR);
+  RS_REQUIRE(Rs >= 0 && Rs <= 24, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs, 24);
   RS_REQUIRE(gamma >= 0 && 2 * gamma + 1 <= 2 * n, "rs_assemble_planes: bad gamma");
   const int64_t planes = x1_hi - x1_lo;
   const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
@@ -841,8 +886,13 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   if ((st = check_launch("tucker_f"))) return st;
   if (nb > 0) {
     ProfScope ps(s, "short_rows");
-    k_short_rows<<<dim3((unsigned)planes, (unsigned)nb), SD_THREADS, 0, s>>>(
-        ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, n, x1_lo, A, lda, r3p);
+    const int BG = (int)std::max<int64_t>(1, SR_COLS / G);
+    size_t smem = (size_t)SR_Q * Rs * 8 + (size_t)(SR_Q + SR_Q + 1 + BG + 1 + SR_THREADS / 32) * 4;
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
+    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb, BG)), SR_THREADS, smem, s>>>(
+        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, (int)nb, n, x1_lo, A, lda, r3p);
     if ((st = check_launch("short_rows"))) return st;
   }
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(V3, (int)r3, (int)r3p, ul, (int)Rs, (int)G,

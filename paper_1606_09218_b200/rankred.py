@@ -339,9 +339,9 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
     return G
 
 
-TOPEIG_BLOCK = 64
+TOPEIG_BLOCK = 32
 TOPEIG_MAX_BLOCK = 96
-TOPEIG_ITERS = 3
+TOPEIG_ITERS = 2
 
 
 def top_eig(G, b: int, iters: int = TOPEIG_ITERS):
