@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(JAC_THREADS)
         }
         double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > tol) {
+        // rotate unless apq is below rounding relative to its diagonal pair or
+        // below the absolute floor (noise block of the Ritz matrix)
+        if (fabs(apq) > tol && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
           double tau = (aqq - app) / (2.0 * apq);
           double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);

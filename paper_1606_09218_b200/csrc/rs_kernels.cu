@@ -128,29 +128,50 @@ __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, i
 // Block = (32 consecutive shifts, one term k); the table window T[s0 : s0+32+n, k]
 // is staged in shared memory and every thread (a, s) streams Z[:, a].
 constexpr int SP_SHIFTS = 32;
+constexpr int SP_ICH = 64;  // Z rows staged per round
 
 __global__ void __launch_bounds__(256)
     k_shift_project(const double *__restrict__ Z, int64_t ldz, int64_t n, int64_t r,
                     const double *__restrict__ T, int64_t ld_table, int64_t R, int64_t n_shift,
                     double *__restrict__ TT) {
-  extern __shared__ double win[];  // n + SP_SHIFTS
+  extern __shared__ double win[];      // n + SP_SHIFTS, then SP_ICH * r
+  double *zs = win + n + SP_SHIFTS;
   const int64_t s0 = (int64_t)blockIdx.x * SP_SHIFTS;
   const int64_t k = blockIdx.y;
   const int64_t len = n + SP_SHIFTS;
-  const int64_t rows = 2 * n;  // doubled table height... bounded by caller
   for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
     int64_t row = s0 + e;
-    win[e] = row < rows ? T[row * ld_table + k] : 0.0;
+    win[e] = row < 2 * n ? T[row * ld_table + k] : 0.0;
   }
-  __syncthreads();
-  for (int64_t t = threadIdx.x; t < r * SP_SHIFTS; t += blockDim.x) {
-    int64_t a = t / SP_SHIFTS, sl = t % SP_SHIFTS;
-    int64_t s = s0 + sl;
-    if (s >= n_shift) continue;
-    const double *w = win + sl;
-    double acc = 0.0;
-    for (int64_t i = 0; i < n; ++i) acc = fma(Z[i * ldz + a], w[i], acc);
-    TT[(a * n_shift + s) * R + k] = acc;
+  // thread -> (a-slot, shift); up to 4 a values per thread
+  const int sl = threadIdx.x % SP_SHIFTS, a0 = threadIdx.x / SP_SHIFTS;  // a0 < 8
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t a_base = 0; a_base < r; a_base += 32) {
+    for (int u = 0; u < 4; ++u) acc[u] = 0.0;
+    for (int64_t i0 = 0; i0 < n; i0 += SP_ICH) {
+      const int64_t ni = n - i0 < SP_ICH ? n - i0 : SP_ICH;
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < ni * 32; e += blockDim.x) {
+        int64_t ii = e / 32, aa = a_base + e % 32;
+        zs[e] = aa < r ? Z[(i0 + ii) * ldz + aa] : 0.0;
+      }
+      __syncthreads();
+      const double *w = win + sl + i0;
+      for (int64_t ii = 0; ii < ni; ++ii) {
+        const double wv = w[ii];
+        const double *zr = zs + ii * 32 + a0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(zr[8 * u], wv, acc[u]);
+      }
+    }
+    const int64_t s = s0 + sl;
+    if (s < n_shift) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int64_t a = a_base + a0 + 8 * u;
+        if (a < r) TT[(a * n_shift + s) * R + k] = acc[u];
+      }
+    }
   }
 }
 
@@ -337,11 +358,20 @@ __global__ void __launch_bounds__(SR_THREADS)
   const int b0 = blockIdx.y * BG;
   const int nbg = min(BG, n_buckets - b0);
   const int p_lo = bstart[b0], p_hi = bstart[b0 + nbg];
-  const int ncols = nbg * G;
-  const int col = tid % SR_COLS, rsub = tid / SR_COLS;
-  const int j = col / G, k = col - (col / G) * G;
-  const bool active = col < ncols;
-  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G + col;
+  // lane -> (row subgroup, k): KL lanes per subgroup (KL >= G), warps
+  // round-robin over the group's buckets so a warp never mixes buckets
+  const int KL = G <= 16 ? 16 : 32;
+  const int subs_per_warp = 32 / KL;
+  const int nwarps = SR_THREADS / 32;
+  const int k = lane % KL;
+  const int j = warp % BG;
+  const int wsub = warp / BG;                      // which warp of bucket j
+  const int warps_per_bucket = (nwarps + BG - 1 - j) / BG;
+  const int rsub = wsub * subs_per_warp + lane / KL;  // row subgroup index
+  const int nsub = warps_per_bucket * subs_per_warp;
+  const bool active = j < nbg && k < G;
+  const int col = j * G + k;
+  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G + (active ? col : 0);
   bool first = true;
   int chunk_lo = p_lo;
   do {
@@ -378,7 +408,7 @@ __global__ void __launch_bounds__(SR_THREADS)
     }
     __syncthreads();
     const int qs = active ? cst[j] : 0, qe = active ? cst[j + 1] : 0;
-    for (int64_t rb = 0; rb < n; rb += SR_ROWS * (SR_THREADS / SR_COLS)) {
+    for (int64_t rb = 0; rb < n; rb += (int64_t)SR_ROWS * nsub) {
       const int64_t r0 = rb + rsub * SR_ROWS;
       double acc[SR_ROWS];
 #pragma unroll
@@ -401,6 +431,10 @@ __global__ void __launch_bounds__(SR_THREADS)
         for (int u = 0; u < SR_ROWS; ++u) {
           if (r0 + u >= n) break;
           double *dst = Ab + (r0 + u) * lda;
+          if (k >= Rs) {
+            if (first) *dst = 0.0;
+            continue;
+          }
           if (first) *dst = acc[u];
           else *dst += acc[u];
         }
@@ -750,7 +784,7 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const d
   RS_REQUIRE(n >= 1 && r >= 1 && R >= 1 && n_shift >= 1 && n_shift <= n && ldz >= r &&
                  ld_table >= R,
              "rs_shift_project: bad shape (table must have 2n rows, n_shift <= n)");
-  size_t smem = (size_t)(n + SP_SHIFTS) * 8;
+  size_t smem = (size_t)(n + SP_SHIFTS + SP_ICH * 32) * 8;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void *)k_shift_project,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -886,7 +920,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   if ((st = check_launch("tucker_f"))) return st;
   if (nb > 0) {
     ProfScope ps(s, "short_rows");
-    const int BG = (int)std::max<int64_t>(1, SR_COLS / G);
+    // buckets per block: each bucket gets >= 1 warp of (32/KL) row subgroups
+    const int BG = (int)std::max<int64_t>(1, std::min<int64_t>(4, SR_COLS / G));
     size_t smem = (size_t)SR_Q * Rs * 8 + (size_t)(SR_Q + SR_Q + 1 + BG + 1 + SR_THREADS / 32) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
