@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(JAC_THREADS)
         double c = 1.0, s = 0.0;
         // rotate unless apq is below rounding relative to its diagonal pair or
         // below the absolute floor (noise block of the Ritz matrix)
-        if (fabs(apq) > tol && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
+        // (relative to the larger diagonal entry: the residual a rotation leaves
+        // behind is rounding of that size, so a geometric-mean test can stall)
+        if (fabs(apq) > tol && fabs(apq) > 1e-14 * fmax(fabs(app), fabs(aqq))) {
           double tau = (aqq - app) / (2.0 * apq);
           double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
