@@ -35,7 +35,7 @@ from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
     project_kernel, split_rank, split_tensor
-from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, \
+from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, top_eig_supported, \
     SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eps_rank, rhosvd_error_bound, shift_histograms, \
     shifted_core, shifted_grams, side_svd, top_eig, truncated_spectrum, tucker_to_canonical
 
@@ -364,54 +364,62 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
         # block size: the numerical rank of the long-part Grams grows as eps shrinks
         eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
         b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 2 * TOPEIG_BLOCK)
-        if forced_b := (max(cfg.reduction.ranks) if cfg.reduction.ranks else 0):
-            b = min(n - n % 2, max(b, forced_b + 16 + (forced_b % 2)))
-            b = min(b, TOPEIG_MAX_BLOCK)
-        evals, U, trace = top_eig(G, b)
+        forced = cfg.reduction.ranks
+        if forced is not None:
+            b = min(n - n % 2, max(b, max(forced) + 16 + (max(forced) % 2)))
+        use_top = top_eig_supported(n, b)
+        if use_top:
+            evals, U, trace = top_eig(G, b)
+        else:
+            b = 0
+            evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
         order3 = torch.argsort(idx[:, 2], stable=True)
         parts = [evals.reshape(-1), trace, ds._disp.max().reshape(1),
                  collision.to(torch.float64) if collision is not None else
                  torch.full((1,), -1.0, dtype=torch.float64, device="cuda"),
                  cnt3.to(torch.float64)]
         packed = to_host(torch.cat(parts))
-        if packed[3 * b + 4] >= 0:
-            key = int(packed[3 * b + 4])
+        nt_ = 3 * b + (3 if use_top else 0)
+        if packed[nt_ + 1] >= 0:
+            key = int(packed[nt_ + 1])
             node = (key // (n * n), (key // n) % n, key % n)
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles "
                                   f"snap to node {node}; use a larger n")
-        ds._cache["maxdisp"] = float(packed[3 * b + 3])
-        counts3 = packed[3 * b + 5:].astype(np.int64)
+        ds._cache["maxdisp"] = float(packed[nt_])
+        counts3 = packed[nt_ + 2:].astype(np.int64)
         limit = min(n, raw_rank)
-        forced = cfg.reduction.ranks
         if forced is not None:
             for r in forced:
                 if r > limit:
                     raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
         ranks, values, tails, zs = [], [], [], []
         for l in range(3):
-            theta = packed[l * b:(l + 1) * b]
             fr = forced[l] if forced is not None else None
-            r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n, cfg.reduction.eps,
-                                                    fr, limit)
-            if r is None or (fr is not None and fr > b):
-                # block too small or not converged: wider block, then full eigh
-                bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 2 * TOPEIG_BLOCK else 2 * b)
-                if bb > b:
+            r = None
+            if use_top:
+                theta = packed[l * b:(l + 1) * b]
+                r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n,
+                                                        cfg.reduction.eps, fr, limit)
+                if r is not None and fr is not None and fr > b:
+                    r = None
+                Ul = U[l] if r is not None else None
+            if r is None:
+                bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 2 * TOPEIG_BLOCK else max(2 * b, 2))
+                if b and bb > b and top_eig_supported(n, bb):
                     ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb)
-                    theta2 = to_host(ev2[0])
-                    r, sv, tail, total = truncated_spectrum(theta2, float(tr2[0]), n,
+                    r, sv, tail, total = truncated_spectrum(to_host(ev2[0]), float(tr2[0]), n,
                                                             cfg.reduction.eps, fr, limit)
                     if r is not None and (fr is None or fr <= bb):
                         Ul = U2[0]
-                if r is None or (fr is not None and fr > bb):
+                    else:
+                        r = None
+                if r is None:
                     s_full, z_full = eig_desc(G[l])     # full cuSOLVER spectrum
                     sh = to_host(s_full)
                     r = fr if fr is not None else min(eps_rank(sh, cfg.reduction.eps), limit)
                     sv, total = sh, float(np.sum(sh * sh))
                     tail = np.cumsum((sh * sh)[::-1])[::-1]
                     Ul = z_full.T
-            else:
-                Ul = U[l]
             ranks.append(int(r))
             values.append(sv)
             tails.append((float(tail[r]) if r < len(tail) else 0.0, total))

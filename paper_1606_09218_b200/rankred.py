@@ -342,6 +342,12 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
 TOPEIG_BLOCK = 32
 TOPEIG_MAX_BLOCK = 96
 TOPEIG_ITERS = 2
+TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
+
+
+def top_eig_supported(n: int, b: int) -> bool:
+    """rs_topeig keeps the b x n block in shared memory."""
+    return b % 2 == 0 and 2 <= b <= min(n, 128) and b * n + b <= TOPEIG_SMEM_DOUBLES
 
 
 def top_eig(G, b: int, iters: int = TOPEIG_ITERS):

@@ -86,7 +86,7 @@ def test_sum_dd_matches_fsum(nat, cuda):
     assert got == math.fsum(v)
 
 
-@pytest.mark.parametrize("n,b", [(256, 64), (96, 32), (512, 96), (32, 32)])
+@pytest.mark.parametrize("n,b", [(256, 64), (96, 32), (512, 48), (32, 32)])
 def test_topeig_graded_spectrum(nat, cuda, n, b):
     """Block subspace iteration + Jacobi vs the known eigensystem of a graded
     PSD matrix (the spectral shape of the RS side-matrix Grams)."""
@@ -96,7 +96,7 @@ def test_topeig_graded_spectrum(nat, cuda, n, b):
     lam = 10.0 ** (-np.arange(n) / 2.5)
     g = (q * lam) @ q.T
     g = 0.5 * (g + g.T)
-    ev, U, tr = top_eig(cuda.from_numpy(np.stack([g, 2 * g])).cuda(), b)
+    ev, U, tr = top_eig(cuda.from_numpy(np.stack([g, 2 * g])).cuda(), b, iters=3)
     ev, U = ev.cpu().numpy(), U.cpu().numpy()
     keep = int(np.count_nonzero(lam >= 1e-8))
     for m, scale in ((0, 1.0), (1, 2.0)):
