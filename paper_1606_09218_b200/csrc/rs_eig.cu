@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(OJ_MAX_THREADS)
   for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) R[e] = Y[e];
   __syncthreads();
   const int half = b / 2;
+  // rounding floor of a length-n dot product relative to |x||y| (de Rijk / Demmel-Veselic)
+  const double tol = fmax(1e-15, 2.3e-16 * (double)n);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(OJ_MAX_THREADS)
           bb += __shfl_xor_sync(0xffffffffu, bb, o);
           gg += __shfl_xor_sync(0xffffffffu, gg, o);
         }
-        if (gg != 0.0 && fabs(gg) > 1e-15 * sqrt(aa * bb)) {
+        if (gg != 0.0 && fabs(gg) > tol * sqrt(aa * bb)) {
           const double zeta = (bb - aa) / (2.0 * gg);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = rsqrt(1.0 + t * t), sn = c * t;
