@@ -37,36 +37,124 @@ __global__ void k_eig_start(double *__restrict__ Qt, int nmat, int b, int64_t n,
     Qt[e] = hash_unit(seed, (uint64_t)e);
 }
 
-// One-sided (Hestenes) Jacobi on the b rows of Y (n each): plane rotations
-// of row pairs until all rows are mutually orthogonal, then rows are
-// normalised and sorted by norm (descending).  For Y = W G with W spanning
-// the dominant invariant subspace of G this yields the eigenvectors of G as
-// rows and the eigenvalues as row norms -- orthonormalisation, Rayleigh-Ritz
-// and the small eigenproblem in one numerically stable step.  Warp per row
-// pair (parallel round-robin ordering), rows in shared memory (b*n <= 27k).
-constexpr int OJ_MAX_THREADS = 1024;
+constexpr int ORTH_THREADS = 256;
 
-__global__ void __launch_bounds__(OJ_MAX_THREADS)
-    k_ojac_rows(const double *__restrict__ Yall, int b, int64_t n, int64_t stride,
-                double *__restrict__ Wall, double *__restrict__ sig_all, int max_sweeps) {
-  extern __shared__ double sm[];
-  double *nrm = sm;                    // b
-  int *flag = (int *)(nrm + b);        // 1 (+pad)
-  double *R = nrm + b + 2;             // b * n rows
-  const double *Y = Yall + blockIdx.x * stride;
-  double *W = Wall + blockIdx.x * stride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) R[e] = Y[e];
+__device__ double block_sum(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;  // identical in every thread (fixed order)
+}
+
+// Orthonormalise the b rows of Q (n each) in place: classical Gram-Schmidt
+// applied twice per vector ("twice is enough"); a vector that collapses is
+// replaced by a fresh pseudo-random one.  One CTA per matrix.  With
+// IN_SMEM the finished rows live in shared memory (n*b*8 bytes) and are
+// written back at the end; otherwise they are read from global/L2.
+template <bool IN_SMEM>
+__global__ void __launch_bounds__(ORTH_THREADS)
+    k_orth_rows(double *__restrict__ Qall, int b, int64_t n, int64_t stride, uint64_t seed) {
+  extern __shared__ double sm[];
+  double *v = sm;           // n
+  double *coef = sm + n;    // b
+  double *red = coef + b;   // 32
+  double *Qs = red + 32;    // b*n when IN_SMEM
+  double *Qg = Qall + blockIdx.x * stride;
+  double *Q = IN_SMEM ? Qs : Qg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int i = 0; i < b; ++i) {
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Qg[i * n + e];
+    __syncthreads();
+    double ss = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+    double nrm0 = sqrt(block_sum(ss, red));
+    double nrm = 0.0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = warp; j < i; j += nwarps) {
+          const double *qj = Q + (int64_t)j * n;
+          double d = 0.0;
+          for (int64_t e = lane; e < n; e += 32) d = fma(qj[e], v[e], d);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (lane == 0) coef[j] = d;
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+          double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int j = 0;
+          for (; j + 4 <= i; j += 4) {
+            a0 -= coef[j] * Q[(int64_t)j * n + e];
+            a1 -= coef[j + 1] * Q[(int64_t)(j + 1) * n + e];
+            a2 -= coef[j + 2] * Q[(int64_t)(j + 2) * n + e];
+            a3 -= coef[j + 3] * Q[(int64_t)(j + 3) * n + e];
+          }
+          for (; j < i; ++j) a0 -= coef[j] * Q[(int64_t)j * n + e];
+          v[e] = (a0 + a1) + (a2 + a3);
+        }
+        __syncthreads();
+      }
+      ss = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+      nrm = sqrt(block_sum(ss, red));
+      if (nrm > 1e-13 * nrm0 && nrm > 0.0) break;
+      // breakdown: restart this vector from a fresh deterministic direction
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x)
+        v[e] = hash_unit(seed + 7919 * (attempt + 1), (uint64_t)(i * n + e));
+      __syncthreads();
+      ss = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+      nrm0 = sqrt(block_sum(ss, red));
+    }
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) Q[i * n + e] = v[e] * inv;
+    __syncthreads();
+  }
+  if (IN_SMEM)
+    for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
+}
+
+// Parallel cyclic Jacobi on the b x b symmetric T (shared memory), one CTA per
+// matrix.  Outputs eigenvalues sorted descending and the matching
+// eigenvectors as rows of Vt.
+constexpr int JAC_THREADS = 128;
+
+__global__ void __launch_bounds__(JAC_THREADS)
+    k_jacobi(const double *__restrict__ Tall, int b, double *__restrict__ evals,
+             double *__restrict__ Vtall, int max_sweeps) {
+  extern __shared__ double sm[];
+  const int ld = b + 1;
+  double *T = sm;                 // b x ld
+  double *V = T + b * ld;         // b x ld
+  double *rc = V + b * ld;        // b/2 x 2 (c, s)
+  int *rp = (int *)(rc + b);      // b/2 x 2 (p, q)
+  int *flag = rp + b;
+  const double *Tg = Tall + (int64_t)blockIdx.x * b * b;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    int r = e / b, c = e % b;
+    // symmetrise (T = W Q^T is symmetric only up to rounding)
+    T[r * ld + c] = 0.5 * (Tg[r * b + c] + Tg[c * b + r]);
+    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // absolute threshold: off-diagonals below 1e-18 max|diag| are already
+  // rounding-level for every eigenvector that matters
+  double dmax = 0.0;
+  for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * ld + i]));
+  const double tol = 1e-18 * dmax;
   const int half = b / 2;
-  // rounding floor of a length-n dot product relative to |x||y| (de Rijk / Demmel-Veselic)
-  const double tol = fmax(1e-15, 2.3e-16 * (double)n);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int round = 0; round < b - 1; ++round) {
-      for (int i = warp; i < half; i += nwarps) {
-        const int a0 = i, a1 = b - 1 - i;
+      for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        int a0 = i, a1 = b - 1 - i;
         int p = a0 == 0 ? 0 : 1 + (a0 - 1 + round) % (b - 1);
         int q = a1 == 0 ? 0 : 1 + (a1 - 1 + round) % (b - 1);
         if (p > q) {
@@ -74,60 +162,79 @@ __global__ void __launch_bounds__(OJ_MAX_THREADS)
           p = q;
           q = t;
         }
-        double *rp = R + (int64_t)p * n, *rq = R + (int64_t)q * n;
-        double aa = 0.0, bb = 0.0, gg = 0.0;
-        for (int64_t e = lane; e < n; e += 32) {
-          const double x = rp[e], y = rq[e];
-          aa = fma(x, x, aa);
-          bb = fma(y, y, bb);
-          gg = fma(x, y, gg);
+        double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
+        double c = 1.0, s = 0.0;
+        // rotate unless apq is below rounding relative to its diagonal pair or
+        // below the absolute floor (noise block of the Ritz matrix)
+        // (relative to the larger diagonal entry: the residual a rotation leaves
+        // behind is rounding of that size, so a geometric-mean test can stall)
+        if (fabs(apq) > tol && fabs(apq) > 1e-14 * fmax(fabs(app), fabs(aqq))) {
+          double tau = (aqq - app) / (2.0 * apq);
+          double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          *flag = 1;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          aa += __shfl_xor_sync(0xffffffffu, aa, o);
-          bb += __shfl_xor_sync(0xffffffffu, bb, o);
-          gg += __shfl_xor_sync(0xffffffffu, gg, o);
-        }
-        if (gg != 0.0 && fabs(gg) > tol * sqrt(aa * bb)) {
-          const double zeta = (bb - aa) / (2.0 * gg);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = rsqrt(1.0 + t * t), sn = c * t;
-          for (int64_t e = lane; e < n; e += 32) {
-            const double x = rp[e], y = rq[e];
-            rp[e] = c * x - sn * y;
-            rq[e] = sn * x + c * y;
-          }
-          if (lane == 0) *flag = 1;
-        }
+        rp[2 * i] = p;
+        rp[2 * i + 1] = q;
+        rc[2 * i] = c;
+        rc[2 * i + 1] = s;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // rows: J^T T
+        int i = e / b, k = e % b;
+        double c = rc[2 * i], s = rc[2 * i + 1];
+        if (s == 0.0) continue;
+        int p = rp[2 * i], q = rp[2 * i + 1];
+        double tp = T[p * ld + k], tq = T[q * ld + k];
+        T[p * ld + k] = c * tp - s * tq;
+        T[q * ld + k] = s * tp + c * tq;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // columns: (.) J, V J
+        int i = e / b, k = e % b;
+        double c = rc[2 * i], s = rc[2 * i + 1];
+        if (s == 0.0) continue;
+        int p = rp[2 * i], q = rp[2 * i + 1];
+        double tp = T[k * ld + p], tq = T[k * ld + q];
+        T[k * ld + p] = c * tp - s * tq;
+        T[k * ld + q] = s * tp + c * tq;
+        double vp = V[k * ld + p], vq = V[k * ld + q];
+        V[k * ld + p] = c * vp - s * vq;
+        V[k * ld + q] = s * vp + c * vq;
       }
       __syncthreads();
     }
     if (*flag == 0) break;
     __syncthreads();
   }
-  for (int i = warp; i < b; i += nwarps) {
-    const double *ri = R + (int64_t)i * n;
-    double ss = 0.0;
-    for (int64_t e = lane; e < n; e += 32) ss = fma(ri[e], ri[e], ss);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) nrm[i] = sqrt(ss);
-  }
-  __syncthreads();
-  // rank rows by norm (descending, ties by index), scatter normalised rows
-  double *sig = sig_all + (int64_t)blockIdx.x * b;
-  __shared__ int dest[128];
+  // sort descending (stable by index) and emit
+  double *ev = evals + (int64_t)blockIdx.x * b;
+  double *Vt = Vtall + (int64_t)blockIdx.x * b * b;
   for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    double ei = T[i * ld + i];
     int pos = 0;
-    for (int j = 0; j < b; ++j) pos += (nrm[j] > nrm[i]) || (nrm[j] == nrm[i] && j < i);
-    dest[i] = pos;
-    sig[pos] = nrm[i];
+    for (int j = 0; j < b; ++j) {
+      double ej = T[j * ld + j];
+      pos += (ej > ei) || (ej == ei && j < i);
+    }
+    ev[pos] = ei;
+    for (int k = 0; k < b; ++k) Vt[(int64_t)pos * b + k] = V[k * ld + i];
   }
-  __syncthreads();
-  for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) {
-    const int i = (int)(e / n);
-    const double inv = nrm[i] > 0.0 ? 1.0 / nrm[i] : 0.0;
-    W[(int64_t)dest[i] * n + (e - (int64_t)i * n)] = R[e] * inv;
+}
+
+// U[m][j][i] = sum_k Vt[m][j][k] Q[m][k][i]   (b x b times b x n, per matrix)
+__global__ void k_ritz(const double *__restrict__ Vt, const double *__restrict__ Q, int b, int64_t n,
+                       int nmat, double *__restrict__ U) {
+  const int64_t total = (int64_t)nmat * b * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e % n, j = (e / n) % b, m = e / (n * b);
+    const double *v = Vt + (m * b + j) * b;
+    const double *q = Q + m * b * n + i;
+    double acc = 0.0;
+    for (int k = 0; k < b; ++k) acc = fma(v[k], q[(int64_t)k * n], acc);
+    U[e] = acc;
   }
 }
 
@@ -221,38 +328,57 @@ using namespace rsb;
 extern "C" {
 
 int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b) {
-  return 2 * nmat * b * n * 8 + 1024;  // Y, W
+  // Q, Y (nmat*b*n each), T (nmat*b*b), Vt (nmat*b*b)
+  return (2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024;
 }
 
 int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters, double *evals,
               double *U, double *trace, void *work, int64_t work_bytes, void *stream) {
-  RS_REQUIRE(nmat >= 1 && n >= 2 && b >= 2 && b <= n && b % 2 == 0 && b <= 128 && iters >= 1,
-             "rs_topeig: bad sizes (need 2 <= b <= min(n, 128), b even)");
+  RS_REQUIRE(nmat >= 1 && n >= 2 && b >= 2 && b <= n && b % 2 == 0 && b <= 96 && iters >= 1,
+             "rs_topeig: bad sizes (need 2 <= b <= min(n, 96), b even)");
   RS_REQUIRE(n % 2 == 0, "rs_topeig: n must be even");
   if (work_bytes < rs_topeig_workspace_bytes(nmat, n, b))
     return fail(RS_ERR_CAPACITY, "rs_topeig: workspace too small");
-  const size_t need = (size_t)(b + 2 + b * n) * 8;
-  if (need > 220 * 1024)
-    return fail(RS_ERR_UNSUPPORTED, "rs_topeig: b*n = %lld exceeds the shared-memory block",
-                (long long)(b * n));
   cudaStream_t s = as_stream(stream);
-  double *Y = (double *)work;
-  double *W = Y + nmat * b * n;
+  double *Q = (double *)work;
+  double *Y = Q + nmat * b * n;
+  double *T = Y + nmat * b * n;
+  double *Vt = T + nmat * b * b;
   int st;
   ProfScope ps(s, "topeig");
-  k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(W, (int)nmat, (int)b, n, 12345);
+  k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Q, (int)nmat, (int)b, n, 12345);
   if ((st = check_launch("eig start"))) return st;
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_ojac_rows,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
-  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "ojac smem: %s", cudaGetErrorString(e));
-  const int threads = (int)std::min<int64_t>(OJ_MAX_THREADS, 32 * (b / 2));
-  for (int64_t it = 0; it < iters; ++it) {
-    // Y = W G, then W <- orthonormal rows of Y (eigen-directions of G)
-    if ((st = gemm_batched(W, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
-    double *dst = (it == iters - 1) ? U : W;
-    k_ojac_rows<<<(unsigned)nmat, threads, need, s>>>(Y, (int)b, n, b * n, dst, evals, 40);
-    if ((st = check_launch("ojac"))) return st;
+  const bool q_smem = (size_t)(n + b + 32 + b * n) * 8 <= 200 * 1024;
+  size_t orth_smem = (size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8;
+  const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
+  if (orth_smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(orth_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)orth_smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth smem: %s", cudaGetErrorString(e));
   }
+  // Y = Q G (rows), orth
+  for (int64_t it = 0; it < iters; ++it) {
+    if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
+    if (q_smem)
+      k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
+    else
+      k_orth_rows<false><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
+    if ((st = check_launch("orth"))) return st;
+    std::swap(Q, Y);
+  }
+  // Rayleigh-Ritz: W = Q G (into Y), T = W Q^T
+  if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
+  if ((st = gemm_batched(Y, n, b * n, Q, n, b * n, T, b, b * b, b, b, n, (int)nmat, s))) return st;
+  size_t jac_smem = (size_t)(2 * b * (b + 1) + b) * 8 + (size_t)(b + 1) * 4;
+  {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_jacobi,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
+  }
+  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 16);
+  if ((st = check_launch("jacobi"))) return st;
+  k_ritz<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Vt, Q, (int)b, n, (int)nmat, U);
+  if ((st = check_launch("ritz"))) return st;
   k_sign_rows<<<(unsigned)(nmat * b), 256, 0, s>>>(U, n);
   if ((st = check_launch("sign"))) return st;
   k_trace<<<(unsigned)nmat, 32, 0, s>>>(G, n, trace);

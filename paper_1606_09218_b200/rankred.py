@@ -346,8 +346,8 @@ TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
 
 
 def top_eig_supported(n: int, b: int) -> bool:
-    """rs_topeig keeps the b x n block in shared memory."""
-    return b % 2 == 0 and 2 <= b <= min(n, 128) and b * n + b <= TOPEIG_SMEM_DOUBLES
+    """Block sizes rs_topeig accepts (Jacobi on the b x b Ritz matrix in smem)."""
+    return b % 2 == 0 and 2 <= b <= min(n, TOPEIG_MAX_BLOCK)
 
 
 def top_eig(G, b: int, iters: int = TOPEIG_ITERS):
