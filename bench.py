@@ -282,9 +282,11 @@ def main():
     out = torch.empty((max(x1_hi - x1_lo, 1), n, n), dtype=torch.float64, device="cuda")
 
     def step(particles):
-        res = rt.build_rs(particles, cfg)
-        if x1_hi > x1_lo:
-            assemble_grid(res.rs.long, res.rs.short, x1_lo, x1_hi, out=out)
+        # public API: build_rs (short-range planes prefetched on a side stream,
+        # overlapping the long-range reduction) + dense_rs of this rank's slab
+        res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi))
+        g = rt.dense_rs(res.rs, limit=1 << 62, device=True, x1_range=(x1_lo, x1_hi))
+        step.last = g
         return res
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -335,7 +337,7 @@ def main():
         pos_e.copy_(pos_h, non_blocking=True)
         q_e.copy_(q_h, non_blocking=True)
         step(rt.DeviceParticles(pos_e, q_e, system.box))
-        out_h.copy_(out, non_blocking=True)
+        out_h.copy_(step.last, non_blocking=True)
 
     for _ in range(2):
         e2e_step()

@@ -111,23 +111,37 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3,
             const int64_t *shift, const double *z, const double *w, int64_t count,
             double *core, void *work, int64_t work_bytes, void *stream);
 
-/* (a12-a14) fused RS grid assembly of x1-planes [x1_lo, x1_hi):
- * out[((x1-x1_lo)*n + x2)*n + x3] = Tucker(core,V1,V2,V3)[x1,x2,x3]
- *                                  + sum_p z_p L0[x - c_p + gamma]
+/* (a12-a14) RS grid assembly of x1-planes [x1_lo, x1_hi):
+ * out[((x1-x1_lo)*n + x2)*n + x3] (=, or += with RS_ASM_ACCUMULATE)
+ *     [RS_ASM_LONG]  Tucker(core,V1,V2,V3)[x1,x2,x3]
+ *   + [RS_ASM_SHORT] sum_p z_p L0[x - c_p + gamma]
  * with L0 = sum_k wl[k] ul[.,k] (x) ul[.,k] (x) ul[.,k] (the normalised CCT
- * local tensor, formats.py:103-118, 432-445) and windows clipped to the grid.
- * Particles must be given bucketed by their x3 index: bucket b holds sorted
- * entries [bstart[b], bstart[b+1]) with x3 index bc3[b] (ascending), x1/x2
- * indices c1/c2 and charges zq.  Workspace: rs_assemble_workspace_bytes. */
+ * local tensor, formats.py:103-118, 432-445), windows clipped to the grid.
+ * Computed as one plane GEMM on FP64 tensor cores: rows (x1,x2), columns x3,
+ * K = [Tucker ranks | copies merged by x3 index x R_s].
+ * Copies are bucketed by their x3 index: bucket b holds the x3-sorted entries
+ * [bstart[b], bstart[b+1]) with x3 index bc3[b] (ascending), x1/x2 indices
+ * c1/c2 and charges zq; *nb_dev buckets (device), nb_max >= *nb_dev sizes
+ * the launch (rs_short_layout produces all of these on the device).
+ * Workspace: rs_assemble_workspace_bytes(n, planes, max rank, nb_max, Rs, flags). */
+#define RS_ASM_LONG 1
+#define RS_ASM_SHORT 2
+#define RS_ASM_ACCUMULATE 4
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax,
-                                    int64_t n_buckets, int64_t Rs); /* rmax = max(r1,r2,r3) */
+                                    int64_t nb_max, int64_t Rs, int flags);
 int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3,
                        const double *V1, const double *V2, const double *V3,
                        int64_t n, const double *ul, const double *wl, int64_t Rs,
                        int64_t gamma, const int32_t *c1, const int32_t *c2,
                        const double *zq, const int32_t *bstart, const int32_t *bc3,
-                       int64_t n_buckets, int64_t x1_lo, int64_t x1_hi,
-                       double *out, void *work, int64_t work_bytes, void *stream);
+                       const int32_t *nb_dev, int64_t nb_max, int64_t x1_lo,
+                       int64_t x1_hi, int flags, double *out, void *work,
+                       int64_t work_bytes, void *stream);
+
+/* Bucket layout of the short-range copies from the x3 occupancy counts
+ * cnt3 (n): bc3 (capacity n), bstart (capacity n+1), *nb (device int). */
+int rs_short_layout(const int32_t *cnt3, int64_t n, int32_t *bstart, int32_t *bc3,
+                    int32_t *nb, void *stream);
 
 /* (a15) Tucker point values, formats.py:347-352 (eval_tucker_many). */
 int rs_eval_tucker(const double *core, int64_t r1, int64_t r2, int64_t r3,

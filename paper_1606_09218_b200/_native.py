@@ -46,10 +46,11 @@ SIGNATURES = {
     "rs_core_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64]),
     "rs_core": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr,
                        _ptr, _i64, _ptr]),
-    "rs_assemble_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
+    "rs_assemble_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i32]),
     "rs_assemble_planes": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _i64,
-                                  _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _i64, _ptr, _ptr,
-                                  _i64, _ptr]),
+                                  _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _i64, _i32,
+                                  _ptr, _ptr, _i64, _ptr]),
+    "rs_short_layout": (_i32, [_ptr, _i64, _ptr, _ptr, _ptr, _ptr]),
     "rs_eval_tucker": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
     "rs_eval_cct": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64, _ptr, _ptr, _ptr]),
     "rs_pair_sums": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _dbl, _ptr, _ptr, _i64, _ptr, _i64, _i32,
@@ -105,6 +106,9 @@ def ptr(t) -> int | None:
 def stream_ptr() -> int:
     torch = _torch()
     return torch.cuda.current_stream().cuda_stream
+
+
+ASM_LONG, ASM_SHORT, ASM_ACCUMULATE = 1, 2, 4
 
 
 def prof_query(name: str):

@@ -29,8 +29,8 @@ import numpy as np
 
 from . import _native as nat
 from .errors import ConfigError, DomainError, ResolutionError
-from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, is_device, storage_report, \
-    to_device, to_host
+from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
+    short_layout, storage_report, to_device, to_host
 from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
@@ -319,11 +319,29 @@ class AssemblyResult:
     report: dict
 
 
-def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream():
+    torch = nat._torch()
+    dev = torch.cuda.current_device()
+    st = _SIDE_STREAMS.get(dev)
+    if st is None:
+        st = torch.cuda.Stream(device=dev)
+        _SIDE_STREAMS[dev] = st
+    return st
+
+
+def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
     ``system`` may be a reference-style :class:`ParticleSystem` /
     :class:`IndexedParticleSystem` (host arrays) or :class:`DeviceParticles`.
+
+    ``prefetch_dense`` (extension): ``True`` or an x1 plane range ``(lo, hi)``
+    starts the short-range part of the dense grid on a side stream right after
+    snapping, concurrently with the long-range reduction (it does not depend on
+    it); a following :func:`dense_rs` then only adds the Tucker part.
     """
     torch = nat._torch()
     grid = cfg.grid
@@ -354,6 +372,24 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
     z = ds.charges
     starts = (n - idx).contiguous()
     report = {"n": n, "b": grid.box.half_width, "particles": ds.count}
+    short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z, mode_sizes=(n, n, n),
+                overlap_policy=cfg.overlap_policy, max_overlap=cfg.max_overlap)
+    if plan.local.rank > 0:
+        lay = short_layout(idx, z, n)
+        lay.update(ul=plan.local_ul, wl=plan.local_wl)
+        short._cache["dev"] = lay
+        if prefetch_dense:
+            lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
+                                                            int(prefetch_dense[1]))
+            main = torch.cuda.current_stream()
+            side = _side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                buf = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
+                assemble_grid(None, short, lo, hi, out=buf, workspace_slot="assemble_side")
+                ev = torch.cuda.Event()
+                ev.record(side)
+            short._cache["prefetch"] = (lo, hi, buf, ev)
 
     tails = None
     if reduce_long and cfg.reduction.max_sweeps == 0:
@@ -373,11 +409,9 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
         else:
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
-        order3 = torch.argsort(idx[:, 2], stable=True)
         parts = [evals.reshape(-1), trace, ds._disp.max().reshape(1),
                  collision.to(torch.float64) if collision is not None else
-                 torch.full((1,), -1.0, dtype=torch.float64, device="cuda"),
-                 cnt3.to(torch.float64)]
+                 torch.full((1,), -1.0, dtype=torch.float64, device="cuda")]
         packed = to_host(torch.cat(parts))
         nt_ = 3 * b + (3 if use_top else 0)
         if packed[nt_ + 1] >= 0:
@@ -386,7 +420,6 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles "
                                   f"snap to node {node}; use a larger n")
         ds._cache["maxdisp"] = float(packed[nt_])
-        counts3 = packed[nt_ + 2:].astype(np.int64)
         limit = min(n, raw_rank)
         if forced is not None:
             for r in forced:
@@ -429,19 +462,7 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
         core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
         tucker = _trusted_tucker(core, zs)
         long_raw = None
-        # CCT device layout from the stable x3 order and the host bucket counts
-        occ = np.flatnonzero(counts3)
-        bstart = np.zeros(occ.size + 1, dtype=np.int32)
-        bstart[1:] = np.cumsum(counts3[occ])
-        cs = idx[order3]
-        short_layout = dict(c1=cs[:, 0].to(torch.int32).contiguous(),
-                            c2=cs[:, 1].to(torch.int32).contiguous(),
-                            zq=z[order3].contiguous(),
-                            bstart=torch.from_numpy(bstart).to("cuda", non_blocking=True),
-                            bc3=torch.from_numpy(occ.astype(np.int32)).to("cuda", non_blocking=True),
-                            n_buckets=int(occ.size), centers=idx, z=z)
     else:
-        short_layout = None
         if collision is not None and int(collision[0]) >= 0:
             key = int(collision[0])
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "
@@ -482,10 +503,6 @@ def build_rs(system, cfg: AssemblyConfig) -> AssemblyResult:
     else:
         long_part = long_raw
 
-    short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z, mode_sizes=(n, n, n),
-                overlap_policy=cfg.overlap_policy, max_overlap=cfg.max_overlap)
-    if short_layout is not None and plan.local.rank > 0:
-        short._cache["dev"] = dict(short_layout, ul=plan.local_ul, wl=plan.local_wl)
     report["gamma"] = plan.gamma
     report["gamma_h"] = plan.gamma * grid.h
     rs = RSTucker(long=long_part, short=short, grid=grid) if cfg.long_format == "tucker" else \

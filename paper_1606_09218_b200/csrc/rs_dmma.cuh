@@ -137,7 +137,7 @@ __device__ __forceinline__ void mainloop(double *smem, Acc<T> &acc, const double
 }
 
 // Store the warp tiles of acc into C (row-major, ldc even), predicated on M/N.
-template <class T>
+template <class T, bool ACC = false>
 __device__ __forceinline__ void store_tile(const Acc<T> &acc, double *C, int64_t ldc, int64_t m0,
                                            int64_t M, int64_t n0, int64_t N) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,10 +152,16 @@ __device__ __forceinline__ void store_tile(const Acc<T> &acc, double *C, int64_t
       int64_t c = n0 + wn0 + j * 8 + tig * 2;
       double *p = C + r * ldc + c;
       if (c + 1 < N && (ldc % 2 == 0)) {
-        *reinterpret_cast<double2 *>(p) = make_double2(acc.v[i][j][0], acc.v[i][j][1]);
+        double2 v = make_double2(acc.v[i][j][0], acc.v[i][j][1]);
+        if (ACC) {
+          const double2 old = *reinterpret_cast<const double2 *>(p);
+          v.x += old.x;
+          v.y += old.y;
+        }
+        *reinterpret_cast<double2 *>(p) = v;
       } else {
-        if (c < N) p[0] = acc.v[i][j][0];
-        if (c + 1 < N) p[1] = acc.v[i][j][1];
+        if (c < N) p[0] = ACC ? p[0] + acc.v[i][j][0] : acc.v[i][j][0];
+        if (c + 1 < N) p[1] = ACC ? p[1] + acc.v[i][j][1] : acc.v[i][j][1];
       }
     }
   }

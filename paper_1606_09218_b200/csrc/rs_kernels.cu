@@ -60,7 +60,7 @@ using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
 
 // C[m0.., n0..] = sum over the K ranges of this column tile of A B^T.
 // ranges: per column tile, nr (lo, hi) pairs; NULL => single range [0, K).
-template <class T>
+template <class T, bool ACC>
 __global__ void __launch_bounds__(T::THREADS)
     k_gemm_nt(const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
               double *__restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(T::THREADS)
   } else {
     mainloop<T>(smem, acc, A, lda, m0, M, B, ldb, n0, N, 0, K);
   }
-  store_tile<T>(acc, C, ldc, m0, M, n0, N);
+  store_tile<T, ACC>(acc, C, ldc, m0, M, n0, N);
 }
 
 __device__ __forceinline__ void tri_decode(int64_t t, int64_t &bi, int64_t &bj) {
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(TileSyrk::THREADS)
   acc.zero();
   mainloop<T>(smem, acc, A, lda, bi * T::BM, n, A, lda, bj * T::BN, n, k_lo, k_hi);
   double *dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (T::BM * T::BN);
-  store_tile<T>(acc, dst, T::BN, 0, T::BM, 0, T::BN);
+  store_tile<T, false>(acc, dst, T::BN, 0, T::BM, 0, T::BN);
 }
 
 __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, int64_t ntiles,
@@ -345,8 +345,11 @@ constexpr int SR_Q = 256;
 __global__ void __launch_bounds__(SR_THREADS)
     k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
-                 const double *__restrict__ zq, const int32_t *__restrict__ bstart, int n_buckets,
-                 int64_t n, int64_t x1_lo, double *__restrict__ A, int64_t lda, int64_t col0) {
+                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, double *__restrict__ A,
+                 int64_t lda, int64_t col0) {
+  const int n_buckets = *nbp;
+  if ((int)blockIdx.y * BG >= n_buckets) return;  // grid sized for the upper bound
   extern __shared__ double sm[];
   double *alpha = sm;                            // SR_Q * Rs
   int *qc2 = (int *)(alpha + SR_Q * Rs);         // SR_Q
@@ -445,48 +448,51 @@ __global__ void __launch_bounds__(SR_THREADS)
   } while (chunk_lo < p_hi);
 }
 
-// Bt[x3, :] = [V3[x3, :r3], 0.., E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in the band.
+// Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
+// the band (r3 = 0: no Tucker columns; Rs = 0: no short columns).
 __global__ void k_build_bt(const double *__restrict__ V3, int r3, int r3p,
                            const double *__restrict__ ul, int Rs, int G, int gamma,
-                           const int32_t *__restrict__ bc3, int64_t n_buckets, int64_t n,
-                           double *__restrict__ Bt, int64_t ldb) {
-  const int64_t total = n * ldb;
+                           const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
+                           int64_t n, double *__restrict__ Bt, int64_t ldb) {
+  const int64_t nb = nbp ? *nbp : 0;
+  const int64_t used = r3p + nb * G;  // columns past `used` are never read by the GEMM
+  const int64_t total = n * used;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t x3 = e / ldb, col = e - x3 * ldb;
+    int64_t x3 = e / used, col = e - x3 * used;
     double v = 0.0;
     if (col < r3) {
       v = V3[x3 * r3 + col];
     } else if (col >= r3p) {
       int64_t q = col - r3p, b = q / G;
       int k = (int)(q - b * G);
-      if (b < n_buckets && k < Rs) {
+      if (k < Rs) {
         int64_t d = x3 - bc3[b];
         if (d >= -gamma && d <= gamma) v = ul[(d + gamma) * Rs + k];
       }
     }
-    Bt[e] = v;
+    Bt[x3 * ldb + col] = v;
   }
 }
 
 // Per column tile t: range 0 = Tucker columns [0, r3p), range 1 = the buckets
-// whose x3 index lies within gamma of the tile's x3 span.
-__global__ void k_band_ranges(const int32_t *__restrict__ bc3, int64_t n_buckets, int64_t n,
-                              int gamma, int BN, int64_t r3p, int G, int64_t ntiles,
+// whose x3 index lies within gamma of the tile's x3 span (bc3 ascending).
+__global__ void k_band_ranges(const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
+                              int64_t n, int gamma, int BN, int64_t r3p, int G, int64_t ntiles,
                               int64_t *__restrict__ ranges) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
+  const int64_t nb = nbp ? *nbp : 0;
   int64_t top = t * BN + BN - 1 < n - 1 ? t * BN + BN - 1 : n - 1;
   int64_t lo_x = t * BN - gamma, hi_x = top + gamma;
-  // first bucket with bc3 >= lo_x, first bucket with bc3 > hi_x (bc3 ascending)
-  int64_t a = 0, b = n_buckets;
+  int64_t a = 0, b = nb;
   while (a < b) {
     int64_t m = (a + b) / 2;
     if (bc3[m] < lo_x) a = m + 1; else b = m;
   }
   int64_t blo = a;
   a = blo;
-  b = n_buckets;
+  b = nb;
   while (a < b) {
     int64_t m = (a + b) / 2;
     if (bc3[m] <= hi_x) a = m + 1; else b = m;
@@ -496,6 +502,59 @@ __global__ void k_band_ranges(const int32_t *__restrict__ bc3, int64_t n_buckets
   ranges[t * 4 + 1] = r3p;
   ranges[t * 4 + 2] = r3p + blo * G;
   ranges[t * 4 + 3] = r3p + bhi * G;
+}
+
+// Buckets of the x3-sorted copies from the occupancy counts: bc3 = occupied x3
+// values ascending, bstart = prefix sums of their counts, *nb = #buckets.
+// One block, fixed-order scan (deterministic).
+__global__ void __launch_bounds__(1024)
+    k_short_layout(const int32_t *__restrict__ cnt3, int64_t n, int32_t *__restrict__ bstart,
+                   int32_t *__restrict__ bc3, int32_t *__restrict__ nbp) {
+  __shared__ int32_t wocc[32], wcnt[32];
+  __shared__ int32_t carry_occ, carry_cnt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    carry_occ = 0;
+    carry_cnt = 0;
+    bstart[0] = 0;
+  }
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t x = base + tid;
+    const int32_t c = x < n ? cnt3[x] : 0;
+    const int32_t occ = c > 0 ? 1 : 0;
+    int32_t so = occ, sc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t to = __shfl_up_sync(0xffffffffu, so, o), tc = __shfl_up_sync(0xffffffffu, sc, o);
+      if (lane >= o) {
+        so += to;
+        sc += tc;
+      }
+    }
+    if (lane == 31) {
+      wocc[warp] = so;
+      wcnt[warp] = sc;
+    }
+    __syncthreads();
+    int32_t po = carry_occ, pc = carry_cnt;
+    for (int w = 0; w < warp; ++w) {
+      po += wocc[w];
+      pc += wcnt[w];
+    }
+    if (occ) {
+      const int32_t pos = po + so - 1;  // exclusive index of this bucket
+      bc3[pos] = (int32_t)x;
+      bstart[pos + 1] = pc + sc;
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) {
+      carry_occ = po + so;
+      carry_cnt = pc + sc;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *nbp = carry_occ;
 }
 
 // ======================================================== point evaluation
@@ -771,10 +830,10 @@ int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb, doubl
   RS_REQUIRE(lda % 2 == 0 && ldb % 2 == 0 && K % 2 == 0, "rs_gemm_nt: lda, ldb, K must be even");
   RS_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0, "rs_gemm_nt: operands must be 16-byte aligned");
   if (M == 0 || N == 0) return RS_OK;
-  int st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane>);
+  int st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, false>);
   if (st) return st;
   dim3 grid((unsigned)ceil_div(N, TilePlane::BN), (unsigned)ceil_div(M, TilePlane::BM));
-  k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, as_stream(stream)>>>(
+  k_gemm_nt<TilePlane, false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, as_stream(stream)>>>(
       A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
   return check_launch("rs_gemm_nt");
 }
@@ -861,15 +920,16 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
 }
 
 // workspace: A (planes*n x lda) | Bt (n x lda) | Y (planes x r2 r3) | ranges
-static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int64_t n_buckets,
-                       int64_t Rs, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
+static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int64_t nb_max,
+                       int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
                        int64_t *offY, int64_t *offR, int64_t *total) {
-  *r3p = round_up(std::max<int64_t>(r3, 1), 2);
+  const bool with_long = flags & RS_ASM_LONG, with_short = (flags & RS_ASM_SHORT) && Rs > 0;
+  *r3p = with_long ? round_up(std::max<int64_t>(r3, 1), 2) : 0;
   *G = round_up(std::max<int64_t>(Rs, 1), 2);
-  *lda = *r3p + n_buckets * *G;
+  *lda = std::max<int64_t>(*r3p + (with_short ? nb_max * *G : 0), 2);
   int64_t a = round_up(planes * n * *lda * 8, 256);
   int64_t b = round_up(n * *lda * 8, 256);
-  int64_t y = round_up(planes * r2r3 * 8, 256);
+  int64_t y = with_long ? round_up(planes * r2r3 * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, TilePlane::BN);
   int64_t rr = round_up(ntiles * 4 * 8, 256);
   *offB = a;
@@ -878,32 +938,49 @@ static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int6
   *total = a + b + y + rr;
 }
 
-int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t n_buckets,
-                                    int64_t Rs) {
+int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t nb_max,
+                                    int64_t Rs, int flags) {
   int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax * rmax, rmax, Rs > 0 ? n_buckets : 0, Rs, &lda, &r3p, &G, &oB, &oY,
-             &oR, &tot);
+  asm_layout(n, planes, rmax * rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
   return tot;
+}
+
+int rs_short_layout(const int32_t *cnt3, int64_t n, int32_t *bstart, int32_t *bc3, int32_t *nb,
+                    void *stream) {
+  RS_REQUIRE(n >= 1 && cnt3 && bstart && bc3 && nb, "rs_short_layout: bad arguments");
+  k_short_layout<<<1, 1024, 0, as_stream(stream)>>>(cnt3, n, bstart, bc3, nb);
+  return check_launch("rs_short_layout");
 }
 
 int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, const double *V1,
                        const double *V2, const double *V3, int64_t n, const double *ul,
                        const double *wl, int64_t Rs, int64_t gamma, const int32_t *c1,
                        const int32_t *c2, const double *zq, const int32_t *bstart,
-                       const int32_t *bc3, int64_t n_buckets, int64_t x1_lo, int64_t x1_hi,
-                       double *out, void *work, int64_t work_bytes, void *stream) {
-  RS_REQUIRE(n >= 2 && r1 >= 1 && r2 >= 1 && r3 >= 1, "rs_assemble_planes: bad ranks");
+                       const int32_t *bc3, const int32_t *nb_dev, int64_t nb_max, int64_t x1_lo,
+                       int64_t x1_hi, int flags, double *out, void *work, int64_t work_bytes,
+                       void *stream) {
+  const bool with_long = flags & RS_ASM_LONG;
+  const bool with_short = (flags & RS_ASM_SHORT) && Rs > 0 && nb_max > 0;
+  const bool accumulate = flags & RS_ASM_ACCUMULATE;
+  RS_REQUIRE(n >= 2 && n % 2 == 0, "rs_assemble_planes: n must be even");
+  RS_REQUIRE(!with_long || (r1 >= 1 && r2 >= 1 && r3 >= 1 && core && V1 && V2 && V3),
+             "rs_assemble_planes: bad long part");
   RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
-  RS_REQUIRE(Rs >= 0 && Rs <= 24, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs, 24);
-  RS_REQUIRE(gamma >= 0 && 2 * gamma + 1 <= 2 * n, "rs_assemble_planes: bad gamma");
+  RS_REQUIRE(Rs >= 0 && Rs <= 64, "rs_assemble_planes: Rs=%lld exceeds 64", (long long)Rs);
+  RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
+  RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
+             "rs_assemble_planes: bad short part");
+  RS_REQUIRE(with_long || with_short || accumulate, "rs_assemble_planes: nothing to do");
   const int64_t planes = x1_hi - x1_lo;
   const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
   int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax * rmax, r3, Rs > 0 ? n_buckets : 0, Rs, &lda, &r3p, &G, &oB, &oY,
-             &oR, &tot);
+  asm_layout(n, planes, rmax * rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
   if (work_bytes < tot)
     return fail(RS_ERR_CAPACITY, "rs_assemble_planes: workspace %lld < %lld",
                 (long long)work_bytes, (long long)tot);
+  if (!with_long && !with_short) {  // accumulate nothing: out unchanged
+    return RS_OK;
+  }
   char *wb = (char *)work;
   double *A = (double *)wb;
   double *Bt = (double *)(wb + oB);
@@ -911,40 +988,48 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   int64_t *ranges = (int64_t *)(wb + oR);
   cudaStream_t s = as_stream(stream);
   int st;
-  const int64_t nb = Rs > 0 ? n_buckets : 0;
-  k_tucker_y<<<grid_for(planes * r2 * r3, 128), 128, 0, s>>>(core, (int)r1, (int)r2, (int)r3, V1,
-                                                             x1_lo, planes, Y);
-  if ((st = check_launch("tucker_y"))) return st;
-  k_tucker_f<<<grid_for(planes * n * r3p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r3p, V2, n,
-                                                             planes, A, lda);
-  if ((st = check_launch("tucker_f"))) return st;
-  if (nb > 0) {
+  if (with_long) {
+    k_tucker_y<<<grid_for(planes * r2 * r3, 128), 128, 0, s>>>(core, (int)r1, (int)r2, (int)r3,
+                                                               V1, x1_lo, planes, Y);
+    if ((st = check_launch("tucker_y"))) return st;
+    k_tucker_f<<<grid_for(planes * n * r3p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r3p, V2,
+                                                               n, planes, A, lda);
+    if ((st = check_launch("tucker_f"))) return st;
+  }
+  if (with_short) {
     ProfScope ps(s, "short_rows");
-    // buckets per block: each bucket gets >= 1 warp of (32/KL) row subgroups
     const int BG = (int)std::max<int64_t>(1, std::min<int64_t>(4, SR_COLS / G));
     size_t smem = (size_t)SR_Q * Rs * 8 + (size_t)(SR_Q + SR_Q + 1 + BG + 1 + SR_THREADS / 32) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
-    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb, BG)), SR_THREADS, smem, s>>>(
-        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, (int)nb, n, x1_lo, A, lda, r3p);
-    if ((st = check_launch("short_rows"))) return st;
+    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb_max, BG)), SR_THREADS, smem, s>>>(
+        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, nb_dev, n, x1_lo, A, lda,
+        r3p);
   }
-  k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(V3, (int)r3, (int)r3p, ul, (int)Rs, (int)G,
-                                                     (int)gamma, bc3, nb, n, Bt, lda);
+  if (with_short && (st = check_launch("short_rows"))) return st;
+  k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
+                                                     with_long ? (int)r3 : 0, (int)r3p, ul,
+                                                     with_short ? (int)Rs : 0, (int)G, (int)gamma,
+                                                     bc3, with_short ? nb_dev : nullptr, n, Bt, lda);
   if ((st = check_launch("build_bt"))) return st;
   const int64_t ntiles = ceil_div(n, TilePlane::BN);
-  if (nb > 0) {
-    k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
-        bc3, nb, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles, ranges);
-    if ((st = check_launch("band_ranges"))) return st;
-  }
-  if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane>))) return st;
+  k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
+      bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
+      ranges);
+  if ((st = check_launch("band_ranges"))) return st;
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
   {
     ProfScope ps(s, "gemm_plane");
-    k_gemm_nt<TilePlane><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-        A, lda, Bt, lda, out, n, planes * n, n, r3p, nb > 0 ? ranges : nullptr, 2);
+    if (accumulate) {
+      if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, true>))) return st;
+      k_gemm_nt<TilePlane, true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+          A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2);
+    } else {
+      if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, false>))) return st;
+      k_gemm_nt<TilePlane, false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+          A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2);
+    }
   }
   return check_launch("plane_gemm");
 }

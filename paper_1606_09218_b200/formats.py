@@ -283,33 +283,43 @@ class CCT:
         return b
 
     def device_layout(self):
-        """Device data of the fused assembly: local factors, and the copies
-        bucketed by x3 index (ascending, stable) -- cached per CCT."""
+        """Device data of the fused assembly, cached per CCT: local factors and
+        the copies bucketed by x3 index (stable order; bucket table built on the
+        device by ``rs_short_layout``, so nothing synchronises the host)."""
         lay = self._cache.get("dev")
         if lay is not None:
             return lay
         torch = nat._torch()
-        ul = to_device(self.local.factors[0])
-        wl = to_device(self.local.weights)
         if self.local.rank > 0:
             f = self.local.factors
-            same = all((to_host(f[0]) == to_host(g)).all() for g in f[1:])
+            same = all(np.array_equal(to_host(f[0]), to_host(g)) for g in f[1:])
             if not same:
                 raise DomainError("fused assembly expects the three local factors to coincide "
                                   "(true for every CCT built by assemble_short)")
         c = to_device(self.centers, torch.int64)
         z = to_device(self.weights)
-        order = torch.argsort(c[:, 2], stable=True)
-        cs = c[order]
-        bc3, counts = torch.unique_consecutive(cs[:, 2], return_counts=True)
-        bstart = torch.zeros(bc3.numel() + 1, dtype=torch.int32, device="cuda")
-        bstart[1:] = torch.cumsum(counts, 0).to(torch.int32)
-        lay = dict(ul=ul.contiguous(), wl=wl.contiguous(), c1=cs[:, 0].to(torch.int32).contiguous(),
-                   c2=cs[:, 1].to(torch.int32).contiguous(), zq=z[order].contiguous(),
-                   bstart=bstart, bc3=bc3.to(torch.int32).contiguous(),
-                   n_buckets=int(bc3.numel()), centers=c, z=z)
+        lay = short_layout(c, z, self.mode_sizes[2])
+        lay.update(ul=to_device(self.local.factors[0]).contiguous(),
+                   wl=to_device(self.local.weights).contiguous())
         self._cache["dev"] = lay
         return lay
+
+
+def short_layout(centers, z, n: int) -> dict:
+    """Copies sorted (stably) by x3 index plus the device bucket table."""
+    torch = nat._torch()
+    count = int(centers.shape[0])
+    order = torch.argsort(centers[:, 2], stable=True)
+    cs = centers[order]
+    cnt3 = torch.bincount(centers[:, 2], minlength=n).to(torch.int32)
+    bstart = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    bc3 = torch.empty(n, dtype=torch.int32, device="cuda")
+    nb = torch.empty(1, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib().rs_short_layout(cnt3.data_ptr(), n, bstart.data_ptr(), bc3.data_ptr(),
+                                        nb.data_ptr(), nat.stream_ptr()), "rs_short_layout")
+    return dict(c1=cs[:, 0].to(torch.int32).contiguous(), c2=cs[:, 1].to(torch.int32).contiguous(),
+                zq=z[order].contiguous(), bstart=bstart, bc3=bc3, nb=nb,
+                nb_max=max(1, min(n, count)), centers=centers, z=z)
 
 
 def _check_disjoint(centers, gamma: int) -> None:
@@ -369,51 +379,69 @@ class RSTucker:
 
 
 # ============================================================ grid assembly
-def assemble_grid(long: TuckerTensor, short: Optional[CCT], x1_lo: int = 0,
-                  x1_hi: Optional[int] = None, out=None, workspace_bytes: int = _ASSEMBLE_WORKSPACE):
-    """x1-planes ``[x1_lo, x1_hi)`` of Tucker(long) + dense(short) on the device.
+def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int = 0,
+                  x1_hi: Optional[int] = None, out=None, accumulate: bool = False,
+                  workspace_bytes: int = _ASSEMBLE_WORKSPACE, workspace_slot: str = "assemble"):
+    """x1-planes ``[x1_lo, x1_hi)`` of Tucker(long) + dense(short) on the device
+    (either part may be None; ``accumulate`` adds into ``out``).
 
-    One ``rs_assemble_planes`` launch sequence per chunk of planes; the grid is
-    written once, in C order, by the plane GEMM's epilogue.
+    One ``rs_assemble_planes`` launch sequence per chunk of planes; every grid
+    point is written once, in C order, by the plane GEMM's epilogue.
     """
     torch = nat._torch()
-    n = long.mode_sizes[0]
-    if long.mode_sizes != (n, n, n):
-        raise CapabilityError("fused assembly expects a cubic grid")
+    if long is not None:
+        n = long.mode_sizes[0]
+        if long.mode_sizes != (n, n, n):
+            raise CapabilityError("fused assembly expects a cubic grid")
+    elif short is not None:
+        n = short.mode_sizes[0]
+    else:
+        raise DomainError("assemble_grid needs a long or a short part")
     x1_hi = n if x1_hi is None else int(x1_hi)
     if not (0 <= x1_lo < x1_hi <= n):
         raise DomainError(f"bad plane range [{x1_lo}, {x1_hi})")
     planes = x1_hi - x1_lo
     if out is None:
-        out = torch.empty((planes, n, n), dtype=torch.float64, device="cuda")
-    r1, r2, r3 = long.ranks
-    core = long.core
-    v1, v2, v3 = long.factors
+        out = (torch.zeros if accumulate else torch.empty)((planes, n, n), dtype=torch.float64,
+                                                           device="cuda")
+    flags = nat.ASM_ACCUMULATE if accumulate else 0
+    if long is not None:
+        flags |= nat.ASM_LONG
+        r1, r2, r3 = long.ranks
+        core, (v1, v2, v3) = long.core, long.factors
+    else:
+        r1 = r2 = r3 = 1
+        core = v1 = v2 = v3 = None
     have_short = short is not None and short.local.rank > 0 and short.count > 0
     if have_short:
+        flags |= nat.ASM_SHORT
         lay = short.device_layout()
-        rs, gamma, nb = short.local.rank, short.gamma, lay["n_buckets"]
+        rs, gamma, nb_max = short.local.rank, short.gamma, lay["nb_max"]
         ul, wl = lay["ul"], lay["wl"]
-        c1, c2, zq, bstart, bc3 = lay["c1"], lay["c2"], lay["zq"], lay["bstart"], lay["bc3"]
+        c1, c2, zq, bstart, bc3, nb = (lay[k] for k in ("c1", "c2", "zq", "bstart", "bc3", "nb"))
     else:
-        rs, gamma, nb = 0, 0, 0
-        ul = wl = c1 = c2 = zq = bstart = bc3 = None
+        rs, gamma, nb_max = 0, 0, 0
+        ul = wl = c1 = c2 = zq = bstart = bc3 = nb = None
+    if not (flags & (nat.ASM_LONG | nat.ASM_SHORT)):
+        if not accumulate:
+            out.zero_()
+        return out
     L = nat.lib()
     rmax = max(r1, r2, r3)
-    per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, nb, rs) - \
-        L.rs_assemble_workspace_bytes(n, 1, rmax, nb, rs)
-    fixed = L.rs_assemble_workspace_bytes(n, 1, rmax, nb, rs) - per_plane
+    one = L.rs_assemble_workspace_bytes(n, 1, rmax, nb_max, rs, flags)
+    per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, nb_max, rs, flags) - one
+    fixed = one - per_plane
     chunk = max(1, min(planes, (workspace_bytes - fixed) // max(per_plane, 1)))
-    ws_bytes = L.rs_assemble_workspace_bytes(n, chunk, rmax, nb, rs)
-    ws = nat.Workspace.get(ws_bytes, "assemble")
+    ws = nat.Workspace.get(L.rs_assemble_workspace_bytes(n, chunk, rmax, nb_max, rs, flags),
+                           workspace_slot)
     stream = nat.stream_ptr()
     for p0 in range(x1_lo, x1_hi, chunk):
         p1 = min(x1_hi, p0 + chunk)
         dst = out[p0 - x1_lo]
         nat.check(L.rs_assemble_planes(
-            core.data_ptr(), r1, r2, r3, v1.data_ptr(), v2.data_ptr(), v3.data_ptr(), n,
-            nat.ptr(ul), nat.ptr(wl), rs, gamma, nat.ptr(c1), nat.ptr(c2), nat.ptr(zq),
-            nat.ptr(bstart), nat.ptr(bc3), nb, p0, p1, dst.data_ptr(), ws.data_ptr(),
+            nat.ptr(core), r1, r2, r3, nat.ptr(v1), nat.ptr(v2), nat.ptr(v3), n, nat.ptr(ul),
+            nat.ptr(wl), rs, gamma, nat.ptr(c1), nat.ptr(c2), nat.ptr(zq), nat.ptr(bstart),
+            nat.ptr(bc3), nat.ptr(nb), nb_max, p0, p1, flags, dst.data_ptr(), ws.data_ptr(),
             ws.numel(), stream), "rs_assemble_planes")
     return out
 
@@ -427,29 +455,38 @@ def dense_cct(short: CCT, limit: int = MAX_DENSE_ELEMENTS, device: bool = False)
         out = torch.zeros(short.mode_sizes, dtype=torch.float64, device="cuda")
         return out if device else to_host(out)
     _guard_dense(short.local.mode_sizes, limit)
-    zero_long = _zero_tucker(n)
-    out = assemble_grid(zero_long, short)
+    out = assemble_grid(None, short)
     return out if device else to_host(out)
 
 
-def _zero_tucker(n: int) -> TuckerTensor:
-    torch = nat._torch()
-    e = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
-    e[0, 0] = 1.0
-    return TuckerTensor(torch.zeros((1, 1, 1), dtype=torch.float64, device="cuda"), (e, e, e))
-
-
-def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False):
+def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=None):
     """Dense RS tensor ``long + short`` (``formats.py:448-453``), fused on device.
 
     ``device=True`` returns the CUDA tensor (grids larger than host RAM);
-    the default returns a numpy array like the reference.
+    the default returns a numpy array like the reference.  ``x1_range``
+    (extension) assembles only the x1 planes ``[lo, hi)`` (multi-GPU slabs).
+    If :func:`build_rs` prefetched the short-range planes, only the Tucker
+    part is added here.
     """
     if isinstance(a, RSTucker):
         _guard_dense(a.long.mode_sizes, limit)
         if a.short.local.rank > 0:
             _guard_dense(a.short.local.mode_sizes, limit)
-        out = assemble_grid(a.long, a.short)
+        n = a.grid.n
+        lo, hi = (0, n) if x1_range is None else (int(x1_range[0]), int(x1_range[1]))
+        pre = a.short._cache.get("prefetch")
+        if pre is not None and pre[0] == lo and pre[1] == hi:
+            del a.short._cache["prefetch"]
+            torch = nat._torch()
+            _, _, out, ev = pre
+            main = torch.cuda.current_stream()
+            main.wait_event(ev)
+            out.record_stream(main)
+            assemble_grid(a.long, None, lo, hi, out=out, accumulate=True)
+        else:
+            out = assemble_grid(a.long, a.short, lo, hi)
+        if x1_range is None:
+            out = out.view(n, n, n)
         return out if device else to_host(out)
     if isinstance(a, RSCanonical):
         long = a.long.dense(limit=limit, device=True)
