@@ -1020,7 +1020,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   if ((st = check_launch("band_ranges"))) return st;
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
   {
-    ProfScope ps(s, "gemm_plane");
+    ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     if (accumulate) {
       if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, true>))) return st;
       k_gemm_nt<TilePlane, true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
