@@ -68,8 +68,12 @@ __global__ void __launch_bounds__(ORTH_THREADS)
   double *Q = IN_SMEM ? Qs : Qg;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
+  if (IN_SMEM) {
+    for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qs[e] = Qg[e];
+    __syncthreads();
+  }
   for (int i = 0; i < b; ++i) {
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Qg[i * n + e];
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] = Q[i * n + e];
     __syncthreads();
     double ss = 0.0;
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
@@ -120,175 +124,11 @@ __global__ void __launch_bounds__(ORTH_THREADS)
     for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
 }
 
-// Single-warp variants (all data in shared memory, only __syncwarp): the
-// eigen block is a chain of tiny dependent steps, so barrier latency, not
-// arithmetic, is what costs -- one warp per matrix removes every block barrier.
-
-// CGS2 on the b rows of Q (n each) by one warp; rows staged in smem.
-__global__ void __launch_bounds__(32)
-    k_orth_warp(double *__restrict__ Qall, int b, int64_t n, int64_t stride, uint64_t seed) {
-  extern __shared__ double sm[];
-  double *Q = sm;            // b * n
-  double *coef = Q + b * n;  // b
-  double *Qg = Qall + blockIdx.x * stride;
-  const int lane = threadIdx.x;
-  for (int64_t e = lane; e < (int64_t)b * n; e += 32) Q[e] = Qg[e];
-  __syncwarp();
-  auto wsum = [](double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-  };
-  for (int i = 0; i < b; ++i) {
-    double *v = Q + (int64_t)i * n;
-    double ss = 0.0;
-    for (int64_t e = lane; e < n; e += 32) ss = fma(v[e], v[e], ss);
-    double nrm0 = sqrt(wsum(ss)), nrm = 0.0;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < i; ++j) {
-          const double *qj = Q + (int64_t)j * n;
-          double d = 0.0;
-          for (int64_t e = lane; e < n; e += 32) d = fma(qj[e], v[e], d);
-          d = wsum(d);
-          if (lane == 0) coef[j] = d;
-        }
-        __syncwarp();
-        for (int64_t e = lane; e < n; e += 32) {
-          double a0 = v[e], a1 = 0.0;
-          int j = 0;
-          for (; j + 2 <= i; j += 2) {
-            a0 -= coef[j] * Q[(int64_t)j * n + e];
-            a1 -= coef[j + 1] * Q[(int64_t)(j + 1) * n + e];
-          }
-          if (j < i) a0 -= coef[j] * Q[(int64_t)j * n + e];
-          v[e] = a0 + a1;
-        }
-        __syncwarp();
-      }
-      ss = 0.0;
-      for (int64_t e = lane; e < n; e += 32) ss = fma(v[e], v[e], ss);
-      nrm = sqrt(wsum(ss));
-      if (nrm > 1e-13 * nrm0 && nrm > 0.0) break;
-      for (int64_t e = lane; e < n; e += 32)
-        v[e] = hash_unit(seed + 7919 * (attempt + 1), (uint64_t)(i * n + e));
-      __syncwarp();
-      ss = 0.0;
-      for (int64_t e = lane; e < n; e += 32) ss = fma(v[e], v[e], ss);
-      nrm0 = sqrt(wsum(ss));
-    }
-    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-    for (int64_t e = lane; e < n; e += 32) v[e] *= inv;
-    __syncwarp();
-  }
-  for (int64_t e = lane; e < (int64_t)b * n; e += 32) Qg[e] = Q[e];
-}
-
-// Cyclic Jacobi on the b x b symmetric T by one warp (b multiple of 32, <= 64).
-template <int B>
-__global__ void __launch_bounds__(32)
-    k_jacobi_warp(const double *__restrict__ Tall, double *__restrict__ evals,
-                  double *__restrict__ Vtall, int max_sweeps) {
-  constexpr int LD = B + 1, HALF = B / 2, PER = B / 32;
-  __shared__ double T[B * LD];
-  __shared__ double V[B * LD];
-  __shared__ double rc[HALF], rs[HALF];
-  __shared__ int rp[HALF], rq[HALF];
-  const int lane = threadIdx.x;
-  const double *Tg = Tall + (int64_t)blockIdx.x * B * B;
-  for (int e = lane; e < B * B; e += 32) {
-    const int r = e / B, c = e % B;
-    T[r * LD + c] = 0.5 * (Tg[r * B + c] + Tg[c * B + r]);
-    V[r * LD + c] = r == c ? 1.0 : 0.0;
-  }
-  __syncwarp();
-  double dmax = 0.0;
-  for (int i = 0; i < B; ++i) dmax = fmax(dmax, fabs(T[i * LD + i]));
-  const double tol = 1e-18 * dmax;
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    bool any = false;
-    for (int round = 0; round < B - 1; ++round) {
-      for (int i = lane; i < HALF; i += 32) {
-        const int a0 = i, a1 = B - 1 - i;
-        int p = a0 == 0 ? 0 : 1 + (a0 - 1 + round) % (B - 1);
-        int q = a1 == 0 ? 0 : 1 + (a1 - 1 + round) % (B - 1);
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
-        const double app = T[p * LD + p], aqq = T[q * LD + q], apq = T[p * LD + q];
-        double c = 1.0, s = 0.0;
-        if (fabs(apq) > tol && fabs(apq) > 1e-14 * fmax(fabs(app), fabs(aqq))) {
-          const double d = aqq - app, e2 = 2.0 * apq;
-          const double r = sqrt(d * d + e2 * e2);
-          const double t = (d >= 0.0 ? e2 : -e2) / (fabs(d) + r);
-          c = rsqrt(1.0 + t * t);
-          s = t * c;
-        }
-        rp[i] = p;
-        rq[i] = q;
-        rc[i] = c;
-        rs[i] = s;
-      }
-      __syncwarp();
-      any |= __any_sync(0xffffffffu, [&] {
-        bool f = false;
-        for (int i = lane; i < HALF; i += 32) f |= rs[i] != 0.0;
-        return f;
-      }());
-      // rows p, q of T  (J^T T): lane owns columns k = lane + 32 u
-      for (int i = 0; i < HALF; ++i) {
-        const double c = rc[i], s = rs[i];
-        if (s == 0.0) continue;
-        const int p = rp[i], q = rq[i];
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int k = lane + 32 * u;
-          const double tp = T[p * LD + k], tq = T[q * LD + k];
-          T[p * LD + k] = c * tp - s * tq;
-          T[q * LD + k] = s * tp + c * tq;
-        }
-      }
-      __syncwarp();
-      // columns p, q of T and V  ((.) J): lane owns rows k
-      for (int i = 0; i < HALF; ++i) {
-        const double c = rc[i], s = rs[i];
-        if (s == 0.0) continue;
-        const int p = rp[i], q = rq[i];
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int k = lane + 32 * u;
-          const double tp = T[k * LD + p], tq = T[k * LD + q];
-          T[k * LD + p] = c * tp - s * tq;
-          T[k * LD + q] = s * tp + c * tq;
-          const double vp = V[k * LD + p], vq = V[k * LD + q];
-          V[k * LD + p] = c * vp - s * vq;
-          V[k * LD + q] = s * vp + c * vq;
-        }
-      }
-      __syncwarp();
-    }
-    if (!any) break;
-  }
-  double *ev = evals + (int64_t)blockIdx.x * B;
-  double *Vt = Vtall + (int64_t)blockIdx.x * B * B;
-  for (int i = lane; i < B; i += 32) {
-    const double ei = T[i * LD + i];
-    int pos = 0;
-    for (int j = 0; j < B; ++j) {
-      const double ej = T[j * LD + j];
-      pos += (ej > ei) || (ej == ei && j < i);
-    }
-    ev[pos] = ei;
-    for (int k = 0; k < B; ++k) Vt[(int64_t)pos * B + k] = V[k * LD + i];
-  }
-}
-
 // Parallel cyclic Jacobi on the b x b symmetric T (shared memory), one CTA per
-// matrix.  Outputs eigenvalues sorted descending and the matching
-// eigenvectors as rows of Vt.
-constexpr int JAC_THREADS = 128;
+// matrix.  Each round rotates b/2 disjoint pairs; T' = J^T T J is applied as
+// independent 2x2 block updates (one phase, in place) and V' = V J alongside.
+// Outputs eigenvalues sorted descending and eigenvectors as rows of Vt.
+constexpr int JAC_THREADS = 256;
 
 __global__ void __launch_bounds__(JAC_THREADS)
     k_jacobi(const double *__restrict__ Tall, int b, double *__restrict__ evals,
@@ -308,8 +148,6 @@ __global__ void __launch_bounds__(JAC_THREADS)
     V[r * ld + c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // absolute threshold: off-diagonals below 1e-18 max|diag| are already
-  // rounding-level for every eigenvector that matters
   double dmax = 0.0;
   for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * ld + i]));
   const double tol = 1e-18 * dmax;
@@ -327,16 +165,14 @@ __global__ void __launch_bounds__(JAC_THREADS)
           p = q;
           q = t;
         }
-        double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
+        const double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
         double c = 1.0, s = 0.0;
-        // rotate unless apq is below rounding relative to its diagonal pair or
-        // below the absolute floor (noise block of the Ritz matrix)
-        // (relative to the larger diagonal entry: the residual a rotation leaves
-        // behind is rounding of that size, so a geometric-mean test can stall)
+        // rotate unless apq is rounding-level relative to the larger diagonal
+        // entry or below the absolute floor (noise block of the Ritz matrix)
         if (fabs(apq) > tol && fabs(apq) > 1e-14 * fmax(fabs(app), fabs(aqq))) {
-          double tau = (aqq - app) / (2.0 * apq);
-          double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
+          const double d = aqq - app, e2 = apq + apq;
+          const double t = (d >= 0.0 ? e2 : -e2) / (fabs(d) + sqrt(d * d + e2 * e2));
+          c = rsqrt(1.0 + t * t);
           s = t * c;
           *flag = 1;
         }
@@ -346,27 +182,33 @@ __global__ void __launch_bounds__(JAC_THREADS)
         rc[2 * i + 1] = s;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // rows: J^T T
-        int i = e / b, k = e % b;
-        double c = rc[2 * i], s = rc[2 * i + 1];
-        if (s == 0.0) continue;
-        int p = rp[2 * i], q = rp[2 * i + 1];
-        double tp = T[p * ld + k], tq = T[q * ld + k];
-        T[p * ld + k] = c * tp - s * tq;
-        T[q * ld + k] = s * tp + c * tq;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < half * b; e += blockDim.x) {  // columns: (.) J, V J
-        int i = e / b, k = e % b;
-        double c = rc[2 * i], s = rc[2 * i + 1];
-        if (s == 0.0) continue;
-        int p = rp[2 * i], q = rp[2 * i + 1];
-        double tp = T[k * ld + p], tq = T[k * ld + q];
-        T[k * ld + p] = c * tp - s * tq;
-        T[k * ld + q] = s * tp + c * tq;
-        double vp = V[k * ld + p], vq = V[k * ld + q];
-        V[k * ld + p] = c * vp - s * vq;
-        V[k * ld + q] = s * vp + c * vq;
+      // T' = J^T T J on 2x2 blocks (row pair i, column pair j), V' = V J
+      for (int e = threadIdx.x; e < half * half + half * b; e += blockDim.x) {
+        if (e < half * half) {
+          const int i = e / half, j = e - (e / half) * half;
+          const double ci = rc[2 * i], si = rc[2 * i + 1], cj = rc[2 * j], sj = rc[2 * j + 1];
+          if (si == 0.0 && sj == 0.0) continue;
+          const int p = rp[2 * i], q = rp[2 * i + 1], u = rp[2 * j], w = rp[2 * j + 1];
+          const double tpu = T[p * ld + u], tpw = T[p * ld + w];
+          const double tqu = T[q * ld + u], tqw = T[q * ld + w];
+          // rows: r_p = c r_p - s r_q, r_q = s r_p + c r_q
+          const double ru_p = ci * tpu - si * tqu, rw_p = ci * tpw - si * tqw;
+          const double ru_q = si * tpu + ci * tqu, rw_q = si * tpw + ci * tqw;
+          // columns: c_u = c c_u - s c_w, c_w = s c_u + c c_w
+          T[p * ld + u] = cj * ru_p - sj * rw_p;
+          T[p * ld + w] = sj * ru_p + cj * rw_p;
+          T[q * ld + u] = cj * ru_q - sj * rw_q;
+          T[q * ld + w] = sj * ru_q + cj * rw_q;
+        } else {
+          const int f = e - half * half;
+          const int j = f / b, k = f - (f / b) * b;
+          const double c = rc[2 * j], s = rc[2 * j + 1];
+          if (s == 0.0) continue;
+          const int p = rp[2 * j], q = rp[2 * j + 1];
+          const double vp = V[k * ld + p], vq = V[k * ld + q];
+          V[k * ld + p] = c * vp - s * vq;
+          V[k * ld + q] = s * vp + c * vq;
+        }
       }
       __syncthreads();
     }
@@ -513,13 +355,6 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   ProfScope ps(s, "topeig");
   k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Q, (int)nmat, (int)b, n, 12345);
   if ((st = check_launch("eig start"))) return st;
-  const size_t warp_smem = (size_t)(b * n + b) * 8;
-  const bool warp_orth = warp_smem <= 200 * 1024;
-  if (warp_orth) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_orth_warp,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_smem);
-    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth_warp smem: %s", cudaGetErrorString(e));
-  }
   const bool q_smem = (size_t)(n + b + 32 + b * n) * 8 <= 200 * 1024;
   size_t orth_smem = (size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8;
   const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
@@ -531,9 +366,7 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // Y = Q G (rows), orth
   for (int64_t it = 0; it < iters; ++it) {
     if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
-    if (warp_orth)
-      k_orth_warp<<<(unsigned)nmat, 32, warp_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
-    else if (q_smem)
+    if (q_smem)
       k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
     else
       k_orth_rows<false><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
@@ -549,10 +382,7 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
   }
-  if (b == 32)
-    k_jacobi_warp<32><<<(unsigned)nmat, 32, 0, s>>>(T, evals, Vt, 16);
-  else
-    k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 16);
+  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 16);
   if ((st = check_launch("jacobi"))) return st;
   k_ritz<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Vt, Q, (int)b, n, (int)nmat, U);
   if ((st = check_launch("ritz"))) return st;
