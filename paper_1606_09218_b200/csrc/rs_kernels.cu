@@ -176,45 +176,46 @@ __global__ void __launch_bounds__(256)
 }
 
 // Per-mode shift histograms c[l][s] = sum_{p: n - idx[p][l] == s} z_p^2 and
-// the x3 occupancy counts cnt[x] = #{p: idx[p][2] == x}; thread per (l, s),
-// particles streamed through shared memory in index order (deterministic).
-constexpr int SH_CHUNK = 1024;
+// the x3 occupancy counts cnt[x] = #{p: idx[p][2] == x}.  Warp per (mode, s):
+// lanes stride the particles (staged in shared memory, shared by the block's
+// 8 warps), then a fixed shuffle tree -- deterministic.
+constexpr int SH_CHUNK = 2048;
 
 __global__ void __launch_bounds__(256)
     k_shift_hist(const int64_t *__restrict__ idx, const double *__restrict__ z, int64_t count,
                  int64_t n, double *__restrict__ c, int32_t *__restrict__ cnt3) {
-  __shared__ int32_t key[SH_CHUNK][3];
+  __shared__ int32_t key[SH_CHUNK];
   __shared__ double zz[SH_CHUNK];
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // shift / x3 value
-  double acc[3] = {0.0, 0.0, 0.0};
+  const int l = blockIdx.y;                      // mode
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * 8 + warp;
+  double acc = 0.0;
   int32_t occ = 0;
   for (int64_t p0 = 0; p0 < count; p0 += SH_CHUNK) {
     const int m = (int)(count - p0 < SH_CHUNK ? count - p0 : SH_CHUNK);
     __syncthreads();
     for (int e = threadIdx.x; e < m; e += blockDim.x) {
-      const int64_t *ip = idx + 3 * (p0 + e);
-      key[e][0] = (int32_t)(n - ip[0]);
-      key[e][1] = (int32_t)(n - ip[1]);
-      key[e][2] = (int32_t)ip[2];
-      double q = z[p0 + e];
+      key[e] = (int32_t)(n - idx[3 * (p0 + e) + l]);
+      const double q = z[p0 + e];
       zz[e] = q * q;
     }
     __syncthreads();
     if (s < n) {
-      for (int e = 0; e < m; ++e) {
-        const double q2 = zz[e];
-        if (key[e][0] == s) acc[0] += q2;
-        if (key[e][1] == s) acc[1] += q2;
-        if ((int32_t)n - key[e][2] == s) acc[2] += q2;
-        occ += key[e][2] == s;
+      for (int e = lane; e < m; e += 32) {
+        const bool hit = key[e] == (int32_t)s;
+        acc += hit ? zz[e] : 0.0;
+        occ += (l == 2 && key[e] == (int32_t)(n - s)) ? 1 : 0;
       }
     }
   }
-  if (s < n) {
-    c[s] = acc[0];
-    c[n + s] = acc[1];
-    c[2 * n + s] = acc[2];
-    cnt3[s] = occ;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    occ += __shfl_xor_sync(0xffffffffu, occ, o);
+  }
+  if (s < n && lane == 0) {
+    c[(int64_t)l * n + s] = acc;
+    if (l == 2) cnt3[s] = occ;
   }
 }
 
@@ -861,7 +862,8 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const d
 int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n, double *c,
                   int32_t *cnt3, void *stream) {
   RS_REQUIRE(count >= 1 && n >= 2, "rs_shift_hist: bad sizes");
-  k_shift_hist<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(idx, z, count, n, c, cnt3);
+  k_shift_hist<<<dim3((unsigned)ceil_div(n, 8), 3), 256, 0, as_stream(stream)>>>(idx, z, count, n,
+                                                                                 c, cnt3);
   return check_launch("rs_shift_hist");
 }
 
@@ -873,7 +875,7 @@ static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t
   *a_tiles = ceil_div(r1, at);
   int64_t r123 = r1 * r2 * r3;
   int64_t by_mem = std::max<int64_t>(1, ((int64_t)1 << 27) / std::max<int64_t>(1, r123));
-  int64_t want = std::max<int64_t>(1, ceil_div(148 * 4, *a_tiles));
+  int64_t want = std::max<int64_t>(1, ceil_div(148, *a_tiles));
   int64_t sp = std::min<int64_t>({want, by_mem, std::max<int64_t>(1, count)});
   *per = ceil_div(count, sp);
   *splits = ceil_div(count, *per);

@@ -47,3 +47,16 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         assemble_grid(res.rs.long, res.rs.short, out=out)
     torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=30))
+
+import cProfile, pstats, io
+pr = cProfile.Profile()
+torch.cuda.synchronize()
+pr.enable()
+for _ in range(10):
+    res = rt.build_rs(dp, cfg, prefetch_dense=True)
+    g = rt.dense_rs(res.rs, limit=1 << 62, device=True)
+torch.cuda.synchronize()
+pr.disable()
+st = io.StringIO()
+pstats.Stats(pr, stream=st).sort_stats("tottime").print_stats(25)
+print(st.getvalue()[:6000])
