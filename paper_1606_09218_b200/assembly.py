@@ -30,7 +30,7 @@ import numpy as np
 from . import _native as nat
 from .errors import ConfigError, DomainError, ResolutionError
 from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
-    short_layout, storage_report, to_device, to_host
+    short_layout, storage_report, to_device, to_host, trusted_cct
 from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
@@ -372,10 +372,20 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResul
     z = ds.charges
     starts = (n - idx).contiguous()
     report = {"n": n, "b": grid.box.half_width, "particles": ds.count}
-    short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z, mode_sizes=(n, n, n),
-                overlap_policy=cfg.overlap_policy, max_overlap=cfg.max_overlap)
+    if cfg.overlap_policy == "strict":
+        short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z,
+                    mode_sizes=(n, n, n), overlap_policy=cfg.overlap_policy,
+                    max_overlap=cfg.max_overlap)
+    else:
+        short = trusted_cct(plan.local, plan.gamma, idx, z, (n, n, n), cfg.overlap_policy,
+                            cfg.max_overlap)
+    if cfg.overlap_policy not in ("strict", "soft"):
+        raise DomainError(f"unknown overlap policy {cfg.overlap_policy!r}")
+    hist = cnt3 = None
+    if reduce_long and cfg.reduction.max_sweeps == 0:
+        hist, cnt3 = shift_histograms(idx, z, n)
     if plan.local.rank > 0:
-        lay = short_layout(idx, z, n)
+        lay = short_layout(idx, z, n, cnt3)
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
         short._cache["dev"] = lay
         if prefetch_dense:
@@ -395,7 +405,6 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResul
     if reduce_long and cfg.reduction.max_sweeps == 0:
         # shift histograms -> per-mode Grams on DMMA -> top-b eigenpairs, then
         # ONE synchronisation for everything the host must decide on
-        hist, cnt3 = shift_histograms(idx, z, n)
         G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
         # block size: the numerical rank of the long-part Grams grows as eps shrinks
         eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12

@@ -305,13 +305,28 @@ class CCT:
         return lay
 
 
-def short_layout(centers, z, n: int) -> dict:
-    """Copies sorted (stably) by x3 index plus the device bucket table."""
+def trusted_cct(local, gamma: int, centers, weights, mode_sizes, overlap_policy="soft",
+                max_overlap=8) -> "CCT":
+    """CCT from device arrays produced by this package (snapped, in range,
+    charges float64): skips the validation probes, which would synchronise."""
+    c = object.__new__(CCT)
+    for k, v in dict(local=local, gamma=int(gamma), centers=centers, weights=weights,
+                     mode_sizes=tuple(int(m) for m in mode_sizes), overlap_policy=overlap_policy,
+                     max_overlap=max_overlap, _cache={}).items():
+        object.__setattr__(c, k, v)
+    return c
+
+
+def short_layout(centers, z, n: int, cnt3=None) -> dict:
+    """Copies sorted (stably) by x3 index plus the device bucket table
+    (no host synchronisation)."""
     torch = nat._torch()
     count = int(centers.shape[0])
     order = torch.argsort(centers[:, 2], stable=True)
     cs = centers[order]
-    cnt3 = torch.bincount(centers[:, 2], minlength=n).to(torch.int32)
+    if cnt3 is None:
+        cnt3 = torch.zeros(n, dtype=torch.int32, device="cuda").index_add_(
+            0, centers[:, 2], torch.ones(count, dtype=torch.int32, device="cuda"))
     bstart = torch.empty(n + 1, dtype=torch.int32, device="cuda")
     bc3 = torch.empty(n, dtype=torch.int32, device="cuda")
     nb = torch.empty(1, dtype=torch.int32, device="cuda")
