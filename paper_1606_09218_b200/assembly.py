@@ -220,16 +220,25 @@ def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
                                _disp=disp)
 
 
-def _collision_flag(idx, n: int):
-    """Device int64: index of the first duplicated node key, or -1."""
+def _node_sort(idx, n: int):
+    """One device sort of the particles by node key ``(x3, x1, x2)`` (x3-major):
+    returns (order, flag) with ``flag`` = the first duplicated node as a
+    linear ``(x1 n + x2) n + x3`` key, or -1.  The order doubles as the x3
+    bucket order of the short-range layout."""
     torch = nat._torch()
+    keys = (idx[:, 2] * n + idx[:, 0]) * n + idx[:, 1]
+    ks, order = torch.sort(keys, stable=True)
     if idx.shape[0] < 2:
-        return torch.full((1,), -1, dtype=torch.int64, device=idx.device)
-    keys = (idx[:, 0] * n + idx[:, 1]) * n + idx[:, 2]
-    ks, _ = torch.sort(keys)
+        return order, torch.full((1,), -1, dtype=torch.int64, device=idx.device)
     dup = ks[1:] == ks[:-1]
-    first = torch.where(dup.any(), ks[:-1][dup.to(torch.int64).argmax()], ks.new_tensor(-1))
-    return first.reshape(1)
+    k = ks[:-1][dup.to(torch.int64).argmax()]
+    x3, x1, x2 = k // (n * n), (k // n) % n, k % n
+    first = torch.where(dup.any(), (x1 * n + x2) * n + x3, ks.new_tensor(-1))
+    return order, first.reshape(1)
+
+
+def _collision_flag(idx, n: int):
+    return _node_sort(idx, n)[1]
 
 
 def _as_device_system(system, grid: Grid3):
@@ -240,7 +249,9 @@ def _as_device_system(system, grid: Grid3):
         return system, None
     if isinstance(system, DeviceParticles):
         ds = snap_device(system.positions, system.charges, system.box, grid)
-        return ds, _collision_flag(ds.indices, grid.n)
+        order, flag = _node_sort(ds.indices, grid.n)
+        ds._cache["node_order"] = order
+        return ds, flag
     if isinstance(system, IndexedParticleSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
@@ -255,7 +266,9 @@ def _as_device_system(system, grid: Grid3):
         return ds, None
     if isinstance(system, ParticleSystem):
         ds = snap_device(system.positions, system.charges, system.box, grid)
-        return ds, _collision_flag(ds.indices, grid.n)
+        order, flag = _node_sort(ds.indices, grid.n)
+        ds._cache["node_order"] = order
+        return ds, flag
     raise ConfigError(f"expected a particle system, got {type(system).__name__}")
 
 
@@ -385,7 +398,7 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResul
     if reduce_long and cfg.reduction.max_sweeps == 0:
         hist, cnt3 = shift_histograms(idx, z, n)
     if plan.local.rank > 0:
-        lay = short_layout(idx, z, n, cnt3)
+        lay = short_layout(idx, z, n, cnt3, ds._cache.get("node_order"))
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
         short._cache["dev"] = lay
         if prefetch_dense:

@@ -317,12 +317,14 @@ def trusted_cct(local, gamma: int, centers, weights, mode_sizes, overlap_policy=
     return c
 
 
-def short_layout(centers, z, n: int, cnt3=None) -> dict:
-    """Copies sorted (stably) by x3 index plus the device bucket table
-    (no host synchronisation)."""
+def short_layout(centers, z, n: int, cnt3=None, order=None) -> dict:
+    """Copies sorted by x3 index (``order``: any permutation that sorts them by
+    x3; default a stable argsort) plus the device bucket table (no host
+    synchronisation)."""
     torch = nat._torch()
     count = int(centers.shape[0])
-    order = torch.argsort(centers[:, 2], stable=True)
+    if order is None:
+        order = torch.argsort(centers[:, 2], stable=True)
     cs = centers[order]
     if cnt3 is None:
         cnt3 = torch.zeros(n, dtype=torch.int32, device="cuda").index_add_(
