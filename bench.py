@@ -221,20 +221,6 @@ def measure_dgemm_peak(torch):
     return 2 * n ** 3 / t / 1e12
 
 
-def slab_bounds(weights, world):
-    """Contiguous x1 slabs with ~equal work (prefix sums of per-plane cost)."""
-    c = np.concatenate([[0.0], np.cumsum(weights)])
-    total = c[-1]
-    bounds = [0]
-    for r in range(1, world):
-        bounds.append(int(np.searchsorted(c, total * r / world)))
-    bounds.append(len(weights))
-    for i in range(1, len(bounds)):
-        bounds[i] = max(bounds[i], bounds[i - 1] + (1 if i < len(bounds) - 1 else 0))
-    bounds[-1] = len(weights)
-    return bounds
-
-
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -250,7 +236,7 @@ def main():
     import paper_1606_09218_b200 as rt
     from paper_1606_09218_b200 import _native as nat
     from paper_1606_09218_b200 import configs
-    from paper_1606_09218_b200.formats import assemble_grid
+    from paper_1606_09218_b200.parallel import plane_costs, slab_bounds
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -267,13 +253,7 @@ def main():
     plan = rt.plan_for(cfg, cfg.split_index)
     gamma = plan.gamma
     # work-balanced x1 slab of this rank: per-plane pair count + n^2 store
-    per_plane = np.full(n, float(n * n))
-    lo = np.maximum(host_idx[:, 0] - gamma, 0)
-    hi = np.minimum(host_idx[:, 0] + gamma, n - 1)
-    w23 = pair_counts(host_idx, gamma, n) / (hi - lo + 1)
-    np.add.at(per_plane, np.concatenate([np.arange(a, b + 1) for a, b in zip(lo, hi)]),
-              np.repeat(w23, hi - lo + 1))
-    bounds = slab_bounds(per_plane, world)
+    bounds = slab_bounds(plane_costs(host_idx, gamma, n), world)
     x1_lo, x1_hi = bounds[rank], bounds[rank + 1]
 
     pos_d = torch.tensor(system.positions, device="cuda")
@@ -284,7 +264,8 @@ def main():
     def step(particles):
         # public API: build_rs (short-range planes prefetched on a side stream,
         # overlapping the long-range reduction) + dense_rs of this rank's slab
-        res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi))
+        res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi),
+                          group=dist.group.WORLD if world > 1 else None)
         g = rt.dense_rs(res.rs, limit=1 << 62, device=True, x1_range=(x1_lo, x1_hi))
         step.last = g
         return res
@@ -374,7 +355,7 @@ def main():
         exec_flops = 2.0 * n * n * 64 * float(np.sum(keff))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            stride = max(1, m["N"] // 8)
+            stride = max(1, m["N"] // 400)   # ~10-30 s of CPU work
             tc, det = reference_assembly_time(name, stride)
             cpu = {"value": n ** 3 / tc, "unit": "grid-pts/s", "cores": threads_used(),
                    "kind": "port",

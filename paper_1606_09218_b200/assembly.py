@@ -31,6 +31,7 @@ from . import _native as nat
 from .errors import ConfigError, DomainError, ResolutionError
 from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
     short_layout, storage_report, to_device, to_host, trusted_cct
+from .parallel import particle_shard, sharded_sum
 from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
@@ -345,7 +346,7 @@ def _side_stream():
     return st
 
 
-def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResult:
+def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
     ``system`` may be a reference-style :class:`ParticleSystem` /
@@ -395,8 +396,22 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResul
     if cfg.overlap_policy not in ("strict", "soft"):
         raise DomainError(f"unknown overlap policy {cfg.overlap_policy!r}")
     hist = cnt3 = None
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    p_lo, p_hi = (0, ds.count) if world == 1 else particle_shard(ds.count, dist.get_rank(group),
+                                                                  world)
     if reduce_long and cfg.reduction.max_sweeps == 0:
-        hist, cnt3 = shift_histograms(idx, z, n)
+        if world == 1:
+            hist, cnt3 = shift_histograms(idx, z, n)
+        else:
+            h_part, c_part = shift_histograms(idx[p_lo:p_hi].contiguous(),
+                                              z[p_lo:p_hi].contiguous(), n)
+            packed_h = sharded_sum(torch.cat([h_part.reshape(-1), c_part.to(torch.float64)]),
+                                   group)
+            hist = packed_h[:3 * n].reshape(3, n)
+            cnt3 = packed_h[3 * n:].to(torch.int32)
     if plan.local.rank > 0:
         lay = short_layout(idx, z, n, cnt3, ds._cache.get("node_order"))
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
@@ -481,7 +496,11 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False) -> AssemblyResul
             zs.append(Ul[:r].T.contiguous())
         ranks = tuple(ranks)
         spectrum = SvdSpectrum(values=tuple(values), vectors=tuple(zs))
-        core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
+        if world == 1:
+            core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
+        else:
+            core = sharded_sum(shifted_core(plan.table_dev, n, zs, starts[p_lo:p_hi].contiguous(),
+                                            z[p_lo:p_hi].contiguous(), plan.w_long), group)
         tucker = _trusted_tucker(core, zs)
         long_raw = None
     else:
