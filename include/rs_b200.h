@@ -103,9 +103,10 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
 /* (a10) RHOSVD core, rankred.py:151-161 (_core_from_projections) on the
  * particle-major term order of assembly.py:127-135:
  * core[(a*r2+b)*r3+c] = sum_p z[p] sum_k w[k] P1(a,p,k) P2(b,p,k) P3(c,p,k)
- * with Pl(a,p,k) = TTl[(a*n_shift + shift[3p+l])*R + k].
- * `work` holds fixed-order split partials (rs_core_workspace_bytes). */
-int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count);
+ * with Pl(a,p,k) = TTl[(a*n_shift + shift[3p+l])*R + k].  Computed as a DMMA
+ * GEMM (Khatri-Rao rows generated on the fly) with fixed-order split-K;
+ * `work` (rs_core_workspace_bytes) holds the gathered P_l and the partials. */
+int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t R);
 int rs_core(const double *TT1, const double *TT2, const double *TT3,
             int64_t r1, int64_t r2, int64_t r3, int64_t n_shift, int64_t R,
             const int64_t *shift, const double *z, const double *w, int64_t count,

@@ -43,7 +43,7 @@ SIGNATURES = {
     "rs_shift_hist": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _ptr]),
     "rs_topeig_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "rs_topeig": (_i32, [_ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
-    "rs_core_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64]),
+    "rs_core_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "rs_core": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr,
                        _ptr, _i64, _ptr]),
     "rs_assemble_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i32]),

@@ -222,18 +222,19 @@ def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
 
 
 def _node_sort(idx, n: int):
-    """One device sort of the particles by node key ``(x3, x1, x2)`` (x3-major):
+    """One device sort of the particles by node key ``(x3, x2, x1)`` (x3-major):
     returns (order, flag) with ``flag`` = the first duplicated node as a
     linear ``(x1 n + x2) n + x3`` key, or -1.  The order doubles as the x3
-    bucket order of the short-range layout."""
+    bucket order of the short-range layout (sorted by x2 inside a bucket,
+    which the row builder's binary search relies on)."""
     torch = nat._torch()
-    keys = (idx[:, 2] * n + idx[:, 0]) * n + idx[:, 1]
+    keys = (idx[:, 2] * n + idx[:, 1]) * n + idx[:, 0]
     ks, order = torch.sort(keys, stable=True)
     if idx.shape[0] < 2:
         return order, torch.full((1,), -1, dtype=torch.int64, device=idx.device)
     dup = ks[1:] == ks[:-1]
     k = ks[:-1][dup.to(torch.int64).argmax()]
-    x3, x1, x2 = k // (n * n), (k // n) % n, k % n
+    x3, x2, x1 = k // (n * n), (k // n) % n, k % n
     first = torch.where(dup.any(), (x1 * n + x2) * n + x3, ks.new_tensor(-1))
     return order, first.reshape(1)
 

@@ -220,70 +220,77 @@ __global__ void __launch_bounds__(256)
 }
 
 // ============================================================ RHOSVD core (K4b)
-constexpr int CORE_THREADS = 256;
-constexpr int CORE_EPT = 24;  // core entries per thread
-constexpr int CORE_COLS = 32; // (particle, term) columns staged per round
+// P_l[a][p*R + k] = TT_l[(a*n_shift + shift[3p+l])*R + k], mode 0 scaled by z_p w_k:
+// the projected side matrices Z_l^T U_l (rankred.py:175) of the shift-structured
+// long part, materialised once for the Khatri-Rao core GEMM.
+__global__ void k_core_gather(const double *__restrict__ TT, int r, int64_t n_shift, int R,
+                              const int64_t *__restrict__ shift, int l, const double *__restrict__ z,
+                              const double *__restrict__ w, int64_t count, double *__restrict__ P) {
+  const int64_t K = count * R;
+  const int64_t total = (int64_t)r * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e / K, col = e - a * K;
+    const int64_t p = col / R;
+    const int k = (int)(col - p * R);
+    double v = TT[(a * n_shift + shift[3 * p + l]) * R + k];
+    if (l == 0) v *= z[p] * w[k];
+    P[e] = v;
+  }
+}
 
-__global__ void __launch_bounds__(CORE_THREADS)
-    k_core_part(const double *__restrict__ TT1, const double *__restrict__ TT2,
-                const double *__restrict__ TT3, int r1, int r2, int r3, int64_t n_shift, int R,
-                const int64_t *__restrict__ shift, const double *__restrict__ z,
-                const double *__restrict__ w, int64_t count, int64_t per_split, int a_tile,
-                double *__restrict__ part) {
-  extern __shared__ __align__(16) double sm[];
-  const int a0 = blockIdx.y * a_tile;
-  const int na = min(a_tile, r1 - a0);
-  const int rs = na + r2 + r3;  // staged values per column
-  double *col = sm;             // CORE_COLS x rs
-  const int64_t p_lo = blockIdx.x * per_split;
-  const int64_t p_hi = min(count, p_lo + per_split);
-  const int entries = na * r2 * r3;
-  double acc[CORE_EPT];
-  int ia[CORE_EPT], ib[CORE_EPT], ic[CORE_EPT];
-#pragma unroll
-  for (int j = 0; j < CORE_EPT; ++j) {
-    int e = threadIdx.x + j * CORE_THREADS;
-    acc[j] = 0.0;
-    int ee = e < entries ? e : 0;
-    ia[j] = ee / (r2 * r3);
-    ib[j] = na + (ee / r3) % r2;
-    ic[j] = na + r2 + ee % r3;
-  }
-  const int64_t ncols = (p_hi - p_lo) * R;
-  for (int64_t c0 = 0; c0 < ncols; c0 += CORE_COLS) {
+// core[(a*r2+b), c] = sum_K P1[a,K] P2[b,K] P3[c,K] as a DMMA GEMM whose A tile is
+// the Khatri-Rao product generated on the fly (never materialised); split-K
+// partials reduced in fixed order by k_split_reduce.
+using TileCore = Tile<128, 64, 32, 32, 2>;
+
+__global__ void __launch_bounds__(TileCore::THREADS)
+    k_core_kr(const double *__restrict__ P1, const double *__restrict__ P2,
+              const double *__restrict__ P3, int r2, int64_t M, int64_t N, int64_t K,
+              int64_t kslice, double *__restrict__ part) {
+  using T = TileCore;
+  __shared__ __align__(16) double sA[T::BM * T::LDS];
+  __shared__ __align__(16) double sB[T::BN * T::LDS];
+  const int64_t m0 = (int64_t)blockIdx.x * T::BM, n0 = (int64_t)blockIdx.y * T::BN;
+  const int64_t k_lo = (int64_t)blockIdx.z * kslice;
+  const int64_t k_hi = k_lo + kslice < K ? k_lo + kslice : K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp / T::WARPS_N) * T::WM, wn0 = (warp % T::WARPS_N) * T::WN;
+  const int gid = lane >> 2, tig = lane & 3;
+  Acc<T> acc;
+  acc.zero();
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += T::BK) {
     __syncthreads();
-    const int nc = (int)(ncols - c0 < CORE_COLS ? ncols - c0 : CORE_COLS);
-    for (int e = threadIdx.x; e < nc * rs; e += CORE_THREADS) {
-      int cc = e / rs, v = e - cc * rs;
-      int64_t gc = c0 + cc;
-      int64_t p = p_lo + gc / R;
-      int k = (int)(gc % R);
-      double val;
-      if (v < na) {
-        int64_t s = shift[3 * p + 0];
-        val = z[p] * w[k] * TT1[((int64_t)(a0 + v) * n_shift + s) * R + k];
-      } else if (v < na + r2) {
-        int64_t s = shift[3 * p + 1];
-        val = TT2[((int64_t)(v - na) * n_shift + s) * R + k];
-      } else {
-        int64_t s = shift[3 * p + 2];
-        val = TT3[((int64_t)(v - na - r2) * n_shift + s) * R + k];
+    for (int e = threadIdx.x; e < T::BM * T::BK; e += T::THREADS) {
+      const int rr = e / T::BK, kk = e - (e / T::BK) * T::BK;
+      const int64_t row = m0 + rr, k = k0 + kk;
+      double v = 0.0;
+      if (row < M && k < k_hi) {
+        const int64_t a = row / r2, b = row - a * r2;
+        v = P1[a * K + k] * P2[b * K + k];
       }
-      col[cc * rs + v] = val;
+      sA[rr * T::LDS + kk] = v;
+    }
+    for (int e = threadIdx.x; e < T::BN * T::BK; e += T::THREADS) {
+      const int rr = e / T::BK, kk = e - (e / T::BK) * T::BK;
+      const int64_t c = n0 + rr, k = k0 + kk;
+      sB[rr * T::LDS + kk] = (c < N && k < k_hi) ? P3[c * K + k] : 0.0;
     }
     __syncthreads();
-    for (int cc = 0; cc < nc; ++cc) {
-      const double *cv = col + cc * rs;
 #pragma unroll
-      for (int j = 0; j < CORE_EPT; ++j) acc[j] = fma(cv[ia[j]] * cv[ib[j]], cv[ic[j]], acc[j]);
+    for (int kk = 0; kk < T::BK; kk += 4) {
+      double a[T::MT], b[T::NT];
+#pragma unroll
+      for (int i = 0; i < T::MT; ++i) a[i] = sA[(wm0 + i * 8 + gid) * T::LDS + kk + tig];
+#pragma unroll
+      for (int j = 0; j < T::NT; ++j) b[j] = sB[(wn0 + j * 8 + gid) * T::LDS + kk + tig];
+#pragma unroll
+      for (int i = 0; i < T::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < T::NT; ++j) dmma_884(acc.v[i][j], a[i], b[j]);
     }
   }
-  const int64_t r123 = (int64_t)r1 * r2 * r3;
-#pragma unroll
-  for (int j = 0; j < CORE_EPT; ++j) {
-    int e = threadIdx.x + j * CORE_THREADS;
-    if (e < entries) part[blockIdx.x * r123 + (int64_t)a0 * r2 * r3 + e] = acc[j];
-  }
+  store_tile<T, false>(acc, part + (int64_t)blockIdx.z * M * N, N, m0, M, n0, N);
 }
 
 __global__ void k_split_reduce(const double *__restrict__ part, int64_t splits, int64_t len,
@@ -334,14 +341,34 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Block = (plane x1, group of BG buckets) -> a (n x BG*G) column panel of A.
-// The group's particles whose window covers x1 are compacted into shared
-// memory (alpha = z w ul[x1 - c1 + g]); each thread then owns one column and
-// 8 consecutive rows, so every row segment is stored coalesced and written once.
+// Block = (plane x1, group of BG buckets).  Per bucket the copies covering x1
+// are compacted into shared memory (alpha = z w ul[x1 - c1 + g]); the bucket's
+// copies arrive sorted by x2 (node key x3-x2-x1), so a thread owning row x2
+// binary-searches the copies whose x2 window contains it and accumulates the
+// R_s values in registers, then stores its G-wide row segment once.
 constexpr int SR_THREADS = 256;
-constexpr int SR_COLS = 64;
-constexpr int SR_ROWS = 8;
-constexpr int SR_Q = 256;
+constexpr int SR_Q = 512;     // staged copies per bucket pass
+constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int base = 0, tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (w < warp) base += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return base + x - v;
+}
 
 __global__ void __launch_bounds__(SR_THREADS)
     k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
@@ -349,104 +376,80 @@ __global__ void __launch_bounds__(SR_THREADS)
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, double *__restrict__ A,
                  int64_t lda, int64_t col0) {
-  const int n_buckets = *nbp;
-  if ((int)blockIdx.y * BG >= n_buckets) return;  // grid sized for the upper bound
   extern __shared__ double sm[];
-  double *alpha = sm;                            // SR_Q * Rs
-  int *qc2 = (int *)(alpha + SR_Q * Rs);         // SR_Q
-  int *scan = qc2 + SR_Q;                        // SR_Q + 1
-  int *cst = scan + SR_Q + 1;                    // BG + 1
-  int *wsum = cst + BG + 1;                      // SR_THREADS / 32
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
+  const int W = 2 * gamma + 1;
+  double *ulT = sm;                       // Rs x W  (transposed local factor)
+  double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
+  int *qc2 = (int *)(alpha + SR_Q * Rs);  // SR_Q
+  int *wsum = qc2 + SR_Q;                 // 32
+  const int n_buckets = *nbp;
   const int b0 = blockIdx.y * BG;
-  const int nbg = min(BG, n_buckets - b0);
-  const int p_lo = bstart[b0], p_hi = bstart[b0 + nbg];
-  // lane -> (row subgroup, k): KL lanes per subgroup (KL >= G), warps
-  // round-robin over the group's buckets so a warp never mixes buckets
-  const int KL = G <= 16 ? 16 : 32;
-  const int subs_per_warp = 32 / KL;
-  const int nwarps = SR_THREADS / 32;
-  const int k = lane % KL;
-  const int j = warp % BG;
-  const int wsub = warp / BG;                      // which warp of bucket j
-  const int warps_per_bucket = (nwarps + BG - 1 - j) / BG;
-  const int rsub = wsub * subs_per_warp + lane / KL;  // row subgroup index
-  const int nsub = warps_per_bucket * subs_per_warp;
-  const bool active = j < nbg && k < G;
-  const int col = j * G + k;
-  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G + (active ? col : 0);
-  bool first = true;
-  int chunk_lo = p_lo;
-  do {
-    const int m = min(SR_Q, p_hi - chunk_lo);
-    __syncthreads();
-    // covering flags + block exclusive scan (order preserving compaction)
-    int d1 = 0;
-    bool cov = false;
-    if (tid < m) {
-      d1 = (int)(x1 - c1[chunk_lo + tid]);
-      cov = d1 >= -gamma && d1 <= gamma;
-    }
-    unsigned bal = __ballot_sync(0xffffffffu, cov);
-    int pre = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 31) wsum[warp] = pre + (cov ? 1 : 0);
-    __syncthreads();
-    int base = 0;
-    for (int w = 0; w < warp; ++w) base += wsum[w];
-    const int pos = base + pre;
-    scan[tid] = pos;
-    if (tid == SR_THREADS - 1) scan[SR_THREADS] = pos + (cov ? 1 : 0);
-    if (cov) {
-      const int p = chunk_lo + tid;
-      qc2[pos] = c2[p];
-      const double zp = zq[p];
-      const double *u1 = ul + (int64_t)(d1 + gamma) * Rs;
-      for (int kk = 0; kk < Rs; ++kk) alpha[pos * Rs + kk] = zp * wl[kk] * u1[kk];
-    }
-    __syncthreads();
-    if (tid <= nbg) {
-      int e = bstart[b0 + tid] - chunk_lo;
-      e = e < 0 ? 0 : (e > m ? m : e);
-      cst[tid] = scan[e];
-    }
-    __syncthreads();
-    const int qs = active ? cst[j] : 0, qe = active ? cst[j + 1] : 0;
-    for (int64_t rb = 0; rb < n; rb += (int64_t)SR_ROWS * nsub) {
-      const int64_t r0 = rb + rsub * SR_ROWS;
-      double acc[SR_ROWS];
+  if (b0 >= n_buckets) return;  // grid sized for the upper bound
+  const int b1 = min(b0 + BG, n_buckets);
+  const int tid = threadIdx.x;
+  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
+  for (int e = tid; e < Rs * W; e += SR_THREADS) {
+    const int k = e / W, d = e - (e / W) * W;
+    ulT[e] = ul[(int64_t)d * Rs + k];
+  }
+  __syncthreads();
+  for (int b = b0; b < b1; ++b) {
+    const int p_lo = bstart[b], p_hi = bstart[b + 1];
+    double *Ab = A + x1l * n * lda + col0 + (int64_t)b * G;
+    bool first = true;
+    int next = p_lo;
+    do {
+      // stage the copies covering x1, in order, until SR_Q are staged
+      int staged = 0;
+      while (next < p_hi && staged + SR_THREADS <= SR_Q) {
+        const int p = next + tid;
+        int d1 = 0;
+        bool cov = false;
+        if (p < p_hi) {
+          d1 = (int)(x1 - c1[p]);
+          cov = d1 >= -gamma && d1 <= gamma;
+        }
+        int tot;
+        const int pos = staged + block_exclusive_scan(cov ? 1 : 0, wsum, &tot);
+        if (cov) {
+          qc2[pos] = c2[p];
+          const double zp = zq[p];
+          for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
+        }
+        staged += tot;
+        next += SR_THREADS;
+      }
+      __syncthreads();
+      for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
+        double acc[SR_MAXR];
 #pragma unroll
-      for (int u = 0; u < SR_ROWS; ++u) acc[u] = 0.0;
-      if (active && k < Rs) {
-        for (int q = qs; q < qe; ++q) {
-          const int c2q = qc2[q];
-          if (c2q + gamma < r0 || c2q - gamma > r0 + SR_ROWS - 1) continue;
-          const double a = alpha[q * Rs + k];
-          const double *uk = ul + k;
+        for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
+        // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
+        int lo = 0, hi = staged;
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
+        }
+        for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
+          const int d = (int)(x2 - qc2[q]) + gamma;
+          const double *aq = alpha + q * Rs;
 #pragma unroll
-          for (int u = 0; u < SR_ROWS; ++u) {
-            const int64_t d = r0 + u - c2q;
-            if (d >= -gamma && d <= gamma) acc[u] = fma(a, uk[(d + gamma) * Rs], acc[u]);
-          }
+          for (int k = 0; k < SR_MAXR; ++k)
+            if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
+        }
+        double *dst = Ab + x2 * lda;
+#pragma unroll
+        for (int k = 0; k < SR_MAXR; ++k) {
+          if (k >= G) break;
+          const double v = k < Rs ? acc[k] : 0.0;
+          if (first) dst[k] = v;
+          else dst[k] += v;
         }
       }
-      if (active) {
-#pragma unroll
-        for (int u = 0; u < SR_ROWS; ++u) {
-          if (r0 + u >= n) break;
-          double *dst = Ab + (r0 + u) * lda;
-          if (k >= Rs) {
-            if (first) *dst = 0.0;
-            continue;
-          }
-          if (first) *dst = acc[u];
-          else *dst += acc[u];
-        }
-      }
-    }
-    first = false;
-    chunk_lo += SR_Q;
-  } while (chunk_lo < p_hi);
+      __syncthreads();
+      first = false;
+    } while (next < p_hi);
+  }
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -867,25 +870,21 @@ int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n,
   return check_launch("rs_shift_hist");
 }
 
-static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t *splits,
-                      int64_t *per, int *a_tile, int64_t *a_tiles) {
-  int64_t cap = (int64_t)CORE_THREADS * CORE_EPT;
-  int64_t at = std::max<int64_t>(1, std::min<int64_t>(r1, cap / std::max<int64_t>(1, r2 * r3)));
-  *a_tile = (int)at;
-  *a_tiles = ceil_div(r1, at);
-  int64_t r123 = r1 * r2 * r3;
-  int64_t by_mem = std::max<int64_t>(1, ((int64_t)1 << 27) / std::max<int64_t>(1, r123));
-  int64_t want = std::max<int64_t>(1, ceil_div(148, *a_tiles));
-  int64_t sp = std::min<int64_t>({want, by_mem, std::max<int64_t>(1, count)});
-  *per = ceil_div(count, sp);
-  *splits = ceil_div(count, *per);
+static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t K, int64_t *splits,
+                      int64_t *kslice) {
+  const int64_t tiles = ceil_div(r1 * r2, TileCore::BM) * ceil_div(r3, TileCore::BN);
+  int64_t sp = std::max<int64_t>(1, ceil_div(148 * 2, tiles));
+  sp = std::min<int64_t>(sp, std::max<int64_t>(1, K / 512));
+  int64_t ks = round_up(ceil_div(K, sp), TileCore::BK);
+  *kslice = ks;
+  *splits = ceil_div(K, ks);
 }
 
-int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count) {
-  int64_t sp, per, at_n;
-  int at;
-  core_plan(r1, r2, r3, count, &sp, &per, &at, &at_n);
-  return sp * r1 * r2 * r3 * 8;
+int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t R) {
+  int64_t sp, ks;
+  const int64_t K = count * R;
+  core_plan(r1, r2, r3, K, &sp, &ks);
+  return round_up((r1 + r2 + r3) * K * 8, 256) + sp * r1 * r2 * r3 * 8;
 }
 
 int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1, int64_t r2,
@@ -893,30 +892,31 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
             const double *w, int64_t count, double *core, void *work, int64_t work_bytes,
             void *stream) {
   RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && R >= 1 && count >= 1, "rs_core: bad shape");
-  RS_REQUIRE(r2 * r3 <= (int64_t)CORE_THREADS * CORE_EPT,
-             "rs_core: r2*r3 = %lld exceeds %d", (long long)(r2 * r3), CORE_THREADS * CORE_EPT);
-  int64_t sp, per, at_n;
-  int at;
-  core_plan(r1, r2, r3, count, &sp, &per, &at, &at_n);
-  int64_t need = sp * r1 * r2 * r3 * 8;
-  if (work_bytes < need) return fail(RS_ERR_CAPACITY, "rs_core: workspace too small");
-  size_t smem = (size_t)CORE_COLS * (at + r2 + r3) * 8;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_core_part,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "rs_core smem: %s", cudaGetErrorString(e));
-  }
+  const int64_t K = count * R;
+  if (work_bytes < rs_core_workspace_bytes(r1, r2, r3, count, R))
+    return fail(RS_ERR_CAPACITY, "rs_core: workspace too small");
+  int64_t sp, ks;
+  core_plan(r1, r2, r3, K, &sp, &ks);
   cudaStream_t s = as_stream(stream);
-  double *part = (double *)work;
-  {
-    ProfScope ps(s, "core");
-    k_core_part<<<dim3((unsigned)sp, (unsigned)at_n), CORE_THREADS, smem, s>>>(
-        TT1, TT2, TT3, (int)r1, (int)r2, (int)r3, n_shift, (int)R, shift, z, w, count, per, at,
-        part);
+  double *P1 = (double *)work;
+  double *P2 = P1 + r1 * K;
+  double *P3 = P2 + r2 * K;
+  double *part = (double *)((char *)work + round_up((r1 + r2 + r3) * K * 8, 256));
+  const double *TTs[3] = {TT1, TT2, TT3};
+  double *Ps[3] = {P1, P2, P3};
+  const int64_t rs_[3] = {r1, r2, r3};
+  int st;
+  ProfScope ps(s, "core");
+  for (int l = 0; l < 3; ++l) {
+    k_core_gather<<<grid_for(rs_[l] * K, 256), 256, 0, s>>>(TTs[l], (int)rs_[l], n_shift, (int)R,
+                                                            shift, l, z, w, count, Ps[l]);
+    if ((st = check_launch("rs_core gather"))) return st;
   }
-  int st = check_launch("rs_core part");
-  if (st) return st;
-  int64_t len = r1 * r2 * r3;
+  dim3 grid((unsigned)ceil_div(r1 * r2, TileCore::BM), (unsigned)ceil_div(r3, TileCore::BN),
+            (unsigned)sp);
+  k_core_kr<<<grid, TileCore::THREADS, 0, s>>>(P1, P2, P3, (int)r2, r1 * r2, r3, K, ks, part);
+  if ((st = check_launch("rs_core kr"))) return st;
+  const int64_t len = r1 * r2 * r3;
   k_split_reduce<<<grid_for(len, 256), 256, 0, s>>>(part, sp, len, core);
   return check_launch("rs_core reduce");
 }
@@ -968,7 +968,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(!with_long || (r1 >= 1 && r2 >= 1 && r3 >= 1 && core && V1 && V2 && V3),
              "rs_assemble_planes: bad long part");
   RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
-  RS_REQUIRE(Rs >= 0 && Rs <= 64, "rs_assemble_planes: Rs=%lld exceeds 64", (long long)Rs);
+  RS_REQUIRE(Rs >= 0 && Rs <= SR_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs,
+             SR_MAXR);
   RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
   RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
              "rs_assemble_planes: bad short part");
@@ -1000,8 +1001,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    const int BG = (int)std::max<int64_t>(1, std::min<int64_t>(4, SR_COLS / G));
-    size_t smem = (size_t)SR_Q * Rs * 8 + (size_t)(SR_Q + SR_Q + 1 + BG + 1 + SR_THREADS / 32) * 4;
+    const int BG = 8;
+    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs) * 8 + (size_t)(SR_Q + 32) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));

@@ -323,8 +323,8 @@ def short_layout(centers, z, n: int, cnt3=None, order=None) -> dict:
     synchronisation)."""
     torch = nat._torch()
     count = int(centers.shape[0])
-    if order is None:
-        order = torch.argsort(centers[:, 2], stable=True)
+    if order is None:  # x3-major, x2 inside a bucket (the row builder needs it)
+        order = torch.argsort((centers[:, 2] * n + centers[:, 1]) * n + centers[:, 0], stable=True)
     cs = centers[order]
     if cnt3 is None:
         cnt3 = torch.zeros(n, dtype=torch.int32, device="cuda").index_add_(

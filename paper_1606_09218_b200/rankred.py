@@ -158,7 +158,7 @@ def core_from_projections(weights, p1, p2, p3):
     shift = torch.stack([ar, ar, ar], dim=1).contiguous()
     one = torch.ones(1, dtype=torch.float64, device="cuda")
     L = nat.lib()
-    ws = nat.Workspace.get(L.rs_core_workspace_bytes(r1, r2, r3, K), "core")
+    ws = nat.Workspace.get(L.rs_core_workspace_bytes(r1, r2, r3, K, 1), "core")
     pp = [p.contiguous() for p in (p1, p2, p3)]
     nat.check(L.rs_core(pp[0].data_ptr(), pp[1].data_ptr(), pp[2].data_ptr(), r1, r2, r3, K, 1,
                         shift.data_ptr(), w.data_ptr(), one.data_ptr(), K, core.data_ptr(),
@@ -418,7 +418,7 @@ def shifted_core(table_dev, n: int, zs, starts, z, w_long):
     r1, r2, r3 = (int(zl.shape[1]) for zl in zs)
     count = int(z.shape[0])
     core = torch.empty((r1, r2, r3), dtype=torch.float64, device="cuda")
-    ws = nat.Workspace.get(L.rs_core_workspace_bytes(r1, r2, r3, count), "core")
+    ws = nat.Workspace.get(L.rs_core_workspace_bytes(r1, r2, r3, count, R_l), "core")
     nat.check(L.rs_core(tts[0].data_ptr(), tts[1].data_ptr(), tts[2].data_ptr(), r1, r2, r3, n,
                         R_l, starts.data_ptr(), z.data_ptr(), w_long.data_ptr(), count,
                         core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr()), "rs_core")

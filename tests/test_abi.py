@@ -26,8 +26,8 @@ def test_library_exports_header_symbols():
 def test_workspace_queries_without_gpu():
     lib = _native.load_library()
     assert lib.rs_syrk_workspace_bytes(256, 700) > 0
-    assert lib.rs_core_workspace_bytes(12, 12, 12, 1000) >= 12 ** 3 * 8
-    assert lib.rs_assemble_workspace_bytes(256, 4, 12, 50, 14) >= 4 * 256 * (12 + 50 * 14) * 8
+    assert lib.rs_core_workspace_bytes(12, 12, 12, 1000, 14) >= 12 ** 3 * 8
+    assert lib.rs_assemble_workspace_bytes(256, 4, 12, 50, 14, 3) >= 4 * 256 * (12 + 50 * 14) * 8
     assert lib.rs_sum_workspace_bytes(1000) >= 16
 
 
@@ -37,4 +37,5 @@ def test_domain_errors_without_gpu():
     assert lib.rs_syrk(None, 3, 4, 3, None, None, 0, None) == 1
     assert b"even" in lib.rs_last_error()
     assert lib.rs_assemble_planes(None, 1, 1, 1, None, None, None, 8, None, None, 99, 1,
-                                  None, None, None, None, None, 0, 0, 4, None, None, 0, None) == 1
+                                  None, None, None, None, None, None, 0, 0, 4, 3, None, None, 0,
+                                  None) == 1
