@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(SR_THREADS)
   const int W = 2 * gamma + 1;
   double *ulT = sm;                       // Rs x W  (transposed local factor)
   double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
-  int *qc2 = (int *)(alpha + SR_Q * Rs);  // SR_Q
+  double *tile = alpha + SR_Q * Rs;       // SR_THREADS x G (row tile staged for coalesced stores)
+  int *qc2 = (int *)(tile + SR_THREADS * G);  // SR_Q
   int *wsum = qc2 + SR_Q;                 // 32
   const int n_buckets = *nbp;
   const int b0 = blockIdx.y * BG;
@@ -420,31 +421,40 @@ __global__ void __launch_bounds__(SR_THREADS)
         next += SR_THREADS;
       }
       __syncthreads();
-      for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
+      for (int64_t r0 = 0; r0 < n; r0 += SR_THREADS) {
+        const int64_t x2 = r0 + tid;
         double acc[SR_MAXR];
 #pragma unroll
         for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
-        // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
-        int lo = 0, hi = staged;
-        while (lo < hi) {
-          const int m = (lo + hi) >> 1;
-          if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
-        }
-        for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
-          const int d = (int)(x2 - qc2[q]) + gamma;
-          const double *aq = alpha + q * Rs;
+        if (x2 < n) {
+          // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
+          int lo = 0, hi = staged;
+          while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
+          }
+          for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
+            const int d = (int)(x2 - qc2[q]) + gamma;
+            const double *aq = alpha + q * Rs;
 #pragma unroll
-          for (int k = 0; k < SR_MAXR; ++k)
-            if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
+            for (int k = 0; k < SR_MAXR; ++k)
+              if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
+          }
         }
-        double *dst = Ab + x2 * lda;
 #pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k) {
-          if (k >= G) break;
-          const double v = k < Rs ? acc[k] : 0.0;
-          if (first) dst[k] = v;
-          else dst[k] += v;
+        for (int k = 0; k < SR_MAXR; ++k)
+          if (k < G) tile[tid * G + k] = k < Rs ? acc[k] : 0.0;
+        __syncthreads();
+        // coalesced store of the (rows x G) tile: consecutive threads write
+        // consecutive doubles of consecutive row segments
+        const int64_t rows = n - r0 < SR_THREADS ? n - r0 : SR_THREADS;
+        for (int e = tid; e < rows * G; e += SR_THREADS) {
+          const int rr = e / G, k = e - (e / G) * G;
+          double *dst = Ab + (r0 + rr) * lda + k;
+          if (first) *dst = tile[e];
+          else *dst += tile[e];
         }
+        __syncthreads();
       }
       __syncthreads();
       first = false;
@@ -1002,7 +1012,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   if (with_short) {
     ProfScope ps(s, "short_rows");
     const int BG = 8;
-    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs) * 8 + (size_t)(SR_Q + 32) * 4;
+    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs + SR_THREADS * G) * 8 +
+                  (size_t)(SR_Q + 32) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
