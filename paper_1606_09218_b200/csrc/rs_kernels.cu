@@ -341,34 +341,15 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Block = (plane x1, group of BG buckets).  Per bucket the copies covering x1
-// are compacted into shared memory (alpha = z w ul[x1 - c1 + g]); the bucket's
-// copies arrive sorted by x2 (node key x3-x2-x1), so a thread owning row x2
-// binary-searches the copies whose x2 window contains it and accumulates the
-// R_s values in registers, then stores its G-wide row segment once.
+// Block = (plane x1, group of BG buckets).  The group's copies covering x1 are
+// compacted into shared memory in one order-preserving scan (alpha = z w
+// ul[x1 - c1 + g]); inside a bucket they ascend in x2 (node key x3-x2-x1), so
+// the thread owning row x2 binary-searches the copies whose window contains
+// it, accumulates R_s values in registers and stores its G-wide segment.
 constexpr int SR_THREADS = 256;
-constexpr int SR_Q = 512;     // staged copies per bucket pass
+constexpr int SR_Q = 256;     // staged copies per pass (== threads: one scan round)
 constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
-
-__device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += t;
-  }
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  int base = 0, tot = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    if (w < warp) base += wsum[w];
-    tot += wsum[w];
-  }
-  *total = tot;
-  __syncthreads();
-  return base + x - v;
-}
+constexpr int SR_BG = 16;     // buckets per block
 
 __global__ void __launch_bounds__(SR_THREADS)
     k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
@@ -380,86 +361,92 @@ __global__ void __launch_bounds__(SR_THREADS)
   const int W = 2 * gamma + 1;
   double *ulT = sm;                       // Rs x W  (transposed local factor)
   double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
-  double *tile = alpha + SR_Q * Rs;       // SR_THREADS x G (row tile staged for coalesced stores)
-  int *qc2 = (int *)(tile + SR_THREADS * G);  // SR_Q
-  int *wsum = qc2 + SR_Q;                 // 32
+  int *qc2 = (int *)(alpha + SR_Q * Rs);  // SR_Q
+  int *cst = qc2 + SR_Q;                  // SR_BG + 1 staged bucket starts
+  int *wsum = cst + SR_BG + 1;            // 32
   const int n_buckets = *nbp;
   const int b0 = blockIdx.y * BG;
   if (b0 >= n_buckets) return;  // grid sized for the upper bound
-  const int b1 = min(b0 + BG, n_buckets);
-  const int tid = threadIdx.x;
+  const int nbg = min(BG, n_buckets - b0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
   for (int e = tid; e < Rs * W; e += SR_THREADS) {
     const int k = e / W, d = e - (e / W) * W;
     ulT[e] = ul[(int64_t)d * Rs + k];
   }
-  __syncthreads();
-  for (int b = b0; b < b1; ++b) {
-    const int p_lo = bstart[b], p_hi = bstart[b + 1];
-    double *Ab = A + x1l * n * lda + col0 + (int64_t)b * G;
-    bool first = true;
-    int next = p_lo;
-    do {
-      // stage the copies covering x1, in order, until SR_Q are staged
-      int staged = 0;
-      while (next < p_hi && staged + SR_THREADS <= SR_Q) {
-        const int p = next + tid;
-        int d1 = 0;
-        bool cov = false;
-        if (p < p_hi) {
-          d1 = (int)(x1 - c1[p]);
-          cov = d1 >= -gamma && d1 <= gamma;
+  const int p_lo = bstart[b0], p_hi = bstart[b0 + nbg];
+  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G;
+  bool first = true;
+  int chunk = p_lo;
+  do {
+    const int m = min(SR_Q, p_hi - chunk);
+    __syncthreads();
+    int d1 = 0;
+    bool cov = false;
+    if (tid < m) {
+      d1 = (int)(x1 - c1[chunk + tid]);
+      cov = d1 >= -gamma && d1 <= gamma;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cov);
+    if (lane == 31) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int pos = __popc(bal & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += wsum[w];
+    if (cov) {
+      const int p = chunk + tid;
+      qc2[pos] = c2[p];
+      const double zp = zq[p];
+      for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
+    }
+    // staged start of each bucket: covering copies before its first particle
+    if (tid <= nbg) {
+      int e = bstart[b0 + tid] - chunk;
+      e = e < 0 ? 0 : (e > m ? m : e);
+      int cnt = 0;
+      for (int w = 0; w < (e >> 5); ++w) cnt += wsum[w];
+      if (e & 31) {
+        // covering copies among the first (e & 31) lanes of warp e>>5
+        const int p0 = chunk + (e & ~31);
+        for (int t = 0; t < (e & 31); ++t) {
+          const int dd = (int)(x1 - c1[p0 + t]);
+          cnt += (dd >= -gamma && dd <= gamma) ? 1 : 0;
         }
-        int tot;
-        const int pos = staged + block_exclusive_scan(cov ? 1 : 0, wsum, &tot);
-        if (cov) {
-          qc2[pos] = c2[p];
-          const double zp = zq[p];
-          for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
-        }
-        staged += tot;
-        next += SR_THREADS;
       }
-      __syncthreads();
-      for (int64_t r0 = 0; r0 < n; r0 += SR_THREADS) {
-        const int64_t x2 = r0 + tid;
+      cst[tid] = cnt;
+    }
+    __syncthreads();
+    for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
+      double *row = Ab + x2 * lda;
+      for (int j = 0; j < nbg; ++j) {
+        const int q0 = cst[j], q1 = cst[j + 1];
         double acc[SR_MAXR];
 #pragma unroll
         for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
-        if (x2 < n) {
-          // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
-          int lo = 0, hi = staged;
-          while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
-          }
-          for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
-            const int d = (int)(x2 - qc2[q]) + gamma;
-            const double *aq = alpha + q * Rs;
-#pragma unroll
-            for (int k = 0; k < SR_MAXR; ++k)
-              if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
-          }
+        int lo = q0, hi = q1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (qc2[mid] < x2 - gamma) lo = mid + 1; else hi = mid;
         }
+        for (int q = lo; q < q1 && qc2[q] <= x2 + gamma; ++q) {
+          const int d = (int)(x2 - qc2[q]) + gamma;
+          const double *aq = alpha + q * Rs;
 #pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k)
-          if (k < G) tile[tid * G + k] = k < Rs ? acc[k] : 0.0;
-        __syncthreads();
-        // coalesced store of the (rows x G) tile: consecutive threads write
-        // consecutive doubles of consecutive row segments
-        const int64_t rows = n - r0 < SR_THREADS ? n - r0 : SR_THREADS;
-        for (int e = tid; e < rows * G; e += SR_THREADS) {
-          const int rr = e / G, k = e - (e / G) * G;
-          double *dst = Ab + (r0 + rr) * lda + k;
-          if (first) *dst = tile[e];
-          else *dst += tile[e];
+          for (int k = 0; k < SR_MAXR; ++k)
+            if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
         }
-        __syncthreads();
+        double *dst = row + j * G;
+#pragma unroll
+        for (int k = 0; k < SR_MAXR; ++k) {
+          if (k >= G) break;
+          const double v = k < Rs ? acc[k] : 0.0;
+          if (first) dst[k] = v;
+          else dst[k] += v;
+        }
       }
-      __syncthreads();
-      first = false;
-    } while (next < p_hi);
-  }
+    }
+    first = false;
+    chunk += SR_Q;
+  } while (chunk < p_hi);
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -1011,9 +998,9 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    const int BG = 8;
-    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs + SR_THREADS * G) * 8 +
-                  (size_t)(SR_Q + 32) * 4;
+    const int BG = SR_BG;
+    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs) * 8 +
+                  (size_t)(SR_Q + SR_BG + 1 + 32) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
