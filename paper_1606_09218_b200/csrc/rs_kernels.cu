@@ -341,112 +341,117 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Block = (plane x1, group of BG buckets).  The group's copies covering x1 are
-// compacted into shared memory in one order-preserving scan (alpha = z w
-// ul[x1 - c1 + g]); inside a bucket they ascend in x2 (node key x3-x2-x1), so
-// the thread owning row x2 binary-searches the copies whose window contains
-// it, accumulates R_s values in registers and stores its G-wide segment.
+// Block = (chunk of SR_PC planes, group of SR_BG buckets).  The group's copies
+// (x1, x2, z: 16 bytes each) are staged in shared memory once per block --
+// inside a bucket they ascend in x2 (node key x3-x2-x1) -- and the local factor
+// is staged transposed.  The thread owning row x2 binary-searches each bucket
+// for the copies whose x2 window contains the row, keeps those covering the
+// plane, accumulates R_s values in registers (w_k applied once at the end) and
+// stores its G-wide row segment.  No barrier inside the plane/row loops.
 constexpr int SR_THREADS = 256;
-constexpr int SR_Q = 256;     // staged copies per pass (== threads: one scan round)
+constexpr int SR_Q = 2048;    // staged copies per pass
 constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
-constexpr int SR_BG = 16;     // buckets per block
+constexpr int SR_BG = 8;      // buckets per block
+constexpr int SR_PC = 4;      // planes per block
 
 __global__ void __launch_bounds__(SR_THREADS)
-    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
+    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
-                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, double *__restrict__ A,
-                 int64_t lda, int64_t col0) {
+                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
+                 double *__restrict__ A, int64_t lda, int64_t col0) {
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
   double *ulT = sm;                       // Rs x W  (transposed local factor)
-  double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
-  int *qc2 = (int *)(alpha + SR_Q * Rs);  // SR_Q
-  int *cst = qc2 + SR_Q;                  // SR_BG + 1 staged bucket starts
-  int *wsum = cst + SR_BG + 1;            // 32
+  double *sz = ulT + (int64_t)Rs * W;     // SR_Q charges
+  int *s1 = (int *)(sz + SR_Q);           // SR_Q x1 indices
+  int *s2 = s1 + SR_Q;                    // SR_Q x2 indices
+  int *bst = s2 + SR_Q;                   // SR_BG + 1 staged bucket starts
   const int n_buckets = *nbp;
-  const int b0 = blockIdx.y * BG;
+  const int b0 = blockIdx.y * SR_BG;
   if (b0 >= n_buckets) return;  // grid sized for the upper bound
-  const int nbg = min(BG, n_buckets - b0);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
+  const int b1 = min(b0 + SR_BG, n_buckets);
+  const int tid = threadIdx.x;
+  const int64_t pl0 = (int64_t)blockIdx.x * SR_PC;
+  const int npl = (int)(planes - pl0 < SR_PC ? planes - pl0 : SR_PC);
   for (int e = tid; e < Rs * W; e += SR_THREADS) {
     const int k = e / W, d = e - (e / W) * W;
     ulT[e] = ul[(int64_t)d * Rs + k];
   }
-  const int p_lo = bstart[b0], p_hi = bstart[b0 + nbg];
-  double *Ab = A + x1l * n * lda + col0 + (int64_t)b0 * G;
-  bool first = true;
-  int chunk = p_lo;
-  do {
-    const int m = min(SR_Q, p_hi - chunk);
-    __syncthreads();
-    int d1 = 0;
-    bool cov = false;
-    if (tid < m) {
-      d1 = (int)(x1 - c1[chunk + tid]);
-      cov = d1 >= -gamma && d1 <= gamma;
+  double wk[SR_MAXR];
+#pragma unroll
+  for (int k = 0; k < SR_MAXR; ++k) wk[k] = k < Rs ? wl[k] : 0.0;
+  int bb = b0;          // first bucket of the current pass
+  int sub_lo = -1;      // >= 0 when splitting one oversized bucket
+  while (bb < b1) {
+    // choose the pass: whole buckets while they fit, else a slice of one bucket
+    int be = bb, p_lo = bstart[bb], p_hi;
+    bool accumulate = false;
+    if (sub_lo >= 0) {
+      p_lo = sub_lo;
+      accumulate = true;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, cov);
-    if (lane == 31) wsum[warp] = __popc(bal);
-    __syncthreads();
-    int pos = __popc(bal & ((1u << lane) - 1u));
-    for (int w = 0; w < warp; ++w) pos += wsum[w];
-    if (cov) {
-      const int p = chunk + tid;
-      qc2[pos] = c2[p];
-      const double zp = zq[p];
-      for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
-    }
-    // staged start of each bucket: covering copies before its first particle
-    if (tid <= nbg) {
-      int e = bstart[b0 + tid] - chunk;
-      e = e < 0 ? 0 : (e > m ? m : e);
-      int cnt = 0;
-      for (int w = 0; w < (e >> 5); ++w) cnt += wsum[w];
-      if (e & 31) {
-        // covering copies among the first (e & 31) lanes of warp e>>5
-        const int p0 = chunk + (e & ~31);
-        for (int t = 0; t < (e & 31); ++t) {
-          const int dd = (int)(x1 - c1[p0 + t]);
-          cnt += (dd >= -gamma && dd <= gamma) ? 1 : 0;
-        }
-      }
-      cst[tid] = cnt;
+    if (sub_lo < 0 && bstart[bb + 1] - bstart[bb] <= SR_Q) {
+      while (be < b1 && bstart[be + 1] - p_lo <= SR_Q) ++be;
+      p_hi = bstart[be];
+    } else {
+      p_hi = min(bstart[bb + 1], p_lo + SR_Q);
+      be = bb + 1;
     }
     __syncthreads();
-    for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
-      double *row = Ab + x2 * lda;
-      for (int j = 0; j < nbg; ++j) {
-        const int q0 = cst[j], q1 = cst[j + 1];
-        double acc[SR_MAXR];
+    for (int e = tid; e < p_hi - p_lo; e += SR_THREADS) {
+      s1[e] = c1[p_lo + e];
+      s2[e] = c2[p_lo + e];
+      sz[e] = zq[p_lo + e];
+    }
+    if (tid <= be - bb) {
+      int v = tid == be - bb ? p_hi : bstart[bb + tid];
+      v = v < p_lo ? p_lo : v;
+      bst[tid] = v - p_lo;
+    }
+    __syncthreads();
+    for (int pl = 0; pl < npl; ++pl) {
+      const int64_t x1l = pl0 + pl, x1 = x1_lo + x1l;
+      for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
+        double *row = A + (x1l * n + x2) * lda + col0;
+        for (int j = bb; j < be; ++j) {
+          const int q0 = bst[j - bb], q1 = bst[j - bb + 1];
+          double acc[SR_MAXR];
 #pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
-        int lo = q0, hi = q1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (qc2[mid] < x2 - gamma) lo = mid + 1; else hi = mid;
-        }
-        for (int q = lo; q < q1 && qc2[q] <= x2 + gamma; ++q) {
-          const int d = (int)(x2 - qc2[q]) + gamma;
-          const double *aq = alpha + q * Rs;
+          for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
+          int lo = q0, hi = q1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s2[mid] < x2 - gamma) lo = mid + 1; else hi = mid;
+          }
+          for (int q = lo; q < q1 && s2[q] <= x2 + gamma; ++q) {
+            const int d1 = (int)(x1 - s1[q]);
+            if (d1 < -gamma || d1 > gamma) continue;
+            const int d2 = (int)(x2 - s2[q]) + gamma;
+            const double zp = sz[q];
+            const double *u1 = ulT + d1 + gamma, *u2 = ulT + d2;
 #pragma unroll
-          for (int k = 0; k < SR_MAXR; ++k)
-            if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
-        }
-        double *dst = row + j * G;
+            for (int k = 0; k < SR_MAXR; ++k)
+              if (k < Rs) acc[k] = fma(zp * u1[k * W], u2[k * W], acc[k]);
+          }
+          double *dst = row + (int64_t)j * G;
 #pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k) {
-          if (k >= G) break;
-          const double v = k < Rs ? acc[k] : 0.0;
-          if (first) dst[k] = v;
-          else dst[k] += v;
+          for (int k = 0; k < SR_MAXR; ++k) {
+            if (k >= G) break;
+            const double v = k < Rs ? wk[k] * acc[k] : 0.0;
+            if (accumulate) dst[k] += v;
+            else dst[k] = v;
+          }
         }
       }
     }
-    first = false;
-    chunk += SR_Q;
-  } while (chunk < p_hi);
+    if (p_hi < bstart[bb + 1] && be == bb + 1) {
+      sub_lo = p_hi;  // continue the oversized bucket
+    } else {
+      sub_lo = -1;
+      bb = be;
+    }
+  }
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -998,15 +1003,13 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    const int BG = SR_BG;
-    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs) * 8 +
-                  (size_t)(SR_Q + SR_BG + 1 + 32) * 4;
+    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q) * 8 + (size_t)(2 * SR_Q + SR_BG + 1) * 4;
     cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
-    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb_max, BG)), SR_THREADS, smem, s>>>(
-        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, nb_dev, n, x1_lo, A, lda,
-        r3p);
+    k_short_rows<<<dim3((unsigned)ceil_div(planes, SR_PC), (unsigned)ceil_div(nb_max, SR_BG)),
+                   SR_THREADS, smem, s>>>(ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart,
+                                          nb_dev, n, x1_lo, planes, A, lda, r3p);
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
