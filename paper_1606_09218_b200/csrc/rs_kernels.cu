@@ -341,117 +341,131 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Block = (chunk of SR_PC planes, group of SR_BG buckets).  The group's copies
-// (x1, x2, z: 16 bytes each) are staged in shared memory once per block --
-// inside a bucket they ascend in x2 (node key x3-x2-x1) -- and the local factor
-// is staged transposed.  The thread owning row x2 binary-searches each bucket
-// for the copies whose x2 window contains the row, keeps those covering the
-// plane, accumulates R_s values in registers (w_k applied once at the end) and
-// stores its G-wide row segment.  No barrier inside the plane/row loops.
+// Warp per (bucket, plane): the bucket's copies covering the plane are
+// compacted with a ballot into a per-warp index list; then, 32 rows at a time
+// (lane = row x2), groups of <= 32 covering copies load their coefficients
+// alpha = z w ul[x1 - c1 + g] into registers (one copy per lane) and are
+// broadcast with shuffles, so every FMA costs one shuffle + one shared load
+// of the local factor (staged once per block, odd row stride: conflict free).
+// No block barrier after the staging; each row segment is written once.
 constexpr int SR_THREADS = 256;
-constexpr int SR_Q = 2048;    // staged copies per pass
-constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
-constexpr int SR_BG = 8;      // buckets per block
+constexpr int SR_WARPS = SR_THREADS / 32;
+constexpr int SR_CAP = 256;   // covering copies compacted per warp pass
 constexpr int SR_PC = 4;      // planes per block
 
+template <int RS>
 __global__ void __launch_bounds__(SR_THREADS)
-    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
-                 int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int G, int gamma,
+                 const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
                  double *__restrict__ A, int64_t lda, int64_t col0) {
   extern __shared__ double sm[];
+  constexpr int S = RS | 1;  // odd row stride of the staged factor
   const int W = 2 * gamma + 1;
-  double *ulT = sm;                       // Rs x W  (transposed local factor)
-  double *sz = ulT + (int64_t)Rs * W;     // SR_Q charges
-  int *s1 = (int *)(sz + SR_Q);           // SR_Q x1 indices
-  int *s2 = s1 + SR_Q;                    // SR_Q x2 indices
-  int *bst = s2 + SR_Q;                   // SR_BG + 1 staged bucket starts
+  double *us = sm;                                   // W x S
+  int *lists = (int *)(us + (int64_t)W * S);         // SR_WARPS x SR_CAP
   const int n_buckets = *nbp;
-  const int b0 = blockIdx.y * SR_BG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b0 = blockIdx.y * SR_WARPS;
   if (b0 >= n_buckets) return;  // grid sized for the upper bound
-  const int b1 = min(b0 + SR_BG, n_buckets);
-  const int tid = threadIdx.x;
+  for (int e = threadIdx.x; e < W * RS; e += SR_THREADS) {
+    const int d = e / RS, k = e - (e / RS) * RS;
+    us[d * S + k] = ul[e];
+  }
+  __syncthreads();
+  const int b = b0 + warp;
+  if (b >= n_buckets) return;
+  int *list = lists + warp * SR_CAP;
+  double wk[RS];
+#pragma unroll
+  for (int k = 0; k < RS; ++k) wk[k] = wl[k];
+  const int p_lo = bstart[b], p_hi = bstart[b + 1];
   const int64_t pl0 = (int64_t)blockIdx.x * SR_PC;
   const int npl = (int)(planes - pl0 < SR_PC ? planes - pl0 : SR_PC);
-  for (int e = tid; e < Rs * W; e += SR_THREADS) {
-    const int k = e / W, d = e - (e / W) * W;
-    ulT[e] = ul[(int64_t)d * Rs + k];
-  }
-  double wk[SR_MAXR];
+  for (int pl = 0; pl < npl; ++pl) {
+    const int64_t x1l = pl0 + pl, x1 = x1_lo + x1l;
+    double *Ab = A + x1l * n * lda + col0 + (int64_t)b * G;
+    bool first = true;
+    int scan = p_lo;
+    do {
+      // compact the copies covering x1 (bucket order = ascending x2)
+      int cnt = 0;
+      while (scan < p_hi && cnt + 32 <= SR_CAP) {
+        const int p = scan + lane;
+        bool cov = false;
+        if (p < p_hi) {
+          const int d1 = (int)(x1 - c1[p]);
+          cov = d1 >= -gamma && d1 <= gamma;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, cov);
+        if (cov) list[cnt + __popc(bal & ((1u << lane) - 1u))] = p;
+        cnt += __popc(bal);
+        scan += 32;
+      }
+      __syncwarp();
+      for (int64_t r0 = 0; r0 < n; r0 += 32) {
+        const int64_t x2 = r0 + lane;
+        double acc[RS];
 #pragma unroll
-  for (int k = 0; k < SR_MAXR; ++k) wk[k] = k < Rs ? wl[k] : 0.0;
-  int bb = b0;          // first bucket of the current pass
-  int sub_lo = -1;      // >= 0 when splitting one oversized bucket
-  while (bb < b1) {
-    // choose the pass: whole buckets while they fit, else a slice of one bucket
-    int be = bb, p_lo = bstart[bb], p_hi;
-    bool accumulate = false;
-    if (sub_lo >= 0) {
-      p_lo = sub_lo;
-      accumulate = true;
-    }
-    if (sub_lo < 0 && bstart[bb + 1] - bstart[bb] <= SR_Q) {
-      while (be < b1 && bstart[be + 1] - p_lo <= SR_Q) ++be;
-      p_hi = bstart[be];
-    } else {
-      p_hi = min(bstart[bb + 1], p_lo + SR_Q);
-      be = bb + 1;
-    }
-    __syncthreads();
-    for (int e = tid; e < p_hi - p_lo; e += SR_THREADS) {
-      s1[e] = c1[p_lo + e];
-      s2[e] = c2[p_lo + e];
-      sz[e] = zq[p_lo + e];
-    }
-    if (tid <= be - bb) {
-      int v = tid == be - bb ? p_hi : bstart[bb + tid];
-      v = v < p_lo ? p_lo : v;
-      bst[tid] = v - p_lo;
-    }
-    __syncthreads();
-    for (int pl = 0; pl < npl; ++pl) {
-      const int64_t x1l = pl0 + pl, x1 = x1_lo + x1l;
-      for (int64_t x2 = tid; x2 < n; x2 += SR_THREADS) {
-        double *row = A + (x1l * n + x2) * lda + col0;
-        for (int j = bb; j < be; ++j) {
-          const int q0 = bst[j - bb], q1 = bst[j - bb + 1];
-          double acc[SR_MAXR];
+        for (int k = 0; k < RS; ++k) acc[k] = 0.0;
+        for (int g0 = 0; g0 < cnt; g0 += 32) {
+          const int m = min(32, cnt - g0);
+          // lane l loads the coefficients of covering copy g0 + l
+          double al[RS];
+          int c2l = INT32_MIN / 2;
+          if (lane < m) {
+            const int p = list[g0 + lane];
+            c2l = c2[p];
+            const double zp = zq[p];
+            const double *u1 = us + ((int)(x1 - c1[p]) + gamma) * S;
 #pragma unroll
-          for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
-          int lo = q0, hi = q1;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s2[mid] < x2 - gamma) lo = mid + 1; else hi = mid;
+            for (int k = 0; k < RS; ++k) al[k] = zp * wk[k] * u1[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < RS; ++k) al[k] = 0.0;
           }
-          for (int q = lo; q < q1 && s2[q] <= x2 + gamma; ++q) {
-            const int d1 = (int)(x1 - s1[q]);
-            if (d1 < -gamma || d1 > gamma) continue;
-            const int d2 = (int)(x2 - s2[q]) + gamma;
-            const double zp = sz[q];
-            const double *u1 = ulT + d1 + gamma, *u2 = ulT + d2;
+          for (int q = 0; q < m; ++q) {
+            const int c2q = __shfl_sync(0xffffffffu, c2l, q);
+            if (c2q + gamma < r0 || c2q - gamma > r0 + 31) continue;  // warp-uniform
+            const int d = (int)(x2 - c2q) + gamma;
+            const bool in = d >= 0 && d < W && x2 < n;
+            const double *u2 = us + (in ? d : 0) * S;
 #pragma unroll
-            for (int k = 0; k < SR_MAXR; ++k)
-              if (k < Rs) acc[k] = fma(zp * u1[k * W], u2[k * W], acc[k]);
-          }
-          double *dst = row + (int64_t)j * G;
-#pragma unroll
-          for (int k = 0; k < SR_MAXR; ++k) {
-            if (k >= G) break;
-            const double v = k < Rs ? wk[k] * acc[k] : 0.0;
-            if (accumulate) dst[k] += v;
-            else dst[k] = v;
+            for (int k = 0; k < RS; ++k) {
+              const double a = __shfl_sync(0xffffffffu, al[k], q);
+              if (in) acc[k] = fma(a, u2[k], acc[k]);
+            }
           }
         }
+        if (x2 < n) {
+          double *dst = Ab + x2 * lda;
+#pragma unroll
+          for (int k = 0; k < RS; ++k) {
+            if (first) dst[k] = acc[k];
+            else dst[k] += acc[k];
+          }
+          if (first)
+            for (int k = RS; k < G; ++k) dst[k] = 0.0;
+        }
       }
-    }
-    if (p_hi < bstart[bb + 1] && be == bb + 1) {
-      sub_lo = p_hi;  // continue the oversized bucket
-    } else {
-      sub_lo = -1;
-      bb = be;
-    }
+      first = false;
+    } while (scan < p_hi);
   }
+}
+
+template <int RS>
+static int launch_short_rows(dim3 grid, size_t smem, cudaStream_t s, const double *ul,
+                             const double *wl, int G, int gamma, const int32_t *c1,
+                             const int32_t *c2, const double *zq, const int32_t *bstart,
+                             const int32_t *nb, int64_t n, int64_t x1_lo, int64_t planes,
+                             double *A, int64_t lda, int64_t col0) {
+  cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows<RS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
+  k_short_rows<RS><<<grid, SR_THREADS, smem, s>>>(ul, wl, G, gamma, c1, c2, zq, bstart, nb, n,
+                                                  x1_lo, planes, A, lda, col0);
+  return check_launch("short_rows");
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -970,8 +984,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(!with_long || (r1 >= 1 && r2 >= 1 && r3 >= 1 && core && V1 && V2 && V3),
              "rs_assemble_planes: bad long part");
   RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
-  RS_REQUIRE(Rs >= 0 && Rs <= SR_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs,
-             SR_MAXR);
+  RS_REQUIRE(Rs >= 0 && Rs <= 24, "rs_assemble_planes: Rs=%lld exceeds 24", (long long)Rs);
   RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
   RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
              "rs_assemble_planes: bad short part");
@@ -1003,15 +1016,25 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q) * 8 + (size_t)(2 * SR_Q + SR_BG + 1) * 4;
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
-    k_short_rows<<<dim3((unsigned)ceil_div(planes, SR_PC), (unsigned)ceil_div(nb_max, SR_BG)),
-                   SR_THREADS, smem, s>>>(ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart,
-                                          nb_dev, n, x1_lo, planes, A, lda, r3p);
+    size_t smem = (size_t)(2 * gamma + 1) * (Rs | 1) * 8 + (size_t)SR_WARPS * SR_CAP * 4;
+    dim3 sgrid((unsigned)ceil_div(planes, SR_PC), (unsigned)ceil_div(nb_max, SR_WARPS));
+    int sst;
+#define RS_SR_CASE(R)                                                                         \
+  case R:                                                                                     \
+    sst = launch_short_rows<R>(sgrid, smem, s, ul, wl, (int)G, (int)gamma, c1, c2, zq, bstart, \
+                               nb_dev, n, x1_lo, planes, A, lda, r3p);                       \
+    break;
+    switch (Rs) {
+      RS_SR_CASE(1) RS_SR_CASE(2) RS_SR_CASE(3) RS_SR_CASE(4) RS_SR_CASE(5) RS_SR_CASE(6)
+      RS_SR_CASE(7) RS_SR_CASE(8) RS_SR_CASE(9) RS_SR_CASE(10) RS_SR_CASE(11) RS_SR_CASE(12)
+      RS_SR_CASE(13) RS_SR_CASE(14) RS_SR_CASE(15) RS_SR_CASE(16) RS_SR_CASE(17) RS_SR_CASE(18)
+      RS_SR_CASE(19) RS_SR_CASE(20) RS_SR_CASE(21) RS_SR_CASE(22) RS_SR_CASE(23) RS_SR_CASE(24)
+      default:
+        return fail(RS_ERR_UNSUPPORTED, "rs_assemble_planes: Rs=%lld", (long long)Rs);
+    }
+#undef RS_SR_CASE
+    if (sst) return sst;
   }
-  if (with_short && (st = check_launch("short_rows"))) return st;
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
                                                      with_long ? (int)r3 : 0, (int)r3p, ul,
                                                      with_short ? (int)Rs : 0, (int)G, (int)gamma,
