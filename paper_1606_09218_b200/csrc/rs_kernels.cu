@@ -364,7 +364,10 @@ __global__ void __launch_bounds__(SR_THREADS)
   constexpr int S = RS | 1;  // odd row stride of the staged factor
   const int W = 2 * gamma + 1;
   double *us = sm;                                   // W x S
-  int *lists = (int *)(us + (int64_t)W * S);         // SR_WARPS x SR_CAP
+  double *ws = us + (int64_t)W * S;                  // RS weights
+  double *lzs = ws + RS;                             // SR_WARPS x SR_CAP charges
+  int *lc2s = (int *)(lzs + SR_WARPS * SR_CAP);      // SR_WARPS x SR_CAP x2 indices
+  int *ld1s = lc2s + SR_WARPS * SR_CAP;              // SR_WARPS x SR_CAP window rows
   const int n_buckets = *nbp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = blockIdx.y * SR_WARPS;
@@ -373,13 +376,13 @@ __global__ void __launch_bounds__(SR_THREADS)
     const int d = e / RS, k = e - (e / RS) * RS;
     us[d * S + k] = ul[e];
   }
+  if (threadIdx.x < RS) ws[threadIdx.x] = wl[threadIdx.x];
   __syncthreads();
   const int b = b0 + warp;
   if (b >= n_buckets) return;
-  int *list = lists + warp * SR_CAP;
-  double wk[RS];
-#pragma unroll
-  for (int k = 0; k < RS; ++k) wk[k] = wl[k];
+  double *lz = lzs + warp * SR_CAP;
+  int *lc2 = lc2s + warp * SR_CAP;
+  int *ld1 = ld1s + warp * SR_CAP;
   const int p_lo = bstart[b], p_hi = bstart[b + 1];
   const int64_t pl0 = (int64_t)blockIdx.x * SR_PC;
   const int npl = (int)(planes - pl0 < SR_PC ? planes - pl0 : SR_PC);
@@ -394,12 +397,18 @@ __global__ void __launch_bounds__(SR_THREADS)
       while (scan < p_hi && cnt + 32 <= SR_CAP) {
         const int p = scan + lane;
         bool cov = false;
+        int d1 = 0;
         if (p < p_hi) {
-          const int d1 = (int)(x1 - c1[p]);
+          d1 = (int)(x1 - c1[p]);
           cov = d1 >= -gamma && d1 <= gamma;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, cov);
-        if (cov) list[cnt + __popc(bal & ((1u << lane) - 1u))] = p;
+        if (cov) {
+          const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
+          lz[slot] = zq[p];
+          lc2[slot] = c2[p];
+          ld1[slot] = d1 + gamma;
+        }
         cnt += __popc(bal);
         scan += 32;
       }
@@ -415,12 +424,11 @@ __global__ void __launch_bounds__(SR_THREADS)
           double al[RS];
           int c2l = INT32_MIN / 2;
           if (lane < m) {
-            const int p = list[g0 + lane];
-            c2l = c2[p];
-            const double zp = zq[p];
-            const double *u1 = us + ((int)(x1 - c1[p]) + gamma) * S;
+            c2l = lc2[g0 + lane];
+            const double zp = lz[g0 + lane];
+            const double *u1 = us + ld1[g0 + lane] * S;
 #pragma unroll
-            for (int k = 0; k < RS; ++k) al[k] = zp * wk[k] * u1[k];
+            for (int k = 0; k < RS; ++k) al[k] = zp * ws[k] * u1[k];
           } else {
 #pragma unroll
             for (int k = 0; k < RS; ++k) al[k] = 0.0;
@@ -1016,7 +1024,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    size_t smem = (size_t)(2 * gamma + 1) * (Rs | 1) * 8 + (size_t)SR_WARPS * SR_CAP * 4;
+    size_t smem = (size_t)((2 * gamma + 1) * (Rs | 1) + Rs + SR_WARPS * SR_CAP) * 8 +
+                  (size_t)2 * SR_WARPS * SR_CAP * 4;
     dim3 sgrid((unsigned)ceil_div(planes, SR_PC), (unsigned)ceil_div(nb_max, SR_WARPS));
     int sst;
 #define RS_SR_CASE(R)                                                                         \
