@@ -341,139 +341,125 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
 // Short-range rows, x3-merged: for plane x1 and x3-bucket b,
 // A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
 //                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Warp per (bucket, plane): the bucket's copies covering the plane are
-// compacted with a ballot into a per-warp index list; then, 32 rows at a time
-// (lane = row x2), groups of <= 32 covering copies load their coefficients
-// alpha = z w ul[x1 - c1 + g] into registers (one copy per lane) and are
-// broadcast with shuffles, so every FMA costs one shuffle + one shared load
-// of the local factor (staged once per block, odd row stride: conflict free).
-// No block barrier after the staging; each row segment is written once.
+// Block = (plane x1, group of BG buckets).  Per bucket the copies covering x1
+// are compacted into shared memory (alpha = z w ul[x1 - c1 + g]); the bucket's
+// copies arrive sorted by x2 (node key x3-x2-x1), so a thread owning row x2
+// binary-searches the copies whose x2 window contains it and accumulates the
+// R_s values in registers, then stores its G-wide row segment once.
 constexpr int SR_THREADS = 256;
-constexpr int SR_WARPS = SR_THREADS / 32;
-constexpr int SR_CAP = 256;   // covering copies compacted per warp pass
-constexpr int SR_PC = 4;      // planes per block
+constexpr int SR_Q = 512;     // staged copies per bucket pass
+constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
 
-template <int RS>
-__global__ void __launch_bounds__(SR_THREADS)
-    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int G, int gamma,
-                 const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
-                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
-                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
-                 double *__restrict__ A, int64_t lda, int64_t col0) {
-  extern __shared__ double sm[];
-  constexpr int S = RS | 1;  // odd row stride of the staged factor
-  const int W = 2 * gamma + 1;
-  double *us = sm;                                   // W x S
-  double *ws = us + (int64_t)W * S;                  // RS weights
-  double *lzs = ws + RS;                             // SR_WARPS x SR_CAP charges
-  int *lc2s = (int *)(lzs + SR_WARPS * SR_CAP);      // SR_WARPS x SR_CAP x2 indices
-  int *ld1s = lc2s + SR_WARPS * SR_CAP;              // SR_WARPS x SR_CAP window rows
-  const int n_buckets = *nbp;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b0 = blockIdx.y * SR_WARPS;
-  if (b0 >= n_buckets) return;  // grid sized for the upper bound
-  for (int e = threadIdx.x; e < W * RS; e += SR_THREADS) {
-    const int d = e / RS, k = e - (e / RS) * RS;
-    us[d * S + k] = ul[e];
+__device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
   }
-  if (threadIdx.x < RS) ws[threadIdx.x] = wl[threadIdx.x];
+  if (lane == 31) wsum[warp] = x;
   __syncthreads();
-  const int b = b0 + warp;
-  if (b >= n_buckets) return;
-  double *lz = lzs + warp * SR_CAP;
-  int *lc2 = lc2s + warp * SR_CAP;
-  int *ld1 = ld1s + warp * SR_CAP;
-  const int p_lo = bstart[b], p_hi = bstart[b + 1];
-  const int64_t pl0 = (int64_t)blockIdx.x * SR_PC;
-  const int npl = (int)(planes - pl0 < SR_PC ? planes - pl0 : SR_PC);
-  for (int pl = 0; pl < npl; ++pl) {
-    const int64_t x1l = pl0 + pl, x1 = x1_lo + x1l;
+  int base = 0, tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (w < warp) base += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(SR_THREADS)
+    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
+                 int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, double *__restrict__ A,
+                 int64_t lda, int64_t col0) {
+  extern __shared__ double sm[];
+  const int W = 2 * gamma + 1;
+  double *ulT = sm;                       // Rs x W  (transposed local factor)
+  double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
+  double *tile = alpha + SR_Q * Rs;       // SR_THREADS x G (row tile staged for coalesced stores)
+  int *qc2 = (int *)(tile + SR_THREADS * G);  // SR_Q
+  int *wsum = qc2 + SR_Q;                 // 32
+  const int n_buckets = *nbp;
+  const int b0 = blockIdx.y * BG;
+  if (b0 >= n_buckets) return;  // grid sized for the upper bound
+  const int b1 = min(b0 + BG, n_buckets);
+  const int tid = threadIdx.x;
+  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
+  for (int e = tid; e < Rs * W; e += SR_THREADS) {
+    const int k = e / W, d = e - (e / W) * W;
+    ulT[e] = ul[(int64_t)d * Rs + k];
+  }
+  __syncthreads();
+  for (int b = b0; b < b1; ++b) {
+    const int p_lo = bstart[b], p_hi = bstart[b + 1];
     double *Ab = A + x1l * n * lda + col0 + (int64_t)b * G;
     bool first = true;
-    int scan = p_lo;
+    int next = p_lo;
     do {
-      // compact the copies covering x1 (bucket order = ascending x2)
-      int cnt = 0;
-      while (scan < p_hi && cnt + 32 <= SR_CAP) {
-        const int p = scan + lane;
-        bool cov = false;
+      // stage the copies covering x1, in order, until SR_Q are staged
+      int staged = 0;
+      while (next < p_hi && staged + SR_THREADS <= SR_Q) {
+        const int p = next + tid;
         int d1 = 0;
+        bool cov = false;
         if (p < p_hi) {
           d1 = (int)(x1 - c1[p]);
           cov = d1 >= -gamma && d1 <= gamma;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, cov);
+        int tot;
+        const int pos = staged + block_exclusive_scan(cov ? 1 : 0, wsum, &tot);
         if (cov) {
-          const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
-          lz[slot] = zq[p];
-          lc2[slot] = c2[p];
-          ld1[slot] = d1 + gamma;
+          qc2[pos] = c2[p];
+          const double zp = zq[p];
+          for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
         }
-        cnt += __popc(bal);
-        scan += 32;
+        staged += tot;
+        next += SR_THREADS;
       }
-      __syncwarp();
-      for (int64_t r0 = 0; r0 < n; r0 += 32) {
-        const int64_t x2 = r0 + lane;
-        double acc[RS];
+      __syncthreads();
+      for (int64_t r0 = 0; r0 < n; r0 += SR_THREADS) {
+        const int64_t x2 = r0 + tid;
+        double acc[SR_MAXR];
 #pragma unroll
-        for (int k = 0; k < RS; ++k) acc[k] = 0.0;
-        for (int g0 = 0; g0 < cnt; g0 += 32) {
-          const int m = min(32, cnt - g0);
-          // lane l loads the coefficients of covering copy g0 + l
-          double al[RS];
-          int c2l = INT32_MIN / 2;
-          if (lane < m) {
-            c2l = lc2[g0 + lane];
-            const double zp = lz[g0 + lane];
-            const double *u1 = us + ld1[g0 + lane] * S;
-#pragma unroll
-            for (int k = 0; k < RS; ++k) al[k] = zp * ws[k] * u1[k];
-          } else {
-#pragma unroll
-            for (int k = 0; k < RS; ++k) al[k] = 0.0;
-          }
-          for (int q = 0; q < m; ++q) {
-            const int c2q = __shfl_sync(0xffffffffu, c2l, q);
-            if (c2q + gamma < r0 || c2q - gamma > r0 + 31) continue;  // warp-uniform
-            const int d = (int)(x2 - c2q) + gamma;
-            const bool in = d >= 0 && d < W && x2 < n;
-            const double *u2 = us + (in ? d : 0) * S;
-#pragma unroll
-            for (int k = 0; k < RS; ++k) {
-              const double a = __shfl_sync(0xffffffffu, al[k], q);
-              if (in) acc[k] = fma(a, u2[k], acc[k]);
-            }
-          }
-        }
+        for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
         if (x2 < n) {
-          double *dst = Ab + x2 * lda;
-#pragma unroll
-          for (int k = 0; k < RS; ++k) {
-            if (first) dst[k] = acc[k];
-            else dst[k] += acc[k];
+          // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
+          int lo = 0, hi = staged;
+          while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
           }
-          if (first)
-            for (int k = RS; k < G; ++k) dst[k] = 0.0;
+          for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
+            const int d = (int)(x2 - qc2[q]) + gamma;
+            const double *aq = alpha + q * Rs;
+#pragma unroll
+            for (int k = 0; k < SR_MAXR; ++k)
+              if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
+          }
         }
+#pragma unroll
+        for (int k = 0; k < SR_MAXR; ++k)
+          if (k < G) tile[tid * G + k] = k < Rs ? acc[k] : 0.0;
+        __syncthreads();
+        // coalesced store of the (rows x G) tile: consecutive threads write
+        // consecutive doubles of consecutive row segments
+        const int64_t rows = n - r0 < SR_THREADS ? n - r0 : SR_THREADS;
+        for (int e = tid; e < rows * G; e += SR_THREADS) {
+          const int rr = e / G, k = e - (e / G) * G;
+          double *dst = Ab + (r0 + rr) * lda + k;
+          if (first) *dst = tile[e];
+          else *dst += tile[e];
+        }
+        __syncthreads();
       }
+      __syncthreads();
       first = false;
-    } while (scan < p_hi);
+    } while (next < p_hi);
   }
-}
-
-template <int RS>
-static int launch_short_rows(dim3 grid, size_t smem, cudaStream_t s, const double *ul,
-                             const double *wl, int G, int gamma, const int32_t *c1,
-                             const int32_t *c2, const double *zq, const int32_t *bstart,
-                             const int32_t *nb, int64_t n, int64_t x1_lo, int64_t planes,
-                             double *A, int64_t lda, int64_t col0) {
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows<RS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
-  k_short_rows<RS><<<grid, SR_THREADS, smem, s>>>(ul, wl, G, gamma, c1, c2, zq, bstart, nb, n,
-                                                  x1_lo, planes, A, lda, col0);
-  return check_launch("short_rows");
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -992,7 +978,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(!with_long || (r1 >= 1 && r2 >= 1 && r3 >= 1 && core && V1 && V2 && V3),
              "rs_assemble_planes: bad long part");
   RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_planes: bad plane range");
-  RS_REQUIRE(Rs >= 0 && Rs <= 24, "rs_assemble_planes: Rs=%lld exceeds 24", (long long)Rs);
+  RS_REQUIRE(Rs >= 0 && Rs <= SR_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs,
+             SR_MAXR);
   RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
   RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
              "rs_assemble_planes: bad short part");
@@ -1024,26 +1011,17 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    size_t smem = (size_t)((2 * gamma + 1) * (Rs | 1) + Rs + SR_WARPS * SR_CAP) * 8 +
-                  (size_t)2 * SR_WARPS * SR_CAP * 4;
-    dim3 sgrid((unsigned)ceil_div(planes, SR_PC), (unsigned)ceil_div(nb_max, SR_WARPS));
-    int sst;
-#define RS_SR_CASE(R)                                                                         \
-  case R:                                                                                     \
-    sst = launch_short_rows<R>(sgrid, smem, s, ul, wl, (int)G, (int)gamma, c1, c2, zq, bstart, \
-                               nb_dev, n, x1_lo, planes, A, lda, r3p);                       \
-    break;
-    switch (Rs) {
-      RS_SR_CASE(1) RS_SR_CASE(2) RS_SR_CASE(3) RS_SR_CASE(4) RS_SR_CASE(5) RS_SR_CASE(6)
-      RS_SR_CASE(7) RS_SR_CASE(8) RS_SR_CASE(9) RS_SR_CASE(10) RS_SR_CASE(11) RS_SR_CASE(12)
-      RS_SR_CASE(13) RS_SR_CASE(14) RS_SR_CASE(15) RS_SR_CASE(16) RS_SR_CASE(17) RS_SR_CASE(18)
-      RS_SR_CASE(19) RS_SR_CASE(20) RS_SR_CASE(21) RS_SR_CASE(22) RS_SR_CASE(23) RS_SR_CASE(24)
-      default:
-        return fail(RS_ERR_UNSUPPORTED, "rs_assemble_planes: Rs=%lld", (long long)Rs);
-    }
-#undef RS_SR_CASE
-    if (sst) return sst;
+    const int BG = 8;
+    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs + SR_THREADS * G) * 8 +
+                  (size_t)(SR_Q + 32) * 4;
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
+    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb_max, BG)), SR_THREADS, smem, s>>>(
+        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, nb_dev, n, x1_lo, A, lda,
+        r3p);
   }
+  if (with_short && (st = check_launch("short_rows"))) return st;
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
                                                      with_long ? (int)r3 : 0, (int)r3p, ul,
                                                      with_short ? (int)Rs : 0, (int)G, (int)gamma,
