@@ -441,7 +441,9 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> A
         forced = cfg.reduction.ranks
         if forced is not None:
             b = min(n - n % 2, max(b, max(forced) + 16 + (max(forced) % 2)))
-        use_top = top_eig_supported(n, b)
+        # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
+        # straight to the full (cuSOLVER) spectrum instead of escalating twice
+        use_top = top_eig_supported(n, b) and eps_ >= 1e-7
         if use_top:
             evals, U, trace = top_eig(G, b)
         else:
