@@ -399,3 +399,76 @@ def small_case(n: int = 32, count: int = 24, seed: int = 5, kind: str = "newton"
     q = rng.uniform(-1.0, 1.0, count)
     return dict(kind=kind, lam=0.5, b=b, n=n, M=15, split_index=7, delta=1e-6, eps=1e-8,
                 positions=pos, charges=q)
+
+
+# --------------------------------------- large configs: shift-merged RHOSVD
+def shift_rhosvd(case: dict, p: dict, idx: np.ndarray, ranks=None, eps=None):
+    """RHOSVD of the long part through the exact shift regrouping
+    ``A A^T = sum_s c_s sum_k w_k^2 u_k[s:s+n] u_k[s:s+n]^T`` (rankred.py:82-126
+    restated; pinned against the literal route at C1/C2 by the tests) -- the
+    CPU oracle for C3-C5 where the literal n x N R_l side matrices are 2-44 GB.
+    Returns (core, zs, spectra, ranks)."""
+    n = case["n"]
+    nt = case["split_index"] + 1
+    table, w = p["table"], p["w"]
+    z = case["charges"]
+    starts = n - idx
+    zs, spectra = [], []
+    for l in range(3):
+        c = np.zeros(n + 1)
+        np.add.at(c, starts[:, l], z * z)
+        s_used = np.nonzero(c)[0]
+        X = np.concatenate([table[s:s + n, :nt] * (np.sqrt(c[s]) * np.abs(w[:nt]))
+                            for s in s_used], axis=1)
+        vals, vecs = np.linalg.eigh(X @ X.T)
+        order = np.argsort(vals)[::-1]
+        vals = np.clip(vals[order], 0.0, None)
+        zz = vecs[:, order]
+        lead = np.abs(zz).argmax(axis=0)
+        sg = np.sign(zz[lead, np.arange(zz.shape[1])])
+        sg[sg == 0] = 1.0
+        zs.append(zz * sg)
+        spectra.append(np.sqrt(vals))
+    if ranks is None:
+        ranks = tuple(min(eps_rank(s, eps if eps is not None else case["eps"]), n) for s in spectra)
+    zs = [zz[:, :r] for zz, r in zip(zs, ranks)]
+    # projections per shift: TT[a, s, k] = sum_i Z[i, a] T[s + i, k]
+    from numpy.lib.stride_tricks import sliding_window_view
+    tts = []
+    for zl in zs:
+        tt = np.empty((zl.shape[1], n, nt))
+        for k in range(nt):
+            H = sliding_window_view(table[:, k], n)[:n]   # H[s, i] = T[s + i, k]
+            tt[:, :, k] = zl.T @ H.T
+        tts.append(tt)
+    # core = sum_p z_p sum_k w_k TT1[:, s1p, k] (x) TT2[:, s2p, k] (x) TT3[:, s3p, k]
+    r1, r2, r3 = ranks
+    core = np.zeros((r1 * r2, r3))
+    chunk = max(1, 4096 // nt)
+    for p0 in range(0, idx.shape[0], chunk):
+        sl = slice(p0, min(idx.shape[0], p0 + chunk))
+        P1 = tts[0][:, starts[sl, 0], :] * (z[sl, None] * w[None, :nt])   # (r1, m, nt)
+        P2 = tts[1][:, starts[sl, 1], :]
+        P3 = tts[2][:, starts[sl, 2], :]
+        kr = (P1[:, None] * P2[None, :]).reshape(r1 * r2, -1)
+        core += kr @ P3.reshape(r3, -1).T
+    return core.reshape(r1, r2, r3), zs, spectra, tuple(ranks)
+
+
+def slab_grid(case: dict, planes, ranks=None):
+    """Oracle grid planes ``planes`` (list of x1 indices) for any config:
+    Tucker part from :func:`shift_rhosvd` evaluated on those planes
+    (formats.py:173-176 restricted to V1[planes]) + the C dense_cct loop on the
+    same planes (formats.py:432-445).  Returns (planes grid, ranks, gamma)."""
+    p = prologue(case["kind"], case.get("lam", 1.0), case["b"], case["n"], case["M"],
+                 case["split_index"], case["delta"])
+    idx, _, _ = snap(case["positions"], case["b"], case["n"])
+    core, zs, _, rk = shift_rhosvd(case, p, idx, ranks=ranks)
+    ul, wl = local_window(p["table"], p["w"], case["split_index"], p["gamma"])
+    L0 = local_dense(ul, wl)
+    out = []
+    for x in planes:
+        t = np.einsum("abc,a,jb,lc->jl", core, zs[0][x], zs[1], zs[2], optimize=True)
+        sh = dense_cct_c(L0, p["gamma"], idx, case["charges"], case["n"], x, x + 1)[0]
+        out.append(t + sh)
+    return np.stack(out), rk, p["gamma"]

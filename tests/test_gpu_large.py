@@ -1,0 +1,70 @@
+"""C3-C5 at full size: device grid planes vs the CPU oracle's slab restatement
+(Tucker part from the shift-regrouped RHOSVD + the C dense_cct loop on the same
+planes), ranks vs the oracle, point values / energy / forces.
+Slow: minutes of oracle CPU time per config."""
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1606_09218_b200 as rt
+from oracle import rs_oracle as orc
+from paper_1606_09218_b200 import configs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+PLANES = {"C3": [1, 200, 256, 511], "C4": [1, 511, 700, 1023], "C5": [1, 1023, 1500, 2047]}
+
+
+@pytest.fixture(scope="module", params=["C3", "C4", "C5"])
+def large(request, cuda):
+    name = request.param
+    case = configs.oracle_case(name)
+    p = orc.prologue(case["kind"], case["lam"], case["b"], case["n"], case["M"],
+                     case["split_index"], case["delta"])
+    idx, _, _ = orc.snap(case["positions"], case["b"], case["n"])
+    core, zs, spectra, ranks = orc.shift_rhosvd(case, p, idx)
+    res = rt.build_rs(configs.system(name), configs.assembly_config(name))
+    return name, case, p, idx, core, zs, ranks, res
+
+
+def test_ranks_and_gamma(large):
+    name, case, p, idx, core, zs, ranks, res = large
+    assert res.report["tucker_ranks"] == list(ranks)
+    assert res.gamma == p["gamma"]
+
+
+def test_grid_planes(large):
+    name, case, p, idx, core, zs, ranks, res = large
+    ul, wl = orc.local_window(p["table"], p["w"], case["split_index"], p["gamma"])
+    L0 = orc.local_dense(ul, wl)
+    for x in PLANES[name]:
+        t = np.einsum("abc,a,jb,lc->jl", core, zs[0][x], zs[1], zs[2], optimize=True)
+        ref = t + orc.dense_cct_c(L0, p["gamma"], idx, case["charges"], case["n"], x, x + 1)[0]
+        got = rt.dense_rs(res.rs, limit=1 << 62, x1_range=(x, x + 1))[0]
+        assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref)), (name, x)
+
+
+def test_point_values_energy_forces(large):
+    name, case, p, idx, core, zs, ranks, res = large
+    h = p["h"]
+    rng = np.random.default_rng(7)
+    sel = rng.choice(idx.shape[0], size=min(200, idx.shape[0]), replace=False)
+    # long-part values at particle nodes -> per-particle potential and rs_energy
+    ref_vals = orc.eval_tucker_many(core, zs, idx) / h ** 3
+    sv = orc.self_value(p["table"], p["w"], case["split_index"], h)
+    phi_ref = ref_vals - case["charges"] * sv
+    phi = rt.particle_potentials(res.rs, res.system, res.reference)
+    scale = np.max(np.abs(phi_ref))
+    assert np.max(np.abs(phi - phi_ref)) <= 1e-11 * scale
+    e_ref = 0.5 * math.fsum(case["charges"] * phi_ref)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        e = rt.rs_energy(res.rs, res.system, res.reference, check_separation=False)
+    assert e == pytest.approx(e_ref, rel=1e-11, abs=1e-12 * np.sum(np.abs(case["charges"] * phi_ref)))
+    # forces on a sample of particles (O(N) each in the oracle)
+    f = rt.forces_fd(res.system, res.reference, targets=sel[:20])
+    fref = np.array([orc.force_fd(idx, case["charges"], p["table"], p["w"], case["split_index"], h,
+                                  int(j)) for j in sel[:20]])
+    assert np.max(np.abs(f - fref)) <= 1e-9 * np.max(np.abs(fref))

@@ -83,3 +83,23 @@ def test_c_dense_cct_matches_numpy_loop():
     assert np.array_equal(a, b)
     c = orc.dense_cct_c(L0, g, centers, z, n, 7, 13)
     assert np.array_equal(a[7:13], c)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_shift_rhosvd_matches_literal_route(name, golden):
+    """The shift-regrouped oracle RHOSVD (used for C3-C5) reproduces the
+    reference's literal Gram route: same ranks, same long-part grid."""
+    case = configs.oracle_case(name)
+    p = orc.prologue(case["kind"], case["lam"], case["b"], case["n"], case["M"],
+                     case["split_index"], case["delta"])
+    idx, _, _ = orc.snap(case["positions"], case["b"], case["n"])
+    core, zs, spectra, ranks = orc.shift_rhosvd(case, p, idx)
+    assert list(ranks) == golden[f"case_{name}"]["ranks"]
+    z = load_npz(f"case_{name}.npz")
+    s = z["sample_idx"][:500]
+    vals = orc.eval_tucker_many(core, zs, s)
+    ref = z["long_sample"][:500]
+    assert np.max(np.abs(vals - ref)) <= 1e-12 * golden[f"case_{name}"]["grid_max_abs"]
+    sref = z["spectrum0"]
+    keep = sref > 1e-6 * sref[0]          # above the Gram-route rounding floor
+    assert np.allclose(spectra[0][:keep.size][keep], sref[keep], rtol=1e-8)
