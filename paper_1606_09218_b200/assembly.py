@@ -233,10 +233,11 @@ def _node_sort(idx, n: int):
     if idx.shape[0] < 2:
         return order, torch.full((1,), -1, dtype=torch.int64, device=idx.device)
     dup = ks[1:] == ks[:-1]
-    k = ks[:-1][dup.to(torch.int64).argmax()]
+    # (no host synchronisation: gather with a device index, device-side -1)
+    k = torch.gather(ks[:-1], 0, dup.to(torch.int64).argmax().reshape(1))
     x3, x2, x1 = k // (n * n), (k // n) % n, k % n
-    first = torch.where(dup.any(), (x1 * n + x2) * n + x3, ks.new_tensor(-1))
-    return order, first.reshape(1)
+    first = torch.where(dup.any(), (x1 * n + x2) * n + x3, torch.full_like(k, -1))
+    return order, first
 
 
 def _collision_flag(idx, n: int):
@@ -334,20 +335,44 @@ class AssemblyResult:
     report: dict
 
 
-_SIDE_STREAMS: dict = {}
+_STREAMS: dict = {}
 
 
-def _side_stream():
+def _stream(kind: str):
+    """Per-device internal streams: "side" (lowest priority) carries the
+    prefetched short-range planes, "chain" (highest priority) the
+    latency-bound long-range reduction, so its small kernels are scheduled
+    ahead of the big plane GEMM's blocks."""
     torch = nat._torch()
     dev = torch.cuda.current_device()
-    st = _SIDE_STREAMS.get(dev)
+    st = _STREAMS.get((dev, kind))
     if st is None:
-        st = torch.cuda.Stream(device=dev)
-        _SIDE_STREAMS[dev] = st
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        st = torch.cuda.Stream(device=dev, priority=(hi if kind == "chain" else lo))
+        _STREAMS[(dev, kind)] = st
     return st
 
 
+def _side_stream():
+    return _stream("side")
+
+
 def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
+    if not prefetch_dense:
+        return _build_rs(system, cfg, False, group)
+    torch = nat._torch()
+    user = torch.cuda.current_stream()
+    chain = _stream("chain")
+    chain.wait_stream(user)
+    chain.wait_stream(_stream("side"))   # earlier prefetches may still read recycled memory
+    with torch.cuda.stream(chain):
+        res = _build_rs(system, cfg, prefetch_dense, group)
+    user.wait_stream(chain)
+    return res
+
+
+def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
     ``system`` may be a reference-style :class:`ParticleSystem` /
