@@ -163,6 +163,16 @@ def reference_assembly_time(name, stride, repeats=1):
     return best
 
 
+def _ncu_traffic(name):
+    """dram read+write bytes per launch of the dominant kernel from the
+    committed ncu --set full summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+            return json.load(fh)[name]["gemm_short"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def threads_used():
     try:
         from threadpoolctl import threadpool_info
@@ -259,9 +269,10 @@ def main():
     pos_d = torch.tensor(system.positions, device="cuda")
     q_d = torch.tensor(system.charges, device="cuda")
     dp = rt.DeviceParticles(pos_d, q_d, system.box)
-    out = torch.empty((max(x1_hi - x1_lo, 1), n, n), dtype=torch.float64, device="cuda")
+    out_shape = (max(x1_hi - x1_lo, 1), n, n)
 
     def step(particles):
+        step.last = None   # free the previous grid before the next prefetch allocates
         # public API: build_rs (short-range planes prefetched on a side stream,
         # overlapping the long-range reduction) + dense_rs of this rank's slab
         res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi),
@@ -310,7 +321,7 @@ def main():
     # ---- end to end through the public API from pinned host buffers
     pos_h = torch.tensor(system.positions).pin_memory()
     q_h = torch.tensor(system.charges).pin_memory()
-    out_h = torch.empty(out.shape, dtype=torch.float64).pin_memory()
+    out_h = torch.empty(out_shape, dtype=torch.float64).pin_memory()
     pos_e = torch.empty_like(pos_d)
     q_e = torch.empty_like(q_d)
 
@@ -390,7 +401,8 @@ def main():
             "roofline": {"bound": "tensor",
                          "kernel": "k_gemm_nt<TilePlane> short-range plane GEMM (gemm_short)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": _ncu_traffic(name),
                          "peak_source": "cuBLAS DGEMM 8192^3 measured live (fp64; "
                                         "MEASURED_PEAKS.json has no FP64 entry)",
                          "algorithmic_flops_per_step": alg_flops,

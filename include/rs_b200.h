@@ -47,9 +47,21 @@ int rs_prof_query(const char *name, double *total_ms, int64_t *count);
 
 /* (a2) snap_to_grid, particles.py:302-329.
  * idx[3p+l] = clip(ceil(pos[3p+l]/h + n/2 - 0.5), 1, n-1);
- * disp[p] = |pos_p - (idx_p - n/2) h|_2 (IEEE-exact, no FMA contraction). */
+ * disp[p] = |pos_p - (idx_p - n/2) h|_2 (IEEE-exact, no FMA contraction);
+ * optional: key[p] = (x3 n + x2) n + x1 (node key, x3-major) and
+ * snapped[3p+l] = (idx - n/2) h (grid.position, particles.py:89-91). */
 int rs_snap(const double *pos, int64_t count, double h, int64_t n,
-            int64_t *idx, double *disp, void *stream);
+            int64_t *idx, double *disp, int64_t *key, double *snapped, void *stream);
+
+/* After sorting the node keys (ks ascending, order = permutation): copies in
+ * bucket order c1s/c2s/zqs, window starts starts = n - idx (assembly.py:131),
+ * *dup_pos = first i with ks[i] == ks[i+1] (UINT64_MAX if none: the
+ * ResolutionError of particles.py:319-325) and the max displacement as the
+ * bits of a non-negative double. */
+int rs_prep(const int64_t *ks, const int64_t *order, const int64_t *idx,
+            const double *z, const double *disp, int64_t count, int64_t n,
+            int32_t *c1s, int32_t *c2s, double *zqs, int64_t *starts,
+            uint64_t *dup_pos, uint64_t *dmax_bits, void *stream);
 
 /* (a7) window gather, assembly.py:111-136 (assemble_long) and the
  * shift-merged Gram operand of rankred.py:90-96.

@@ -33,7 +33,9 @@ SIGNATURES = {
     "rs_launch_count": (_i64, []),
     "rs_prof_enable": (_i32, [_i32]),
     "rs_prof_query": (_i32, [ctypes.c_char_p, ctypes.POINTER(_dbl), ctypes.POINTER(_i64)]),
-    "rs_snap": (_i32, [_ptr, _i64, _dbl, _i64, _ptr, _ptr, _ptr]),
+    "rs_snap": (_i32, [_ptr, _i64, _dbl, _i64, _ptr, _ptr, _ptr, _ptr, _ptr]),
+    "rs_prep": (_i32, [_ptr, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                       _ptr]),
     "rs_gather_windows": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64,
                                  _ptr]),
     "rs_syrk_workspace_bytes": (_i64, [_i64, _i64]),

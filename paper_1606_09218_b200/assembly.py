@@ -214,34 +214,56 @@ def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
     count = int(pos.shape[0])
     idx = torch.empty((count, 3), dtype=torch.int64, device="cuda")
     disp = torch.empty(count, dtype=torch.float64, device="cuda")
+    key = torch.empty(count, dtype=torch.int64, device="cuda")
+    snapped = torch.empty((count, 3), dtype=torch.float64, device="cuda")
     nat.check(nat.lib().rs_snap(pos.data_ptr(), count, grid.h, grid.n, idx.data_ptr(),
-                                disp.data_ptr(), nat.stream_ptr()), "rs_snap")
-    snapped = (idx.to(torch.float64) - grid.n // 2) * grid.h
-    return DeviceIndexedSystem(positions=snapped, charges=z, grid=grid, indices=idx, box=box,
-                               _disp=disp)
+                                disp.data_ptr(), key.data_ptr(), snapped.data_ptr(),
+                                nat.stream_ptr()), "rs_snap")
+    ds = DeviceIndexedSystem(positions=snapped, charges=z, grid=grid, indices=idx, box=box,
+                             _disp=disp)
+    ds._cache["key"] = key
+    return ds
 
 
-def _node_sort(idx, n: int):
-    """One device sort of the particles by node key ``(x3, x2, x1)`` (x3-major):
-    returns (order, flag) with ``flag`` = the first duplicated node as a
-    linear ``(x1 n + x2) n + x3`` key, or -1.  The order doubles as the x3
-    bucket order of the short-range layout (sorted by x2 inside a bucket,
-    which the row builder's binary search relies on)."""
+def _node_sort(ds, n: int):
+    """One device sort of the particles by node key ``(x3, x2, x1)`` (x3-major)
+    plus ``rs_prep``: the bucket-ordered copies (the x3 buckets of the
+    short-range layout, ascending x2 inside a bucket as the row builder's
+    binary search needs), window starts, the first duplicated node key (-1 if
+    none) and the max snap displacement -- all on the device, no sync."""
     torch = nat._torch()
-    keys = (idx[:, 2] * n + idx[:, 1]) * n + idx[:, 0]
-    ks, order = torch.sort(keys, stable=True)
-    if idx.shape[0] < 2:
-        return order, torch.full((1,), -1, dtype=torch.int64, device=idx.device)
-    dup = ks[1:] == ks[:-1]
-    # (no host synchronisation: gather with a device index, device-side -1)
-    k = torch.gather(ks[:-1], 0, dup.to(torch.int64).argmax().reshape(1))
-    x3, x2, x1 = k // (n * n), (k // n) % n, k % n
-    first = torch.where(dup.any(), (x1 * n + x2) * n + x3, torch.full_like(k, -1))
-    return order, first
+    idx, z = ds.indices, ds.charges
+    key = ds._cache.get("key")
+    if key is None:
+        key = (idx[:, 2] * n + idx[:, 1]) * n + idx[:, 0]
+    count = int(idx.shape[0])
+    ks, order = torch.sort(key, stable=True)
+    c1s = torch.empty(count, dtype=torch.int32, device="cuda")
+    c2s = torch.empty(count, dtype=torch.int32, device="cuda")
+    zqs = torch.empty(count, dtype=torch.float64, device="cuda")
+    starts = torch.empty((count, 3), dtype=torch.int64, device="cuda")
+    scal = torch.empty(2, dtype=torch.int64, device="cuda")
+    disp = ds._disp if ds._disp is not None and ds._disp.numel() == count else \
+        torch.zeros(count, dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().rs_prep(ks.data_ptr(), order.data_ptr(), idx.data_ptr(), z.data_ptr(),
+                                disp.data_ptr(), count, n, c1s.data_ptr(), c2s.data_ptr(),
+                                zqs.data_ptr(), starts.data_ptr(), scal.data_ptr(),
+                                scal.data_ptr() + 8, nat.stream_ptr()), "rs_prep")
+    pos = scal[0:1]
+    dup_key = torch.where(pos >= 0, torch.gather(ks, 0, pos.clamp_min(0)), torch.full_like(pos, -1))
+    prep = dict(order=order, c1=c1s, c2=c2s, zq=zqs, starts=starts, dup_key=dup_key,
+                dmax=scal[1:2].view(torch.float64))
+    ds._cache["prep"] = prep
+    return prep
 
 
-def _collision_flag(idx, n: int):
-    return _node_sort(idx, n)[1]
+def _decode_key(key: int, n: int) -> tuple:
+    """x3-major node key -> (x1, x2, x3)."""
+    return (key % n, (key // n) % n, key // (n * n))
+
+
+def _collision_flag(ds, n: int):
+    return _node_sort(ds, n)["dup_key"]
 
 
 def _as_device_system(system, grid: Grid3):
@@ -252,9 +274,7 @@ def _as_device_system(system, grid: Grid3):
         return system, None
     if isinstance(system, DeviceParticles):
         ds = snap_device(system.positions, system.charges, system.box, grid)
-        order, flag = _node_sort(ds.indices, grid.n)
-        ds._cache["node_order"] = order
-        return ds, flag
+        return ds, _node_sort(ds, grid.n)["dup_key"]
     if isinstance(system, IndexedParticleSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
@@ -269,9 +289,7 @@ def _as_device_system(system, grid: Grid3):
         return ds, None
     if isinstance(system, ParticleSystem):
         ds = snap_device(system.positions, system.charges, system.box, grid)
-        order, flag = _node_sort(ds.indices, grid.n)
-        ds._cache["node_order"] = order
-        return ds, flag
+        return ds, _node_sort(ds, grid.n)["dup_key"]
     raise ConfigError(f"expected a particle system, got {type(system).__name__}")
 
 
@@ -410,7 +428,12 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
 
     idx = ds.indices
     z = ds.charges
-    starts = (n - idx).contiguous()
+    prep = ds._cache.get("prep")
+    if prep is None:  # already-indexed input: sort/prep now (no sync)
+        prep = _node_sort(ds, n)
+        if collision is None:
+            collision = prep["dup_key"]
+    starts = prep["starts"]
     report = {"n": n, "b": grid.box.half_width, "particles": ds.count}
     if cfg.overlap_policy == "strict":
         short = CCT(local=plan.local, gamma=plan.gamma, centers=idx, weights=z,
@@ -439,7 +462,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             hist = packed_h[:3 * n].reshape(3, n)
             cnt3 = packed_h[3 * n:].to(torch.int32)
     if plan.local.rank > 0:
-        lay = short_layout(idx, z, n, cnt3, ds._cache.get("node_order"))
+        lay = short_layout(idx, z, n, cnt3, prep)
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
         short._cache["dev"] = lay
         if prefetch_dense:
@@ -474,17 +497,15 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         else:
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
-        parts = [evals.reshape(-1), trace, ds._disp.max().reshape(1),
-                 collision.to(torch.float64) if collision is not None else
-                 torch.full((1,), -1.0, dtype=torch.float64, device="cuda")]
+        parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
         packed = to_host(torch.cat(parts))
         nt_ = 3 * b + (3 if use_top else 0)
         if packed[nt_ + 1] >= 0:
-            key = int(packed[nt_ + 1])
-            node = (key // (n * n), (key // n) % n, key % n)
+            node = _decode_key(int(packed[nt_ + 1]), n)
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles "
                                   f"snap to node {node}; use a larger n")
-        ds._cache["maxdisp"] = float(packed[nt_])
+        if ds._disp is not None and ds._disp.numel() == ds.count:
+            ds._cache["maxdisp"] = float(packed[nt_])
         limit = min(n, raw_rank)
         if forced is not None:
             for r in forced:
@@ -532,11 +553,9 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         tucker = _trusted_tucker(core, zs)
         long_raw = None
     else:
-        if collision is not None and int(collision[0]) >= 0:
-            key = int(collision[0])
+        if int(collision[0]) >= 0:
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "
-                                  f"to node {(key // (n * n), (key // n) % n, key % n)}; use a "
-                                  f"larger n")
+                                  f"to node {_decode_key(int(collision[0]), n)}; use a larger n")
         long_raw = assemble_long(ref2n, ds, split_index)
         if reduce_long:
             spectrum = side_svd(long_raw)

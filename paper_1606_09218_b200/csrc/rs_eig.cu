@@ -124,48 +124,54 @@ __global__ void __launch_bounds__(ORTH_THREADS)
     for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
 }
 
-// Parallel cyclic Jacobi on the b x b symmetric T (shared memory), one CTA per
-// matrix.  Each round rotates b/2 disjoint pairs; T' = J^T T J is applied as
-// independent 2x2 block updates (one phase, in place) and V' = V J alongside.
-// Outputs eigenvalues sorted descending and eigenvectors as rows of Vt.
+// Parallel cyclic Jacobi on the B x B symmetric T (shared memory), one CTA per
+// matrix.  Each round rotates B/2 disjoint pairs (round-robin table built once
+// in shared memory); the rotations are computed by B/2 threads, then
+// T' = J^T T J is applied as independent 2x2 block updates and V' = V J in a
+// single phase.  B is a template parameter so every index computation is a
+// constant shift/mask.  Outputs eigenvalues sorted descending and the
+// matching eigenvectors as rows of Vt.
 constexpr int JAC_THREADS = 256;
 
+template <int B>
 __global__ void __launch_bounds__(JAC_THREADS)
-    k_jacobi(const double *__restrict__ Tall, int b, double *__restrict__ evals,
+    k_jacobi(const double *__restrict__ Tall, double *__restrict__ evals,
              double *__restrict__ Vtall, int max_sweeps) {
+  constexpr int LD = B + 1, HALF = B / 2;
   extern __shared__ double sm[];
-  const int ld = b + 1;
-  double *T = sm;                 // b x ld
-  double *V = T + b * ld;         // b x ld
-  double *rc = V + b * ld;        // b/2 x 2 (c, s)
-  int *rp = (int *)(rc + b);      // b/2 x 2 (p, q)
-  int *flag = rp + b;
-  const double *Tg = Tall + (int64_t)blockIdx.x * b * b;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    int r = e / b, c = e % b;
-    // symmetrise (T = W Q^T is symmetric only up to rounding)
-    T[r * ld + c] = 0.5 * (Tg[r * b + c] + Tg[c * b + r]);
-    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  double *T = sm;                       // B x LD
+  double *V = T + B * LD;               // B x LD
+  double *rc = V + B * LD;              // HALF (c), HALF (s)
+  double *rs = rc + HALF;
+  int *pairs = (int *)(rs + HALF);      // (B-1) x HALF x 2
+  int *flag = pairs + (B - 1) * B;
+  const double *Tg = Tall + (int64_t)blockIdx.x * B * B;
+  for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+    const int r = e / B, c = e % B;
+    T[r * LD + c] = 0.5 * (Tg[r * B + c] + Tg[c * B + r]);  // symmetrise
+    V[r * LD + c] = (r == c) ? 1.0 : 0.0;
+  }
+  for (int e = threadIdx.x; e < (B - 1) * HALF; e += blockDim.x) {
+    const int round = e / HALF, i = e % HALF;
+    const int a0 = i, a1 = B - 1 - i;
+    int p = a0 == 0 ? 0 : 1 + (a0 - 1 + round) % (B - 1);
+    int q = a1 == 0 ? 0 : 1 + (a1 - 1 + round) % (B - 1);
+    pairs[2 * e] = p < q ? p : q;
+    pairs[2 * e + 1] = p < q ? q : p;
   }
   __syncthreads();
   double dmax = 0.0;
-  for (int i = 0; i < b; ++i) dmax = fmax(dmax, fabs(T[i * ld + i]));
+  for (int i = 0; i < B; ++i) dmax = fmax(dmax, fabs(T[i * LD + i]));
   const double tol = 1e-18 * dmax;
-  const int half = b / 2;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
-    for (int round = 0; round < b - 1; ++round) {
-      for (int i = threadIdx.x; i < half; i += blockDim.x) {
-        int a0 = i, a1 = b - 1 - i;
-        int p = a0 == 0 ? 0 : 1 + (a0 - 1 + round) % (b - 1);
-        int q = a1 == 0 ? 0 : 1 + (a1 - 1 + round) % (b - 1);
-        if (p > q) {
-          int t = p;
-          p = q;
-          q = t;
-        }
-        const double app = T[p * ld + p], aqq = T[q * ld + q], apq = T[p * ld + q];
+    for (int round = 0; round < B - 1; ++round) {
+      const int *pr = pairs + round * B;
+      if (threadIdx.x < HALF) {
+        const int i = threadIdx.x;
+        const int p = pr[2 * i], q = pr[2 * i + 1];
+        const double app = T[p * LD + p], aqq = T[q * LD + q], apq = T[p * LD + q];
         double c = 1.0, s = 0.0;
         // rotate unless apq is rounding-level relative to the larger diagonal
         // entry or below the absolute floor (noise block of the Ritz matrix)
@@ -176,38 +182,33 @@ __global__ void __launch_bounds__(JAC_THREADS)
           s = t * c;
           *flag = 1;
         }
-        rp[2 * i] = p;
-        rp[2 * i + 1] = q;
-        rc[2 * i] = c;
-        rc[2 * i + 1] = s;
+        rc[i] = c;
+        rs[i] = s;
       }
       __syncthreads();
-      // T' = J^T T J on 2x2 blocks (row pair i, column pair j), V' = V J
-      for (int e = threadIdx.x; e < half * half + half * b; e += blockDim.x) {
-        if (e < half * half) {
-          const int i = e / half, j = e - (e / half) * half;
-          const double ci = rc[2 * i], si = rc[2 * i + 1], cj = rc[2 * j], sj = rc[2 * j + 1];
+      for (int e = threadIdx.x; e < HALF * HALF + HALF * B; e += JAC_THREADS) {
+        if (e < HALF * HALF) {
+          const int i = e / HALF, j = e % HALF;
+          const double ci = rc[i], si = rs[i], cj = rc[j], sj = rs[j];
           if (si == 0.0 && sj == 0.0) continue;
-          const int p = rp[2 * i], q = rp[2 * i + 1], u = rp[2 * j], w = rp[2 * j + 1];
-          const double tpu = T[p * ld + u], tpw = T[p * ld + w];
-          const double tqu = T[q * ld + u], tqw = T[q * ld + w];
-          // rows: r_p = c r_p - s r_q, r_q = s r_p + c r_q
+          const int p = pr[2 * i], q = pr[2 * i + 1], u = pr[2 * j], w = pr[2 * j + 1];
+          const double tpu = T[p * LD + u], tpw = T[p * LD + w];
+          const double tqu = T[q * LD + u], tqw = T[q * LD + w];
           const double ru_p = ci * tpu - si * tqu, rw_p = ci * tpw - si * tqw;
           const double ru_q = si * tpu + ci * tqu, rw_q = si * tpw + ci * tqw;
-          // columns: c_u = c c_u - s c_w, c_w = s c_u + c c_w
-          T[p * ld + u] = cj * ru_p - sj * rw_p;
-          T[p * ld + w] = sj * ru_p + cj * rw_p;
-          T[q * ld + u] = cj * ru_q - sj * rw_q;
-          T[q * ld + w] = sj * ru_q + cj * rw_q;
+          T[p * LD + u] = cj * ru_p - sj * rw_p;
+          T[p * LD + w] = sj * ru_p + cj * rw_p;
+          T[q * LD + u] = cj * ru_q - sj * rw_q;
+          T[q * LD + w] = sj * ru_q + cj * rw_q;
         } else {
-          const int f = e - half * half;
-          const int j = f / b, k = f - (f / b) * b;
-          const double c = rc[2 * j], s = rc[2 * j + 1];
+          const int f = e - HALF * HALF;
+          const int j = f / B, k = f % B;
+          const double c = rc[j], s = rs[j];
           if (s == 0.0) continue;
-          const int p = rp[2 * j], q = rp[2 * j + 1];
-          const double vp = V[k * ld + p], vq = V[k * ld + q];
-          V[k * ld + p] = c * vp - s * vq;
-          V[k * ld + q] = s * vp + c * vq;
+          const int p = pr[2 * j], q = pr[2 * j + 1];
+          const double vp = V[k * LD + p], vq = V[k * LD + q];
+          V[k * LD + p] = c * vp - s * vq;
+          V[k * LD + q] = s * vp + c * vq;
         }
       }
       __syncthreads();
@@ -215,19 +216,30 @@ __global__ void __launch_bounds__(JAC_THREADS)
     if (*flag == 0) break;
     __syncthreads();
   }
-  // sort descending (stable by index) and emit
-  double *ev = evals + (int64_t)blockIdx.x * b;
-  double *Vt = Vtall + (int64_t)blockIdx.x * b * b;
-  for (int i = threadIdx.x; i < b; i += blockDim.x) {
-    double ei = T[i * ld + i];
+  double *ev = evals + (int64_t)blockIdx.x * B;
+  double *Vt = Vtall + (int64_t)blockIdx.x * B * B;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const double ei = T[i * LD + i];
     int pos = 0;
-    for (int j = 0; j < b; ++j) {
-      double ej = T[j * ld + j];
+    for (int j = 0; j < B; ++j) {
+      const double ej = T[j * LD + j];
       pos += (ej > ei) || (ej == ei && j < i);
     }
     ev[pos] = ei;
-    for (int k = 0; k < b; ++k) Vt[(int64_t)pos * b + k] = V[k * ld + i];
+    for (int k = 0; k < B; ++k) Vt[(int64_t)pos * B + k] = V[k * LD + i];
   }
+}
+
+template <int B>
+static int launch_jacobi(const double *T, int nmat, double *evals, double *Vt, size_t reserve,
+                         cudaStream_t s) {
+  const size_t need = (size_t)(2 * B * (B + 1) + B) * 8 + (size_t)((B - 1) * B + 1) * 4;
+  const size_t smem = std::max(need, reserve);
+  cudaError_t e = cudaFuncSetAttribute((const void *)k_jacobi<B>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
+  k_jacobi<B><<<(unsigned)nmat, JAC_THREADS, smem, s>>>(T, evals, Vt, 16);
+  return check_launch("jacobi");
 }
 
 // U[m][j][i] = sum_k Vt[m][j][k] Q[m][k][i]   (b x b times b x n, per matrix)
@@ -356,7 +368,10 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   k_eig_start<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Q, (int)nmat, (int)b, n, 12345);
   if ((st = check_launch("eig start"))) return st;
   const bool q_smem = (size_t)(n + b + 32 + b * n) * 8 <= 200 * 1024;
-  size_t orth_smem = (size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8;
+  // the latency-bound single-CTA kernels reserve a whole SM (shared-memory
+  // request near the limit) so concurrent plane-GEMM blocks cannot co-reside
+  const size_t reserve = 200 * 1024;
+  size_t orth_smem = std::max<size_t>((size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8, reserve);
   const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
   if (orth_smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(orth_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -376,14 +391,16 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // Rayleigh-Ritz: W = Q G (into Y), T = W Q^T
   if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
   if ((st = gemm_batched(Y, n, b * n, Q, n, b * n, T, b, b * b, b, b, n, (int)nmat, s))) return st;
-  size_t jac_smem = (size_t)(2 * b * (b + 1) + b) * 8 + (size_t)(b + 1) * 4;
-  {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_jacobi,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem);
-    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
+  switch (b) {
+    case 16: st = launch_jacobi<16>(T, (int)nmat, evals, Vt, reserve, s); break;
+    case 32: st = launch_jacobi<32>(T, (int)nmat, evals, Vt, reserve, s); break;
+    case 48: st = launch_jacobi<48>(T, (int)nmat, evals, Vt, reserve, s); break;
+    case 64: st = launch_jacobi<64>(T, (int)nmat, evals, Vt, reserve, s); break;
+    case 96: st = launch_jacobi<96>(T, (int)nmat, evals, Vt, reserve, s); break;
+    default: return fail(RS_ERR_UNSUPPORTED, "rs_topeig: block size %lld not in {16,32,48,64,96}",
+                         (long long)b);
   }
-  k_jacobi<<<(unsigned)nmat, JAC_THREADS, jac_smem, s>>>(T, (int)b, evals, Vt, 16);
-  if ((st = check_launch("jacobi"))) return st;
+  if (st) return st;
   k_ritz<<<grid_blocks(nmat * b * n), 256, 0, s>>>(Vt, Q, (int)b, n, (int)nmat, U);
   if ((st = check_launch("ritz"))) return st;
   k_sign_rows<<<(unsigned)(nmat * b), 256, 0, s>>>(U, n);

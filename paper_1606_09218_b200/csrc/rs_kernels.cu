@@ -16,11 +16,13 @@ bool g_prof_on = false;
 
 // ===================================================================== snap
 __global__ void k_snap(const double *__restrict__ pos, int64_t count, double h, int64_t n,
-                       int64_t *__restrict__ idx, double *__restrict__ disp) {
+                       int64_t *__restrict__ idx, double *__restrict__ disp,
+                       int64_t *__restrict__ key, double *__restrict__ snapped_out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= count) return;
   const double half = (double)(n / 2);
   double sq[3];
+  int64_t ii[3];
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     double x = pos[3 * p + l];
@@ -28,11 +30,36 @@ __global__ void k_snap(const double *__restrict__ pos, int64_t count, double h, 
     int64_t i = (int64_t)ceil(f);
     i = i < 1 ? 1 : (i > n - 1 ? n - 1 : i);
     idx[3 * p + l] = i;
+    ii[l] = i;
     double snapped = __dmul_rn(__dsub_rn((double)i, half), h);
+    if (snapped_out) snapped_out[3 * p + l] = snapped;
     double d = __dsub_rn(x, snapped);
     sq[l] = __dmul_rn(d, d);
   }
   disp[p] = __dsqrt_rn(__dadd_rn(__dadd_rn(sq[0], sq[1]), sq[2]));
+  if (key) key[p] = (ii[2] * n + ii[1]) * n + ii[0];  // node key, x3-major
+}
+
+// After the key sort: copies in bucket order (c1, c2 int32, charges), window
+// starts n - idx, the first duplicated node key (or -1) and the max snap
+// displacement (as ordered bits of a non-negative double) -- deterministic.
+__global__ void k_prep(const int64_t *__restrict__ ks, const int64_t *__restrict__ order,
+                       const int64_t *__restrict__ idx, const double *__restrict__ z,
+                       const double *__restrict__ disp, int64_t count, int64_t n,
+                       int32_t *__restrict__ c1s, int32_t *__restrict__ c2s,
+                       double *__restrict__ zqs, int64_t *__restrict__ starts,
+                       unsigned long long *__restrict__ dup_pos,
+                       unsigned long long *__restrict__ dmax_bits) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t p = order[i];
+  c1s[i] = (int32_t)idx[3 * p];
+  c2s[i] = (int32_t)idx[3 * p + 1];
+  zqs[i] = z[p];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) starts[3 * i + l] = n - idx[3 * i + l];
+  if (i + 1 < count && ks[i] == ks[i + 1]) atomicMin(dup_pos, (unsigned long long)i);
+  atomicMax(dmax_bits, (unsigned long long)__double_as_longlong(disp[i]));
 }
 
 // ======================================================== window gather (K1)
@@ -773,12 +800,26 @@ int rs_prof_query(const char *name, double *total_ms, int64_t *count) {
 }
 
 int rs_snap(const double *pos, int64_t count, double h, int64_t n, int64_t *idx, double *disp,
-            void *stream) {
+            int64_t *key, double *snapped, void *stream) {
   RS_REQUIRE(count >= 0 && n >= 2 && h > 0, "rs_snap: bad arguments");
   if (count == 0) return RS_OK;
   RS_REQUIRE(pos && idx && disp, "rs_snap: null pointer");
-  k_snap<<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(pos, count, h, n, idx, disp);
+  k_snap<<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(pos, count, h, n, idx, disp,
+                                                                       key, snapped);
   return check_launch("rs_snap");
+}
+
+int rs_prep(const int64_t *ks, const int64_t *order, const int64_t *idx, const double *z,
+            const double *disp, int64_t count, int64_t n, int32_t *c1s, int32_t *c2s, double *zqs,
+            int64_t *starts, uint64_t *dup_pos, uint64_t *dmax_bits, void *stream) {
+  RS_REQUIRE(count >= 1 && n >= 2, "rs_prep: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(dup_pos, 0xff, 8, s);
+  cudaMemsetAsync(dmax_bits, 0, 8, s);
+  k_prep<<<(unsigned)ceil_div(count, 256), 256, 0, s>>>(
+      ks, order, idx, z, disp, count, n, c1s, c2s, zqs, starts, (unsigned long long *)dup_pos,
+      (unsigned long long *)dmax_bits);
+  return check_launch("rs_prep");
 }
 
 int rs_gather_windows(const double *table, int64_t ld_table, int64_t n_rows, const int64_t *starts,

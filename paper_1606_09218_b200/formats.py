@@ -317,15 +317,20 @@ def trusted_cct(local, gamma: int, centers, weights, mode_sizes, overlap_policy=
     return c
 
 
-def short_layout(centers, z, n: int, cnt3=None, order=None) -> dict:
-    """Copies sorted by x3 index (``order``: any permutation that sorts them by
-    x3; default a stable argsort) plus the device bucket table (no host
-    synchronisation)."""
+def short_layout(centers, z, n: int, cnt3=None, prep=None) -> dict:
+    """Copies in bucket order (x3-major, ascending x2 inside a bucket: the row
+    builder's binary search relies on it) plus the device bucket table; no
+    host synchronisation.  ``prep``: the output of the build path's node sort
+    (``rs_prep``), reused when given."""
     torch = nat._torch()
     count = int(centers.shape[0])
-    if order is None:  # x3-major, x2 inside a bucket (the row builder needs it)
+    if prep is None:
         order = torch.argsort((centers[:, 2] * n + centers[:, 1]) * n + centers[:, 0], stable=True)
-    cs = centers[order]
+        cs = centers[order]
+        c1, c2, zq = (cs[:, 0].to(torch.int32).contiguous(), cs[:, 1].to(torch.int32).contiguous(),
+                      z[order].contiguous())
+    else:
+        c1, c2, zq = prep["c1"], prep["c2"], prep["zq"]
     if cnt3 is None:
         cnt3 = torch.zeros(n, dtype=torch.int32, device="cuda").index_add_(
             0, centers[:, 2], torch.ones(count, dtype=torch.int32, device="cuda"))
@@ -334,8 +339,7 @@ def short_layout(centers, z, n: int, cnt3=None, order=None) -> dict:
     nb = torch.empty(1, dtype=torch.int32, device="cuda")
     nat.check(nat.lib().rs_short_layout(cnt3.data_ptr(), n, bstart.data_ptr(), bc3.data_ptr(),
                                         nb.data_ptr(), nat.stream_ptr()), "rs_short_layout")
-    return dict(c1=cs[:, 0].to(torch.int32).contiguous(), c2=cs[:, 1].to(torch.int32).contiguous(),
-                zq=z[order].contiguous(), bstart=bstart, bc3=bc3, nb=nb,
+    return dict(c1=c1, c2=c2, zq=zq, bstart=bstart, bc3=bc3, nb=nb,
                 nb_max=max(1, min(n, count)), centers=centers, z=z)
 
 
