@@ -492,8 +492,11 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
         # straight to the full (cuSOLVER) spectrum instead of escalating twice
         use_top = top_eig_supported(n, b) and eps_ >= 1e-7
+        # one subspace iteration suffices when the block reaches far below the
+        # truncation level (eps >= 1e-6 with b = 32); tighter eps: two
+        iters = TOPEIG_ITERS if eps_ >= 1e-6 else 2
         if use_top:
-            evals, U, trace = top_eig(G, b)
+            evals, U, trace = top_eig(G, b, iters)
         else:
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
@@ -518,16 +521,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             if use_top:
                 theta = packed[l * b:(l + 1) * b]
                 r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n,
-                                                        cfg.reduction.eps, fr, limit)
+                                                        cfg.reduction.eps, fr, limit, iters)
                 if r is not None and fr is not None and fr > b:
                     r = None
                 Ul = U[l] if r is not None else None
             if r is None:
                 bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 2 * TOPEIG_BLOCK else max(2 * b, 2))
                 if b and bb > b and top_eig_supported(n, bb):
-                    ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb)
+                    ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb, 2)
                     r, sv, tail, total = truncated_spectrum(to_host(ev2[0]), float(tr2[0]), n,
-                                                            cfg.reduction.eps, fr, limit)
+                                                            cfg.reduction.eps, fr, limit, 2)
                     if r is not None and (fr is None or fr <= bb):
                         Ul = U2[0]
                     else:
