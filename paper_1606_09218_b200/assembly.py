@@ -492,9 +492,9 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
         # straight to the full (cuSOLVER) spectrum instead of escalating twice
         use_top = top_eig_supported(n, b) and eps_ >= 1e-7
-        # one subspace iteration suffices when the block reaches far below the
-        # truncation level (eps >= 1e-6 with b = 32); tighter eps: two
-        iters = TOPEIG_ITERS if eps_ >= 1e-6 else 2
+        # two subspace iterations: one already gives grid parity (1e-10) at
+        # eps >= 1e-6, but point values / energies (1e-12) need the second
+        iters = TOPEIG_ITERS
         if use_top:
             evals, U, trace = top_eig(G, b, iters)
         else:

@@ -341,7 +341,7 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
 
 TOPEIG_BLOCK = 32
 TOPEIG_MAX_BLOCK = 96
-TOPEIG_ITERS = 1
+TOPEIG_ITERS = 2
 TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
 
 
