@@ -102,6 +102,14 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r,
 int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n,
                   double *c, int32_t *cnt3, void *stream);
 
+/* The three per-mode Grams of the shift-structured long part in one call
+ * (G: 3 x n x n): operands X_l[:, (s,k)] = sqrt(c[l][s]) |w_k| T[s:s+n, k]
+ * (c from rs_shift_hist, wabs = |w_k|, k < R) and X_l X_l^T on DMMA. */
+int64_t rs_gram_shifted_workspace_bytes(int64_t n, int64_t R);
+int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R,
+                    const double *c, const double *wabs, double *G, void *work,
+                    int64_t work_bytes, void *stream);
+
 /* Top-b eigenpairs of nmat symmetric PSD n x n matrices G (contiguous), for
  * the eigen-truncation of rankred.py:90-96/129-148: block subspace iteration
  * (iters steps, CGS2), Rayleigh-Ritz, cyclic Jacobi.  evals (nmat x b,
@@ -111,6 +119,12 @@ int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b);
 int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters,
               double *evals, double *U, double *trace, void *work, int64_t work_bytes,
               void *stream);
+
+/* The three modes of rs_shift_project in one launch (Z_l contiguous n x r_l). */
+int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3,
+                      int64_t r1, int64_t r2, int64_t r3, int64_t n,
+                      const double *table, int64_t ld_table, int64_t R, int64_t n_shift,
+                      double *TT1, double *TT2, double *TT3, void *stream);
 
 /* (a10) RHOSVD core, rankred.py:151-161 (_core_from_projections) on the
  * particle-major term order of assembly.py:127-135:

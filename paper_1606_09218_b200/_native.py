@@ -40,11 +40,15 @@ SIGNATURES = {
                                  _ptr]),
     "rs_syrk_workspace_bytes": (_i64, [_i64, _i64]),
     "rs_syrk": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr]),
+    "rs_gram_shifted_workspace_bytes": (_i64, [_i64, _i64]),
+    "rs_gram_shifted": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
     "rs_gemm_nt": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
     "rs_shift_project": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr]),
     "rs_shift_hist": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _ptr]),
     "rs_topeig_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "rs_topeig": (_i32, [_ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
+    "rs_shift_project3": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _i64,
+                                 _ptr, _ptr, _ptr, _ptr]),
     "rs_core_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "rs_core": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _i64, _ptr,
                        _ptr, _i64, _ptr]),

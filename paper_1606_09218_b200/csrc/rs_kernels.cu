@@ -81,6 +81,28 @@ __global__ void k_gather(const double *__restrict__ table, int64_t ld_table, int
   }
 }
 
+// Shift-merged Gram operands of the three modes in one launch:
+// X[l][i][s*R + k] = sqrt(c[l][s]) |w_k| T[(s + i)*ld + k]   (s < n, k < R)
+__global__ void k_gram_operands(const double *__restrict__ table, int64_t ld_table, int64_t n,
+                                int64_t R, const double *__restrict__ c,
+                                const double *__restrict__ wabs, double *__restrict__ X,
+                                int64_t ldx) {
+  const int64_t cols = n * R;
+  const int64_t total = 3 * n * ldx;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = e / (n * ldx), rem = e - l * n * ldx;
+    const int64_t i = rem / ldx, col = rem - i * ldx;
+    double v = 0.0;
+    if (col < cols) {
+      const int64_t sft = col / R, k = col - sft * R;
+      const double cs = c[l * n + sft];
+      if (cs != 0.0) v = sqrt(cs) * wabs[k] * table[(sft + i) * ld_table + k];
+    }
+    X[e] = v;
+  }
+}
+
 // ============================================================ GEMM kernels
 using TilePlane = Tile<128, 64, 32, 32, 3>;  // plane GEMM / generic NT GEMM
 using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
@@ -119,9 +141,11 @@ __device__ __forceinline__ void tri_decode(int64_t t, int64_t &bi, int64_t &bj) 
 // Lower-triangle Gram tiles, one K slice per blockIdx.y, partials to `part`.
 __global__ void __launch_bounds__(TileSyrk::THREADS)
     k_syrk_part(const double *__restrict__ A, int64_t lda, int64_t n, int64_t K, int64_t kslice,
-                double *__restrict__ part) {
+                double *__restrict__ part, int64_t a_stride, int64_t part_stride) {
   using T = TileSyrk;
   extern __shared__ __align__(16) double smem[];
+  A += blockIdx.z * a_stride;
+  part += blockIdx.z * part_stride;
   int64_t bi, bj;
   tri_decode(blockIdx.x, bi, bj);
   const int64_t k_lo = (int64_t)blockIdx.y * kslice;
@@ -134,9 +158,11 @@ __global__ void __launch_bounds__(TileSyrk::THREADS)
 }
 
 __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, int64_t ntiles,
-                              int64_t n, double *__restrict__ G) {
+                              int64_t n, double *__restrict__ G, int64_t part_stride) {
   using T = TileSyrk;
   const int64_t per = T::BM * T::BN;
+  part += blockIdx.z * part_stride;
+  G += blockIdx.z * n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntiles * per;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e / per, loc = e - t * per;
@@ -157,10 +183,18 @@ __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, i
 constexpr int SP_SHIFTS = 32;
 constexpr int SP_ICH = 64;  // Z rows staged per round
 
+struct Proj3 {
+  const double *Z[3];
+  double *TT[3];
+  int64_t r[3];
+};
+
 __global__ void __launch_bounds__(256)
-    k_shift_project(const double *__restrict__ Z, int64_t ldz, int64_t n, int64_t r,
-                    const double *__restrict__ T, int64_t ld_table, int64_t R, int64_t n_shift,
-                    double *__restrict__ TT) {
+    k_shift_project(Proj3 pj, int64_t n, const double *__restrict__ T, int64_t ld_table, int64_t R,
+                    int64_t n_shift) {
+  const double *__restrict__ Z = pj.Z[blockIdx.z];
+  double *__restrict__ TT = pj.TT[blockIdx.z];
+  const int64_t r = pj.r[blockIdx.z], ldz = r;
   extern __shared__ double win[];      // n + SP_SHIFTS, then SP_ICH * r
   double *zs = win + n + SP_SHIFTS;
   const int64_t s0 = (int64_t)blockIdx.x * SP_SHIFTS;
@@ -286,24 +320,46 @@ __global__ void __launch_bounds__(TileCore::THREADS)
   const int gid = lane >> 2, tig = lane & 3;
   Acc<T> acc;
   acc.zero();
-  for (int64_t k0 = k_lo; k0 < k_hi; k0 += T::BK) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < T::BM * T::BK; e += T::THREADS) {
-      const int rr = e / T::BK, kk = e - (e / T::BK) * T::BK;
+  // register double buffer: the next chunk's Khatri-Rao and P3 values are
+  // fetched from L2 while the current chunk's DMMAs run
+  constexpr int EA = T::BM * T::BK / T::THREADS, EB = T::BN * T::BK / T::THREADS;
+  double ra[EA], rb[EB];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int u = 0; u < EA; ++u) {
+      const int e = threadIdx.x + u * T::THREADS;
+      const int rr = e / T::BK, kk = e % T::BK;
       const int64_t row = m0 + rr, k = k0 + kk;
       double v = 0.0;
       if (row < M && k < k_hi) {
         const int64_t a = row / r2, b = row - a * r2;
         v = P1[a * K + k] * P2[b * K + k];
       }
-      sA[rr * T::LDS + kk] = v;
+      ra[u] = v;
     }
-    for (int e = threadIdx.x; e < T::BN * T::BK; e += T::THREADS) {
-      const int rr = e / T::BK, kk = e - (e / T::BK) * T::BK;
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int e = threadIdx.x + u * T::THREADS;
+      const int rr = e / T::BK, kk = e % T::BK;
       const int64_t c = n0 + rr, k = k0 + kk;
-      sB[rr * T::LDS + kk] = (c < N && k < k_hi) ? P3[c * K + k] : 0.0;
+      rb[u] = (c < N && k < k_hi) ? P3[c * K + k] : 0.0;
+    }
+  };
+  if (k_lo < k_hi) fetch(k_lo);
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += T::BK) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < EA; ++u) {
+      const int e = threadIdx.x + u * T::THREADS;
+      sA[(e / T::BK) * T::LDS + e % T::BK] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int e = threadIdx.x + u * T::THREADS;
+      sB[(e / T::BK) * T::LDS + e % T::BK] = rb[u];
     }
     __syncthreads();
+    if (k0 + T::BK < k_hi) fetch(k0 + T::BK);
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4) {
       double a[T::MT], b[T::NT];
@@ -870,13 +926,50 @@ int rs_syrk(const double *A, int64_t lda, int64_t n, int64_t K, double *G, void 
   double *part = (double *)work;
   {
     ProfScope ps(s, "syrk");
-    k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
-        A, lda, n, K, ks, part);
+      k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
+        A, lda, n, K, ks, part, 0, 0);
   }
   if ((st = check_launch("rs_syrk part"))) return st;
   int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
-  k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G);
+  k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G, 0);
   return check_launch("rs_syrk reduce");
+}
+
+int64_t rs_gram_shifted_workspace_bytes(int64_t n, int64_t R) {
+  const int64_t ldx = round_up(n * R, 2);
+  int64_t ks;
+  const int64_t sp = syrk_splits(n, ldx, &ks);
+  const int64_t nt = ceil_div(n, TileSyrk::BM);
+  return round_up(3 * n * ldx * 8, 256) + 3 * sp * (nt * (nt + 1) / 2) * TileSyrk::BM * TileSyrk::BN * 8;
+}
+
+int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R, const double *c,
+                    const double *wabs, double *G, void *work, int64_t work_bytes, void *stream) {
+  RS_REQUIRE(n >= 2 && R >= 1 && ld_table >= R, "rs_gram_shifted: bad shape");
+  if (work_bytes < rs_gram_shifted_workspace_bytes(n, R))
+    return fail(RS_ERR_CAPACITY, "rs_gram_shifted: workspace too small");
+  const int64_t ldx = round_up(n * R, 2);
+  int64_t ks;
+  const int64_t sp = syrk_splits(n, ldx, &ks);
+  const int64_t nt = ceil_div(n, TileSyrk::BM), ntp = nt * (nt + 1) / 2;
+  const int64_t part_stride = sp * ntp * TileSyrk::BM * TileSyrk::BN;
+  double *X = (double *)work;
+  double *part = (double *)((char *)work + round_up(3 * n * ldx * 8, 256));
+  cudaStream_t s = as_stream(stream);
+  int st;
+  k_gram_operands<<<grid_for(3 * n * ldx, 256), 256, 0, s>>>(table, ld_table, n, R, c, wabs, X,
+                                                              ldx);
+  if ((st = check_launch("gram operands"))) return st;
+  if ((st = set_smem<TileSyrk>((const void *)k_syrk_part))) return st;
+  {
+    ProfScope ps(s, "syrk");
+    k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp, 3), TileSyrk::THREADS, TileSyrk::SMEM_BYTES,
+                  s>>>(X, ldx, n, ldx, ks, part, n * ldx, part_stride);
+  }
+  if ((st = check_launch("gram syrk"))) return st;
+  const int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
+  k_syrk_reduce<<<dim3(grid_for(tot, 256), 1, 3), 256, 0, s>>>(part, sp, ntp, n, G, part_stride);
+  return check_launch("gram reduce");
 }
 
 int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
@@ -904,13 +997,35 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const d
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
   }
+  RS_REQUIRE(ldz == r, "rs_shift_project: Z must be contiguous (ldz == r)");
+  Proj3 pj{{Z, Z, Z}, {TT, TT, TT}, {r, r, r}};
   {
     ProfScope ps(as_stream(stream), "shift_project");
-    dim3 grid((unsigned)ceil_div(n_shift, SP_SHIFTS), (unsigned)R);
-    k_shift_project<<<grid, 256, smem, as_stream(stream)>>>(Z, ldz, n, r, table, ld_table, R,
-                                                             n_shift, TT);
+    dim3 grid((unsigned)ceil_div(n_shift, SP_SHIFTS), (unsigned)R, 1);
+    k_shift_project<<<grid, 256, smem, as_stream(stream)>>>(pj, n, table, ld_table, R, n_shift);
   }
   return check_launch("rs_shift_project");
+}
+
+int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3, int64_t r1, int64_t r2,
+                      int64_t r3, int64_t n, const double *table, int64_t ld_table, int64_t R,
+                      int64_t n_shift, double *TT1, double *TT2, double *TT3, void *stream) {
+  RS_REQUIRE(n >= 1 && r1 >= 1 && r2 >= 1 && r3 >= 1 && R >= 1 && n_shift >= 1 && n_shift <= n &&
+                 ld_table >= R,
+             "rs_shift_project3: bad shape");
+  size_t smem = (size_t)(n + SP_SHIFTS + SP_ICH * 32) * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_shift_project,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
+  }
+  Proj3 pj{{Z1, Z2, Z3}, {TT1, TT2, TT3}, {r1, r2, r3}};
+  {
+    ProfScope ps(as_stream(stream), "shift_project");
+    dim3 grid((unsigned)ceil_div(n_shift, SP_SHIFTS), (unsigned)R, 3);
+    k_shift_project<<<grid, 256, smem, as_stream(stream)>>>(pj, n, table, ld_table, R, n_shift);
+  }
+  return check_launch("rs_shift_project3");
 }
 
 int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n, double *c,
@@ -925,7 +1040,7 @@ static void core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t K, int64_t *sp
                       int64_t *kslice) {
   const int64_t tiles = ceil_div(r1 * r2, TileCore::BM) * ceil_div(r3, TileCore::BN);
   int64_t sp = std::max<int64_t>(1, ceil_div(148 * 2, tiles));
-  sp = std::min<int64_t>(sp, std::max<int64_t>(1, K / 512));
+  sp = std::min<int64_t>(sp, std::max<int64_t>(1, K / 64));
   int64_t ks = round_up(ceil_div(K, sp), TileCore::BK);
   *kslice = ks;
   *splits = ceil_div(K, ks);

@@ -318,24 +318,15 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
     """Per-mode Grams of the |z w|-weighted long side matrices from the shift
     histograms: ``X_l[:, s R_l + k] = sqrt(c_ls) |w_k| T[s:s+n, k]`` for every
     start s in [0, n) (empty shifts give zero columns), ``G_l = X_l X_l^T`` on
-    DMMA.  Returns (3, n, n)."""
+    DMMA -- all three modes in one ``rs_gram_shifted`` call.  Returns (3, n, n)."""
     torch = nat._torch()
     R_l = int(w_long_abs.shape[0])
-    k = n * R_l
-    kp = k + (k % 2)
-    starts = torch.arange(n, dtype=torch.int64, device="cuda")
-    gs = torch.sqrt(c)
     G = torch.empty((3, n, n), dtype=torch.float64, device="cuda")
-    x = torch.zeros((n, kp), dtype=torch.float64, device="cuda") if kp != k else \
-        torch.empty((n, kp), dtype=torch.float64, device="cuda")
     L = nat.lib()
-    ws = nat.Workspace.get(L.rs_syrk_workspace_bytes(n, kp), "syrk")
-    for l in range(3):
-        nat.check(L.rs_gather_windows(table_dev.data_ptr(), table_dev.shape[1], n, starts.data_ptr(),
-                                      n, R_l, 0, gs[l].data_ptr(), w_long_abs.data_ptr(),
-                                      x.data_ptr(), kp, nat.stream_ptr()), "rs_gather_windows")
-        nat.check(L.rs_syrk(x.data_ptr(), kp, n, kp, G[l].data_ptr(), ws.data_ptr(), ws.numel(),
-                            nat.stream_ptr()), "rs_syrk")
+    ws = nat.Workspace.get(L.rs_gram_shifted_workspace_bytes(n, R_l), "syrk")
+    nat.check(L.rs_gram_shifted(table_dev.data_ptr(), table_dev.shape[1], n, R_l, c.data_ptr(),
+                                w_long_abs.data_ptr(), G.data_ptr(), ws.data_ptr(), ws.numel(),
+                                nat.stream_ptr()), "rs_gram_shifted")
     return G
 
 
@@ -414,13 +405,12 @@ def shifted_core(table_dev, n: int, zs, starts, z, w_long):
     R_l = int(w_long.shape[0])
     ld = int(table_dev.shape[1])
     L = nat.lib()
-    tts = []
-    for zl in zs:
-        r = int(zl.shape[1])
-        tt = torch.empty((r, n, R_l), dtype=torch.float64, device="cuda")
-        nat.check(L.rs_shift_project(zl.data_ptr(), r, n, r, table_dev.data_ptr(), ld, R_l, n,
-                                     tt.data_ptr(), nat.stream_ptr()), "rs_shift_project")
-        tts.append(tt)
+    tts = [torch.empty((int(zl.shape[1]), n, R_l), dtype=torch.float64, device="cuda") for zl in zs]
+    nat.check(L.rs_shift_project3(zs[0].data_ptr(), zs[1].data_ptr(), zs[2].data_ptr(),
+                                  int(zs[0].shape[1]), int(zs[1].shape[1]), int(zs[2].shape[1]), n,
+                                  table_dev.data_ptr(), ld, R_l, n, tts[0].data_ptr(),
+                                  tts[1].data_ptr(), tts[2].data_ptr(), nat.stream_ptr()),
+              "rs_shift_project3")
     r1, r2, r3 = (int(zl.shape[1]) for zl in zs)
     count = int(z.shape[0])
     core = torch.empty((r1, r2, r3), dtype=torch.float64, device="cuda")
