@@ -55,7 +55,7 @@ int rs_snap(const double *pos, int64_t count, double h, int64_t n,
 
 /* After sorting the node keys (ks ascending, order = permutation): copies in
  * bucket order c1s/c2s/zqs, window starts starts = n - idx (assembly.py:131),
- * *dup_pos = first i with ks[i] == ks[i+1] (UINT64_MAX if none: the
+ * *dup_pos = the first duplicated node key (int64; -1 if none: the
  * ResolutionError of particles.py:319-325) and the max displacement as the
  * bits of a non-negative double. */
 int rs_prep(const int64_t *ks, const int64_t *order, const int64_t *idx,

@@ -249,9 +249,7 @@ def _node_sort(ds, n: int):
                                 disp.data_ptr(), count, n, c1s.data_ptr(), c2s.data_ptr(),
                                 zqs.data_ptr(), starts.data_ptr(), scal.data_ptr(),
                                 scal.data_ptr() + 8, nat.stream_ptr()), "rs_prep")
-    pos = scal[0:1]
-    dup_key = torch.where(pos >= 0, torch.gather(ks, 0, pos.clamp_min(0)), torch.full_like(pos, -1))
-    prep = dict(order=order, c1=c1s, c2=c2s, zq=zqs, starts=starts, dup_key=dup_key,
+    prep = dict(order=order, c1=c1s, c2=c2s, zq=zqs, starts=starts, dup_key=scal[0:1],
                 dmax=scal[1:2].view(torch.float64))
     ds._cache["prep"] = prep
     return prep
@@ -485,7 +483,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
         # block size: the numerical rank of the long-part Grams grows as eps shrinks
         eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
-        b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 2 * TOPEIG_BLOCK)
+        b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 64)
         forced = cfg.reduction.ranks
         if forced is not None:
             b = min(n - n % 2, max(b, max(forced) + 16 + (max(forced) % 2)))
@@ -526,7 +524,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
                     r = None
                 Ul = U[l] if r is not None else None
             if r is None:
-                bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 2 * TOPEIG_BLOCK else max(2 * b, 2))
+                bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 48 else 2 * b)
                 if b and bb > b and top_eig_supported(n, bb):
                     ev2, U2, tr2 = top_eig(G[l:l + 1].contiguous(), bb, 2)
                     r, sv, tail, total = truncated_spectrum(to_host(ev2[0]), float(tr2[0]), n,

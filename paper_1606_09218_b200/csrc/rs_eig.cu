@@ -299,13 +299,14 @@ __global__ void k_sign_rows(double *__restrict__ U, int64_t n) {
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) row[e] = -row[e];
 }
 
-// trace of each matrix (fixed order)
+// trace of each matrix (fixed-order warp reduction)
 __global__ void k_trace(const double *__restrict__ G, int64_t n, double *__restrict__ tr) {
-  if (threadIdx.x != 0) return;
   const double *g = G + (int64_t)blockIdx.x * n * n;
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += g[i * n + i];
-  tr[blockIdx.x] = s;
+  for (int64_t i = threadIdx.x; i < n; i += 32) s += g[i * n + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) tr[blockIdx.x] = s;
 }
 
 template <class T>
@@ -393,11 +394,12 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   if ((st = gemm_batched(Y, n, b * n, Q, n, b * n, T, b, b * b, b, b, n, (int)nmat, s))) return st;
   switch (b) {
     case 16: st = launch_jacobi<16>(T, (int)nmat, evals, Vt, reserve, s); break;
+    case 24: st = launch_jacobi<24>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 32: st = launch_jacobi<32>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 48: st = launch_jacobi<48>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 64: st = launch_jacobi<64>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 96: st = launch_jacobi<96>(T, (int)nmat, evals, Vt, reserve, s); break;
-    default: return fail(RS_ERR_UNSUPPORTED, "rs_topeig: block size %lld not in {16,32,48,64,96}",
+    default: return fail(RS_ERR_UNSUPPORTED, "rs_topeig: block size %lld not in {16,24,32,48,64,96}",
                          (long long)b);
   }
   if (st) return st;

@@ -62,6 +62,13 @@ __global__ void k_prep(const int64_t *__restrict__ ks, const int64_t *__restrict
   atomicMax(dmax_bits, (unsigned long long)__double_as_longlong(disp[i]));
 }
 
+// dup_pos -> duplicated node key (or -1), as int64 in place (one thread)
+__global__ void k_prep_finish(const int64_t *__restrict__ ks, int64_t count,
+                              unsigned long long *__restrict__ dup_pos) {
+  const unsigned long long p = *dup_pos;
+  *reinterpret_cast<long long *>(dup_pos) = p < (unsigned long long)count ? (long long)ks[p] : -1LL;
+}
+
 // ======================================================== window gather (K1)
 __global__ void k_gather(const double *__restrict__ table, int64_t ld_table, int64_t n_rows,
                          const int64_t *__restrict__ starts, int64_t n_groups, int64_t n_terms,
@@ -875,7 +882,10 @@ int rs_prep(const int64_t *ks, const int64_t *order, const int64_t *idx, const d
   k_prep<<<(unsigned)ceil_div(count, 256), 256, 0, s>>>(
       ks, order, idx, z, disp, count, n, c1s, c2s, zqs, starts, (unsigned long long *)dup_pos,
       (unsigned long long *)dmax_bits);
-  return check_launch("rs_prep");
+  int st = check_launch("rs_prep");
+  if (st) return st;
+  k_prep_finish<<<1, 1, 0, s>>>(ks, count, (unsigned long long *)dup_pos);
+  return check_launch("rs_prep finish");
 }
 
 int rs_gather_windows(const double *table, int64_t ld_table, int64_t n_rows, const int64_t *starts,

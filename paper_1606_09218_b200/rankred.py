@@ -330,7 +330,7 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
     return G
 
 
-TOPEIG_BLOCK = 32
+TOPEIG_BLOCK = 24
 TOPEIG_MAX_BLOCK = 96
 TOPEIG_ITERS = 2
 TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
@@ -338,7 +338,7 @@ TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
 
 def top_eig_supported(n: int, b: int) -> bool:
     """Block sizes rs_topeig accepts (Jacobi on the b x b Ritz matrix in smem)."""
-    return b in (16, 32, 48, 64, 96) and b <= n
+    return b in (16, 24, 32, 48, 64, 96) and b <= n
 
 
 def top_eig(G, b: int, iters: int = TOPEIG_ITERS):
