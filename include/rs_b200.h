@@ -200,6 +200,14 @@ int rs_sum_dd(const double *v, int64_t m, double *out, void *work,
               int64_t work_bytes, void *stream);
 int64_t rs_sum_workspace_bytes(int64_t m);
 
+/* ---- tcgen05 int8 engine (building block of the Ozaki-split FP64 GEMM) --
+ * C (M x N int32, ldc) = A (M x K int8, lda) * B (N x K int8, ldb)^T,
+ * tcgen05.mma kind::i8 with the accumulator in TMEM.  K, lda, ldb multiples
+ * of 16; 16-byte aligned bases.  No reference counterpart (kernel level). */
+int rs_tc8_gemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb,
+                   int32_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                   void *stream);
+
 #ifdef __cplusplus
 }
 #endif

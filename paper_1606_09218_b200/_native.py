@@ -63,6 +63,7 @@ SIGNATURES = {
                             _ptr, _ptr, _ptr]),
     "rs_sum_workspace_bytes": (_i64, [_i64]),
     "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
+    "rs_tc8_gemm_s8": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
 }
 
 _lib = None

@@ -121,3 +121,21 @@ def test_shift_hist_deterministic(nat, cuda):
         np.add.at(ref, n - idx[:, l], z * z)
         assert np.allclose(c[l], ref, rtol=1e-14, atol=0)
     assert np.array_equal(cnt.cpu().numpy(), np.bincount(idx[:, 2], minlength=n))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 128), (128, 64, 32), (300, 200, 1040), (1, 5, 16),
+                                   (1000, 513, 4096)])
+def test_tc8_gemm_s8_exact(nat, cuda, M, N, K):
+    """tcgen05 kind::i8 GEMM: int32 result bit-exact against numpy int64."""
+    rng = np.random.default_rng(M + 7 * N + K)
+    a = rng.integers(-128, 128, size=(M, K), dtype=np.int8)
+    b = rng.integers(-128, 128, size=(N, K), dtype=np.int8)
+    A = cuda.from_numpy(a).cuda()
+    B = cuda.from_numpy(b).cuda()
+    C = cuda.full((M, N), 7, dtype=cuda.int32, device="cuda")
+    nat.check(nat.lib().rs_tc8_gemm_s8(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N,
+                                       M, N, K, nat.stream_ptr()), "tc8")
+    cuda.cuda.synchronize()
+    ref = a.astype(np.int64) @ b.astype(np.int64).T
+    got = C.cpu().numpy()
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:5]
