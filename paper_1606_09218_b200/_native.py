@@ -70,9 +70,11 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load_library(path: str = LIB_PATH):
-    """Load and type the shared library (no CUDA device needed)."""
+def load_library(path: str = None):
+    """Load and type the shared library (no CUDA device needed).  ``RSB200_LIB``
+    overrides the in-tree path (kernel-variant A/B runs)."""
     global _lib
+    path = path or os.environ.get("RSB200_LIB", LIB_PATH)
     with _lock:
         if _lib is not None:
             return _lib

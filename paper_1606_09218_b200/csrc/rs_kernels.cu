@@ -428,17 +428,7 @@ __global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p
   }
 }
 
-// Short-range rows, x3-merged: for plane x1 and x3-bucket b,
-// A[(x1l*n + x2), col0 + b*G + k] = sum_{p in bucket b, |x1-c1p|<=g, |x2-c2p|<=g}
-//                                   zq[p] wl[k] ul[x1-c1p+g, k] ul[x2-c2p+g, k]
-// Block = (plane x1, group of BG buckets).  Per bucket the copies covering x1
-// are compacted into shared memory (alpha = z w ul[x1 - c1 + g]); the bucket's
-// copies arrive sorted by x2 (node key x3-x2-x1), so a thread owning row x2
-// binary-searches the copies whose x2 window contains it and accumulates the
-// R_s values in registers, then stores its G-wide row segment once.
-constexpr int SR_THREADS = 256;
-constexpr int SR_Q = 512;     // staged copies per bucket pass
-constexpr int SR_MAXR = 24;   // registers per row (R_s <= 24)
+constexpr int SR_MAXR = 24;  // largest short rank R_s of the row builder
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -460,95 +450,177 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total
   return base + x - v;
 }
 
-__global__ void __launch_bounds__(SR_THREADS)
-    k_short_rows(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G, int BG,
+// Short-range rows on FP64 tensor cores.  For a bucket b and rank term k the
+// (x1, x2) panel of D is a sum of rank-1 window products,
+//   D_bk[x1, x2] = sum_{p in b} (zq_p wl_k ul[x1-c1p+g, k]) * ul[x2-c2p+g, k],
+// i.e. a GEMM over the bucket's copies.  A CTA owns an 8-plane x 64-row tile
+// and SD_BG consecutive buckets; each warp owns 8 rows and issues
+// mma.m8n8k4.f64 with m = planes, n = rows, k = 4 copies, holding all R_s
+// accumulators in registers.  The buckets' copies are one contiguous candidate
+// range (x3-major node order); each pass stages 256 candidates, keeps those
+// whose window meets the tile (block scan, order preserving, so each bucket's
+// survivors stay contiguous) and runs the MMAs bucket by bucket; a bucket that
+// straddles two passes keeps its accumulators.  Window factors are gathered
+// from shared memory with clamped indices and a validity mask.
+constexpr int SD_THREADS = 256;
+constexpr int SD_TX1 = 8;    // planes per tile (MMA m)
+constexpr int SD_TX2 = 64;   // rows per tile (8 warps x MMA n)
+constexpr int SD_BG = 8;     // buckets per CTA
+constexpr int SD_PADA = SD_TX1;  // plane offsets stay within [-TX1, W + TX1)
+constexpr int SD_PADB = SD_TX2;  // row offsets stay within [-TX2, W + TX2)
+
+template <int GK>
+__global__ void __launch_bounds__(SD_THREADS)
+    k_short_dmma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
-                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, double *__restrict__ A,
-                 int64_t lda, int64_t col0) {
+                 const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
+                 double *__restrict__ A, int64_t lda, int64_t col0) {
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
-  double *ulT = sm;                       // Rs x W  (transposed local factor)
-  double *alpha = ulT + (int64_t)Rs * W;  // SR_Q x Rs
-  double *tile = alpha + SR_Q * Rs;       // SR_THREADS x G (row tile staged for coalesced stores)
-  int *qc2 = (int *)(tile + SR_THREADS * G);  // SR_Q
-  int *wsum = qc2 + SR_Q;                 // 32
-  const int n_buckets = *nbp;
-  const int b0 = blockIdx.y * BG;
-  if (b0 >= n_buckets) return;  // grid sized for the upper bound
-  const int b1 = min(b0 + BG, n_buckets);
-  const int tid = threadIdx.x;
-  const int64_t x1l = blockIdx.x, x1 = x1_lo + x1l;
-  for (int e = tid; e < Rs * W; e += SR_THREADS) {
-    const int k = e / W, d = e - (e / W) * W;
-    ulT[e] = ul[(int64_t)d * Rs + k];
+  constexpr int P = GK + 1;  // odd pitch (doubles): conflict-light row gathers
+  const int WA = W + 2 * SD_PADA, WB = W + 2 * SD_PADB;
+  double *uA = sm;                      // WA x P : wl_k ul[d, k], zero padded
+  double *uB = uA + (int64_t)WA * P;    // WB x P : ul[d, k], zero padded
+  double *szq = uB + (int64_t)WB * P;   // staged charges (SD_THREADS + 4)
+  int *sc1 = (int *)(szq + SD_THREADS + 4);
+  int *sc2 = sc1 + SD_THREADS + 4;
+  int *sbk = sc2 + SD_THREADS + 4;     // staged copy -> local bucket
+  int *wsum = sbk + SD_THREADS + 4;    // 32
+  __shared__ int s_bst[SD_BG + 1];     // bucket offsets in the candidate list
+  __shared__ int s_slo[SD_BG + 1];     // bucket starts within the staged list
+  __shared__ int s_plo[SD_BG];         // first candidate copy of each bucket
+  const int nb = *nbp;
+  const int b0 = blockIdx.z * SD_BG;
+  if (b0 >= nb) return;
+  const int nbk = min(SD_BG, nb - b0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t y0 = (int64_t)blockIdx.x * SD_TX2;
+  const int64_t x1l0 = (int64_t)blockIdx.y * SD_TX1;
+  const int64_t X0 = x1_lo + x1l0;
+  for (int e = tid; e < (WA + WB) * P; e += SD_THREADS) uA[e] = 0.0;  // k >= Rs rows stay zero
+  __syncthreads();
+  for (int e = tid; e < Rs * W; e += SD_THREADS) {  // coalesced read of ul (W x Rs)
+    const int d = e / Rs, k = e - (e / Rs) * Rs;
+    const double u = ul[e];
+    uA[(d + SD_PADA) * P + k] = wl[k] * u;
+    uB[(d + SD_PADB) * P + k] = u;
+  }
+  const int64_t yw = y0 + warp * 8;
+  const int ar = lane >> 2, kq = lane & 3;  // fragment row (plane / row) and k slot
+  const int64_t c1lo = X0 - gamma, c1hi = X0 + SD_TX1 - 1 + gamma;
+  const int64_t c2lo = y0 - gamma, c2hi = y0 + SD_TX2 - 1 + gamma;
+  if (tid < nbk) {  // per bucket: the copies whose x2 window meets the tile (c2 ascending)
+    const int p_lo = bstart[b0 + tid], p_hi = bstart[b0 + tid + 1];
+    int lo = p_lo, hi = p_hi;
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if (c2[m] < c2lo) lo = m + 1; else hi = m;
+    }
+    int e = lo;
+    hi = p_hi;
+    while (e < hi) {
+      const int m = (e + hi) >> 1;
+      if (c2[m] <= c2hi) e = m + 1; else hi = m;
+    }
+    s_plo[tid] = lo;
+    s_bst[tid + 1] = e - lo;
   }
   __syncthreads();
-  for (int b = b0; b < b1; ++b) {
-    const int p_lo = bstart[b], p_hi = bstart[b + 1];
-    double *Ab = A + x1l * n * lda + col0 + (int64_t)b * G;
-    bool first = true;
-    int next = p_lo;
-    do {
-      // stage the copies covering x1, in order, until SR_Q are staged
-      int staged = 0;
-      while (next < p_hi && staged + SR_THREADS <= SR_Q) {
-        const int p = next + tid;
-        int d1 = 0;
-        bool cov = false;
-        if (p < p_hi) {
-          d1 = (int)(x1 - c1[p]);
-          cov = d1 >= -gamma && d1 <= gamma;
-        }
-        int tot;
-        const int pos = staged + block_exclusive_scan(cov ? 1 : 0, wsum, &tot);
-        if (cov) {
-          qc2[pos] = c2[p];
-          const double zp = zq[p];
-          for (int k = 0; k < Rs; ++k) alpha[pos * Rs + k] = zp * wl[k] * ulT[k * W + d1 + gamma];
-        }
-        staged += tot;
-        next += SR_THREADS;
-      }
-      __syncthreads();
-      for (int64_t r0 = 0; r0 < n; r0 += SR_THREADS) {
-        const int64_t x2 = r0 + tid;
-        double acc[SR_MAXR];
+  if (tid == 0) {  // candidate offsets of the buckets in the concatenated c2 ranges
+    s_bst[0] = 0;
+    for (int j = 0; j < nbk; ++j) s_bst[j + 1] += s_bst[j];
+  }
+  __syncthreads();
+  const int V = s_bst[nbk];
+  double acc[GK][2];
 #pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k) acc[k] = 0.0;
+  for (int k = 0; k < GK; ++k) acc[k][0] = acc[k][1] = 0.0;
+  int jb = 0;  // first bucket not yet stored
+  for (int cs = 0; cs < V; cs += SD_THREADS) {
+    const int v = cs + tid;
+    bool cov = false;
+    int bk = 0, p = 0;
+    if (v < V) {
+      while (bk + 1 < nbk && s_bst[bk + 1] <= v) ++bk;
+      p = s_plo[bk] + (v - s_bst[bk]);
+      const int64_t a1 = c1[p];
+      cov = a1 >= c1lo && a1 <= c1hi;
+    }
+    int tot;
+    const int pos = block_exclusive_scan(cov ? 1 : 0, wsum, &tot);
+    if (cov) {
+      sc1[pos] = c1[p];
+      sc2[pos] = c2[p];
+      szq[pos] = zq[p];
+      sbk[pos] = bk;
+    }
+    if (tid < 4) {  // guard entries: an MMA k-step may run past a bucket's end
+      szq[tot + tid] = 0.0;
+      sc1[tot + tid] = (int)X0;
+      sc2[tid + tot] = (int)y0;
+      sbk[tot + tid] = nbk;
+    }
+    __syncthreads();
+    if (tid <= nbk) {  // first staged index of local bucket tid (sbk ascending)
+      int lo = 0, hi = tot;
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (sbk[m] < tid) lo = m + 1; else hi = m;
+      }
+      s_slo[tid] = lo;
+    }
+    __syncthreads();
+    const int cend = cs + SD_THREADS;
+    for (int j = jb; j < nbk && s_bst[j] < cend; ++j) {
+      const int q_lo = s_slo[j], q_hi = s_slo[j + 1];
+#pragma unroll 2
+      for (int q0 = q_lo; q0 < q_hi; q0 += 4) {
+        // staged copies meet the tile, so both offsets land inside the padding;
+        // slots past the bucket's end carry z = 0
+        const int q = q0 + kq;
+        const double z = q < q_hi ? szq[q] : 0.0;
+        const double *pa = uA + ((int)(X0 + ar - sc1[q]) + gamma + SD_PADA) * P;
+        const double *pb = uB + ((int)(yw + ar - sc2[q]) + gamma + SD_PADB) * P;
+#pragma unroll
+        for (int k = 0; k < GK; ++k) dmma_884(acc[k], z * pa[k], pb[k]);
+      }
+      if (s_bst[j + 1] <= cend) {  // bucket complete: store its G-wide row segments
+        const int64_t x1l = x1l0 + ar;
+        if (x1l < planes) {
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int64_t x2 = yw + 2 * kq + jj;
+            if (x2 < n) {
+              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
+#pragma unroll
+              for (int k = 0; k < GK; k += 2)
+                *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < GK; ++k) acc[k][0] = acc[k][1] = 0.0;
+        jb = j + 1;
+      }
+    }
+    __syncthreads();
+  }
+  // buckets without candidates after the last pass: zero segments
+  const int64_t x1l = x1l0 + ar;
+  for (int j = jb; j < nbk; ++j) {
+    if (x1l < planes) {
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int64_t x2 = yw + 2 * kq + jj;
         if (x2 < n) {
-          // first staged copy with c2 >= x2 - gamma (staged copies ascend in c2)
-          int lo = 0, hi = staged;
-          while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (qc2[m] < x2 - gamma) lo = m + 1; else hi = m;
-          }
-          for (int q = lo; q < staged && qc2[q] <= x2 + gamma; ++q) {
-            const int d = (int)(x2 - qc2[q]) + gamma;
-            const double *aq = alpha + q * Rs;
+          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
 #pragma unroll
-            for (int k = 0; k < SR_MAXR; ++k)
-              if (k < Rs) acc[k] = fma(aq[k], ulT[k * W + d], acc[k]);
-          }
+          for (int k = 0; k < GK; k += 2)
+            *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
         }
-#pragma unroll
-        for (int k = 0; k < SR_MAXR; ++k)
-          if (k < G) tile[tid * G + k] = k < Rs ? acc[k] : 0.0;
-        __syncthreads();
-        // coalesced store of the (rows x G) tile: consecutive threads write
-        // consecutive doubles of consecutive row segments
-        const int64_t rows = n - r0 < SR_THREADS ? n - r0 : SR_THREADS;
-        for (int e = tid; e < rows * G; e += SR_THREADS) {
-          const int rr = e / G, k = e - (e / G) * G;
-          double *dst = Ab + (r0 + rr) * lda + k;
-          if (first) *dst = tile[e];
-          else *dst += tile[e];
-        }
-        __syncthreads();
       }
-      __syncthreads();
-      first = false;
-    } while (next < p_hi);
+    }
   }
 }
 
@@ -823,6 +895,43 @@ int set_smem(const void *fn) {
 using namespace rsb;
 
 // ============================================================== C ABI
+template <int GK>
+static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int gamma,
+                               const int32_t *c1, const int32_t *c2, const double *zq,
+                               const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
+                               int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
+                               int64_t col0, cudaStream_t s) {
+  const int W = 2 * gamma + 1;
+  const size_t smem = (size_t)(GK + 1) * (2 * W + 2 * SD_PADA + 2 * SD_PADB) * 8 +
+                      (SD_THREADS + 4) * (8 + 4 + 4 + 4) + 32 * 4;
+  cudaError_t e = cudaFuncSetAttribute((const void *)k_short_dmma<GK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_dmma smem: %s", cudaGetErrorString(e));
+  dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
+            (unsigned)ceil_div(nb_max, SD_BG));
+  k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, GK, gamma, c1, c2, zq, bstart, nb_dev,
+                                                  n, x1_lo, planes, A, lda, col0);
+  return check_launch("short_dmma");
+}
+
+// one instantiation per even row width G = R_s rounded up to even
+static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, int gamma,
+                             const int32_t *c1, const int32_t *c2, const double *zq,
+                             const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
+                             int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
+                             int64_t col0, cudaStream_t s) {
+  switch (G) {
+#define RS_SD(R)                                                                              \
+  case R:                                                                                     \
+    return launch_short_dmma_t<R>(ul, wl, Rs, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
+                                  x1_lo, planes, A, lda, col0, s);
+    RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14) RS_SD(16) RS_SD(18)
+    RS_SD(20) RS_SD(22) RS_SD(24)
+#undef RS_SD
+  }
+  return fail(RS_ERR_UNSUPPORTED, "short_dmma: R_s=%d exceeds 24", Rs);
+}
+
 extern "C" {
 
 int rs_abi_version(void) { return 1; }
@@ -1177,15 +1286,9 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");
-    const int BG = 8;
-    size_t smem = (size_t)(Rs * (2 * gamma + 1) + SR_Q * Rs + SR_THREADS * G) * 8 +
-                  (size_t)(SR_Q + 32) * 4;
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_short_rows,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_rows smem: %s", cudaGetErrorString(e));
-    k_short_rows<<<dim3((unsigned)planes, (unsigned)ceil_div(nb_max, BG)), SR_THREADS, smem, s>>>(
-        ul, wl, (int)Rs, (int)G, BG, (int)gamma, c1, c2, zq, bstart, nb_dev, n, x1_lo, A, lda,
-        r3p);
+    if ((st = launch_short_dmma(ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, nb_dev,
+                                nb_max, n, x1_lo, planes, A, lda, r3p, s)))
+      return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
