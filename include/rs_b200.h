@@ -200,6 +200,13 @@ int rs_sum_dd(const double *v, int64_t m, double *out, void *work,
               int64_t work_bytes, void *stream);
 int64_t rs_sum_workspace_bytes(int64_t m);
 
+/* ---- SM partitions ------------------------------------------------------
+ * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs
+ * (green context, created once per (device, sms)); *sms_out = its SM count.
+ * Used to keep SMs free for the latency-bound long-range chain while the
+ * short-range planes are assembled concurrently.  No reference counterpart. */
+int rs_partition_stream(int sms, int priority, void **stream_out, int *sms_out);
+
 /* ---- tcgen05 int8 engine (building block of the Ozaki-split FP64 GEMM) --
  * C (M x N int32, ldc) = A (M x K int8, lda) * B (N x K int8, ldb)^T,
  * tcgen05.mma kind::i8 with the accumulator in TMEM.  K, lda, ldb multiples

@@ -63,6 +63,8 @@ SIGNATURES = {
                             _ptr, _ptr, _ptr]),
     "rs_sum_workspace_bytes": (_i64, [_i64]),
     "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
+    "rs_partition_stream": (_i32, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                   ctypes.POINTER(ctypes.c_int)]),
     "rs_tc8_gemm_s8": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
 }
 
@@ -94,12 +96,18 @@ def lib():
     return _lib if _lib is not None else load_library()
 
 
-def _torch():
-    import torch
+_TORCH = None
 
-    if not torch.cuda.is_available():
-        raise CapabilityError("the RS assembly path needs a CUDA device (no CPU fallback)")
-    return torch
+
+def _torch():
+    global _TORCH
+    if _TORCH is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise CapabilityError("the RS assembly path needs a CUDA device (no CPU fallback)")
+        _TORCH = torch
+    return _TORCH
 
 
 def check(status: int, what: str) -> None:
@@ -113,8 +121,9 @@ def ptr(t) -> int | None:
 
 
 def stream_ptr() -> int:
+    """Raw handle of the current torch stream of the current device."""
     torch = _torch()
-    return torch.cuda.current_stream().cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 ASM_LONG, ASM_SHORT, ASM_ACCUMULATE = 1, 2, 4

@@ -20,6 +20,8 @@ with ``rs_gather_windows`` for callers that want them.
 
 from __future__ import annotations
 
+import os
+
 import dataclasses
 import math
 from dataclasses import dataclass, field
@@ -216,12 +218,14 @@ def snap_device(positions, charges, box, grid: Grid3) -> DeviceIndexedSystem:
     disp = torch.empty(count, dtype=torch.float64, device="cuda")
     key = torch.empty(count, dtype=torch.int64, device="cuda")
     snapped = torch.empty((count, 3), dtype=torch.float64, device="cuda")
+    _mark("snap_alloc")
     nat.check(nat.lib().rs_snap(pos.data_ptr(), count, grid.h, grid.n, idx.data_ptr(),
                                 disp.data_ptr(), key.data_ptr(), snapped.data_ptr(),
                                 nat.stream_ptr()), "rs_snap")
     ds = DeviceIndexedSystem(positions=snapped, charges=z, grid=grid, indices=idx, box=box,
                              _disp=disp)
     ds._cache["key"] = key
+    _mark("snap_done")
     return ds
 
 
@@ -237,7 +241,9 @@ def _node_sort(ds, n: int):
     if key is None:
         key = (idx[:, 2] * n + idx[:, 1]) * n + idx[:, 0]
     count = int(idx.shape[0])
+    _mark("sort_in")
     ks, order = torch.sort(key, stable=True)
+    _mark("sorted")
     c1s = torch.empty(count, dtype=torch.int32, device="cuda")
     c2s = torch.empty(count, dtype=torch.int32, device="cuda")
     zqs = torch.empty(count, dtype=torch.float64, device="cuda")
@@ -252,6 +258,7 @@ def _node_sort(ds, n: int):
     prep = dict(order=order, c1=c1s, c2=c2s, zq=zqs, starts=starts, dup_key=scal[0:1],
                 dmax=scal[1:2].view(torch.float64))
     ds._cache["prep"] = prep
+    _mark("prep_done")
     return prep
 
 
@@ -365,9 +372,22 @@ def _stream(kind: str):
     if st is None:
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
             else (0, -1)
-        st = torch.cuda.Stream(device=dev, priority=(hi if kind == "chain" else lo))
+        if kind == "side" and _SIDE_SMS > 0:
+            # the wide short-range kernels on an SM partition (green context):
+            # the SMs outside it stay free for the latency-bound chain
+            import ctypes
+            ptr, got = ctypes.c_void_p(), ctypes.c_int()
+            if nat.lib().rs_partition_stream(min(_SIDE_SMS, _device_sms(dev)), int(lo),
+                                             ctypes.byref(ptr), ctypes.byref(got)) == 0:
+                st = torch.cuda.ExternalStream(ptr.value, device=dev)
+        if st is None:
+            st = torch.cuda.Stream(device=dev, priority=(hi if kind == "chain" else lo))
         _STREAMS[(dev, kind)] = st
     return st
+
+
+def _device_sms(dev: int) -> int:
+    return nat._torch().cuda.get_device_properties(dev).multi_processor_count
 
 
 def _side_stream():
@@ -388,6 +408,25 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> A
     return res
 
 
+# where the short-range prefetch enters the side stream: right after snapping
+# ("snap", maximal overlap) or behind the eigen block ("eig": the latency-bound
+# Gram/eigen kernels then run on an otherwise idle GPU)
+_PREFETCH_AT = os.environ.get("RSB200_PREFETCH_AT", "snap")
+_TUCKER_IN_BUILD = os.environ.get("RSB200_TUCKER_IN_BUILD", "1") == "1"
+_TRACE = [] if os.environ.get("RSB200_HOST_TRACE") else None
+
+
+def _mark(label: str) -> None:
+    """Host-time trace point (diagnostics; no-op unless RSB200_HOST_TRACE)."""
+    if _TRACE is not None:
+        import time
+        _TRACE.append((label, time.perf_counter()))
+
+
+# SMs of the side stream's partition (0: ordinary stream on the whole device)
+_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "128"))
+
+
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
@@ -402,6 +441,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
     torch = nat._torch()
     grid = cfg.grid
     n = grid.n
+    _mark("start")
     ds, collision = _as_device_system(system, grid)
     if cfg.sigma is not None:
         sigma = float(cfg.sigma)
@@ -414,7 +454,10 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         split_index = int(cfg.split_index)
     else:
         split_index = split_rank(_reference_cached(cfg), sigma, cfg.delta, cfg.criterion)
+    _mark("snapped")
+    _mark("split")
     plan = plan_for(cfg, split_index)
+    _mark("plan")
     ref2n = plan.ref2n
     nt = split_index + 1
     raw_rank = ds.count * nt
@@ -460,26 +503,36 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             hist = packed_h[:3 * n].reshape(3, n)
             cnt3 = packed_h[3 * n:].to(torch.int32)
     if plan.local.rank > 0:
+        _mark("hist")
         lay = short_layout(idx, z, n, cnt3, prep)
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
         short._cache["dev"] = lay
-        if prefetch_dense:
-            lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
-                                                            int(prefetch_dense[1]))
-            main = torch.cuda.current_stream()
-            side = _side_stream()
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                buf = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
-                assemble_grid(None, short, lo, hi, out=buf, workspace_slot="assemble_side")
-                ev = torch.cuda.Event()
-                ev.record(side)
-            short._cache["prefetch"] = (lo, hi, buf, ev)
+
+    def launch_prefetch():
+        lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
+                                                        int(prefetch_dense[1]))
+        main = torch.cuda.current_stream()
+        side = _side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            buf = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
+            assemble_grid(None, short, lo, hi, out=buf, workspace_slot="assemble_side")
+            ev = torch.cuda.Event()
+            ev.record(side)
+        short._cache["prefetch"] = (lo, hi, buf, ev)
+
+    prefetch_pending = bool(prefetch_dense) and plan.local.rank > 0
+    if prefetch_pending and (_PREFETCH_AT == "snap" or not (reduce_long and
+                                                           cfg.reduction.max_sweeps == 0)):
+        _mark("layout")
+        launch_prefetch()
+        prefetch_pending = False
 
     tails = None
     if reduce_long and cfg.reduction.max_sweeps == 0:
         # shift histograms -> per-mode Grams on DMMA -> top-b eigenpairs, then
         # ONE synchronisation for everything the host must decide on
+        _mark("prefetch")
         G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
         # block size: the numerical rank of the long-part Grams grows as eps shrinks
         eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
@@ -494,11 +547,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         # eps >= 1e-6, but point values / energies (1e-12) need the second
         iters = TOPEIG_ITERS
         if use_top:
+            _mark("grams")
             evals, U, trace = top_eig(G, b, iters)
         else:
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
+        if prefetch_pending:  # short-range planes behind the latency-bound eigen block
+            launch_prefetch()
+            prefetch_pending = False
         parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
+        _mark("eig_enq")
         packed = to_host(torch.cat(parts))
         nt_ = 3 * b + (3 if use_top else 0)
         if packed[nt_ + 1] >= 0:
@@ -545,14 +603,27 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             tails.append((float(tail[r]) if r < len(tail) else 0.0, total))
             zs.append(Ul[:r].T.contiguous())
         ranks = tuple(ranks)
+        _mark("d2h")
         spectrum = SvdSpectrum(values=tuple(values), vectors=tuple(zs))
         if world == 1:
             core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
         else:
             core = sharded_sum(shifted_core(plan.table_dev, n, zs, starts[p_lo:p_hi].contiguous(),
                                             z[p_lo:p_hi].contiguous(), plan.w_long), group)
+        _mark("ranks")
         tucker = _trusted_tucker(core, zs)
         long_raw = None
+        pre = short._cache.get("prefetch") if cfg.long_format == "tucker" else None
+        if pre is not None and _TUCKER_IN_BUILD:
+            # finish the prefetched slab here: the Tucker part is enqueued right
+            # behind the core, before the host packages the result
+            lo, hi, buf, ev = pre
+            torch.cuda.current_stream().wait_event(ev)
+            buf.record_stream(torch.cuda.current_stream())
+            assemble_grid(tucker, None, lo, hi, out=buf, accumulate=True)
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream())
+            short._cache["prefetch"] = (lo, hi, buf, done, "complete")
     else:
         if int(collision[0]) >= 0:
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "
@@ -599,5 +670,6 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
     sto = storage_report(rs)
     report["storage_floats"] = sto.total
     report["storage_bound"] = sto.bound
+    _mark("core_enq")
     return AssemblyResult(rs=rs, reference=ref2n, system=_host_system(ds),
                           split_index=split_index, sigma=sigma, gamma=plan.gamma, report=report)

@@ -499,11 +499,12 @@ def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=
         if pre is not None and pre[0] == lo and pre[1] == hi:
             del a.short._cache["prefetch"]
             torch = nat._torch()
-            _, _, out, ev = pre
+            out, ev = pre[2], pre[3]
             main = torch.cuda.current_stream()
             main.wait_event(ev)
             out.record_stream(main)
-            assemble_grid(a.long, None, lo, hi, out=out, accumulate=True)
+            if len(pre) < 5:  # short part only so far: add the Tucker part
+                assemble_grid(a.long, None, lo, hi, out=out, accumulate=True)
         else:
             out = assemble_grid(a.long, a.short, lo, hi)
         if x1_range is None:
