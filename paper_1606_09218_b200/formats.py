@@ -480,14 +480,86 @@ def dense_cct(short: CCT, limit: int = MAX_DENSE_ELEMENTS, device: bool = False)
     return out if device else to_host(out)
 
 
-def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=None):
+_PINNED: dict = {}          # shape -> pinned host tensor we may hand out again
+_HOST_CHUNKS = 8            # plane chunks of the overlapped device->host path
+
+
+def _pinned_host(shape):
+    """A pinned host float64 tensor of ``shape``; the previous one is reused
+    once every numpy view handed out from it is gone (weak liveness token)."""
+    torch = nat._torch()
+    ent = _PINNED.get(shape)
+    if ent is not None and (ent[1] is None or ent[1]() is None):
+        return ent[0]
+    t = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+    _PINNED[shape] = (t, None)
+    return t
+
+
+def _hand_out(t) -> np.ndarray:
+    """numpy view of a pooled pinned tensor; its base (a tensor wrapper kept
+    alive by every derived view) becomes the buffer's liveness token."""
+    import weakref
+    arr = t.numpy()
+    key = tuple(t.shape)
+    if key in _PINNED and _PINNED[key][0] is t:
+        _PINNED[key] = (t, weakref.ref(arr.base))
+    return arr
+
+
+def _copy_stream():
+    torch = nat._torch()
+    dev = torch.cuda.current_device()
+    st = _PINNED.get(("copy", dev))
+    if st is None:
+        st = torch.cuda.Stream(device=dev)
+        _PINNED[("copy", dev)] = st
+    return st
+
+
+def _dense_to_host(a: "RSTucker", lo: int, hi: int, out=None):
+    """Planes ``[lo, hi)`` into pinned host memory, chunk by chunk: the
+    device->host copy of chunk k (on a copy stream) overlaps the assembly of
+    chunk k+1, so the transfer -- the bound of a host-returning call -- starts
+    as soon as the first planes exist.  Two rotating device chunk buffers."""
+    torch = nat._torch()
+    n = a.grid.n
+    planes = hi - lo
+    host = out if out is not None else _pinned_host((planes, n, n))
+    chunk = max(1, -(-planes // _HOST_CHUNKS))
+    main = torch.cuda.current_stream()
+    cp = _copy_stream()
+    bufs = [torch.empty((chunk, n, n), dtype=torch.float64, device="cuda") for _ in range(2)]
+    free = [None, None]            # copy-done events guarding buffer reuse
+    for i, p0 in enumerate(range(lo, hi, chunk)):
+        p1 = min(hi, p0 + chunk)
+        b = bufs[i % 2]
+        if free[i % 2] is not None:
+            main.wait_event(free[i % 2])
+        assemble_grid(a.long, a.short, p0, p1, out=b[: p1 - p0])
+        ready = torch.cuda.Event()
+        ready.record(main)
+        cp.wait_event(ready)
+        with torch.cuda.stream(cp):
+            host[p0 - lo:p1 - lo].copy_(b[: p1 - p0], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cp)
+        free[i % 2] = done
+        b.record_stream(cp)
+    cp.synchronize()
+    return host
+
+
+def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=None, out=None):
     """Dense RS tensor ``long + short`` (``formats.py:448-453``), fused on device.
 
     ``device=True`` returns the CUDA tensor (grids larger than host RAM);
-    the default returns a numpy array like the reference.  ``x1_range``
-    (extension) assembles only the x1 planes ``[lo, hi)`` (multi-GPU slabs).
-    If :func:`build_rs` prefetched the short-range planes, only the Tucker
-    part is added here.
+    the default returns a numpy array like the reference, streamed to pinned
+    host memory chunk by chunk while later chunks are still being assembled
+    (``out``: an optional pinned host tensor of the result shape to fill).
+    ``x1_range`` (extension) assembles only the x1 planes ``[lo, hi)``
+    (multi-GPU slabs).  If :func:`build_rs` prefetched the short-range
+    planes, only the Tucker part is added here.
     """
     if isinstance(a, RSTucker):
         _guard_dense(a.long.mode_sizes, limit)
@@ -499,22 +571,31 @@ def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=
         if pre is not None and pre[0] == lo and pre[1] == hi:
             del a.short._cache["prefetch"]
             torch = nat._torch()
-            out, ev = pre[2], pre[3]
+            res, ev = pre[2], pre[3]
             main = torch.cuda.current_stream()
             main.wait_event(ev)
-            out.record_stream(main)
+            res.record_stream(main)
             if len(pre) < 5:  # short part only so far: add the Tucker part
-                assemble_grid(a.long, None, lo, hi, out=out, accumulate=True)
+                assemble_grid(a.long, None, lo, hi, out=res, accumulate=True)
+        elif not device:
+            host = _dense_to_host(a, lo, hi, out)
+            arr = _hand_out(host)
+            return arr.reshape(n, n, n) if x1_range is None else arr
         else:
-            out = assemble_grid(a.long, a.short, lo, hi)
+            res = assemble_grid(a.long, a.short, lo, hi)
         if x1_range is None:
-            out = out.view(n, n, n)
-        return out if device else to_host(out)
+            res = res.view(n, n, n)
+        if device:
+            return res
+        if out is not None:
+            out.copy_(res.reshape(out.shape))
+            return out.numpy()
+        return to_host(res)
     if isinstance(a, RSCanonical):
         long = a.long.dense(limit=limit, device=True)
         short = dense_cct(a.short, limit=limit, device=True)
-        out = long.add_(short)
-        return out if device else to_host(out)
+        res = long.add_(short)
+        return res if device else to_host(res)
     raise ConfigError(f"dense_rs expects an RS tensor, got {type(a).__name__}")
 
 
