@@ -200,6 +200,23 @@ int rs_sum_dd(const double *v, int64_t m, double *out, void *work,
               int64_t work_bytes, void *stream);
 int64_t rs_sum_workspace_bytes(int64_t m);
 
+/* ---- build front ---------------------------------------------------------
+ * snap + node sort (CUB radix) + bucket-ordered copies + shift histograms +
+ * short-range bucket table in ONE call (replaces rs_snap, a torch sort,
+ * rs_prep, rs_shift_hist, rs_short_layout issued one by one from Python).
+ * Buffers: one region, byte offsets from rs_front_offsets (18 slots + total):
+ * idx | disp | key | snapped | sorted keys | order | c1 | c2 | zq | starts |
+ * scal (dup key, dmax) | hist (3,n) | cnt3 | bstart | bc3 | nb | iota | scratch.
+ * Reference: particles.py:302-329, assembly.py:139-184, rankred.py:82-126. */
+int rs_front_offsets(int64_t count, int64_t n, int64_t *offsets);
+int rs_front(const double *pos, const double *z, int64_t count, double h, int64_t n,
+             void *buf, int64_t buf_bytes, void *stream,
+             /* optional: short-range planes [x1_lo, x1_hi) into `out` on `side`
+              * (after the bucket table; NULL side = none) */
+             const double *ul, const double *wl, int64_t Rs, int64_t gamma,
+             int64_t x1_lo, int64_t x1_hi, double *out, void *work,
+             int64_t work_bytes, void *side);
+
 /* ---- SM partitions ------------------------------------------------------
  * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs
  * (green context, created once per (device, sms)); *sms_out = its SM count.

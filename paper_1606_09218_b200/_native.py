@@ -63,6 +63,9 @@ SIGNATURES = {
                             _ptr, _ptr, _ptr]),
     "rs_sum_workspace_bytes": (_i64, [_i64]),
     "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
+    "rs_front_offsets": (_i32, [_i64, _i64, ctypes.POINTER(ctypes.c_int64)]),
+    "rs_front": (_i32, [_ptr, _ptr, _i64, ctypes.c_double, _i64, _ptr, _i64, _ptr,
+                        _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr]),
     "rs_partition_stream": (_i32, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int)]),
     "rs_tc8_gemm_s8": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
@@ -117,7 +120,10 @@ def check(status: int, what: str) -> None:
 
 
 def ptr(t) -> int | None:
-    return None if t is None else t.data_ptr()
+    """Device address of a tensor (ints pass through: raw front-buffer slots)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 def stream_ptr() -> int:

@@ -262,6 +262,104 @@ def _node_sort(ds, n: int):
     return prep
 
 
+_FRONT_POOL: dict = {}   # (device, count, n) -> {"offs": [...], "bufs": [(tensor, base use count)]}
+_FRONT_SLOTS = 18
+
+
+def _use_count(t) -> int:
+    return nat._torch()._C._storage_Use_Count(t.untyped_storage()._cdata)
+
+
+def _front_buffer(count: int, n: int):
+    """Pooled device region for rs_front.  A region is handed out again only
+    when no view of it is alive (storage use count back at its base), so a
+    result the caller still holds is never overwritten."""
+    import ctypes
+    torch = nat._torch()
+    key = (torch.cuda.current_device(), count, n)
+    ent = _FRONT_POOL.get(key)
+    if ent is None:
+        offs = (ctypes.c_int64 * (_FRONT_SLOTS + 1))()
+        nat.check(nat.lib().rs_front_offsets(count, n, offs), "rs_front_offsets")
+        ent = _FRONT_POOL[key] = {"offs": list(offs), "bufs": []}
+    for buf, base in ent["bufs"]:
+        if _use_count(buf) == base:
+            return buf, ent["offs"]
+    buf = torch.empty(ent["offs"][-1], dtype=torch.uint8, device="cuda")
+    ent["bufs"].append((buf, _use_count(buf)))
+    return buf, ent["offs"]
+
+
+_SIDE_WS: dict = {}
+
+
+def _short_ws_bytes(n: int, planes: int, nb_max: int, rs: int) -> int:
+    """Workspace of the short-range plane assembly (chunked like assemble_grid)."""
+    key = (n, planes, nb_max, rs)
+    v = _SIDE_WS.get(key)
+    if v is None:
+        from .formats import _ASSEMBLE_WORKSPACE
+        L = nat.lib()
+        one = L.rs_assemble_workspace_bytes(n, 1, 1, nb_max, rs, nat.ASM_SHORT)
+        per = L.rs_assemble_workspace_bytes(n, 2, 1, nb_max, rs, nat.ASM_SHORT) - one
+        chunk = max(1, min(planes, (_ASSEMBLE_WORKSPACE - (one - per)) // max(per, 1)))
+        v = _SIDE_WS[key] = L.rs_assemble_workspace_bytes(n, chunk, 1, nb_max, rs, nat.ASM_SHORT)
+    return v
+
+
+def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
+    """Snap, node sort, bucket-ordered copies, shift histograms and the
+    short-range bucket table in one native call (``rs_front``), no sync.
+    ``prefetch = (plan, lo, hi)`` also enqueues the short-range planes
+    [lo, hi) on the side stream (returned as (buf, event) in the cache).
+    Returns the device system; its cache carries the sort/prep products and
+    the raw addresses of the histogram and bucket-table slots."""
+    torch = nat._torch()
+    pos = to_device(positions)
+    z = to_device(charges)
+    count, n = int(pos.shape[0]), grid.n
+    _mark("f_todev")
+    buf, o = _front_buffer(count, n)
+    _mark("f_buf")
+    pf = (None, None, 0, 0, 0, 0, None, None, 0, None)
+    if prefetch is not None:
+        plan, lo, hi = prefetch
+        side = _side_stream()
+        rs = int(plan.local.rank)
+        out = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
+        out.record_stream(side)
+        ws = nat.Workspace.get(_short_ws_bytes(n, hi - lo, max(1, min(n, count)), rs),
+                               "assemble_side")
+        ws.record_stream(side)
+        pf = (plan.local_ul.data_ptr(), plan.local_wl.data_ptr(), rs, plan.gamma, lo, hi,
+              out.data_ptr(), ws.data_ptr(), ws.numel(), side.cuda_stream)
+    nat.check(nat.lib().rs_front(pos.data_ptr(), z.data_ptr(), count, grid.h, n, buf.data_ptr(),
+                                 buf.numel(), nat.stream_ptr(), *pf), "rs_front")
+    _mark("f_call")
+    if prefetch is not None:
+        ev = torch.cuda.Event()
+        ev.record(side)
+        buf.record_stream(side)
+    def view(slot, dtype, shape, nbytes):
+        return buf[o[slot]:o[slot] + nbytes].view(dtype).view(shape)
+
+    base = buf.data_ptr()
+    idx = view(0, torch.int64, (count, 3), 24 * count)
+    ds = DeviceIndexedSystem(positions=view(3, torch.float64, (count, 3), 24 * count), charges=z,
+                             grid=grid, indices=idx, box=box,
+                             _disp=view(1, torch.float64, (count,), 8 * count))
+    prep = dict(c1=base + o[6], c2=base + o[7], zq=base + o[8],
+                starts=view(9, torch.int64, (count, 3), 24 * count),
+                dup_key=view(10, torch.int64, (1,), 8),
+                dmax=buf[o[10] + 8:o[10] + 16].view(torch.float64))
+    ds._cache["prep"] = prep
+    ds._cache["front"] = dict(hist=base + o[11], cnt3=base + o[12], bstart=base + o[13],
+                              bc3=base + o[14], nb=base + o[15], buf=buf)
+    if prefetch is not None:
+        ds._cache["front"]["prefetch"] = (lo, hi, out, ev)
+    return ds, prep["dup_key"]
+
+
 def _decode_key(key: int, n: int) -> tuple:
     """x3-major node key -> (x1, x2, x3)."""
     return (key % n, (key // n) % n, key // (n * n))
@@ -271,15 +369,16 @@ def _collision_flag(ds, n: int):
     return _node_sort(ds, n)["dup_key"]
 
 
-def _as_device_system(system, grid: Grid3):
-    """Accept the reference's types or :class:`DeviceParticles`."""
+def _as_device_system(system, grid: Grid3, prefetch=None):
+    """Accept the reference's types or :class:`DeviceParticles`.  ``prefetch``
+    (plan, lo, hi) rides along with the native front when the input is snapped
+    here."""
     if isinstance(system, DeviceIndexedSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
         return system, None
     if isinstance(system, DeviceParticles):
-        ds = snap_device(system.positions, system.charges, system.box, grid)
-        return ds, _node_sort(ds, grid.n)["dup_key"]
+        return _front_system(system.positions, system.charges, system.box, grid, prefetch)
     if isinstance(system, IndexedParticleSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
@@ -293,8 +392,7 @@ def _as_device_system(system, grid: Grid3):
         ds._cache["host"] = system
         return ds, None
     if isinstance(system, ParticleSystem):
-        ds = snap_device(system.positions, system.charges, system.box, grid)
-        return ds, _node_sort(ds, grid.n)["dup_key"]
+        return _front_system(system.positions, system.charges, system.box, grid, prefetch)
     raise ConfigError(f"expected a particle system, got {type(system).__name__}")
 
 
@@ -442,7 +540,15 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
     grid = cfg.grid
     n = grid.n
     _mark("start")
-    ds, collision = _as_device_system(system, grid)
+    fused = None
+    if (prefetch_dense and _PREFETCH_AT == "snap" and cfg.split_index is not None
+            and isinstance(system, (DeviceParticles, ParticleSystem))):
+        plan0 = plan_for(cfg, int(cfg.split_index))
+        if plan0.local.rank > 0:
+            lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
+                                                            int(prefetch_dense[1]))
+            fused = (plan0, lo, hi)
+    ds, collision = _as_device_system(system, grid, fused)
     if cfg.sigma is not None:
         sigma = float(cfg.sigma)
     elif ds.count >= 2:
@@ -492,8 +598,11 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         world = dist.get_world_size(group) if dist.is_initialized() else 1
     p_lo, p_hi = (0, ds.count) if world == 1 else particle_shard(ds.count, dist.get_rank(group),
                                                                   world)
+    front = ds._cache.get("front")
     if reduce_long and cfg.reduction.max_sweeps == 0:
-        if world == 1:
+        if world == 1 and front is not None:
+            hist, cnt3 = front["hist"], front["cnt3"]
+        elif world == 1:
             hist, cnt3 = shift_histograms(idx, z, n)
         else:
             h_part, c_part = shift_histograms(idx[p_lo:p_hi].contiguous(),
@@ -504,7 +613,12 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             cnt3 = packed_h[3 * n:].to(torch.int32)
     if plan.local.rank > 0:
         _mark("hist")
-        lay = short_layout(idx, z, n, cnt3, prep)
+        if front is not None:
+            lay = dict(c1=prep["c1"], c2=prep["c2"], zq=prep["zq"], bstart=front["bstart"],
+                       bc3=front["bc3"], nb=front["nb"], nb_max=max(1, min(n, ds.count)),
+                       centers=idx, z=z, buf=front["buf"])
+        else:
+            lay = short_layout(idx, z, n, cnt3, prep)
         lay.update(ul=plan.local_ul, wl=plan.local_wl)
         short._cache["dev"] = lay
 
@@ -522,6 +636,10 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         short._cache["prefetch"] = (lo, hi, buf, ev)
 
     prefetch_pending = bool(prefetch_dense) and plan.local.rank > 0
+    fpre = ds._cache.get("front", {}).get("prefetch")
+    if prefetch_pending and fpre is not None:  # launched with the native front
+        short._cache["prefetch"] = fpre
+        prefetch_pending = False
     if prefetch_pending and (_PREFETCH_AT == "snap" or not (reduce_long and
                                                            cfg.reduction.max_sweeps == 0)):
         _mark("layout")

@@ -324,7 +324,7 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
     G = torch.empty((3, n, n), dtype=torch.float64, device="cuda")
     L = nat.lib()
     ws = nat.Workspace.get(L.rs_gram_shifted_workspace_bytes(n, R_l), "syrk")
-    nat.check(L.rs_gram_shifted(table_dev.data_ptr(), table_dev.shape[1], n, R_l, c.data_ptr(),
+    nat.check(L.rs_gram_shifted(table_dev.data_ptr(), table_dev.shape[1], n, R_l, nat.ptr(c),
                                 w_long_abs.data_ptr(), G.data_ptr(), ws.data_ptr(), ws.numel(),
                                 nat.stream_ptr()), "rs_gram_shifted")
     return G

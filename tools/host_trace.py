@@ -31,3 +31,4 @@ for it in range(25):
 for k, v in acc.items():
     print(f"{k:22s} {np.median(v):8.1f} us")
 print("total", sum(np.median(v) for v in acc.values()))
+print("front pool:", {k: len(v["bufs"]) for k, v in assembly._FRONT_POOL.items()})
