@@ -154,6 +154,8 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3,
 #define RS_ASM_LONG 1
 #define RS_ASM_SHORT 2
 #define RS_ASM_ACCUMULATE 4
+/* plane GEMM as Ozaki-split FP64 with s int8 slices (tcgen05 kind::i8), s in 6..8 */
+#define RS_ASM_OZ(s) ((s) << 8)
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax,
                                     int64_t nb_max, int64_t Rs, int flags);
 int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3,
@@ -215,7 +217,7 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
               * (after the bucket table; NULL side = none) */
              const double *ul, const double *wl, int64_t Rs, int64_t gamma,
              int64_t x1_lo, int64_t x1_hi, double *out, void *work,
-             int64_t work_bytes, void *side);
+             int64_t work_bytes, void *side, int oz_slices);
 
 /* ---- SM partitions ------------------------------------------------------
  * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs
@@ -231,6 +233,20 @@ int rs_partition_stream(int sms, int priority, void **stream_out, int *sms_out);
 int rs_tc8_gemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb,
                    int32_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                    void *stream);
+
+/* ---- Ozaki-split FP64 GEMM on the int8 tensor cores -----------------------
+ * C (=, or += with accumulate) = A (M x K) B (N x K)^T in FP64: per-row
+ * power-of-two scaling, `slices` (6..8) signed 7-bit int8 slices per operand,
+ * the slice products with p + q < slices exact in int32 TMEM accumulators
+ * (tcgen05.mma kind::i8), recombined in fp64.  Relative error per entry
+ * ~ K 2^(-7 slices) of max|A_i.| max|B_j.|.  ranges: NULL or nr fp64 column
+ * ranges per 64-column tile of C (columns outside them must hold zero B
+ * entries for that tile).  No reference counterpart (kernel level). */
+int64_t rs_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int slices);
+int rs_oz_gemm(const double *A, int64_t lda, const double *B, int64_t ldb,
+               double *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+               const int64_t *ranges, int nr, int slices, int accumulate,
+               void *work, int64_t work_bytes, void *stream);
 
 #ifdef __cplusplus
 }

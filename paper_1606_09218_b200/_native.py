@@ -65,9 +65,12 @@ SIGNATURES = {
     "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
     "rs_front_offsets": (_i32, [_i64, _i64, ctypes.POINTER(ctypes.c_int64)]),
     "rs_front": (_i32, [_ptr, _ptr, _i64, ctypes.c_double, _i64, _ptr, _i64, _ptr,
-                        _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr]),
+                        _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i32]),
     "rs_partition_stream": (_i32, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int)]),
+    "rs_oz_workspace_bytes": (_i64, [_i64, _i64, _i64, _i32]),
+    "rs_oz_gemm": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr, _i32, _i32,
+                          _i32, _ptr, _i64, _ptr]),
     "rs_tc8_gemm_s8": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
 }
 
@@ -133,6 +136,13 @@ def stream_ptr() -> int:
 
 
 ASM_LONG, ASM_SHORT, ASM_ACCUMULATE = 1, 2, 4
+# short-range plane GEMM as Ozaki-split FP64 on the int8 tensor cores with this
+# many slices (0: FP64 DMMA); RSB200_OZ_SLICES overrides
+OZ_SLICES = int(os.environ.get("RSB200_OZ_SLICES", "0"))
+
+
+def asm_oz(slices: int) -> int:
+    return (int(slices) & 0xF) << 8
 
 
 def prof_query(name: str):

@@ -300,10 +300,11 @@ def _short_ws_bytes(n: int, planes: int, nb_max: int, rs: int) -> int:
     if v is None:
         from .formats import _ASSEMBLE_WORKSPACE
         L = nat.lib()
-        one = L.rs_assemble_workspace_bytes(n, 1, 1, nb_max, rs, nat.ASM_SHORT)
-        per = L.rs_assemble_workspace_bytes(n, 2, 1, nb_max, rs, nat.ASM_SHORT) - one
+        fl = nat.ASM_SHORT | nat.asm_oz(nat.OZ_SLICES)
+        one = L.rs_assemble_workspace_bytes(n, 1, 1, nb_max, rs, fl)
+        per = L.rs_assemble_workspace_bytes(n, 2, 1, nb_max, rs, fl) - one
         chunk = max(1, min(planes, (_ASSEMBLE_WORKSPACE - (one - per)) // max(per, 1)))
-        v = _SIDE_WS[key] = L.rs_assemble_workspace_bytes(n, chunk, 1, nb_max, rs, nat.ASM_SHORT)
+        v = _SIDE_WS[key] = L.rs_assemble_workspace_bytes(n, chunk, 1, nb_max, rs, fl)
     return v
 
 
@@ -321,7 +322,7 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     _mark("f_todev")
     buf, o = _front_buffer(count, n)
     _mark("f_buf")
-    pf = (None, None, 0, 0, 0, 0, None, None, 0, None)
+    pf = (None, None, 0, 0, 0, 0, None, None, 0, None, 0)
     if prefetch is not None:
         plan, lo, hi = prefetch
         side = _side_stream()
@@ -332,7 +333,7 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
                                "assemble_side")
         ws.record_stream(side)
         pf = (plan.local_ul.data_ptr(), plan.local_wl.data_ptr(), rs, plan.gamma, lo, hi,
-              out.data_ptr(), ws.data_ptr(), ws.numel(), side.cuda_stream)
+              out.data_ptr(), ws.data_ptr(), ws.numel(), side.cuda_stream, nat.OZ_SLICES)
     nat.check(nat.lib().rs_front(pos.data_ptr(), z.data_ptr(), count, grid.h, n, buf.data_ptr(),
                                  buf.numel(), nat.stream_ptr(), *pf), "rs_front")
     _mark("f_call")

@@ -93,7 +93,7 @@ int rs_front_offsets(int64_t count, int64_t n, int64_t *offsets) {
 int rs_front(const double *pos, const double *z, int64_t count, double h, int64_t n, void *buf,
              int64_t buf_bytes, void *stream, const double *ul, const double *wl, int64_t Rs,
              int64_t gamma, int64_t x1_lo, int64_t x1_hi, double *out, void *work,
-             int64_t work_bytes, void *side) {
+             int64_t work_bytes, void *side, int oz_slices) {
   RS_REQUIRE(count >= 1 && n >= 2 && h > 0 && pos && z && buf, "rs_front: bad arguments");
   int64_t off[F_END + 1];
   layout(count, n, off);
@@ -140,8 +140,9 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
       cudaStreamWaitEvent(as_stream(side), ev[dev & 63], 0) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_front: stream dependency");
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(n, count));
-  const int64_t one = rs_assemble_workspace_bytes(n, 1, 1, nb_max, Rs, RS_ASM_SHORT);
-  const int64_t per = rs_assemble_workspace_bytes(n, 2, 1, nb_max, Rs, RS_ASM_SHORT) - one;
+  const int flags = RS_ASM_SHORT | RS_ASM_OZ(oz_slices);
+  const int64_t one = rs_assemble_workspace_bytes(n, 1, 1, nb_max, Rs, flags);
+  const int64_t per = rs_assemble_workspace_bytes(n, 2, 1, nb_max, Rs, flags) - one;
   const int64_t chunk = std::max<int64_t>(
       1, std::min<int64_t>(x1_hi - x1_lo, (work_bytes - (one - per)) / std::max<int64_t>(per, 1)));
   for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += chunk) {
@@ -150,7 +151,7 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
                                  (const int32_t *)P(F_C1), (const int32_t *)P(F_C2),
                                  (const double *)P(F_ZQ), (const int32_t *)P(F_BSTART),
                                  (const int32_t *)P(F_BC3), (const int32_t *)P(F_NB), nb_max, p0,
-                                 p1, RS_ASM_SHORT, out + (p0 - x1_lo) * n * n, work, work_bytes,
+                                 p1, flags, out + (p0 - x1_lo) * n * n, work, work_bytes,
                                  side)))
       return st;
   }

@@ -933,6 +933,10 @@ static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, 
 }
 
 extern "C" {
+int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
+                    int slices, int accumulate, void *work, int64_t work_bytes,
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream);
 
 int rs_abi_version(void) { return 1; }
 const char *rs_last_error(void) { return g_err; }
@@ -1223,6 +1227,8 @@ static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int6
   *offY = a + b;
   *offR = a + b + y;
   *total = a + b + y + rr;
+  const int slices = (flags >> 8) & 0xF;
+  if (slices) *total += round_up(rs_oz_workspace_bytes(planes * n, n, *lda, slices), 256);
 }
 
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t nb_max,
@@ -1301,6 +1307,14 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
       ranges);
   if ((st = check_launch("band_ranges"))) return st;
+  const int slices = (flags >> 8) & 0xF;
+  if (slices) {  // Ozaki-split FP64 on the int8 tensor cores (same tiles, same K ranges)
+    ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
+    const int64_t oz_off = tot - round_up(rs_oz_workspace_bytes(planes * n, n, lda, slices), 256);
+    return rs_oz_gemm_cols(A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2, slices,
+                           accumulate ? 1 : 0, wb + oz_off, tot - oz_off,
+                           with_short ? nb_dev : nullptr, r3p, G, stream);
+  }
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
   {
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));

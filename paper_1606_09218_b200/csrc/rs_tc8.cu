@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "rs_common.cuh"
 
@@ -46,6 +47,18 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// K-major SWIZZLE_64B descriptor: 64-byte rows, 8-row atoms of 512 B (SBO),
+// LBO unused (1), layout type 4.  Chunk c of row r sits at c ^ ((r >> 1) & 3).
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
 // Instruction descriptor: c_format S32 (2) at [4,6), a/b format INT8 (1) at
 // [7,10) / [10,13), K-major A/B, N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
@@ -64,6 +77,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+
+// 1-D bulk copy global -> shared, completion counted on `bar` (tx bytes)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
@@ -202,6 +230,330 @@ __global__ void __launch_bounds__(THREADS)
                  "r"(TMEM_COLS));
 }
 
+
+// ============================================ Ozaki-split FP64 GEMM (int8)
+// X (fp64) = 2^e_row * sum_p d_p 2^(-6-7p), d_p in [-64, 64] (int8): the row
+// scale e is the exponent of the row's max |x|; digit p is the rounded
+// remainder after p digits.  C = A B^T in fp64 then is
+//   C_ij = 2^(ea_i + eb_j - 12) * sum_t 2^(-7t) * sum_{p+q=t} (D^A_p D^B_q^T)_ij
+// where every slice product is exact in int32 (|d| <= 64, K * 8 * 4096 < 2^31
+// for K < 65536) and accumulates in its own TMEM accumulator t.  Terms with
+// p + q >= S are dropped: relative error ~ K 2^(-7S) of 2^(ea_i + eb_j).
+constexpr int OZ_BN = 64;   // output columns per CTA (S accumulators x 64 <= 512 TMEM cols)
+constexpr int OZ_BK = 64;   // int8 columns per stage
+
+// e[r] = exponent with max_k |X[r, k]| < 2^e (0 for an all-zero row); warp per row
+// Used columns: `cols`, or r3p + (*nb) * G when the bucket count lives on the
+// device (the plane-assembly operands are allocated for the upper bound).
+__device__ __forceinline__ int64_t oz_cols(int64_t cols, const int32_t *nb, int64_t r3p, int64_t G) {
+  if (!nb) return cols;
+  const int64_t u = r3p + (int64_t)(*nb) * G;
+  return u < cols ? u : cols;
+}
+
+__global__ void k_oz_rowexp(const double *__restrict__ X, int64_t rows, int64_t ld, int64_t cols0,
+                            const int32_t *__restrict__ nb, int64_t r3p, int64_t G,
+                            int *__restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  const int64_t cols = oz_cols(cols0, nb, r3p, G);
+  const double *x = X + r * ld;
+  double m = 0.0;
+  for (int64_t c = lane; c < cols; c += 32) m = fmax(m, fabs(x[c]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) {
+    int ex = 0;
+    if (m > 0.0) frexp(m, &ex);
+    e[r] = ex;
+  }
+}
+
+// out[p][r][k] (slice stride sstride, row stride ldk) for k < ldk (zeros past
+// cols); thread per (row, 16 columns), 16-byte stores per slice
+template <int S>
+__global__ void k_oz_slice(const double *__restrict__ X, int64_t rows, int64_t ld, int64_t cols0,
+                           const int32_t *__restrict__ nb, int64_t r3p, int64_t G,
+                           const int *__restrict__ e, int8_t *__restrict__ out, int64_t ldk,
+                           int64_t sstride) {
+  const int64_t groups = ldk / 16;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * groups) return;
+  const int64_t r = t / groups, c0 = (t - r * groups) * 16;
+  const int64_t cols = oz_cols(cols0, nb, r3p, G);
+  if (c0 >= (cols + 63) / 64 * 64) return;  // never inside a K range
+  const int ex = e[r];
+  uint32_t w[S][4];
+#pragma unroll
+  for (int p = 0; p < S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+  const double *x = X + r * ld;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t c = c0 + j;
+    double a = c < cols ? ldexp(x[c], 6 - ex) : 0.0;  // |a| < 64
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+      const double d = rint(a);
+      a = (a - d) * 128.0;
+      const uint32_t b = (uint32_t)((int32_t)d & 0xff);
+      w[p][j >> 2] |= b << (8 * (j & 3));
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < S; ++p)
+    *reinterpret_cast<uint4 *>(out + p * sstride + r * ldk + c0) =
+        make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+// Tiled form for the bulk-copy GEMM: per slice, (tile of `TR` rows) x
+// (32-column step) blocks of TR*32 bytes, each already in the SWIZZLE_32B
+// K-major shared-memory image (row r at r*32, 16-byte chunk c at
+// c ^ ((r >> 2) & 1)).  Thread per (row, 16 columns), rows fastest; rows past
+// `rows` (tile padding) are zero.
+template <int S>
+__global__ void k_oz_slice_t(const double *__restrict__ X, int64_t rows, int64_t rows_pad,
+                             int64_t ld, int64_t cols0, const int32_t *__restrict__ nb,
+                             int64_t r3p, int64_t G, const int *__restrict__ e,
+                             int8_t *__restrict__ out, int TR, int64_t ksteps, int64_t sstride) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows_pad * ksteps * 2) return;
+  const int64_t r = t % rows_pad, g = t / rows_pad;
+  const int64_t cols = oz_cols(cols0, nb, r3p, G);
+  if (g * 16 >= (cols + 31) / 32 * 32) return;  // never inside a K range
+  const int ex = r < rows ? e[r] : 0;
+  uint32_t w[S][4];
+#pragma unroll
+  for (int p = 0; p < S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+  if (r < rows) {
+    const double *x = X + r * ld + g * 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      double a = g * 16 + j < cols ? ldexp(x[j], 6 - ex) : 0.0;  // |a| < 64
+#pragma unroll
+      for (int p = 0; p < S; ++p) {
+        const double d = rint(a);
+        a = (a - d) * 128.0;
+        w[p][j >> 2] |= ((uint32_t)((int32_t)d & 0xff)) << (8 * (j & 3));
+      }
+    }
+  }
+  const int64_t rt = r / TR, rr = r - rt * TR, ks = g >> 1, c = g & 1;
+  const int64_t off = (rt * ksteps + ks) * (int64_t)TR * 32 + rr * 32 + ((c ^ ((rr >> 2) & 1)) << 4);
+#pragma unroll
+  for (int p = 0; p < S; ++p)
+    *reinterpret_cast<uint4 *>(out + p * sstride + off) =
+        make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+// fp64-column ranges (nr per column tile) -> int8-slice ranges rounded out to
+// multiples of 32 (the UMMA K step) and merged when they touch; columns added
+// by the rounding hold zero operands for this tile (outside its band).
+__global__ void k_oz_ranges(const int64_t *__restrict__ in, int nr, int64_t ntiles, int64_t ldk,
+                            int64_t *__restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  int64_t lo_prev = -1, hi_prev = -1;
+  int k = 0;
+  for (int r = 0; r < nr; ++r) {
+    int64_t lo = in[(t * nr + r) * 2], hi = in[(t * nr + r) * 2 + 1];
+    if (hi <= lo) continue;
+    lo = lo / 32 * 32;
+    hi = (hi + 31) / 32 * 32;
+    if (hi > ldk) hi = ldk;
+    if (hi_prev >= 0 && lo <= hi_prev) {
+      if (hi > hi_prev) hi_prev = hi;
+      continue;
+    }
+    if (hi_prev >= 0) {
+      out[(t * nr + k) * 2] = lo_prev;
+      out[(t * nr + k) * 2 + 1] = hi_prev;
+      ++k;
+    }
+    lo_prev = lo;
+    hi_prev = hi;
+  }
+  if (hi_prev >= 0) {
+    out[(t * nr + k) * 2] = lo_prev;
+    out[(t * nr + k) * 2 + 1] = hi_prev;
+    ++k;
+  }
+  for (; k < nr; ++k) out[(t * nr + k) * 2] = out[(t * nr + k) * 2 + 1] = 0;
+}
+
+template <int S>
+struct OzCfg {
+  // one stage = all S slices of a 32-column K step of the A (128 rows) and
+  // B (64 rows) tiles, SWIZZLE_32B K-major (32-byte rows, 8-row atoms)
+  static constexpr int A_SLICE = BM * 32, B_SLICE = OZ_BN * 32;
+  static constexpr int STAGE = S * (A_SLICE + B_SLICE);
+  static constexpr int NST = (220 * 1024) / STAGE < 8 ? (220 * 1024) / STAGE : 8;
+  static constexpr int SMEM = NST * STAGE + 1024;
+};
+
+// K-major SWIZZLE_32B descriptor: 32-byte rows, 8-row atoms of 256 B (SBO),
+// LBO unused (1), layout type 6.  Chunk c of row r sits at c ^ ((r >> 2) & 1).
+__device__ __forceinline__ uint64_t make_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
+
+// C[m0.., n0..] (=, or += with ACC) = Ozaki product over this column tile's
+// K ranges.  One CTA per 128 x 64 tile; S accumulators in TMEM.  Thread 0
+// drives an NST-deep ring: per 32-column step it posts 2S bulk copies of
+// pre-tiled, pre-swizzled slice blocks (one mbarrier, tx-counted), and once
+// a step's operands landed issues its S(S+1)/2 slice MMAs round-robin over
+// the accumulators and commits them to the step's "empty" barrier.
+template <int S, bool ACC>
+__global__ void __launch_bounds__(THREADS)
+    k_oz_gemm(const int8_t *__restrict__ SA, int64_t sa_stride, const int8_t *__restrict__ SB,
+              int64_t sb_stride, int64_t ksteps, const int *__restrict__ ea,
+              const int *__restrict__ eb, const int64_t *__restrict__ ranges, int nr,
+              double *__restrict__ C, int64_t ldc, int64_t M, int64_t N) {
+  using Cfg = OzCfg<S>;
+  constexpr int NST = Cfg::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ __align__(8) uint64_t empty[NST];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n0 = (int64_t)blockIdx.x * OZ_BN, m0 = (int64_t)blockIdx.y * BM;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = make_idesc(BM, OZ_BN);
+
+  // K steps: 32-column pieces of this tile's ranges (multiples of 32)
+  const int64_t lo0 = ranges[(blockIdx.x * nr) * 2], hi0 = ranges[(blockIdx.x * nr) * 2 + 1];
+  const int64_t n_first = hi0 > lo0 ? (hi0 - lo0) / 32 : 0;
+  int64_t nsteps = n_first;
+  for (int r = 1; r < nr; ++r) {
+    const int64_t lo = ranges[(blockIdx.x * nr + r) * 2], hi = ranges[(blockIdx.x * nr + r) * 2 + 1];
+    if (hi > lo) nsteps += (hi - lo) / 32;
+  }
+  if (threadIdx.x == 0 && nsteps > 0) {
+    auto step_ks = [&](int64_t c) -> int64_t {
+      if (c < n_first) return lo0 / 32 + c;
+      c -= n_first;
+      for (int r = 1; r < nr; ++r) {
+        const int64_t lo = ranges[(blockIdx.x * nr + r) * 2],
+                      hi = ranges[(blockIdx.x * nr + r) * 2 + 1];
+        if (hi <= lo) continue;
+        const int64_t cnt = (hi - lo) / 32;
+        if (c < cnt) return lo / 32 + c;
+        c -= cnt;
+      }
+      return 0;
+    };
+    const uint32_t sbase = smem_u32(smem);
+    const int8_t *gA = SA + blockIdx.y * ksteps * (int64_t)Cfg::A_SLICE;
+    const int8_t *gB = SB + blockIdx.x * ksteps * (int64_t)Cfg::B_SLICE;
+    auto load = [&](int st, int64_t ks) {
+      const uint32_t base = sbase + st * Cfg::STAGE;
+      mbar_expect_tx(&full[st], (uint32_t)Cfg::STAGE);
+#pragma unroll
+      for (int p = 0; p < S; ++p) {
+        bulk_g2s(base + p * Cfg::A_SLICE, gA + p * sa_stride + ks * Cfg::A_SLICE, Cfg::A_SLICE,
+                 &full[st]);
+        bulk_g2s(base + S * Cfg::A_SLICE + p * Cfg::B_SLICE, gB + p * sb_stride + ks * Cfg::B_SLICE,
+                 Cfg::B_SLICE, &full[st]);
+      }
+    };
+    uint32_t fph = 0, eph = 0;  // parity bits per stage
+    for (int i = 0; i < NST && i < nsteps; ++i) load(i, step_ks(i));
+    const uint64_t desc0 = make_desc_sw32(sbase);
+    for (int64_t c = 0; c < nsteps; ++c) {
+      const int st = (int)(c % NST);
+      mbar_wait(&full[st], (fph >> st) & 1u);
+      fph ^= 1u << st;
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const uint64_t ds = desc0 + (uint64_t)((st * Cfg::STAGE) >> 4);
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+#pragma unroll
+        for (int t = j; t < S; ++t) {
+          const uint64_t da = ds + (uint64_t)((j * Cfg::A_SLICE) >> 4);
+          const uint64_t db = ds + (uint64_t)((S * Cfg::A_SLICE + (t - j) * Cfg::B_SLICE) >> 4);
+          umma_i8(tmem + t * OZ_BN, da, db, idesc, (c > 0 || j > 0) ? 1u : 0u);
+        }
+      }
+      umma_commit(&empty[st]);
+      // refill the stage of step c-1 with step c-1+NST once its MMAs retired
+      if (c >= 1 && c - 1 + NST < nsteps) {
+        const int sp = (int)((c - 1) % NST);
+        mbar_wait(&empty[sp], (eph >> sp) & 1u);
+        eph ^= 1u << sp;
+        load(sp, step_ks(c - 1 + NST));
+      }
+    }
+    // remaining MMA commits: steps max(0, nsteps-NST) .. nsteps-1
+    for (int64_t c = nsteps - NST > 0 ? nsteps - NST : 0; c < nsteps; ++c) {
+      const int sp = (int)(c % NST);
+      mbar_wait(&empty[sp], (eph >> sp) & 1u);
+      eph ^= 1u << sp;
+    }
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  // epilogue: warp w owns rows 32w..32w+31 (TMEM lanes); Horner over the
+  // accumulators t = S-1 .. 0, then the power-of-two row/column scale
+  const int64_t row = m0 + warp * 32 + lane;
+  const bool any = nsteps > 0;
+  const int er = (row < M) ? ea[row] : 0;
+#pragma unroll 1
+  for (int j = 0; j < OZ_BN; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = 0.0;
+#pragma unroll
+    for (int t = S - 1; t >= 0; --t) {
+      uint32_t a[8];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(t * OZ_BN + j);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]),
+                     "=r"(a[6]), "=r"(a[7])
+                   : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = fma(v[u], 0.0078125, (double)(int32_t)a[u]);
+    }
+    if (row < M) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t col = n0 + j + u;
+        if (col < N) {
+          const double val = any ? ldexp(v[u], er + eb[col] - 12) : 0.0;
+          double *dst = C + row * ldc + col;
+          if (ACC) *dst += val; else *dst = val;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
 }  // namespace tc8
 }  // namespace rsb
 
@@ -226,6 +578,111 @@ int rs_tc8_gemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb, i
   tc8::k_gemm_s8<BN><<<grid, tc8::THREADS, smem, as_stream(stream)>>>(A, lda, B, ldb, C, ldc, M, N,
                                                                       K);
   return check_launch("rs_tc8_gemm_s8");
+}
+
+
+/* Ozaki-split FP64 GEMM workspace for C (M x N) = A (M x K) B (N x K)^T. */
+int64_t rs_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int slices) {
+  const int64_t ldk = round_up(std::max<int64_t>(K, 1), 64);
+  return round_up(slices * (round_up(M, 128) + round_up(N, 64)) * ldk, 256) +
+         round_up((M + N) * 4, 256) +
+         round_up(ceil_div(N, tc8::OZ_BN) * 2 * (4 * 2 * 8), 256);  // ranges in + out
+}
+
+/* C (=, or += with accumulate) = A B^T in FP64 via `slices` int8 slices on
+ * tcgen05 (slices in {6, 7, 8}).  ranges (optional, NULL = [0, K)): nr fp64
+ * column ranges per 64-column tile of C (K columns outside them must hold
+ * zero B entries for that tile). */
+int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
+                    int slices, int accumulate, void *work, int64_t work_bytes,
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream);
+
+int rs_oz_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+               int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr, int slices,
+               int accumulate, void *work, int64_t work_bytes, void *stream) {
+  return rs_oz_gemm_cols(A, lda, B, ldb, C, ldc, M, N, K, ranges, nr, slices, accumulate, work,
+                         work_bytes, nullptr, 0, 0, stream);
+}
+
+/* as rs_oz_gemm; with nb != NULL only the first r3p + (*nb) * G columns of A
+ * and B are live (device-side count; the rest is never read). */
+int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
+                    int slices, int accumulate, void *work, int64_t work_bytes,
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream) {
+  RS_REQUIRE(M >= 1 && N >= 1 && K >= 1 && lda >= K && ldb >= K && ldc >= N,
+             "rs_oz_gemm: bad shape");
+  RS_REQUIRE(slices >= 6 && slices <= 8, "rs_oz_gemm: slices must be 6..8");
+  RS_REQUIRE(nr >= 1 && nr <= 4, "rs_oz_gemm: nr must be 1..4");
+  if (work_bytes < rs_oz_workspace_bytes(M, N, K, slices))
+    return fail(RS_ERR_CAPACITY, "rs_oz_gemm: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t ldk = round_up(K, 64), ksteps = ldk / 32;
+  const int64_t Mp = round_up(M, 128), Np = round_up(N, 64);
+  char *w = (char *)work;
+  int8_t *SA = (int8_t *)w;
+  int8_t *SB = SA + slices * Mp * ldk;
+  int *ea = (int *)(w + round_up(slices * (Mp + Np) * ldk, 256));
+  int *eb = ea + M;
+  int64_t *rg = (int64_t *)((char *)ea + round_up((M + N) * 4, 256));
+  int64_t *rin = rg + ceil_div(N, tc8::OZ_BN) * 4 * 2;  // 4 ranges x 2 per tile each
+  const int64_t ntn = ceil_div(N, tc8::OZ_BN);
+  int st;
+  tc8::k_oz_rowexp<<<(unsigned)ceil_div(M * 32, 256), 256, 0, s>>>(A, M, lda, K, nb, r3p, G, ea);
+  if ((st = check_launch("oz_rowexp A"))) return st;
+  tc8::k_oz_rowexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, s>>>(B, N, ldb, K, nb, r3p, G, eb);
+  if ((st = check_launch("oz_rowexp B"))) return st;
+  auto slice = [&](const double *X, int64_t rows, int64_t rows_pad, int TR, int64_t ld,
+                   const int *e, int8_t *out) {
+    const unsigned g = (unsigned)ceil_div(rows_pad * ksteps * 2, 256);
+    const int64_t ss = rows_pad * ldk;
+    switch (slices) {
+      case 6:
+        tc8::k_oz_slice_t<6><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
+                                                ksteps, ss);
+        break;
+      case 7:
+        tc8::k_oz_slice_t<7><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
+                                                ksteps, ss);
+        break;
+      default:
+        tc8::k_oz_slice_t<8><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
+                                                ksteps, ss);
+        break;
+    }
+    return check_launch("oz_slice");
+  };
+  if ((st = slice(A, M, Mp, 128, lda, ea, SA))) return st;
+  if ((st = slice(B, N, Np, 64, ldb, eb, SB))) return st;
+  const int64_t *use = ranges;
+  if (!ranges) {  // one full range per tile
+    std::vector<int64_t> h(ntn * nr * 2, 0);
+    for (int64_t t = 0; t < ntn; ++t) { h[t * nr * 2] = 0; h[t * nr * 2 + 1] = K; }
+    cudaMemcpyAsync(rin, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    use = rin;
+  }
+  tc8::k_oz_ranges<<<(unsigned)ceil_div(ntn, 128), 128, 0, s>>>(use, nr, ntn, ldk, rg);
+  if ((st = check_launch("oz_ranges"))) return st;
+  dim3 grid((unsigned)ntn, (unsigned)ceil_div(M, tc8::BM));
+  auto go = [&](auto kern, int smem) -> int {
+    cudaError_t e = cudaFuncSetAttribute((const void *)kern,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "oz smem: %s", cudaGetErrorString(e));
+    kern<<<grid, tc8::THREADS, smem, s>>>(SA, Mp * ldk, SB, Np * ldk, ksteps, ea, eb, rg, nr, C,
+                                          ldc, M, N);
+    return check_launch("oz_gemm");
+  };
+  ProfScope ps(s, "oz_mma");
+  if (slices == 6)
+    return accumulate ? go(tc8::k_oz_gemm<6, true>, tc8::OzCfg<6>::SMEM)
+                      : go(tc8::k_oz_gemm<6, false>, tc8::OzCfg<6>::SMEM);
+  if (slices == 7)
+    return accumulate ? go(tc8::k_oz_gemm<7, true>, tc8::OzCfg<7>::SMEM)
+                      : go(tc8::k_oz_gemm<7, false>, tc8::OzCfg<7>::SMEM);
+  return accumulate ? go(tc8::k_oz_gemm<8, true>, tc8::OzCfg<8>::SMEM)
+                    : go(tc8::k_oz_gemm<8, false>, tc8::OzCfg<8>::SMEM);
 }
 
 }  // extern "C"

@@ -435,7 +435,7 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
         core = v1 = v2 = v3 = None
     have_short = short is not None and short.local.rank > 0 and short.count > 0
     if have_short:
-        flags |= nat.ASM_SHORT
+        flags |= nat.ASM_SHORT | nat.asm_oz(nat.OZ_SLICES)
         lay = short.device_layout()
         rs, gamma, nb_max = short.local.rank, short.gamma, lay["nb_max"]
         ul, wl = lay["ul"], lay["wl"]

@@ -139,3 +139,26 @@ def test_tc8_gemm_s8_exact(nat, cuda, M, N, K):
     ref = a.astype(np.int64) @ b.astype(np.int64).T
     got = C.cpu().numpy()
     assert np.array_equal(got, ref), np.argwhere(got != ref)[:5]
+
+
+@pytest.mark.parametrize("M,N,K,slices", [(128, 64, 64, 7), (300, 200, 1040, 7), (1000, 256, 712, 8),
+                                          (77, 130, 32, 6), (513, 70, 3000, 7)])
+def test_oz_gemm_fp64(nat, cuda, M, N, K, slices):
+    """Ozaki-split FP64 GEMM on tcgen05 int8 vs numpy fp64: error within the
+    split bound K 2^(-7 S) max|A_i.| max|B_j.| (graded magnitudes per row)."""
+    rng = np.random.default_rng(M + N + K)
+    a = rng.normal(size=(M, K)) * np.exp(rng.uniform(-8, 8, size=(M, 1)))
+    b = rng.normal(size=(N, K)) * np.exp(rng.uniform(-8, 8, size=(N, 1)))
+    a[:, ::7] *= 1e-6   # mixed magnitudes inside a row
+    A = cuda.from_numpy(a).cuda()
+    B = cuda.from_numpy(b).cuda()
+    C = cuda.empty((M, N), dtype=cuda.float64, device="cuda")
+    L = nat.lib()
+    ws = cuda.empty(L.rs_oz_workspace_bytes(M, N, K, slices), dtype=cuda.uint8, device="cuda")
+    nat.check(L.rs_oz_gemm(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, None, 1,
+                           slices, 0, ws.data_ptr(), ws.numel(), nat.stream_ptr()), "oz")
+    cuda.cuda.synchronize()
+    ref = a @ b.T
+    scale = np.abs(a).max(1)[:, None] * np.abs(b).max(1)[None, :]
+    err = np.abs(C.cpu().numpy() - ref) / scale
+    assert err.max() <= 4 * K * 2.0 ** (-7 * slices + 1), err.max()
