@@ -219,6 +219,16 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
              int64_t x1_lo, int64_t x1_hi, double *out, void *work,
              int64_t work_bytes, void *side, int oz_slices);
 
+/* ---- build back: Ritz rows -> Tucker factors + shift projections + core in
+ * one call (rs_shift_project3 + rs_core behind a transpose).  Reference:
+ * rankred.py:151-177. */
+int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3,
+                                int64_t count, int64_t R);
+int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+            const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+            const double *z, const double *w, int64_t count, double *Z1, double *Z2,
+            double *Z3, double *core, void *work, int64_t work_bytes, void *stream);
+
 /* ---- SM partitions ------------------------------------------------------
  * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs
  * (green context, created once per (device, sms)); *sms_out = its SM count.

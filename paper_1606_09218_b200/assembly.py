@@ -523,7 +523,7 @@ def _mark(label: str) -> None:
 
 
 # SMs of the side stream's partition (0: ordinary stream on the whole device)
-_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "128"))
+_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "140"))
 
 
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
@@ -689,10 +689,11 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             for r in forced:
                 if r > limit:
                     raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
-        ranks, values, tails, zs = [], [], [], []
+        ranks, values, tails, zs, from_top = [], [], [], [], []
         for l in range(3):
             fr = forced[l] if forced is not None else None
             r = None
+            top = False
             if use_top:
                 theta = packed[l * b:(l + 1) * b]
                 r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n,
@@ -700,6 +701,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
                 if r is not None and fr is not None and fr > b:
                     r = None
                 Ul = U[l] if r is not None else None
+                top = r is not None
             if r is None:
                 bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 48 else 2 * b)
                 if b and bb > b and top_eig_supported(n, bb):
@@ -720,11 +722,34 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             ranks.append(int(r))
             values.append(sv)
             tails.append((float(tail[r]) if r < len(tail) else 0.0, total))
-            zs.append(Ul[:r].T.contiguous())
+            zs.append(Ul)
+            from_top.append(top)
         ranks = tuple(ranks)
         _mark("d2h")
+        core = None
+        if world == 1 and use_top and all(t is True for t in from_top):
+            # common case: factors + projections + core in one native call
+            r1, r2, r3 = ranks
+            flat = torch.empty(n * (r1 + r2 + r3) + r1 * r2 * r3, dtype=torch.float64,
+                               device="cuda")
+            zs = [flat[:n * r1].view(n, r1), flat[n * r1:n * (r1 + r2)].view(n, r2),
+                  flat[n * (r1 + r2):n * (r1 + r2 + r3)].view(n, r3)]
+            core = flat[n * (r1 + r2 + r3):].view(r1, r2, r3)
+            L = nat.lib()
+            ws = nat.Workspace.get(L.rs_back_workspace_bytes(n, r1, r2, r3, ds.count,
+                                                             int(plan.w_long.shape[0])), "core")
+            nat.check(L.rs_back(U.data_ptr(), b, n, r1, r2, r3, plan.table_dev.data_ptr(),
+                                plan.table_dev.shape[1], int(plan.w_long.shape[0]),
+                                nat.ptr(starts), z.data_ptr(), plan.w_long.data_ptr(), ds.count,
+                                zs[0].data_ptr(), zs[1].data_ptr(), zs[2].data_ptr(),
+                                core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr()),
+                      "rs_back")
+        else:
+            zs = [zl[:r].T.contiguous() for zl, r in zip(zs, ranks)]
         spectrum = SvdSpectrum(values=tuple(values), vectors=tuple(zs))
-        if world == 1:
+        if core is not None:
+            pass
+        elif world == 1:
             core = shifted_core(plan.table_dev, n, zs, starts, z, plan.w_long)
         else:
             core = sharded_sum(shifted_core(plan.table_dev, n, zs, starts[p_lo:p_hi].contiguous(),

@@ -25,8 +25,23 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 extern std::vector<ProfRec> g_prof;
+extern std::vector<cudaEvent_t> g_prof_pool;  // recycled timing events
 extern std::mutex g_prof_mu;
 extern bool g_prof_on;
+
+inline cudaEvent_t prof_event() {
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_pool.empty()) {
+      cudaEvent_t e = g_prof_pool.back();
+      g_prof_pool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
 
 struct ProfScope {
   cudaStream_t s;
@@ -34,8 +49,8 @@ struct ProfScope {
   cudaEvent_t a = nullptr, b = nullptr;
   ProfScope(cudaStream_t s_, const char *n_) : s(s_), name(n_) {
     if (!g_prof_on) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+    a = prof_event();
+    b = prof_event();
     cudaEventRecord(a, s);
   }
   ~ProfScope() {

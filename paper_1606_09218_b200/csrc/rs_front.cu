@@ -159,3 +159,77 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ back
+// After the host picked the ranks: Ritz rows -> Tucker factors (transpose),
+// per-shift projections and the RHOSVD core, in one host call (reference:
+// rankred.py:151-177 with the shift regrouping of rankred.py:82-126).
+namespace {
+__global__ void k_ritz_to_factors(const double *__restrict__ U, int64_t b, int64_t n, int r1,
+                                  int r2, int r3, double *__restrict__ Z1, double *__restrict__ Z2,
+                                  double *__restrict__ Z3) {
+  const int64_t tot = n * (int64_t)(r1 + r2 + r3);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / (r1 + r2 + r3);
+    int a = (int)(e - i * (r1 + r2 + r3));
+    int l = 0;
+    double *Z = Z1;
+    int r = r1;
+    if (a >= r1) {
+      a -= r1;
+      l = 1;
+      Z = Z2;
+      r = r2;
+      if (a >= r2) {
+        a -= r2;
+        l = 2;
+        Z = Z3;
+        r = r3;
+      }
+    }
+    Z[i * r + a] = U[((int64_t)l * b + a) * n + i];
+  }
+}
+}  // namespace
+
+extern "C" {
+int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3, int64_t r1, int64_t r2,
+                      int64_t r3, int64_t n, const double *table, int64_t ld_table, int64_t R,
+                      int64_t n_shift, double *TT1, double *TT2, double *TT3, void *stream);
+int64_t rs_core_workspace_bytes(int64_t r1, int64_t r2, int64_t r3, int64_t count, int64_t R);
+int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1, int64_t r2,
+            int64_t r3, int64_t n_shift, int64_t R, const int64_t *shift, const double *z,
+            const double *w, int64_t count, double *core, void *work, int64_t work_bytes,
+            void *stream);
+
+int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3, int64_t count,
+                                int64_t R) {
+  return round_up((r1 + r2 + r3) * n * R * 8, 256) + rs_core_workspace_bytes(r1, r2, r3, count, R);
+}
+
+/* U: (3, b, n) Ritz rows (descending); Z_l (n, r_l) = U[l, :r_l]^T; core
+ * (r1, r2, r3) of the shift-structured long part. */
+int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+            const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+            const double *z, const double *w, int64_t count, double *Z1, double *Z2, double *Z3,
+            double *core, void *work, int64_t work_bytes, void *stream) {
+  RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && r1 <= b && r2 <= b && r3 <= b && n >= 2,
+             "rs_back: bad ranks");
+  if (work_bytes < rs_back_workspace_bytes(n, r1, r2, r3, count, R))
+    return fail(RS_ERR_CAPACITY, "rs_back: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int64_t tot = n * (r1 + r2 + r3);
+  k_ritz_to_factors<<<(unsigned)std::min<int64_t>(ceil_div(tot, 256), 1024), 256, 0, s>>>(
+      U, b, n, (int)r1, (int)r2, (int)r3, Z1, Z2, Z3);
+  int st;
+  if ((st = check_launch("rs_back factors"))) return st;
+  double *TT1 = (double *)work, *TT2 = TT1 + r1 * n * R, *TT3 = TT2 + r2 * n * R;
+  if ((st = rs_shift_project3(Z1, Z2, Z3, r1, r2, r3, n, table, ld_table, R, n, TT1, TT2, TT3,
+                              stream)))
+    return st;
+  char *cw = (char *)work + round_up((r1 + r2 + r3) * n * R * 8, 256);
+  return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
+                 rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
+}
+}  // extern "C"

@@ -11,6 +11,7 @@ namespace rsb {
 thread_local char g_err[512] = "";
 std::atomic<int64_t> g_launches{0};
 std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 
@@ -945,10 +946,10 @@ int64_t rs_launch_count(void) { return g_launches.load(); }
 
 int rs_prof_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  if (on) {
+  if (on) {  // recycle the recorded events (no create/destroy in timed regions)
     for (auto &r : g_prof) {
-      cudaEventDestroy(r.a);
-      cudaEventDestroy(r.b);
+      g_prof_pool.push_back(r.a);
+      g_prof_pool.push_back(r.b);
     }
     g_prof.clear();
   }
