@@ -177,7 +177,19 @@ def _trusted_tucker(core, factors) -> TuckerTensor:
 
 # ------------------------------------------------------- explicit operands
 def _thin_svd_dev(a):
-    return eig_desc(gram(a))
+    """Left singular pairs by the reference's route (``rankred.py:82-102``):
+    Gram + eigh on DMMA for very wide matrices (K > 8n and K > 512), else a
+    direct SVD (cuSOLVER) -- the Gram route squares the condition number,
+    which the ALS subspaces notice at the 1e-10 level."""
+    n, k = int(a.shape[0]), int(a.shape[1])
+    if k > 8 * n and k > 512:
+        return eig_desc(gram(a))
+    torch = nat._torch()
+    try:
+        u, sv, _ = torch.linalg.svd(a, full_matrices=False)
+    except RuntimeError as exc:
+        raise NumericalError(f"SVD failed on a {tuple(a.shape)} side matrix") from exc
+    return sv, fix_signs(u)
 
 
 def side_svd(c: CanonicalTensor, weighted: bool = True) -> SvdSpectrum:
