@@ -116,6 +116,55 @@ def rs_energy(rs, system, reference, check_separation: bool = True) -> float:
     return 0.5 * float(dd_sum(terms))
 
 
+def _fd_rows(u, h: float):
+    """Central differences inside, one-sided at the two ends, on every column
+    (``observables.py:132-139``); device tensor in, device tensor out."""
+    out = torch_().empty_like(u)
+    out[1:-1] = (u[2:] - u[:-2]) / (2.0 * h)
+    out[0] = (u[1] - u[0]) / h
+    out[-1] = (u[-1] - u[-2]) / h
+    return out
+
+
+def torch_():
+    return nat._torch()
+
+
+def grad_long(rs, h: Optional[float] = None):
+    """Discrete gradient of the long part, one tensor per component
+    (``observables.py:142-172``): the differentiated mode's factor gets the 1D
+    finite difference; Tucker factors are re-orthogonalised by a QR whose R is
+    folded into the core.  Runs on the device (cuSOLVER QR)."""
+    from .formats import to_device
+    torch = torch_()
+    if isinstance(rs, (RSCanonical, RSTucker)):
+        h = rs.grid.h
+        long = rs.long
+    else:
+        long = rs
+        if h is None:
+            raise ConfigError("grad_long needs the mesh size for a bare tensor")
+    comps = []
+    if isinstance(long, CanonicalTensor):
+        facs = [to_device(f) for f in long.factors]
+        w = to_device(long.weights)
+        for mode in range(3):
+            f = list(facs)
+            f[mode] = _fd_rows(facs[mode], h)
+            comps.append(CanonicalTensor(w, tuple(f)))
+    elif isinstance(long, TuckerTensor):
+        for mode in range(3):
+            f = list(long.factors)
+            q, r = torch.linalg.qr(_fd_rows(f[mode], h))
+            core = torch.movedim(torch.tensordot(r, torch.movedim(long.core, mode, 0), dims=1),
+                                 0, mode).contiguous()
+            f[mode] = q.contiguous()
+            comps.append(TuckerTensor(core, tuple(f)))
+    else:
+        raise ConfigError(f"grad_long cannot handle {type(long).__name__}")
+    return tuple(comps)
+
+
 def _pair_sums(system, reference, r_l: int, targets, mode: int):
     torch = nat._torch()
     idx, z = _system_arrays(system)

@@ -21,7 +21,7 @@ import numpy as np
 import rstensor as rt  # the reference (pkg/src/rstensor)
 from rstensor.container import write_reference, write_rs
 from rstensor.formats import eval_rs_many
-from rstensor.observables import rs_energy
+from rstensor.observables import grad_long, rs_energy
 
 sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..", "..")))
 from make_golden import sha, tiny  # noqa: E402
@@ -69,6 +69,11 @@ def main():
     cfg = cfg_for(32, 8.0, 15, 7, "newton", 1.0, 1e-6, 1e-8, 3, "tucker")
     res, out["tiny_tucker_als3"] = case("tiny_tucker_als3", tiny_sys, cfg)
     write_rs(res.rs, os.path.join(HERE, "next_tiny_tucker.rsc"))
+    # grad_long of the reference's own RS tensor: the
+    # container above carries its inputs, these are its dense components
+    comps = grad_long(res.rs)
+    np.savez_compressed(os.path.join(HERE, "next_tiny_grad.npz"),
+                        **{f"g{a}": c.dense(limit=32 ** 3) for a, c in enumerate(comps)})
     ref = rt.reference_for(cfg_for(32, 8.0, 15, 7, "newton", 1.0, 1e-6, 1e-8, 0, "tucker"))
     write_reference(ref, os.path.join(HERE, "next_tiny_reference.rsc"))
     m = configs.MANIFEST["C1"]
@@ -83,6 +88,12 @@ def main():
         res, out[name] = case(name, s, cfg)
         if fmt == "canonical" and sweeps == 3:
             write_rs(res.rs, os.path.join(HERE, "next_C1_canonical.rsc"))
+            comps = grad_long(res.rs)
+            rng = np.random.default_rng(7)
+            smp = rng.integers(0, m["n"], size=(4000, 3))
+            np.savez_compressed(os.path.join(HERE, "next_C1_canonical_grad.npz"), sample_idx=smp,
+                                **{f"g{a}": c.dense(limit=m["n"] ** 3)[smp[:, 0], smp[:, 1], smp[:, 2]]
+                                   for a, c in enumerate(comps)})
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".rsc"):
             with open(os.path.join(HERE, f), "rb") as fh:

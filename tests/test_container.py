@@ -81,3 +81,22 @@ def test_container_of_a_device_build(cuda, tmp_path):
     assert np.array_equal(g0, g1)
     assert hashlib.sha256(p.read_bytes()).hexdigest() == hashlib.sha256(
         container.encode_sections(container.rs_sections(back))).hexdigest()
+
+
+@pytest.mark.gpu
+def test_grad_long_matches_reference(cuda):
+    """grad_long of the reference's RS tensors, read from
+    the reference-written containers: dense components vs the reference."""
+    import paper_1606_09218_b200 as rt
+    rs = container.read_rs(os.path.join(GOLD, "next_tiny_tucker.rsc"))
+    g = np.load(os.path.join(GOLD, "next_tiny_grad.npz"))
+    for a, c in enumerate(rt.grad_long(rs)):
+        ref = g[f"g{a}"]
+        assert np.max(np.abs(c.dense(limit=1 << 20) - ref)) <= 1e-12 * np.abs(ref).max()
+    rs = container.read_rs(os.path.join(GOLD, "next_C1_canonical.rsc"))
+    g = np.load(os.path.join(GOLD, "next_C1_canonical_grad.npz"))
+    s = g["sample_idx"]
+    for a, c in enumerate(rt.grad_long(rs)):
+        d = c.dense(limit=1 << 24)[s[:, 0], s[:, 1], s[:, 2]]
+        ref = g[f"g{a}"]
+        assert np.max(np.abs(d - ref)) <= 1e-12 * np.abs(ref).max()
