@@ -223,11 +223,17 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
  * one call (rs_shift_project3 + rs_core behind a transpose).  Reference:
  * rankred.py:151-177. */
 int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3,
-                                int64_t count, int64_t R);
+                                int64_t count, int64_t R, int64_t nq);
 int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
             const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
             const double *z, const double *w, int64_t count, double *Z1, double *Z2,
-            double *Z3, double *core, void *work, int64_t work_bytes, void *stream);
+            double *Z3, double *core, void *work, int64_t work_bytes, void *stream,
+            /* optional (NULL: particle-K core): the x3-bucket layout of the
+             * short part (rs_front) -> the core GEMM runs over occupied x3
+             * values x terms instead of particles x terms */
+            const int32_t *c1, const int32_t *c2, const double *zq,
+            const int32_t *bstart, const int32_t *bc3, const int32_t *nb,
+            int64_t nq /* occupied x3 values if known on the host, else 0 */);
 
 /* ---- SM partitions ------------------------------------------------------
  * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs

@@ -66,9 +66,10 @@ SIGNATURES = {
     "rs_front_offsets": (_i32, [_i64, _i64, ctypes.POINTER(ctypes.c_int64)]),
     "rs_front": (_i32, [_ptr, _ptr, _i64, ctypes.c_double, _i64, _ptr, _i64, _ptr,
                         _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i32]),
-    "rs_back_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64]),
+    "rs_back_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _i64]),
     "rs_back": (_i32, [_ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64,
-                       _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
+                       _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                       _ptr, _i64]),
     "rs_partition_stream": (_i32, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int)]),
     "rs_oz_workspace_bytes": (_i64, [_i64, _i64, _i64, _i32]),

@@ -675,8 +675,12 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             launch_prefetch()
             prefetch_pending = False
         parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
+        if front is not None:  # occupied x3 values: sizes the bucket-K core
+            nb_view = front["buf"][front["nb"] - front["buf"].data_ptr():][:4].view(torch.int32)
+            parts.append(nb_view.to(torch.float64))
         _mark("eig_enq")
         packed = to_host(torch.cat(parts))
+        nq_host = int(packed[-1]) if front is not None else 0
         nt_ = 3 * b + (3 if use_top else 0)
         if packed[nt_ + 1] >= 0:
             node = _decode_key(int(packed[nt_ + 1]), n)
@@ -727,9 +731,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         ranks = tuple(ranks)
         _mark("d2h")
         core = None
-        if world == 1 and use_top and all(t is True for t in from_top):
-            # common case: factors + projections + core in one native call
+        if world == 1:
+            # factors + projections + core in one native call (bucket-K core)
             r1, r2, r3 = ranks
+            Ub, bu = U, b
+            if not (use_top and all(t is True for t in from_top)):
+                # escalated modes: gather their leading rows into one (3, r, n) block
+                bu = max(ranks)
+                Ub = torch.zeros((3, bu, n), dtype=torch.float64, device="cuda")
+                for l, (zl, r) in enumerate(zip(zs, ranks)):
+                    Ub[l, :r] = zl[:r]
             flat = torch.empty(n * (r1 + r2 + r3) + r1 * r2 * r3, dtype=torch.float64,
                                device="cuda")
             zs = [flat[:n * r1].view(n, r1), flat[n * r1:n * (r1 + r2)].view(n, r2),
@@ -737,12 +748,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             core = flat[n * (r1 + r2 + r3):].view(r1, r2, r3)
             L = nat.lib()
             ws = nat.Workspace.get(L.rs_back_workspace_bytes(n, r1, r2, r3, ds.count,
-                                                             int(plan.w_long.shape[0])), "core")
-            nat.check(L.rs_back(U.data_ptr(), b, n, r1, r2, r3, plan.table_dev.data_ptr(),
+                                                             int(plan.w_long.shape[0]), nq_host),
+                                   "core")
+            nat.check(L.rs_back(Ub.data_ptr(), bu, n, r1, r2, r3, plan.table_dev.data_ptr(),
                                 plan.table_dev.shape[1], int(plan.w_long.shape[0]),
                                 nat.ptr(starts), z.data_ptr(), plan.w_long.data_ptr(), ds.count,
                                 zs[0].data_ptr(), zs[1].data_ptr(), zs[2].data_ptr(),
-                                core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr()),
+                                core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr(),
+                                *((prep["c1"], prep["c2"], prep["zq"], front["bstart"],
+                                   front["bc3"], front["nb"]) if front is not None
+                                  else (None,) * 6), nq_host),
                       "rs_back")
         else:
             zs = [zl[:r].T.contiguous() for zl, r in zip(zs, ranks)]

@@ -191,9 +191,109 @@ __global__ void k_ritz_to_factors(const double *__restrict__ U, int64_t b, int64
     Z[i * r + a] = U[((int64_t)l * b + a) * n + i];
   }
 }
+// Core by mode-3 buckets: core[(a,b), c] = sum_{(q,k)} H[(a,b),(q,k)] T3[c,(q,k)]
+// with H[(a,b),(q,k)] = sum_{i in bucket q} zq_i w_k TT1[a, n-c1_i, k] TT2[b, n-c2_i, k]
+// and T3[c,(q,k)] = TT3[c, n - x3_q, k]: the K of the core GEMM drops from
+// N R_l (particles x terms) to (occupied x3 values) x R_l.
+constexpr int CH_CHUNK = 32;   // bucket copies staged per pass
+constexpr int CH_RMAX = 24;
+
+// TTt[s][k][a] = TT[a][s][k]: per-(shift, term) vectors contiguous in a
+__global__ void k_tt_transpose(const double *__restrict__ TT, int r, int64_t n, int R,
+                               double *__restrict__ TTt) {
+  const int64_t tot = (int64_t)r * n * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e % r, sk = e / r;  // output order (s, k, a)
+    const int64_t sh = sk / R, k = sk - sh * R;
+    TTt[e] = TT[(a * n + sh) * R + k];
+  }
+}
+
+// Block = (bucket q, CH_TA consecutive a); thread = one b (blockDim >= r2).
+// Per staged chunk of the bucket's copies and per term k: the copies' TT2
+// vectors (all b) and TT1 entries (the block's a) land in shared memory with
+// coalesced loads; every thread accumulates CH_TA x R outputs in registers
+// and finally writes its rows' R-wide segments.
+constexpr int CH_TA = 2;
+__global__ void k_core_h(const double *__restrict__ TT1t, const double *__restrict__ TT2t, int r1,
+                         int r2, int64_t n, int R, const double *__restrict__ w,
+                         const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+                         const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+                         double *__restrict__ H, int64_t ldH) {
+  extern __shared__ double sh[];
+  double *sY = sh;                          // CH_CHUNK x r2
+  double *sX = sh + CH_CHUNK * r2;          // CH_CHUNK x CH_TA
+  const int q = blockIdx.y;
+  const int a0 = blockIdx.x * CH_TA;
+  const int bcol = threadIdx.x;
+  double acc[CH_TA][CH_RMAX];
+#pragma unroll
+  for (int u = 0; u < CH_TA; ++u)
+#pragma unroll
+    for (int k = 0; k < CH_RMAX; ++k) acc[u][k] = 0.0;
+  const int p_lo = bstart[q], p_hi = bstart[q + 1];
+  for (int i0 = p_lo; i0 < p_hi; i0 += CH_CHUNK) {
+    const int cnt = min(CH_CHUNK, p_hi - i0);
+#pragma unroll
+    for (int k = 0; k < CH_RMAX; ++k) {
+      if (k < R) {
+        for (int e = threadIdx.x; e < cnt * r2; e += blockDim.x) {
+          const int j = e / r2, t = e - j * r2;
+          sY[e] = TT2t[((int64_t)(n - c2[i0 + j]) * R + k) * r2 + t];
+        }
+        for (int e = threadIdx.x; e < cnt * CH_TA; e += blockDim.x) {
+          const int j = e / CH_TA, u = e - j * CH_TA;
+          const int i = i0 + j;
+          sX[e] = a0 + u < r1 ? zq[i] * w[k] * TT1t[((int64_t)(n - c1[i]) * R + k) * r1 + a0 + u]
+                              : 0.0;
+        }
+        __syncthreads();
+        if (bcol < r2) {
+          for (int j = 0; j < cnt; ++j) {
+            const double y = sY[j * r2 + bcol];
+#pragma unroll
+            for (int u = 0; u < CH_TA; ++u) acc[u][k] = fma(sX[j * CH_TA + u], y, acc[u][k]);
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (bcol < r2) {
+#pragma unroll
+    for (int u = 0; u < CH_TA; ++u) {
+      const int a = a0 + u;
+      if (a >= r1) continue;
+      double *dst = H + ((int64_t)a * r2 + bcol) * ldH + (int64_t)q * R;
+#pragma unroll
+      for (int k = 0; k < CH_RMAX; ++k)
+        if (k < R) dst[k] = acc[u][k];
+      if (q == (int)gridDim.y - 1)  // even-K padding column(s)
+        for (int64_t c = (int64_t)(q + 1) * R; c < ldH; ++c) H[((int64_t)a * r2 + bcol) * ldH + c] = 0.0;
+    }
+  }
+}
+
+// T3[c, q*R + k] = TT3[c, n - bc3[q], k] for occupied buckets, 0 past *nb
+__global__ void k_core_t3(const double *__restrict__ TT3, int r3, int64_t n, int R,
+                          const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
+                          int64_t nq, double *__restrict__ T3, int64_t ldT) {
+  const int64_t tot = (int64_t)r3 * ldT;
+  const int nb = *nbp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / ldT, col = e - c * ldT;
+    const int64_t q = col / R;
+    const int k = (int)(col - q * R);
+    T3[e] = (q < nb && q < nq) ? TT3[((int64_t)c * n + (n - bc3[q])) * R + k] : 0.0;
+  }
+}
 }  // namespace
 
 extern "C" {
+int rs_gemm_nt(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+               int64_t M, int64_t N, int64_t K, void *stream);
 int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3, int64_t r1, int64_t r2,
                       int64_t r3, int64_t n, const double *table, int64_t ld_table, int64_t R,
                       int64_t n_shift, double *TT1, double *TT2, double *TT3, void *stream);
@@ -203,9 +303,16 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
             const double *w, int64_t count, double *core, void *work, int64_t work_bytes,
             void *stream);
 
+static int64_t ldh_of(int64_t nq, int64_t R) { return round_up(std::max<int64_t>(nq * R, 2), 2); }
+
 int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3, int64_t count,
-                                int64_t R) {
-  return round_up((r1 + r2 + r3) * n * R * 8, 256) + rs_core_workspace_bytes(r1, r2, r3, count, R);
+                                int64_t R, int64_t nq_host) {
+  // projections | max(particle-K core scratch, bucket-K H + T3)
+  const int64_t nq = nq_host > 0 ? nq_host : std::min<int64_t>(n, count), ld = ldh_of(nq, R);
+  const int64_t hb = round_up(r1 * r2 * ld * 8, 256) + round_up(r3 * ld * 8, 256) +
+                     (r1 + r2) * n * R * 8;
+  return round_up((r1 + r2 + r3) * n * R * 8, 256) +
+         std::max<int64_t>(rs_core_workspace_bytes(r1, r2, r3, count, R), hb);
 }
 
 /* U: (3, b, n) Ritz rows (descending); Z_l (n, r_l) = U[l, :r_l]^T; core
@@ -213,10 +320,12 @@ int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3, i
 int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
             const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
             const double *z, const double *w, int64_t count, double *Z1, double *Z2, double *Z3,
-            double *core, void *work, int64_t work_bytes, void *stream) {
+            double *core, void *work, int64_t work_bytes, void *stream,
+            const int32_t *c1, const int32_t *c2, const double *zq, const int32_t *bstart,
+            const int32_t *bc3, const int32_t *nb, int64_t nq_host) {
   RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && r1 <= b && r2 <= b && r3 <= b && n >= 2,
              "rs_back: bad ranks");
-  if (work_bytes < rs_back_workspace_bytes(n, r1, r2, r3, count, R))
+  if (work_bytes < rs_back_workspace_bytes(n, r1, r2, r3, count, R, nq_host))
     return fail(RS_ERR_CAPACITY, "rs_back: workspace too small");
   cudaStream_t s = as_stream(stream);
   const int64_t tot = n * (r1 + r2 + r3);
@@ -229,7 +338,37 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
                               stream)))
     return st;
   char *cw = (char *)work + round_up((r1 + r2 + r3) * n * R * 8, 256);
-  return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
-                 rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
+  // the particle-K Khatri-Rao GEMM is latency-bound and cheap below ~1e10
+  // flops (C1-C3); the bucket-K form wins once N R_l r1 r2 r3 dominates (C4, C5)
+  const double kr_flops = 2.0 * (double)r1 * r2 * r3 * (double)count * R;
+  if (!bstart || nq_host <= 0 || R > CH_RMAX || kr_flops < 1e10 || r2 > 1024)
+    return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
+                   rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
+  // bucket-K core: H (r1 r2 x nq R) on CUDA cores, then one DMMA GEMM
+  // nq_host: the occupied x3 count the host read back (0: the upper bound)
+  const int64_t nq = nq_host > 0 ? nq_host : std::min<int64_t>(n, count), ldH = ldh_of(nq, R);
+  double *H = (double *)cw;
+  double *T3 = (double *)(cw + round_up(r1 * r2 * ldH * 8, 256));
+  double *TT1t = (double *)((char *)T3 + round_up(r3 * ldH * 8, 256));
+  double *TT2t = TT1t + r1 * n * R;
+  ProfScope ps(s, "core");
+  k_tt_transpose<<<(unsigned)std::min<int64_t>(ceil_div(r1 * n * R, 256), 4096), 256, 0, s>>>(
+      TT1, (int)r1, n, (int)R, TT1t);
+  k_tt_transpose<<<(unsigned)std::min<int64_t>(ceil_div(r2 * n * R, 256), 4096), 256, 0, s>>>(
+      TT2, (int)r2, n, (int)R, TT2t);
+  if ((st = check_launch("core transpose"))) return st;
+  RS_REQUIRE(r2 <= 1024, "rs_back: r2 = %lld exceeds the H kernel's block", (long long)r2);
+  const int threads = (int)round_up(r2, 32);
+  const size_t smem = (size_t)CH_CHUNK * (r2 + CH_TA) * 8;
+  cudaError_t e = cudaFuncSetAttribute((const void *)k_core_h,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
+  k_core_h<<<dim3((unsigned)ceil_div(r1, CH_TA), (unsigned)nq), threads, smem, s>>>(
+      TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq, bstart, H, ldH);
+  if ((st = check_launch("core_h"))) return st;
+  k_core_t3<<<(unsigned)std::min<int64_t>(ceil_div(r3 * ldH, 256), 4096), 256, 0, s>>>(
+      TT3, (int)r3, n, (int)R, bc3, nb, nq, T3, ldH);
+  if ((st = check_launch("core_t3"))) return st;
+  return rs_gemm_nt(H, ldH, T3, ldH, core, r3, r1 * r2, r3, ldH, stream);
 }
 }  // extern "C"
