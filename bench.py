@@ -350,9 +350,17 @@ def main():
         pos_e.copy_(pos_h, non_blocking=True)
         q_e.copy_(q_h, non_blocking=True)
         step.last = None
-        if os.environ.get("BENCH_E2E", "pipelined") == "prefetch":
+        mode = os.environ.get("BENCH_E2E", "pipelined")
+        if mode == "prefetch":
             step(rt.DeviceParticles(pos_e, q_e, system.box))
             out_h.copy_(step.last, non_blocking=True)
+        elif mode == "grouped":
+            # short planes prefetched in 8 groups; each group's Tucker part and
+            # device->host copy start as soon as its planes are final
+            res = rt.build_rs(rt.DeviceParticles(pos_e, q_e, system.box), cfg,
+                              prefetch_dense=(x1_lo, x1_hi), prefetch_groups=8,
+                              group=dist.group.WORLD if world > 1 else None)
+            rt.dense_rs(res.rs, limit=1 << 62, x1_range=(x1_lo, x1_hi), out=out_h)
         else:
             res = rt.build_rs(rt.DeviceParticles(pos_e, q_e, system.box), cfg,
                               group=dist.group.WORLD if world > 1 else None)

@@ -115,6 +115,13 @@ int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R,
  * (iters steps, CGS2), Rayleigh-Ritz, cyclic Jacobi.  evals (nmat x b,
  * descending), U (nmat x b x n, rows = Ritz vectors, largest-|entry|
  * positive), trace (nmat).  b even, b <= min(n, 96). */
+/* (a8) full spectra of m symmetric n x n matrices (cuSOLVER syevd, one forked
+ * stream per matrix, no host sync): G is overwritten with the eigenvectors as
+ * the ROWS of each row-major block, evals (m x n) ascending.  Reference:
+ * rankred.py:92 (eigh of the side Gram). */
+int64_t rs_eigh_workspace_bytes(int64_t m, int64_t n);
+int rs_eigh(double *G, int64_t m, int64_t n, double *evals, void *work, int64_t work_bytes,
+            void *stream);
 int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b);
 int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters,
               double *evals, double *U, double *trace, void *work, int64_t work_bytes,
@@ -167,6 +174,23 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3,
                        int64_t x1_hi, int flags, double *out, void *work,
                        int64_t work_bytes, void *stream);
 
+/* Short-range part by dense-L0 gather (low window overlap):
+ * out[((x1-x1_lo)*n + x2)*n + x3] (= or +=) sum_p zq_p L0[x - c_p + gamma]
+ * over the same bucket layout as rs_assemble_planes; L0 (W^3, W = 2 gamma+1)
+ * from rs_short_l0_table.  rs_short_method picks RS_SHORT_GEMM (plane GEMM)
+ * or RS_SHORT_L0 from the mean window overlap (env RSB200_SHORT=gemm|l0
+ * forces one).  Reference: formats.py:423-445 (dense_cct). */
+#define RS_SHORT_GEMM 0
+#define RS_SHORT_L0 1
+int rs_short_method(int64_t n, int64_t count, int64_t gamma, int64_t Rs);
+int64_t rs_short_l0_bytes(int64_t gamma);
+int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
+                      double *L0, void *stream);
+int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32_t *c1,
+                         const int32_t *c2, const double *zq, const int32_t *bstart,
+                         const int32_t *bc3, const int32_t *nb_dev, int64_t x1_lo,
+                         int64_t x1_hi, int accumulate, double *out, void *stream);
+
 /* Bucket layout of the short-range copies from the x3 occupancy counts
  * cnt3 (n): bc3 (capacity n), bstart (capacity n+1), *nb (device int). */
 int rs_short_layout(const int32_t *cnt3, int64_t n, int32_t *bstart, int32_t *bc3,
@@ -217,7 +241,11 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
               * (after the bucket table; NULL side = none) */
              const double *ul, const double *wl, int64_t Rs, int64_t gamma,
              int64_t x1_lo, int64_t x1_hi, double *out, void *work,
-             int64_t work_bytes, void *side, int oz_slices);
+             int64_t work_bytes, void *side, int oz_slices,
+             /* planes in groups of `group` (<= 0: one group); events[g]
+              * (caller-created cudaEvent_t, or NULL) recorded on `side` when
+              * group g is complete */
+             int64_t group, void **events);
 
 /* ---- build back: Ritz rows -> Tucker factors + shift projections + core in
  * one call (rs_shift_project3 + rs_core behind a transpose).  Reference:

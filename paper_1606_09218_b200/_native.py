@@ -45,6 +45,8 @@ SIGNATURES = {
     "rs_gemm_nt": (_i32, [_ptr, _i64, _ptr, _i64, _ptr, _i64, _i64, _i64, _i64, _ptr]),
     "rs_shift_project": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _i64, _i64, _i64, _ptr, _ptr]),
     "rs_shift_hist": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _ptr]),
+    "rs_eigh_workspace_bytes": (_i64, [_i64, _i64]),
+    "rs_eigh": (_i32, [_ptr, _i64, _i64, _ptr, _ptr, _i64, _ptr]),
     "rs_topeig_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "rs_topeig": (_i32, [_ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr]),
     "rs_shift_project3": (_i32, [_ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _i64,
@@ -57,6 +59,11 @@ SIGNATURES = {
                                   _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _i64, _i32,
                                   _ptr, _ptr, _i64, _ptr]),
     "rs_short_layout": (_i32, [_ptr, _i64, _ptr, _ptr, _ptr, _ptr]),
+    "rs_short_method": (_i32, [_i64, _i64, _i64, _i64]),
+    "rs_short_l0_bytes": (_i64, [_i64]),
+    "rs_short_l0_table": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr]),
+    "rs_assemble_short_l0": (_i32, [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i64,
+                                    _i64, _i32, _ptr, _ptr]),
     "rs_eval_tucker": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr]),
     "rs_eval_cct": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i64, _ptr, _ptr, _ptr]),
     "rs_pair_sums": (_i32, [_ptr, _i64, _i64, _ptr, _i64, _dbl, _ptr, _ptr, _i64, _ptr, _i64, _i32,
@@ -65,7 +72,8 @@ SIGNATURES = {
     "rs_sum_dd": (_i32, [_ptr, _i64, _ptr, _ptr, _i64, _ptr]),
     "rs_front_offsets": (_i32, [_i64, _i64, ctypes.POINTER(ctypes.c_int64)]),
     "rs_front": (_i32, [_ptr, _ptr, _i64, ctypes.c_double, _i64, _ptr, _i64, _ptr,
-                        _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i32]),
+                        _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i32,
+                        _i64, _ptr]),
     "rs_back_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _i64]),
     "rs_back": (_i32, [_ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64,
                        _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
@@ -140,6 +148,7 @@ def stream_ptr() -> int:
 
 
 ASM_LONG, ASM_SHORT, ASM_ACCUMULATE = 1, 2, 4
+SHORT_GEMM, SHORT_L0 = 0, 1   # rs_short_method: plane GEMM or dense-L0 gather
 # short-range plane GEMM as Ozaki-split FP64 on the int8 tensor cores with this
 # many slices (0: FP64 DMMA); RSB200_OZ_SLICES overrides
 OZ_SLICES = int(os.environ.get("RSB200_OZ_SLICES", "0"))

@@ -39,7 +39,7 @@ from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
     project_kernel, split_rank, split_tensor
 from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, top_eig_supported, \
-    SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eps_rank, rhosvd_error_bound, shift_histograms, \
+    SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eig_desc_batched, eps_rank, rhosvd_error_bound, shift_histograms, \
     shifted_core, shifted_grams, side_svd, top_eig, truncated_spectrum, tucker_to_canonical
 
 
@@ -322,18 +322,29 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     _mark("f_todev")
     buf, o = _front_buffer(count, n)
     _mark("f_buf")
-    pf = (None, None, 0, 0, 0, 0, None, None, 0, None, 0)
+    pf = (None, None, 0, 0, 0, 0, None, None, 0, None, 0, 0, None)
     if prefetch is not None:
-        plan, lo, hi = prefetch
+        plan, lo, hi, groups = prefetch
         side = _side_stream()
         rs = int(plan.local.rank)
         out = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
         out.record_stream(side)
-        ws = nat.Workspace.get(_short_ws_bytes(n, hi - lo, max(1, min(n, count)), rs),
-                               "assemble_side")
+        L = nat.lib()
+        if L.rs_short_method(n, count, plan.gamma, rs) == nat.SHORT_L0:
+            wsb = L.rs_short_l0_bytes(plan.gamma)   # the gather needs only L0
+        else:
+            wsb = _short_ws_bytes(n, hi - lo, max(1, min(n, count)), rs)
+        ws = nat.Workspace.get(wsb, "assemble_side")
         ws.record_stream(side)
+        grp, gev, evarr = hi - lo, None, None
+        if groups > 1:
+            import ctypes
+            grp = -(-(hi - lo) // groups)
+            gev = _group_events(-(-(hi - lo) // grp))
+            evarr = (ctypes.c_void_p * len(gev))(*[e.cuda_event for e in gev])
         pf = (plan.local_ul.data_ptr(), plan.local_wl.data_ptr(), rs, plan.gamma, lo, hi,
-              out.data_ptr(), ws.data_ptr(), ws.numel(), side.cuda_stream, nat.OZ_SLICES)
+              out.data_ptr(), ws.data_ptr(), ws.numel(), side.cuda_stream, nat.OZ_SLICES,
+              grp, evarr)
     nat.check(nat.lib().rs_front(pos.data_ptr(), z.data_ptr(), count, grid.h, n, buf.data_ptr(),
                                  buf.numel(), nat.stream_ptr(), *pf), "rs_front")
     _mark("f_call")
@@ -357,8 +368,25 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     ds._cache["front"] = dict(hist=base + o[11], cnt3=base + o[12], bstart=base + o[13],
                               bc3=base + o[14], nb=base + o[15], buf=buf)
     if prefetch is not None:
-        ds._cache["front"]["prefetch"] = (lo, hi, out, ev)
+        ds._cache["front"]["prefetch"] = dict(lo=lo, hi=hi, buf=out, ev=ev, complete=False,
+                                              groups=(grp, gev) if gev else None)
     return ds, prep["dup_key"]
+
+
+_GROUP_EVENTS: dict = {}
+
+
+def _group_events(k: int):
+    """``k`` pooled CUDA events (created eagerly) for rs_front's plane groups;
+    re-recording is safe: a wait enqueued earlier keeps the record it saw."""
+    torch = nat._torch()
+    dev = torch.cuda.current_device()
+    pool = _GROUP_EVENTS.setdefault(dev, [])
+    while len(pool) < k:
+        e = torch.cuda.Event()
+        e.record()          # materialise the cudaEvent_t
+        pool.append(e)
+    return pool[:k]
 
 
 def _decode_key(key: int, n: int) -> tuple:
@@ -493,7 +521,15 @@ def _side_stream():
     return _stream("side")
 
 
-def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
+def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
+             prefetch_groups: int = 1) -> AssemblyResult:
+    """Reference ``build_rs`` (``assembly.py:187-279``) on the device.
+
+    Extensions: ``prefetch_dense`` (see :func:`_build_rs`); ``group`` (a
+    ``torch.distributed`` group: particle-sharded histograms/core);
+    ``prefetch_groups`` splits the prefetched planes into that many groups
+    finished one by one, so a host-returning :func:`dense_rs` starts the
+    device->host copy of the first planes while later ones are computed."""
     if not prefetch_dense:
         return _build_rs(system, cfg, False, group)
     torch = nat._torch()
@@ -502,7 +538,7 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> A
     chain.wait_stream(user)
     chain.wait_stream(_stream("side"))   # earlier prefetches may still read recycled memory
     with torch.cuda.stream(chain):
-        res = _build_rs(system, cfg, prefetch_dense, group)
+        res = _build_rs(system, cfg, prefetch_dense, group, max(1, int(prefetch_groups)))
     user.wait_stream(chain)
     return res
 
@@ -526,7 +562,8 @@ def _mark(label: str) -> None:
 _SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "140"))
 
 
-def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> AssemblyResult:
+def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
+              prefetch_groups: int = 1) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
     ``system`` may be a reference-style :class:`ParticleSystem` /
@@ -548,7 +585,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         if plan0.local.rank > 0:
             lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
                                                             int(prefetch_dense[1]))
-            fused = (plan0, lo, hi)
+            fused = (plan0, lo, hi, prefetch_groups)
     ds, collision = _as_device_system(system, grid, fused)
     if cfg.sigma is not None:
         sigma = float(cfg.sigma)
@@ -634,7 +671,8 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
             assemble_grid(None, short, lo, hi, out=buf, workspace_slot="assemble_side")
             ev = torch.cuda.Event()
             ev.record(side)
-        short._cache["prefetch"] = (lo, hi, buf, ev)
+        short._cache["prefetch"] = dict(lo=lo, hi=hi, buf=buf, ev=ev, complete=False,
+                                        groups=None)
 
     prefetch_pending = bool(prefetch_dense) and plan.local.rank > 0
     fpre = ds._cache.get("front", {}).get("prefetch")
@@ -665,16 +703,22 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         # two subspace iterations: one already gives grid parity (1e-10) at
         # eps >= 1e-6, but point values / energies (1e-12) need the second
         iters = TOPEIG_ITERS
+        full = None
         if use_top:
             _mark("grams")
             evals, U, trace = top_eig(G, b, iters)
         else:
+            # full spectra of the three modes at once (forked cuSOLVER streams),
+            # values fetched with the one packed synchronisation below
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
+            full = eig_desc_batched(G)
         if prefetch_pending:  # short-range planes behind the latency-bound eigen block
             launch_prefetch()
             prefetch_pending = False
         parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
+        if full is not None:
+            parts.append(full[0].reshape(-1))
         if front is not None:  # occupied x3 values: sizes the bucket-K core
             nb_view = front["buf"][front["nb"] - front["buf"].data_ptr():][:4].view(torch.int32)
             parts.append(nb_view.to(torch.float64))
@@ -717,12 +761,17 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
                     else:
                         r = None
                 if r is None:
-                    s_full, z_full = eig_desc(G[l])     # full cuSOLVER spectrum
-                    sh = to_host(s_full)
+                    if full is not None:   # batched spectra, already on the host
+                        o = nt_ + 2
+                        sh = np.sqrt(packed[o + l * n:o + (l + 1) * n])
+                        Ul = full[1][l]
+                    else:
+                        s_full, z_full = eig_desc(G[l])     # full cuSOLVER spectrum
+                        sh = to_host(s_full)
+                        Ul = z_full.T
                     r = fr if fr is not None else min(eps_rank(sh, cfg.reduction.eps), limit)
                     sv, total = sh, float(np.sum(sh * sh))
                     tail = np.cumsum((sh * sh)[::-1])[::-1]
-                    Ul = z_full.T
             ranks.append(int(r))
             values.append(sv)
             tails.append((float(tail[r]) if r < len(tail) else 0.0, total))
@@ -776,13 +825,28 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None) -> 
         if pre is not None and _TUCKER_IN_BUILD:
             # finish the prefetched slab here: the Tucker part is enqueued right
             # behind the core, before the host packages the result
-            lo, hi, buf, ev = pre
-            torch.cuda.current_stream().wait_event(ev)
-            buf.record_stream(torch.cuda.current_stream())
-            assemble_grid(tucker, None, lo, hi, out=buf, accumulate=True)
-            done = torch.cuda.Event()
-            done.record(torch.cuda.current_stream())
-            short._cache["prefetch"] = (lo, hi, buf, done, "complete")
+            lo, hi, buf = pre["lo"], pre["hi"], pre["buf"]
+            cur = torch.cuda.current_stream()
+            buf.record_stream(cur)
+            if pre["groups"] is None:
+                cur.wait_event(pre["ev"])
+                assemble_grid(tucker, None, lo, hi, out=buf, accumulate=True)
+                done = torch.cuda.Event()
+                done.record(cur)
+                short._cache["prefetch"] = dict(pre, ev=done, complete=True)
+            else:   # group by group, behind each group's short planes
+                grp, gev = pre["groups"]
+                dones = []
+                for g, ev in enumerate(gev):
+                    g0, g1 = g * grp, min(hi - lo, (g + 1) * grp)
+                    cur.wait_event(ev)
+                    assemble_grid(tucker, None, lo + g0, lo + g1, out=buf[g0:g1],
+                                  accumulate=True)
+                    done = torch.cuda.Event()
+                    done.record(cur)
+                    dones.append(done)
+                short._cache["prefetch"] = dict(pre, ev=dones[-1], complete=True,
+                                                groups=(grp, dones))
     else:
         if int(collision[0]) >= 0:
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "

@@ -341,6 +341,12 @@ static int gemm_batched(const double *A, int64_t lda, int64_t sA, const double *
   return check_launch("eig gemm");
 }
 
+int gemm_batched_nt(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
+                    int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
+                    int64_t K, int nb, cudaStream_t s) {
+  return gemm_batched(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
+}
+
 }  // namespace rsb
 
 using namespace rsb;
@@ -409,6 +415,119 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   if ((st = check_launch("sign"))) return st;
   k_trace<<<(unsigned)nmat, 32, 0, s>>>(G, n, trace);
   return check_launch("trace");
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// Full spectra of m Gram matrices, one cuSOLVER syevd per matrix on its own
+// forked stream (the tridiagonal reduction of one n = 2048 matrix is
+// latency-bound: the three modes overlap instead of running back to back),
+// no host synchronisation (info stays on the device).  Reference:
+// rankred.py:92 (np.linalg.eigh of the side Gram).
+#include <cusolverDn.h>
+
+#include <thread>
+
+namespace {
+constexpr int EIGH_SLOTS = 3;
+struct EighCtx {
+  cusolverDnHandle_t h[EIGH_SLOTS] = {};
+  cudaStream_t s[EIGH_SLOTS] = {};
+  cudaEvent_t fork = nullptr, join[EIGH_SLOTS] = {};
+};
+std::mutex g_eigh_mu;
+EighCtx g_eigh[64];
+
+int eigh_ctx(EighCtx **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_eigh_mu);
+  EighCtx &c = g_eigh[dev & 63];
+  if (!c.fork) {
+    for (int i = 0; i < EIGH_SLOTS; ++i) {
+      if (cudaStreamCreateWithFlags(&c.s[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c.join[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "rs_eigh: stream/event");
+      if (cusolverDnCreate(&c.h[i]) != CUSOLVER_STATUS_SUCCESS ||
+          cusolverDnSetStream(c.h[i], c.s[i]) != CUSOLVER_STATUS_SUCCESS)
+        return fail(RS_ERR_CUDA, "rs_eigh: cusolverDnCreate");
+    }
+    if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess)
+      return fail(RS_ERR_CUDA, "rs_eigh: event");
+  }
+  *out = &c;
+  return RS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t rs_eigh_workspace_bytes(int64_t m, int64_t n) {
+  EighCtx *c = nullptr;
+  if (m < 1 || n < 1 || eigh_ctx(&c)) return -1;
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(c->h[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  (int)n, nullptr, (int)n, nullptr, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return -1;
+  return m * (round_up((int64_t)lwork * 8, 256) + 256);
+}
+
+int rs_eigh(double *G, int64_t m, int64_t n, double *evals, void *work, int64_t work_bytes,
+            void *stream) {
+  RS_REQUIRE(G && evals && work && m >= 1 && n >= 1 && n < (1 << 30), "rs_eigh: bad arguments");
+  EighCtx *c = nullptr;
+  int st;
+  if ((st = eigh_ctx(&c))) return st;
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(c->h[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  (int)n, G, (int)n, evals, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(RS_ERR_CUDA, "rs_eigh: bufferSize");
+  const int64_t per = round_up((int64_t)lwork * 8, 256) + 256;
+  if (work_bytes < m * per)
+    return fail(RS_ERR_CAPACITY, "rs_eigh: workspace %lld < %lld", (long long)work_bytes,
+                (long long)(m * per));
+  cudaStream_t s = as_stream(stream);
+  if (cudaEventRecord(c->fork, s) != cudaSuccess) return fail(RS_ERR_CUDA, "rs_eigh: fork");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // one host thread per slot: syevd synchronises internally (divide and
+  // conquer bookkeeping), so issuing the modes from one thread serialises them
+  for (int64_t i0 = 0; i0 < m; i0 += EIGH_SLOTS) {
+    const int k = (int)std::min<int64_t>(EIGH_SLOTS, m - i0);
+    int rc[EIGH_SLOTS] = {0, 0, 0};
+    std::thread th[EIGH_SLOTS];
+    for (int j = 0; j < k; ++j) {
+      th[j] = std::thread([&, j] {
+        const int64_t i = i0 + j;
+        cudaSetDevice(dev);
+        char *w = (char *)work + i * per;
+        // symmetric input: row-major G is its own column-major transpose; the
+        // eigenvectors come back column-major, i.e. as the ROWS of the
+        // row-major (n, n) block, ascending eigenvalues
+        if (cudaStreamWaitEvent(c->s[j], c->fork, 0) != cudaSuccess) { rc[j] = 1; return; }
+        if (cusolverDnDsyevd(c->h[j], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n,
+                             G + i * n * n, (int)n, evals + i * n, (double *)w, lwork,
+                             (int *)(w + per - 256)) != CUSOLVER_STATUS_SUCCESS) {
+          rc[j] = 2;
+          return;
+        }
+        if (cudaEventRecord(c->join[j], c->s[j]) != cudaSuccess) rc[j] = 3;
+      });
+    }
+    for (int j = 0; j < k; ++j) th[j].join();
+    for (int j = 0; j < k; ++j) {
+      if (rc[j]) return fail(RS_ERR_CUDA, "rs_eigh: syevd step %d failed on matrix %lld", rc[j],
+                             (long long)(i0 + j));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (cudaStreamWaitEvent(s, c->join[j], 0) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "rs_eigh: join");
+    }
+    if (i0 + EIGH_SLOTS < m && cudaEventRecord(c->fork, s) != cudaSuccess)
+      return fail(RS_ERR_CUDA, "rs_eigh: fork");
+  }
+  return RS_OK;
 }
 
 }  // extern "C"

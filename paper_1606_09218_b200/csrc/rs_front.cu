@@ -93,7 +93,7 @@ int rs_front_offsets(int64_t count, int64_t n, int64_t *offsets) {
 int rs_front(const double *pos, const double *z, int64_t count, double h, int64_t n, void *buf,
              int64_t buf_bytes, void *stream, const double *ul, const double *wl, int64_t Rs,
              int64_t gamma, int64_t x1_lo, int64_t x1_hi, double *out, void *work,
-             int64_t work_bytes, void *side, int oz_slices) {
+             int64_t work_bytes, void *side, int oz_slices, int64_t group, void **events) {
   RS_REQUIRE(count >= 1 && n >= 2 && h > 0 && pos && z && buf, "rs_front: bad arguments");
   int64_t off[F_END + 1];
   layout(count, n, off);
@@ -139,21 +139,56 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
   if (cudaEventRecord(ev[dev & 63], s) != cudaSuccess ||
       cudaStreamWaitEvent(as_stream(side), ev[dev & 63], 0) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_front: stream dependency");
+  // planes are produced in groups of `group` (<= 0: one group); events[g]
+  // (caller-created, may be NULL) is recorded on `side` when group g is done,
+  // so a consumer can start on the first planes (e.g. their D2H) early
+  const int64_t span = x1_hi - x1_lo;
+  const int64_t grp = group > 0 ? std::min<int64_t>(group, span) : span;
+  auto mark = [&](int64_t p1) -> int {
+    if (!events) return RS_OK;
+    if ((p1 - x1_lo) % grp != 0 && p1 != x1_hi) return RS_OK;
+    cudaEvent_t e = (cudaEvent_t)events[(p1 - x1_lo - 1) / grp];
+    if (e && cudaEventRecord(e, as_stream(side)) != cudaSuccess)
+      return fail(RS_ERR_CUDA, "rs_front: group event");
+    return RS_OK;
+  };
+  if (rs_short_method(n, count, gamma, Rs) == RS_SHORT_L0) {  // dense-L0 gather, L0 in `work`
+    if (work_bytes < rs_short_l0_bytes(gamma))
+      return fail(RS_ERR_CAPACITY, "rs_front: workspace %lld < L0 %lld", (long long)work_bytes,
+                  (long long)rs_short_l0_bytes(gamma));
+    double *L0 = (double *)work;
+    if ((st = rs_short_l0_table(ul, wl, Rs, gamma, L0, side))) return st;
+    for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += grp) {
+      const int64_t p1 = std::min<int64_t>(x1_hi, p0 + grp);
+      if ((st = rs_assemble_short_l0(L0, gamma, n, (const int32_t *)P(F_C1),
+                                     (const int32_t *)P(F_C2), (const double *)P(F_ZQ),
+                                     (const int32_t *)P(F_BSTART), (const int32_t *)P(F_BC3),
+                                     (const int32_t *)P(F_NB), p0, p1, 0,
+                                     out + (p0 - x1_lo) * n * n, side)) ||
+          (st = mark(p1)))
+        return st;
+    }
+    return RS_OK;
+  }
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(n, count));
   const int flags = RS_ASM_SHORT | RS_ASM_OZ(oz_slices);
   const int64_t one = rs_assemble_workspace_bytes(n, 1, 1, nb_max, Rs, flags);
   const int64_t per = rs_assemble_workspace_bytes(n, 2, 1, nb_max, Rs, flags) - one;
   const int64_t chunk = std::max<int64_t>(
-      1, std::min<int64_t>(x1_hi - x1_lo, (work_bytes - (one - per)) / std::max<int64_t>(per, 1)));
-  for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += chunk) {
-    const int64_t p1 = std::min<int64_t>(x1_hi, p0 + chunk);
-    if ((st = rs_assemble_planes(nullptr, 1, 1, 1, nullptr, nullptr, nullptr, n, ul, wl, Rs, gamma,
-                                 (const int32_t *)P(F_C1), (const int32_t *)P(F_C2),
-                                 (const double *)P(F_ZQ), (const int32_t *)P(F_BSTART),
-                                 (const int32_t *)P(F_BC3), (const int32_t *)P(F_NB), nb_max, p0,
-                                 p1, flags, out + (p0 - x1_lo) * n * n, work, work_bytes,
-                                 side)))
-      return st;
+      1, std::min<int64_t>(grp, (work_bytes - (one - per)) / std::max<int64_t>(per, 1)));
+  for (int64_t g0 = x1_lo; g0 < x1_hi; g0 += grp) {
+    const int64_t g1 = std::min<int64_t>(x1_hi, g0 + grp);
+    for (int64_t p0 = g0; p0 < g1; p0 += chunk) {
+      const int64_t p1 = std::min<int64_t>(g1, p0 + chunk);
+      if ((st = rs_assemble_planes(nullptr, 1, 1, 1, nullptr, nullptr, nullptr, n, ul, wl, Rs,
+                                   gamma, (const int32_t *)P(F_C1), (const int32_t *)P(F_C2),
+                                   (const double *)P(F_ZQ), (const int32_t *)P(F_BSTART),
+                                   (const int32_t *)P(F_BC3), (const int32_t *)P(F_NB), nb_max,
+                                   p0, p1, flags, out + (p0 - x1_lo) * n * n, work, work_bytes,
+                                   side)))
+        return st;
+    }
+    if ((st = mark(g1))) return st;
   }
   return RS_OK;
 }

@@ -410,22 +410,30 @@ __global__ void k_tucker_y(const double *__restrict__ core, int r1, int r2, int 
   }
 }
 
-// A[(x1l*n + x2), c] = sum_b V2[x2, b] Y[x1l, b, c] for c < r3, 0 for r3 <= c < r3p
-__global__ void k_tucker_f(const double *__restrict__ Y, int r2, int r3, int r3p,
-                           const double *__restrict__ V2, int64_t n, int64_t planes,
-                           double *__restrict__ A, int64_t lda) {
-  const int64_t total = planes * n * r3p;
+// Yt[x1l, c, b] = Y[x1l, b, c] zero-padded to (r3p, r2p): the B operand of the
+// per-plane DMMA GEMM A[(x1l, x2), c] = sum_b V2[x2, b] Y[x1l, b, c]
+__global__ void k_tucker_yt(const double *__restrict__ Y, int r2, int r3, int r2p, int r3p,
+                            int64_t planes, double *__restrict__ Yt) {
+  const int64_t total = planes * r3p * r2p;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t c = e % r3p, row = e / r3p;
-    int64_t x2 = row % n, x1l = row / n;
-    double acc = 0.0;
-    if (c < r3) {
-      const double *y = Y + x1l * r2 * r3 + c;
-      const double *v = V2 + x2 * r2;
-      for (int b = 0; b < r2; ++b) acc = fma(v[b], y[(int64_t)b * r3], acc);
-    }
-    A[row * lda + c] = acc;
+    const int b = (int)(e % r2p);
+    const int64_t q = e / r2p;
+    const int c = (int)(q % r3p);
+    const int64_t x1l = q / r3p;
+    Yt[e] = (b < r2 && c < r3) ? Y[(x1l * r2 + b) * r3 + c] : 0.0;
+  }
+}
+
+// V2p = V2 (n x r2) with columns zero-padded to r2p (16-byte aligned K rows)
+__global__ void k_pad_cols(const double *__restrict__ V, int64_t n, int r, int rp,
+                           double *__restrict__ Vp) {
+  const int64_t total = n * rp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rp;
+    const int c = (int)(e - i * rp);
+    Vp[e] = c < r ? V[i * r + c] : 0.0;
   }
 }
 
@@ -893,6 +901,12 @@ int set_smem(const void *fn) {
 
 }  // namespace rsb
 
+namespace rsb {
+int gemm_batched_nt(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
+                    int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
+                    int64_t K, int nb, cudaStream_t s);  // rs_eig.cu
+}
+
 using namespace rsb;
 
 // ============================================================== C ABI
@@ -1212,7 +1226,7 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
 }
 
 // workspace: A (planes*n x lda) | Bt (n x lda) | Y (planes x r2 r3) | ranges
-static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int64_t nb_max,
+static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int64_t nb_max,
                        int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
                        int64_t *offY, int64_t *offR, int64_t *total) {
   const bool with_long = flags & RS_ASM_LONG, with_short = (flags & RS_ASM_SHORT) && Rs > 0;
@@ -1221,7 +1235,9 @@ static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int6
   *lda = std::max<int64_t>(*r3p + (with_short ? nb_max * *G : 0), 2);
   int64_t a = round_up(planes * n * *lda * 8, 256);
   int64_t b = round_up(n * *lda * 8, 256);
-  int64_t y = with_long ? round_up(planes * r2r3 * 8, 256) : 0;
+  const int64_t rp = round_up(std::max<int64_t>(rmax, 1), 2);
+  // Y (planes x r2 x r3) | Yt (planes x r3p x r2p) | V2p (n x r2p)
+  int64_t y = with_long ? round_up((2 * planes * rp * rp + n * rp) * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, TilePlane::BN);
   int64_t rr = round_up(ntiles * 4 * 8, 256);
   *offB = a;
@@ -1235,7 +1251,7 @@ static void asm_layout(int64_t n, int64_t planes, int64_t r2r3, int64_t r3, int6
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t nb_max,
                                     int64_t Rs, int flags) {
   int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax * rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
+  asm_layout(n, planes, rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
   return tot;
 }
 
@@ -1269,7 +1285,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   const int64_t planes = x1_hi - x1_lo;
   const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
   int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax * rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
+  asm_layout(n, planes, rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
   if (work_bytes < tot)
     return fail(RS_ERR_CAPACITY, "rs_assemble_planes: workspace %lld < %lld",
                 (long long)work_bytes, (long long)tot);
@@ -1284,12 +1300,22 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   cudaStream_t s = as_stream(stream);
   int st;
   if (with_long) {
+    ProfScope ps(s, "tucker_f");
     k_tucker_y<<<grid_for(planes * r2 * r3, 128), 128, 0, s>>>(core, (int)r1, (int)r2, (int)r3,
                                                                V1, x1_lo, planes, Y);
     if ((st = check_launch("tucker_y"))) return st;
-    k_tucker_f<<<grid_for(planes * n * r3p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r3p, V2,
-                                                               n, planes, A, lda);
-    if ((st = check_launch("tucker_f"))) return st;
+    const int64_t rp = round_up(rmax, 2), r2p = round_up(r2, 2);
+    double *Yt = Y + planes * rp * rp;
+    double *V2p = Yt + planes * rp * rp;
+    k_tucker_yt<<<grid_for(planes * r3p * r2p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r2p,
+                                                                  (int)r3p, planes, Yt);
+    if ((st = check_launch("tucker_yt"))) return st;
+    k_pad_cols<<<grid_for(n * r2p, 256), 256, 0, s>>>(V2, n, (int)r2, (int)r2p, V2p);
+    if ((st = check_launch("pad_cols"))) return st;
+    // per plane: A[x1l][x2, c] = V2p[x2, :] . Yt[x1l][c, :]  (DMMA, batched over planes)
+    if ((st = gemm_batched_nt(V2p, r2p, 0, Yt, r2p, r3p * r2p, A, lda, n * lda, n, r3p, r2p,
+                              (int)planes, s)))
+      return st;
   }
   if (with_short) {
     ProfScope ps(s, "short_rows");

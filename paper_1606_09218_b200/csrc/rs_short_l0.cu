@@ -1,0 +1,322 @@
+// Short-range agglomeration as an output-stationary gather from the dense
+// local tensor L0 (formats.py:423-445, dense_cct):
+//
+//   P_short[x] = sum_p z_p L0[x - c_p + gamma],   L0 = sum_k wl_k ul_k (x) ul_k (x) ul_k
+//
+// The plane GEMM (rs_assemble_planes) evaluates the same sum through the
+// separable form, paying 2 R_s flops per (point, occupied x3 bucket) on the
+// FP64 tensor cores.  When the mean window overlap is low (C5: 15 copies per
+// grid point, 363 occupied x3 values) that is ~50x the 2 flops per (point,
+// copy) pair; here every pair is one 8-byte L0 read (L2-resident: W^3 doubles,
+// 33 MB at W = 161, loaded with an L2 evict_last policy) and one DFMA, and
+// every grid point is stored once (streaming store).  Roofline: L2 load
+// bandwidth, 8 B per pair.
+//
+// A CTA owns an 8 (x1) x 16 (x2) x 128 (x3) output tile.  Its candidate copies
+// are found from the x3-bucket layout of rs_front (bucket range by binary
+// search over bc3, x2 window by binary search inside each c2-sorted bucket,
+// x1 filter by an order-preserving block scan) and staged in shared memory;
+// the accumulation then runs plane by plane with the candidates in bucket
+// order, so results are deterministic.
+#include "rs_common.cuh"
+
+#include <algorithm>
+#include <stdlib.h>
+#include <string.h>
+
+namespace rsb {
+namespace {
+
+constexpr int L0_T1 = 8;                  // x1 planes per tile
+constexpr int L0_T2 = 16;                 // x2 rows per tile (8 warps x 2)
+constexpr int L0_J = 4;                   // x3 points per lane
+constexpr int L0_T3 = 32 * L0_J;          // x3 columns per tile
+constexpr int L0_THREADS = 256;
+constexpr int L0_CAP = 1024;              // staged candidates per flush
+
+__device__ __forceinline__ int l0_block_scan(int v, int *wsum, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < L0_THREADS / 32; ++w) {
+    if (w < warp) base += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return base + x - v;
+}
+
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ double ld_l0(const double *p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// predicated L0 load: 0.0 (and no memory access) when !ok
+__device__ __forceinline__ double ld_l0_pred(const double *p, bool ok, uint64_t pol) {
+  double v = 0.0;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+      " @q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n}"
+      : "+d"(v)
+      : "l"(p), "r"((int)ok), "l"(pol));
+  return v;
+}
+
+// L0[(a W + b) W + c] = sum_k wl[k] ul[a,k] ul[b,k] ul[c,k]   (ul: W x Rs)
+__global__ void k_build_l0(const double *__restrict__ ul, const double *__restrict__ wl, int Rs,
+                           int W, double *__restrict__ L0) {
+  const int64_t tot = (int64_t)W * W * W;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ab = e / W;
+    const int c = (int)(e - ab * W);
+    const int a = (int)(ab / W), b = (int)(ab - (int64_t)a * W);
+    double s = 0.0;
+    for (int k = 0; k < Rs; ++k) s += wl[k] * ul[a * Rs + k] * ul[b * Rs + k] * ul[c * Rs + k];
+    L0[e] = s;
+  }
+}
+
+template <int UNROLL, int MINB>
+__global__ void __launch_bounds__(L0_THREADS, MINB)
+    k_short_l0(const double *__restrict__ L0, int W, int gamma, int64_t n,
+               const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+               const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+               const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp, int64_t x1_lo,
+               int64_t x1_hi, int accumulate, double *__restrict__ out) {
+  __shared__ int s_c1[L0_CAP], s_c2[L0_CAP], s_c3[L0_CAP];
+  __shared__ double s_z[L0_CAP];
+  __shared__ int s_lo[L0_THREADS], s_off[L0_THREADS], s_b3[L0_THREADS];
+  __shared__ int wsum[L0_THREADS / 32];
+  __shared__ int s_br[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t X3 = (int64_t)blockIdx.x * L0_T3;
+  const int64_t X2 = (int64_t)blockIdx.y * L0_T2;
+  const int64_t X1 = x1_lo + (int64_t)blockIdx.z * L0_T1;
+  if (X1 >= x1_hi) return;
+  const int64_t x1e = min(X1 + L0_T1, x1_hi), x2e = min(X2 + L0_T2, n), x3e = min(X3 + L0_T3, n);
+  const int64_t c1lo = X1 - gamma, c1hi = x1e - 1 + gamma;
+  const int64_t c2lo = X2 - gamma, c2hi = x2e - 1 + gamma;
+  if (tid == 0) {  // buckets whose x3 index lies within gamma of the tile
+    const int nb = *nbp;
+    const int64_t lo_x = X3 - gamma, hi_x = x3e - 1 + gamma;
+    int a = 0, b = nb;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (bc3[m] < lo_x) a = m + 1; else b = m;
+    }
+    s_br[0] = a;
+    b = nb;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (bc3[m] <= hi_x) a = m + 1; else b = m;
+    }
+    s_br[1] = a;
+  }
+  __syncthreads();
+  const int blo = s_br[0], bhi = s_br[1];
+  const uint64_t pol = l2_evict_last_policy();
+  // thread -> (2 rows, J columns)
+  const int64_t xr0 = X2 + 2 * warp;
+  const uint64_t Wu = (uint64_t)W;
+  int len = 0;
+  bool first = !accumulate;
+  auto flush = [&]() {
+    for (int64_t x1 = X1; x1 < x1e; ++x1) {
+      double acc[2][L0_J];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t x2 = xr0 + r;
+#pragma unroll
+        for (int j = 0; j < L0_J; ++j) {
+          const int64_t x3 = X3 + lane + 32 * j;
+          acc[r][j] = (!first && x2 < x2e && x3 < x3e)
+                          ? __ldcs(out + ((x1 - x1_lo) * n + x2) * n + x3)
+                          : 0.0;
+        }
+      }
+      // branch-free body (validity as load predicates) so consecutive
+      // candidates' loads are in flight together
+#pragma unroll UNROLL
+      for (int e = 0; e < len; ++e) {
+        const int a = (int)(x1 - s_c1[e]) + gamma;
+        const bool av = (unsigned)a < (unsigned)W;
+        const double z = s_z[e];
+        const int c0 = (int)(X3 + lane - s_c3[e]) + gamma;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int b = (int)(xr0 + r - s_c2[e]) + gamma;
+          const bool rv = av && (unsigned)b < (unsigned)W;
+          const double *row = L0 + ((uint64_t)(rv ? a : 0) * Wu + (uint64_t)(rv ? b : 0)) * Wu;
+#pragma unroll
+          for (int j = 0; j < L0_J; ++j) {
+            const int c = c0 + 32 * j;
+            const double v = ld_l0_pred(row + c, rv && (unsigned)c < (unsigned)W, pol);
+            acc[r][j] = fma(z, v, acc[r][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t x2 = xr0 + r;
+        if (x2 >= x2e) continue;
+#pragma unroll
+        for (int j = 0; j < L0_J; ++j) {
+          const int64_t x3 = X3 + lane + 32 * j;
+          if (x3 < x3e) __stcs(out + ((x1 - x1_lo) * n + x2) * n + x3, acc[r][j]);
+        }
+      }
+    }
+    first = false;
+  };
+  for (int g = blo; g < bhi; g += L0_THREADS) {
+    const int b = g + tid;
+    int lo = 0, cnt = 0, b3 = 0;
+    if (b < bhi) {  // copies of bucket b whose x2 window meets the tile (c2 ascending)
+      const int p_lo = bstart[b], p_hi = bstart[b + 1];
+      int l = p_lo, h = p_hi;
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (c2[m] < c2lo) l = m + 1; else h = m;
+      }
+      int e = l;
+      h = p_hi;
+      while (e < h) {
+        const int m = (e + h) >> 1;
+        if (c2[m] <= c2hi) e = m + 1; else h = m;
+      }
+      lo = l;
+      cnt = e - l;
+      b3 = bc3[b];
+    }
+    int tot;
+    const int off = l0_block_scan(cnt, wsum, &tot);
+    s_lo[tid] = lo;
+    s_off[tid] = off;
+    s_b3[tid] = b3;
+    const int nbk = min(L0_THREADS, bhi - g);
+    __syncthreads();
+    for (int cs = 0; cs < tot; cs += L0_THREADS) {
+      if (len > L0_CAP - L0_THREADS) {  // uniform: flush the staged candidates
+        __syncthreads();
+        flush();
+        __syncthreads();
+        len = 0;
+      }
+      const int v = cs + tid;
+      bool cov = false;
+      int p = 0, k = 0;
+      if (v < tot) {  // last bucket with offset <= v (empty buckets share offsets)
+        int l = 0, h = nbk;
+        while (h - l > 1) {
+          const int m = (l + h) >> 1;
+          if (s_off[m] <= v) l = m; else h = m;
+        }
+        k = l;
+        p = s_lo[k] + (v - s_off[k]);
+        const int64_t a1 = c1[p];
+        cov = a1 >= c1lo && a1 <= c1hi;
+      }
+      int t2;
+      const int pos = l0_block_scan(cov ? 1 : 0, wsum, &t2);
+      if (cov) {
+        s_c1[len + pos] = c1[p];
+        s_c2[len + pos] = c2[p];
+        s_c3[len + pos] = s_b3[k];
+        s_z[len + pos] = zq[p];
+      }
+      len += t2;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (len > 0 || first) flush();
+}
+
+int short_l0_env() {  // RSB200_SHORT=gemm|l0 forces a method (tests, tuning)
+  const char *e = getenv("RSB200_SHORT");
+  if (!e) return -1;
+  if (!strcmp(e, "l0")) return 1;
+  if (!strcmp(e, "gemm")) return 0;
+  return -1;
+}
+
+}  // namespace
+}  // namespace rsb
+
+using namespace rsb;
+
+extern "C" {
+
+int rs_short_method(int64_t n, int64_t count, int64_t gamma, int64_t Rs) {
+  if (n < 1 || count < 1 || gamma < 0 || Rs < 1) return RS_SHORT_GEMM;
+  const int forced = short_l0_env();
+  if (forced >= 0) return forced ? RS_SHORT_L0 : RS_SHORT_GEMM;
+  // mean number of windows covering a grid point (clipped at the grid)
+  const double w = (double)std::min<int64_t>(2 * gamma + 1, n);
+  const double ov = (double)count * (w / n) * (w / n) * (w / n);
+  // L0 reads 8 B per (point, copy) from L2; the plane GEMM pays 2 R_s flops
+  // per (point, occupied x3 bucket), so the gather wins at low overlap
+  return ov <= 64.0 ? RS_SHORT_L0 : RS_SHORT_GEMM;
+}
+
+int64_t rs_short_l0_bytes(int64_t gamma) {
+  const int64_t W = 2 * gamma + 1;
+  return W * W * W * 8;
+}
+
+int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t gamma, double *L0,
+                      void *stream) {
+  RS_REQUIRE(ul && wl && L0 && Rs >= 1 && gamma >= 0, "rs_short_l0_table: bad arguments");
+  const int64_t W = 2 * gamma + 1;
+  k_build_l0<<<grid_blocks(W * W * W), 256, 0, as_stream(stream)>>>(ul, wl, (int)Rs, (int)W, L0);
+  return check_launch("short_l0_table");
+}
+
+int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32_t *c1,
+                         const int32_t *c2, const double *zq, const int32_t *bstart,
+                         const int32_t *bc3, const int32_t *nb_dev, int64_t x1_lo, int64_t x1_hi,
+                         int accumulate, double *out, void *stream) {
+  RS_REQUIRE(L0 && c1 && c2 && zq && bstart && bc3 && nb_dev && out,
+             "rs_assemble_short_l0: bad arguments");
+  RS_REQUIRE(n >= 1 && gamma >= 0 && 0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n,
+             "rs_assemble_short_l0: bad plane range");
+  RS_REQUIRE(2 * gamma + 1 <= 46340, "rs_assemble_short_l0: gamma too large");
+  dim3 grid((unsigned)ceil_div(n, L0_T3), (unsigned)ceil_div(n, L0_T2),
+            (unsigned)ceil_div(x1_hi - x1_lo, L0_T1));
+  RS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "rs_assemble_short_l0: grid too large");
+  ProfScope ps(as_stream(stream), "short_l0");
+  const char *uenv = getenv("RSB200_L0_VARIANT");
+  const int var = uenv ? atoi(uenv) : 0;
+#define RS_L0_LAUNCH(U, B)                                                                    \
+  k_short_l0<U, B><<<grid, L0_THREADS, 0, as_stream(stream)>>>(                              \
+      L0, (int)(2 * gamma + 1), (int)gamma, n, c1, c2, zq, bstart, bc3, nb_dev, x1_lo, x1_hi, \
+      accumulate ? 1 : 0, out)
+  switch (var) {  // RSB200_L0_VARIANT: tuning experiments (unroll, min CTAs per SM)
+    case 1: RS_L0_LAUNCH(2, 1); break;
+    case 2: RS_L0_LAUNCH(4, 1); break;
+    case 3: RS_L0_LAUNCH(2, 4); break;
+    case 4: RS_L0_LAUNCH(8, 2); break;
+    case 5: RS_L0_LAUNCH(4, 4); break;
+    default: RS_L0_LAUNCH(4, 3); break;
+  }
+#undef RS_L0_LAUNCH
+  return check_launch("short_l0");
+}
+
+}  // extern "C"

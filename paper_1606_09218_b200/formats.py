@@ -305,6 +305,23 @@ class CCT:
         return lay
 
 
+    def l0_table(self):
+        """Dense local tensor L0 (W^3, device) for the low-overlap gather,
+        built on the device from the normalised factors and cached per CCT
+        (``formats.py:432``: ``local.dense()``)."""
+        t = self._cache.get("l0")
+        if t is None:
+            torch = nat._torch()
+            lay = self.device_layout()
+            w = 2 * self.gamma + 1
+            t = torch.empty((w, w, w), dtype=torch.float64, device=lay["ul"].device)
+            nat.check(nat.lib().rs_short_l0_table(nat.ptr(lay["ul"]), nat.ptr(lay["wl"]),
+                                                  self.local.rank, self.gamma, t.data_ptr(),
+                                                  nat.stream_ptr()), "rs_short_l0_table")
+            self._cache["l0"] = t
+        return t
+
+
 def trusted_cct(local, gamma: int, centers, weights, mode_sizes, overlap_policy="soft",
                 max_overlap=8) -> "CCT":
     """CCT from device arrays produced by this package (snapped, in range,
@@ -434,6 +451,23 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
         r1 = r2 = r3 = 1
         core = v1 = v2 = v3 = None
     have_short = short is not None and short.local.rank > 0 and short.count > 0
+    L = nat.lib()
+    if have_short and L.rs_short_method(n, short.count, short.gamma,
+                                        short.local.rank) == nat.SHORT_L0:
+        # low window overlap: Tucker planes by the plane GEMM, then the short
+        # part as a dense-L0 gather on top (rs_assemble_short_l0)
+        if long is not None:
+            assemble_grid(long, None, x1_lo, x1_hi, out=out, accumulate=accumulate,
+                          workspace_bytes=workspace_bytes, workspace_slot=workspace_slot)
+        lay = short.device_layout()
+        l0 = short.l0_table()
+        stream = nat.stream_ptr()
+        nat.check(L.rs_assemble_short_l0(
+            nat.ptr(l0), short.gamma, n, nat.ptr(lay["c1"]), nat.ptr(lay["c2"]),
+            nat.ptr(lay["zq"]), nat.ptr(lay["bstart"]), nat.ptr(lay["bc3"]), nat.ptr(lay["nb"]),
+            x1_lo, x1_hi, 1 if (accumulate or long is not None) else 0, out.data_ptr(), stream),
+            "rs_assemble_short_l0")
+        return out
     if have_short:
         flags |= nat.ASM_SHORT | nat.asm_oz(nat.OZ_SLICES)
         lay = short.device_layout()
@@ -447,7 +481,6 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
         if not accumulate:
             out.zero_()
         return out
-    L = nat.lib()
     rmax = max(r1, r2, r3)
     one = L.rs_assemble_workspace_bytes(n, 1, rmax, nb_max, rs, flags)
     per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, nb_max, rs, flags) - one
@@ -568,14 +601,29 @@ def dense_rs(a, limit: int = MAX_DENSE_ELEMENTS, device: bool = False, x1_range=
         n = a.grid.n
         lo, hi = (0, n) if x1_range is None else (int(x1_range[0]), int(x1_range[1]))
         pre = a.short._cache.get("prefetch")
-        if pre is not None and pre[0] == lo and pre[1] == hi:
+        if pre is not None and pre["lo"] == lo and pre["hi"] == hi:
             del a.short._cache["prefetch"]
             torch = nat._torch()
-            res, ev = pre[2], pre[3]
+            res = pre["buf"]
+            if not device and pre["complete"] and pre["groups"] is not None:
+                # finished group by group (build_rs): each group's D2H starts
+                # as soon as its planes are final
+                host = out if out is not None else _pinned_host((hi - lo, n, n))
+                cp = _copy_stream()
+                grp, done = pre["groups"]
+                for g, ev in enumerate(done):
+                    g0, g1 = g * grp, min(hi - lo, (g + 1) * grp)
+                    cp.wait_event(ev)
+                    with torch.cuda.stream(cp):
+                        host[g0:g1].copy_(res[g0:g1], non_blocking=True)
+                res.record_stream(cp)
+                cp.synchronize()
+                arr = _hand_out(host)
+                return arr.reshape(n, n, n) if x1_range is None else arr
             main = torch.cuda.current_stream()
-            main.wait_event(ev)
+            main.wait_event(pre["ev"])
             res.record_stream(main)
-            if len(pre) < 5:  # short part only so far: add the Tucker part
+            if not pre["complete"]:  # short part only so far: add the Tucker part
                 assemble_grid(a.long, None, lo, hi, out=res, accumulate=True)
         elif not device:
             host = _dense_to_host(a, lo, hi, out)

@@ -112,6 +112,28 @@ def eig_desc(g):
     return torch.sqrt(vals), fix_signs(z)
 
 
+def eig_desc_batched(G):
+    """Full spectra of a (m, n, n) stack of Grams (``rs_eigh``: one cuSOLVER
+    syevd per matrix on forked streams, no host sync), in :func:`eig_desc`'s
+    post-processing.  Returns device (values (m, n) descending, clipped at 0,
+    not square-rooted; vectors (m, n, n) with the eigenvectors as ROWS,
+    largest-|entry| positive)."""
+    torch = nat._torch()
+    m, n = int(G.shape[0]), int(G.shape[1])
+    V = G.contiguous().clone()
+    ev = torch.empty((m, n), dtype=torch.float64, device=V.device)
+    L = nat.lib()
+    wsb = L.rs_eigh_workspace_bytes(m, n)
+    if wsb < 0:
+        raise NumericalError("rs_eigh: workspace query failed")
+    ws = nat.Workspace.get(wsb, "eigh")
+    nat.check(L.rs_eigh(V.data_ptr(), m, n, ev.data_ptr(), ws.data_ptr(), ws.numel(),
+                        nat.stream_ptr()), "rs_eigh")
+    vals = torch.flip(ev, dims=(-1,)).clamp_min(0.0)
+    z = fix_signs(torch.flip(V, dims=(-2,)).transpose(-1, -2))   # columns = vectors
+    return vals, z.transpose(-1, -2)
+
+
 def fix_signs(z):
     torch = nat._torch()
     if z.numel() == 0:

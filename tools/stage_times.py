@@ -37,7 +37,7 @@ for _ in range(reps):
     assemble_grid(res.rs.long, res.rs.short, out=out)
 torch.cuda.synchronize()
 L.rs_prof_enable(0)
-for k in ("topeig", "syrk", "shift_project", "core", "short_rows", "gemm_plane", "gemm_short", "gemm_tucker", "oz_mma"):
+for k in ("topeig", "syrk", "shift_project", "core", "short_rows", "gemm_plane", "gemm_short", "gemm_tucker", "oz_mma", "short_l0", "tucker_f"):
     ms, c = nat.prof_query(k)
     print(f"  {k:14s} {ms/reps:.4f} ms/step  ({c/reps:.0f} launches)")
 from torch.profiler import profile, ProfilerActivity
