@@ -90,21 +90,27 @@ class ClockSampler:
         self.stop = threading.Event()
         self.thread = None
         self.nvml = None
+        self.period = float(os.environ.get("BENCH_CLOCK_MS", "10")) / 1e3
+
+    def _sample(self, h):
+        nv = self.nvml
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.rows.append((sm, mx, rs))
+        except Exception:
+            pass
 
     def _run(self, h):
-        nv = self.nvml
-        while True:
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append((sm, mx, rs))
-            except Exception:
-                pass
-            if self.stop.wait(0.010):
-                break
+        # first sample one period in: the NVML calls contend with the CUDA
+        # driver calls of the step being launched
+        while not self.stop.wait(self.period):
+            self._sample(h)
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return self
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -113,6 +119,7 @@ class ClockSampler:
                 else self.device
             h = nv.nvmlDeviceGetHandleByIndex(idx)
             self.nvml = nv
+            self.handle = h
             self.thread = threading.Thread(target=self._run, args=(h,), daemon=True)
             self.thread.start()
         except Exception:
@@ -120,9 +127,12 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        # (called right after the timed region's closing synchronize)
         self.stop.set()
         if self.thread is not None:
             self.thread.join(timeout=2)
+            if not self.rows:  # region shorter than one period: one sample at its end
+                self._sample(self.handle)
 
     def summary(self):
         rows = self.rows
@@ -239,6 +249,22 @@ def measure_dgemm_peak(torch):
     return 2 * n ** 3 / t / 1e12
 
 
+def term_supports(ul, wl, gamma, drop=1e-18):
+    """Host mirror of k_term_support (per-term x3 band of the plane GEMM)."""
+    mx = np.abs(ul).max(axis=0)
+    thr = drop * float(np.sum(np.abs(wl) * mx ** 3))
+    out = []
+    for k in range(ul.shape[1]):
+        f = abs(wl[k]) * mx[k] ** 2
+        g = 0
+        for d in range(gamma, -1, -1):
+            if f * max(abs(ul[gamma + d, k]), abs(ul[gamma - d, k])) > thr:
+                g = d
+                break
+        out.append(g)
+    return out
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -311,8 +337,11 @@ def main():
     barrier()
     launches0 = L.rs_launch_count()
     L.rs_prof_enable(1)
-    if os.environ.get("BENCH_NOGC"):
-        import gc
+    # host hygiene of a latency-bound loop: collect garbage now, pause Python's
+    # cyclic GC during the timed steps (BENCH_GC=1 keeps it running)
+    import gc
+    gc.collect()
+    if not os.environ.get("BENCH_GC"):
         gc.disable()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -379,6 +408,7 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
+    gc.enable()
 
     if rank == 0:
         peak = measure_dgemm_peak(torch)
@@ -389,15 +419,15 @@ def main():
         gemm_avg_s = gemm_ms / max(gemm_n, 1) / 1e3
         launches_per_step = max(gemm_n, 1) / args.steps
         achieved = alg_flops * slab_frac / launches_per_step / gemm_avg_s / 1e12 if gemm_n else None
-        # executed flops of the banded GEMM (K per column tile)
+        # executed flops of the banded GEMM: per column tile and short term k,
+        # the occupied x3 buckets within that term's support gk of the tile
         bc3 = np.unique(host_idx[:, 2])
-        G = m["M"] - m["split_index"] + (m["M"] - m["split_index"]) % 2
-        r3p = r3 + r3 % 2
+        gk = term_supports(plan.local_ul.cpu().numpy(), plan.local_wl.cpu().numpy(), gamma)
         keff = []
         for t0 in range(0, n, 64):
-            lo_x, hi_x = t0 - gamma, min(n - 1, t0 + 63) + gamma
-            nb = np.count_nonzero((bc3 >= lo_x) & (bc3 <= hi_x))
-            keff.append(nb * G)
+            for g in gk:
+                lo_x, hi_x = t0 - g, min(n - 1, t0 + 63) + g
+                keff.append(np.count_nonzero((bc3 >= lo_x) & (bc3 <= hi_x)))
         exec_flops = 2.0 * n * n * 64 * float(np.sum(keff))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

@@ -40,7 +40,7 @@ from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effe
     project_kernel, split_rank, split_tensor
 from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, top_eig_supported, \
     SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eig_desc_batched, eps_rank, rhosvd_error_bound, shift_histograms, \
-    shifted_core, shifted_grams, side_svd, top_eig, truncated_spectrum, tucker_to_canonical
+    shifted_core, shifted_grams, side_svd, top_eig, truncated_spectra, truncated_spectrum, tucker_to_canonical
 
 
 @dataclass(frozen=True)
@@ -724,6 +724,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
             parts.append(nb_view.to(torch.float64))
         _mark("eig_enq")
         packed = to_host(torch.cat(parts))
+        _mark("synced_eig")
         nq_host = int(packed[-1]) if front is not None else 0
         nt_ = 3 * b + (3 if use_top else 0)
         if packed[nt_ + 1] >= 0:
@@ -738,14 +739,15 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                 if r > limit:
                     raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
         ranks, values, tails, zs, from_top = [], [], [], [], []
+        if use_top:
+            spectra3 = truncated_spectra(packed[:3 * b].reshape(3, b), packed[3 * b:3 * b + 3], n,
+                                         cfg.reduction.eps, forced, limit, iters)
         for l in range(3):
             fr = forced[l] if forced is not None else None
             r = None
             top = False
             if use_top:
-                theta = packed[l * b:(l + 1) * b]
-                r, sv, tail, total = truncated_spectrum(theta, packed[3 * b + l], n,
-                                                        cfg.reduction.eps, fr, limit, iters)
+                r, sv, tail, total = spectra3[l]
                 if r is not None and fr is not None and fr > b:
                     r = None
                 Ul = U[l] if r is not None else None
@@ -808,6 +810,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                                    front["bc3"], front["nb"]) if front is not None
                                   else (None,) * 6), nq_host),
                       "rs_back")
+            _mark("back_enq")
         else:
             zs = [zl[:r].T.contiguous() for zl, r in zip(zs, ranks)]
         spectrum = SvdSpectrum(values=tuple(values), vectors=tuple(zs))
@@ -820,6 +823,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                                             z[p_lo:p_hi].contiguous(), plan.w_long), group)
         _mark("ranks")
         tucker = _trusted_tucker(core, zs)
+        _mark("tucker_obj")
         long_raw = None
         pre = short._cache.get("prefetch") if cfg.long_format == "tucker" else None
         if pre is not None and _TUCKER_IN_BUILD:
@@ -847,6 +851,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                     dones.append(done)
                 short._cache["prefetch"] = dict(pre, ev=dones[-1], complete=True,
                                                 groups=(grp, dones))
+        _mark("tucker_enq")
     else:
         if int(collision[0]) >= 0:
             raise ResolutionError(f"grid n={n} cannot resolve the system: several particles snap "

@@ -57,7 +57,7 @@ struct Acc {
 };
 
 // One BK-wide K chunk of both operand tiles -> shared memory.  Columns at or
-// beyond k_hi and rows beyond M/N are zero-filled (k_hi must be even).
+// beyond k_hi and rows beyond M/N are zero-filled (k even, k_hi may be odd).
 template <class T>
 __device__ __forceinline__ void stage_load(double *s, const double *A, int64_t lda, int64_t m0,
                                            int64_t M, const double *B, int64_t ldb, int64_t n0,
@@ -82,7 +82,11 @@ __device__ __forceinline__ void stage_load(double *s, const double *A, int64_t l
       ok = kin && g < N;
       src = ok ? B + g * ldb + kk : B;
     }
-    cp_async16(smem_addr(s + row * T::LDS + 2 * ch), src, ok);
+    // odd k_hi: the last pair reads one element and zero-fills the other
+    const int bytes = ok ? (kk + 1 < k_hi ? 16 : 8) : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                     smem_addr(s + row * T::LDS + 2 * ch)),
+                 "l"(src), "r"(bytes));
   }
 }
 
@@ -93,6 +97,27 @@ __device__ __forceinline__ void stage_mma(const double *s, Acc<T> &acc, int wm0,
   const double *sB = s + T::BM * T::LDS;
 #pragma unroll
   for (int kk = 0; kk < T::BK; kk += 4) {
+    double a[T::MT], b[T::NT];
+#pragma unroll
+    for (int i = 0; i < T::MT; ++i) a[i] = sA[(wm0 + i * 8 + gid) * T::LDS + kk + tig];
+#pragma unroll
+    for (int j = 0; j < T::NT; ++j) b[j] = sB[(wn0 + j * 8 + gid) * T::LDS + kk + tig];
+#pragma unroll
+    for (int i = 0; i < T::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < T::NT; ++j) dmma_884(acc.v[i][j], a[i], b[j]);
+  }
+}
+
+// as stage_mma, only the first `kv` (<= BK, rounded up to 4) columns of the chunk
+template <class T>
+__device__ __forceinline__ void stage_mma_kv(const double *s, Acc<T> &acc, int wm0, int wn0,
+                                             int gid, int tig, int kv) {
+  const double *sA = s;
+  const double *sB = s + T::BM * T::LDS;
+#pragma unroll
+  for (int kk = 0; kk < T::BK; kk += 4) {
+    if (kk >= kv) break;  // uniform across the CTA
     double a[T::MT], b[T::NT];
 #pragma unroll
     for (int i = 0; i < T::MT; ++i) a[i] = sA[(wm0 + i * 8 + gid) * T::LDS + kk + tig];

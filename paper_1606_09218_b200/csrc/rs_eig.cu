@@ -11,6 +11,7 @@
 // largest-|entry|-positive signs.  The host checks convergence with the
 // returned Ritz values (and escalates b, see rankred.top_eig).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -162,7 +163,9 @@ __global__ void __launch_bounds__(JAC_THREADS)
   __syncthreads();
   double dmax = 0.0;
   for (int i = 0; i < B; ++i) dmax = fmax(dmax, fabs(T[i * LD + i]));
-  const double tol = 1e-18 * dmax;
+  // absolute floor at the rounding level of T: the Ritz values below it are
+  // noise (their rotations only shuffle rounding errors, sweep after sweep)
+  const double tol = 1e-16 * dmax;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
@@ -327,19 +330,32 @@ __global__ void __launch_bounds__(T::THREADS)
 }
 
 using TileEig = Tile<64, 64, 32, 32, 3>;
+using TileEigS = Tile<32, 32, 16, 16, 3>;  // skinny Ritz blocks (b <= 32): 4x the CTAs
+
+template <class T>
+static int gemm_batched_t(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
+                          int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
+                          int64_t K, int nb, cudaStream_t s) {
+  if (T::SMEM_BYTES > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_gemm_nt_batched<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         T::SMEM_BYTES);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+  }
+  dim3 grid((unsigned)ceil_div(N, T::BN), (unsigned)ceil_div(M, T::BM), (unsigned)nb);
+  k_gemm_nt_batched<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, sA, B, ldb, sB, C, ldc,
+                                                                sC, M, N, K);
+  return check_launch("eig gemm");
+}
 
 static int gemm_batched(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
                         int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
                         int64_t K, int nb, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_gemm_nt_batched<TileEig>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       TileEig::SMEM_BYTES);
-  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-  dim3 grid((unsigned)ceil_div(N, TileEig::BN), (unsigned)ceil_div(M, TileEig::BM), (unsigned)nb);
-  k_gemm_nt_batched<TileEig><<<grid, TileEig::THREADS, TileEig::SMEM_BYTES, s>>>(
-      A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
-  return check_launch("eig gemm");
+  if (M <= 32 || N <= 32)
+    return gemm_batched_t<TileEigS>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
+  return gemm_batched_t<TileEig>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
 }
+
 
 int gemm_batched_nt(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
                     int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,

@@ -395,24 +395,10 @@ __global__ void k_split_reduce(const double *__restrict__ part, int64_t splits, 
 }
 
 // ===================================================== grid assembly (K5)
-// Y[x1l, b, c] = sum_a V1[x1, a] core[a, b, c]
-__global__ void k_tucker_y(const double *__restrict__ core, int r1, int r2, int r3,
-                           const double *__restrict__ V1, int64_t x1_lo, int64_t planes,
-                           double *__restrict__ Y) {
-  const int64_t total = planes * r2 * r3;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t bc = e % ((int64_t)r2 * r3), x1l = e / ((int64_t)r2 * r3);
-    const double *v = V1 + (x1_lo + x1l) * r1;
-    double acc = 0.0;
-    for (int a = 0; a < r1; ++a) acc = fma(v[a], core[(int64_t)a * r2 * r3 + bc], acc);
-    Y[e] = acc;
-  }
-}
-
-// Yt[x1l, c, b] = Y[x1l, b, c] zero-padded to (r3p, r2p): the B operand of the
-// per-plane DMMA GEMM A[(x1l, x2), c] = sum_b V2[x2, b] Y[x1l, b, c]
-__global__ void k_tucker_yt(const double *__restrict__ Y, int r2, int r3, int r2p, int r3p,
+// Yt[x1l, c, b] = sum_a V1[x1, a] core[a, b, c], zero-padded to (r3p, r2p): the
+// B operand of the per-plane DMMA GEMM A[(x1l, x2), c] = sum_b V2[x2, b] Yt[x1l, c, b]
+__global__ void k_tucker_yt(const double *__restrict__ core, int r1, int r2, int r3,
+                            const double *__restrict__ V1, int64_t x1_lo, int r2p, int r3p,
                             int64_t planes, double *__restrict__ Yt) {
   const int64_t total = planes * r3p * r2p;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -421,7 +407,12 @@ __global__ void k_tucker_yt(const double *__restrict__ Y, int r2, int r3, int r2
     const int64_t q = e / r2p;
     const int c = (int)(q % r3p);
     const int64_t x1l = q / r3p;
-    Yt[e] = (b < r2 && c < r3) ? Y[(x1l * r2 + b) * r3 + c] : 0.0;
+    double acc = 0.0;
+    if (b < r2 && c < r3) {
+      const double *v = V1 + (x1_lo + x1l) * r1;
+      for (int a = 0; a < r1; ++a) acc = fma(v[a], core[((int64_t)a * r2 + b) * r3 + c], acc);
+    }
+    Yt[e] = acc;
   }
 }
 
@@ -438,6 +429,7 @@ __global__ void k_pad_cols(const double *__restrict__ V, int64_t n, int r, int r
 }
 
 constexpr int SR_MAXR = 24;  // largest short rank R_s of the row builder
+#define SR_MAXR_DEV 24
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -631,6 +623,193 @@ __global__ void __launch_bounds__(SD_THREADS)
       }
     }
   }
+}
+
+// Per-term supports of the short part -> per-distance prefix widths.  Term k
+// can contribute more than RS_TERM_DROP of the largest possible L0 entry only
+// within gk[k] cells of its centre,
+//   |wl_k ul[g+d,k]| max|ul_k|^2 > RS_TERM_DROP * sum_j |wl_j| max|ul_j|^3,
+// and the narrow short-range Gaussians die out long before gamma (C4: 107 for
+// the widest term, 1 for the narrowest).  kofd[d] = 1 + max{k : gk[k] >= d}:
+// a bucket whose x3 index lies d cells outside a column tile needs only its
+// first kofd[d] term columns (terms are ordered widest first).  What is
+// dropped is below 1e-18 of max|L0| per (grid point, copy, term).
+#define RS_TERM_DROP 1e-18
+__global__ void __launch_bounds__(256)
+    k_term_prefix(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
+                  int *__restrict__ kofd) {
+  __shared__ double smx[SR_MAXR_DEV];
+  __shared__ int sgk[SR_MAXR_DEV];
+  __shared__ double stot;
+  const int W = 2 * gamma + 1;
+  const int k = threadIdx.x;
+  double mx = 0.0;
+  if (k < Rs) {
+    for (int d = 0; d < W; ++d) mx = fmax(mx, fabs(ul[d * Rs + k]));
+    smx[k] = mx;
+  }
+  __syncthreads();
+  if (k == 0) {
+    double t = 0.0;
+    for (int j = 0; j < Rs; ++j) t += fabs(wl[j]) * smx[j] * smx[j] * smx[j];
+    stot = t;
+  }
+  __syncthreads();
+  if (k < Rs) {
+    const double thr = RS_TERM_DROP * stot, f = fabs(wl[k]) * mx * mx;
+    int g = 0;
+    for (int d = gamma; d >= 0; --d)
+      if (f * fmax(fabs(ul[(gamma + d) * Rs + k]), fabs(ul[(gamma - d) * Rs + k])) > thr) {
+        g = d;
+        break;
+      }
+    sgk[k] = g;
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d <= gamma; d += blockDim.x) {
+    int K = 0;
+    for (int j = 0; j < Rs; ++j)
+      if (sgk[j] >= d) K = j + 1;
+    kofd[d] = K;
+  }
+}
+
+// The plane GEMM: C[(x1,x2), x3] (=, +=) sum over K of A B^T where, per
+// 64-wide x3 column tile, K = the Tucker columns [0, r3p) followed by, for
+// every occupied x3 bucket b within gamma of the tile, the first
+// kofd[distance] of its G term columns [r3p + b G, ...): per-term bands, so the
+// narrow terms cost flops only near their buckets (C2-C4: ~0.5x the flops of
+// the full band).  The segments (each rounded to an even width) are packed
+// back to back into 16-column chunks of ONE cp.async pipeline: each thread
+// always stages the same 2-column pair slot of a chunk, and a cursor walked
+// identically by every thread maps the slot to its source column.
+// nbp == NULL: Tucker columns only.
+constexpr int PLANE_SEGS = 1024;  // segments per column tile (1 + occupied x3 in the band)
+
+template <bool ACC>
+__global__ void __launch_bounds__(TilePlane::THREADS)
+    k_gemm_plane(const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                 int64_t ldb, double *__restrict__ C, int64_t ldc, int64_t M, int64_t N,
+                 int64_t r3p, int64_t G, const int32_t *__restrict__ bc3,
+                 const int32_t *__restrict__ nbp, int gamma, const int *__restrict__ kofd) {
+  using T = TilePlane;
+  constexpr int CH = T::BK / 2;                  // 2-column pair slots per chunk row
+  static_assert(T::THREADS % CH == 0, "pair slot must be fixed per thread");
+  constexpr int ROWS_PER_PASS = T::THREADS / CH;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_col[PLANE_SEGS], s_len[PLANE_SEGS], s_pp[PLANE_SEGS];
+  __shared__ int s_band[2], s_wsum[T::THREADS / 32];
+  const int64_t n0 = (int64_t)blockIdx.x * T::BN;
+  const int64_t m0 = (int64_t)blockIdx.y * T::BM;
+  const int64_t top = min(n0 + T::BN, N) - 1;
+  if (threadIdx.x == 0) {
+    int a = 0, bb = 0;
+    if (nbp) {
+      const int nb = *nbp;
+      const int64_t lo_x = n0 - gamma, hi_x = top + gamma;
+      int l = 0, h = nb;
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (bc3[m] < lo_x) l = m + 1; else h = m;
+      }
+      a = l;
+      h = nb;
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (bc3[m] <= hi_x) l = m + 1; else h = m;
+      }
+      bb = l;
+    }
+    s_band[0] = a;
+    s_band[1] = bb;
+  }
+  __syncthreads();
+  // segment list of this column tile in shared memory (order preserving) with
+  // the exclusive prefix of their 2-column pair counts
+  const int blo = s_band[0], bhi = s_band[1];
+  int nseg = 0, npair = 0;
+  if (r3p > 0) {
+    if (threadIdx.x == 0) {
+      s_col[0] = 0;
+      s_len[0] = (int)r3p;
+      s_pp[0] = 0;
+    }
+    nseg = 1;
+    npair = (int)((r3p + 1) / 2);
+  }
+  for (int i0 = blo; i0 < bhi; i0 += T::THREADS) {
+    const int bi = i0 + threadIdx.x;
+    int K = 0;
+    if (bi < bhi) {
+      const int64_t s3 = bc3[bi];
+      const int64_t d = max((int64_t)0, max(n0 - s3, s3 - top));
+      K = d <= gamma ? kofd[d] : 0;
+    }
+    int tot, ptot;
+    const int pos = block_exclusive_scan(K > 0 ? 1 : 0, s_wsum, &tot);
+    const int pp = block_exclusive_scan((K + 1) / 2, s_wsum, &ptot);
+    if (K > 0 && nseg + pos < PLANE_SEGS) {
+      s_col[nseg + pos] = (int)(r3p + (int64_t)bi * G);
+      s_len[nseg + pos] = K;
+      s_pp[nseg + pos] = npair + pp;
+    }
+    nseg += tot;
+    npair += ptot;
+  }
+  nseg = min(nseg, PLANE_SEGS - 1);  // host guarantees 1 + BN + 2 gamma < PLANE_SEGS
+  if (threadIdx.x == 0) s_pp[nseg] = npair;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp / T::WARPS_N) * T::WM, wn0 = (warp % T::WARPS_N) * T::WN;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int my = threadIdx.x % CH, row0 = threadIdx.x / CH;
+  const int chunks = (npair + CH - 1) / CH;
+  int si = 0;  // my slot's segment (advances monotonically)
+  Acc<T> acc;
+  acc.zero();
+  auto load_chunk = [&](int c) {
+    const int P = c * CH + my;
+    int64_t col = 0;
+    int bytes = 0;
+    if (P < npair) {
+      while (s_pp[si + 1] <= P) ++si;
+      const int off = 2 * (P - s_pp[si]);
+      col = s_col[si] + off;
+      bytes = off + 1 < s_len[si] ? 16 : 8;
+    }
+    double *st = smem + (c % T::STAGES) * T::STAGE_DOUBLES;
+#pragma unroll
+    for (int r = row0; r < T::BM + T::BN; r += ROWS_PER_PASS) {
+      const double *src;
+      bool ok;
+      if (r < T::BM) {
+        const int64_t g = m0 + r;
+        ok = bytes > 0 && g < M;
+        src = ok ? A + g * lda + col : A;
+      } else {
+        const int64_t g = n0 + (r - T::BM);
+        ok = bytes > 0 && g < N;
+        src = ok ? B + g * ldb + col : B;
+      }
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                       smem_addr(st + r * T::LDS + 2 * my)),
+                   "l"(src), "r"(ok ? bytes : 0));
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < T::STAGES - 1; ++st) {
+    if (st < chunks) load_chunk(st);
+    cp_async_commit();
+  }
+  for (int c = 0; c < chunks; ++c) {
+    cp_async_wait<T::STAGES - 2>();
+    __syncthreads();
+    if (c + T::STAGES - 1 < chunks) load_chunk(c + T::STAGES - 1);
+    cp_async_commit();
+    stage_mma<T>(smem + (c % T::STAGES) * T::STAGE_DOUBLES, acc, wm0, wn0, gid, tig);
+  }
+  cp_async_wait<0>();
+  store_tile<T, ACC>(acc, C, ldc, m0, M, n0, N);
 }
 
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
@@ -1236,10 +1415,10 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
   int64_t a = round_up(planes * n * *lda * 8, 256);
   int64_t b = round_up(n * *lda * 8, 256);
   const int64_t rp = round_up(std::max<int64_t>(rmax, 1), 2);
-  // Y (planes x r2 x r3) | Yt (planes x r3p x r2p) | V2p (n x r2p)
-  int64_t y = with_long ? round_up((2 * planes * rp * rp + n * rp) * 8, 256) : 0;
+  // Yt (planes x r3p x r2p) | V2p (n x r2p)
+  int64_t y = with_long ? round_up((planes * rp * rp + n * rp) * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, TilePlane::BN);
-  int64_t rr = round_up(ntiles * 4 * 8, 256);
+  int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256);  // ranges | kofd
   *offB = a;
   *offY = a + b;
   *offR = a + b + y;
@@ -1279,6 +1458,9 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(Rs >= 0 && Rs <= SR_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs,
              SR_MAXR);
   RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
+  RS_REQUIRE(1 + TilePlane::BN + 2 * gamma < PLANE_SEGS,
+             "rs_assemble_planes: gamma=%lld too wide for the plane GEMM's segment list",
+             (long long)gamma);
   RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
              "rs_assemble_planes: bad short part");
   RS_REQUIRE(with_long || with_short || accumulate, "rs_assemble_planes: nothing to do");
@@ -1301,14 +1483,11 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   int st;
   if (with_long) {
     ProfScope ps(s, "tucker_f");
-    k_tucker_y<<<grid_for(planes * r2 * r3, 128), 128, 0, s>>>(core, (int)r1, (int)r2, (int)r3,
-                                                               V1, x1_lo, planes, Y);
-    if ((st = check_launch("tucker_y"))) return st;
     const int64_t rp = round_up(rmax, 2), r2p = round_up(r2, 2);
-    double *Yt = Y + planes * rp * rp;
+    double *Yt = Y;
     double *V2p = Yt + planes * rp * rp;
-    k_tucker_yt<<<grid_for(planes * r3p * r2p, 256), 256, 0, s>>>(Y, (int)r2, (int)r3, (int)r2p,
-                                                                  (int)r3p, planes, Yt);
+    k_tucker_yt<<<grid_for(planes * r3p * r2p, 256), 256, 0, s>>>(
+        core, (int)r1, (int)r2, (int)r3, V1, x1_lo, (int)r2p, (int)r3p, planes, Yt);
     if ((st = check_launch("tucker_yt"))) return st;
     k_pad_cols<<<grid_for(n * r2p, 256), 256, 0, s>>>(V2, n, (int)r2, (int)r2p, V2p);
     if ((st = check_launch("pad_cols"))) return st;
@@ -1330,29 +1509,35 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                                                      bc3, with_short ? nb_dev : nullptr, n, Bt, lda);
   if ((st = check_launch("build_bt"))) return st;
   const int64_t ntiles = ceil_div(n, TilePlane::BN);
-  k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
-      bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
-      ranges);
-  if ((st = check_launch("band_ranges"))) return st;
   const int slices = (flags >> 8) & 0xF;
   if (slices) {  // Ozaki-split FP64 on the int8 tensor cores (same tiles, same K ranges)
+    k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
+        bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
+        ranges);
+    if ((st = check_launch("band_ranges"))) return st;
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int64_t oz_off = tot - round_up(rs_oz_workspace_bytes(planes * n, n, lda, slices), 256);
     return rs_oz_gemm_cols(A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2, slices,
                            accumulate ? 1 : 0, wb + oz_off, tot - oz_off,
                            with_short ? nb_dev : nullptr, r3p, G, stream);
   }
+  int *kofd = (int *)((char *)ranges + round_up(ntiles * 4 * 8, 256));
+  if (with_short) {
+    k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
+    if ((st = check_launch("term_prefix"))) return st;
+  }
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
   {
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
+    const int32_t *nbs = with_short ? nb_dev : nullptr;
     if (accumulate) {
-      if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, true>))) return st;
-      k_gemm_nt<TilePlane, true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2);
+      if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<true>))) return st;
+      k_gemm_plane<true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd);
     } else {
-      if ((st = set_smem<TilePlane>((const void *)k_gemm_nt<TilePlane, false>))) return st;
-      k_gemm_nt<TilePlane, false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2);
+      if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<false>))) return st;
+      k_gemm_plane<false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
+          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd);
     }
   }
   return check_launch("plane_gemm");

@@ -61,12 +61,6 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   return pol;
 }
 
-__device__ __forceinline__ double ld_l0(const double *p, uint64_t pol) {
-  double v;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
 // predicated L0 load: 0.0 (and no memory access) when !ok
 __device__ __forceinline__ double ld_l0_pred(const double *p, bool ok, uint64_t pol) {
   double v = 0.0;

@@ -417,6 +417,9 @@ class RSTucker:
 
 
 # ============================================================ grid assembly
+_ASM_PLANS: dict = {}   # (sizes, flags) -> (planes per chunk, workspace bytes)
+
+
 def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int = 0,
                   x1_hi: Optional[int] = None, out=None, accumulate: bool = False,
                   workspace_bytes: int = _ASSEMBLE_WORKSPACE, workspace_slot: str = "assemble"):
@@ -482,12 +485,17 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
             out.zero_()
         return out
     rmax = max(r1, r2, r3)
-    one = L.rs_assemble_workspace_bytes(n, 1, rmax, nb_max, rs, flags)
-    per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, nb_max, rs, flags) - one
-    fixed = one - per_plane
-    chunk = max(1, min(planes, (workspace_bytes - fixed) // max(per_plane, 1)))
-    ws = nat.Workspace.get(L.rs_assemble_workspace_bytes(n, chunk, rmax, nb_max, rs, flags),
-                           workspace_slot)
+    key = (n, planes, rmax, nb_max, rs, flags, workspace_bytes)
+    plan = _ASM_PLANS.get(key)
+    if plan is None:
+        one = L.rs_assemble_workspace_bytes(n, 1, rmax, nb_max, rs, flags)
+        per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, nb_max, rs, flags) - one
+        fixed = one - per_plane
+        chunk = max(1, min(planes, (workspace_bytes - fixed) // max(per_plane, 1)))
+        plan = _ASM_PLANS[key] = (chunk, L.rs_assemble_workspace_bytes(n, chunk, rmax, nb_max,
+                                                                        rs, flags))
+    chunk = plan[0]
+    ws = nat.Workspace.get(plan[1], workspace_slot)
     stream = nat.stream_ptr()
     for p0 in range(x1_lo, x1_hi, chunk):
         p1 = min(x1_hi, p0 + chunk)

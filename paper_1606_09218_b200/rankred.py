@@ -433,6 +433,46 @@ def truncated_spectrum(theta: np.ndarray, trace: float, n: int, eps, forced_rank
     return r, s, tail, total
 
 
+def truncated_spectra(thetas: np.ndarray, traces, n: int, eps, forced=None, limit=None,
+                      iters: int = TOPEIG_ITERS):
+    """:func:`truncated_spectrum` for all modes at once (one vectorised pass
+    over the (m, b) Ritz values: this runs on the critical path between the
+    eigen block's synchronisation and the core launch).  Returns a list of
+    (rank or None, s, tail, total) per mode, identical to the scalar rule."""
+    th = np.clip(np.asarray(thetas, dtype=np.float64), 0.0, None)
+    m, b = th.shape
+    sums = th.sum(axis=1)
+    rem = np.maximum(np.asarray(traces, dtype=np.float64) - sums, 0.0) if b < n else np.zeros(m)
+    totals = sums + rem
+    tails = np.cumsum(th[:, ::-1], axis=1)[:, ::-1] + rem[:, None]
+    ok = tails <= eps * totals[:, None]
+    first = np.where(ok.any(axis=1), ok.argmax(axis=1), -1)
+    out = []
+    for l in range(m):
+        s = np.zeros(n)
+        s[:b] = np.sqrt(th[l])
+        tail, total = tails[l], float(totals[l])
+        if forced is not None and forced[l] is not None:
+            r = int(forced[l])
+        elif total == 0.0:
+            r = 1
+        elif first[l] < 0:
+            out.append((None, s, tail, total))
+            continue
+        else:
+            r = max(int(first[l]), 1)
+        if limit is not None:
+            r = min(r, limit)
+        if b < n:
+            lam_r = th[l, r - 1] if 0 < r <= b else 0.0
+            if (r >= b or lam_r <= 0.0 or th[l, 0] <= 0.0 or
+                    1e2 * (th[l, b - 1] / lam_r) ** iters * np.sqrt(lam_r / th[l, 0]) > 1e-11):
+                out.append((None, s, tail, total))
+                continue
+        out.append((r, s, tail, total))
+    return out
+
+
 def shifted_core(table_dev, n: int, zs, starts, z, w_long):
     """RHOSVD core of the shift-structured long part."""
     torch = nat._torch()

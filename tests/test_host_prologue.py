@@ -117,3 +117,32 @@ def test_separation_distance_matches_bruteforce():
     s = rt.generate_random_cluster(5000, rt.Box3(20.0), 0.3, seed=4)
     from scipy.spatial.distance import pdist
     assert rt.separation_distance(s) == float(pdist(s.positions).min())
+
+
+def test_truncated_spectra_matches_scalar_rule():
+    """The vectorised rank rule (critical path after the eigen sync) equals
+    the per-mode rule on decaying, flat, zero and forced spectra."""
+    import numpy as np
+    from paper_1606_09218_b200.rankred import truncated_spectra, truncated_spectrum
+
+    rng = np.random.default_rng(3)
+    n, b = 256, 24
+    cases = []
+    for decay in (0.3, 0.8, 2.0):
+        th = np.sort(np.exp(-decay * np.arange(b)) * rng.uniform(0.5, 1.5, b))[::-1]
+        cases.append(th)
+    cases.append(np.zeros(b))
+    thetas = np.stack(cases[:3])
+    traces = thetas.sum(axis=1) * (1 + 1e-9)
+    for eps in (1e-6, 1e-8, 1e-12):
+        for forced in (None, (3, 4, 5)):
+            got = truncated_spectra(thetas, traces, n, eps, forced, 200, 2)
+            for l in range(3):
+                ref = truncated_spectrum(thetas[l], traces[l], n, eps,
+                                         None if forced is None else forced[l], 200, 2)
+                assert got[l][0] == ref[0]
+                assert np.array_equal(got[l][1], ref[1])
+                assert np.allclose(got[l][2], ref[2], rtol=0, atol=0)
+                assert got[l][3] == ref[3]
+    z = truncated_spectra(np.zeros((1, b)), [0.0], n, 1e-6, None, 200, 2)
+    assert z[0][0] == truncated_spectrum(np.zeros(b), 0.0, n, 1e-6, None, 200, 2)[0]
