@@ -471,14 +471,18 @@ constexpr int SD_PADA = SD_TX1;  // plane offsets stay within [-TX1, W + TX1)
 constexpr int SD_PADB = SD_TX2;  // row offsets stay within [-TX2, W + TX2)
 
 template <int GK>
-__global__ void __launch_bounds__(SD_THREADS)
+__global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
     k_short_dmma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
-                 double *__restrict__ A, int64_t lda, int64_t col0) {
+                 double *__restrict__ A, int64_t lda, int64_t col0, int kslices) {
+  // G: bucket stride of A (R_s rounded up to even); this CTA builds the term
+  // slice [k_off, k_off + GK) of its buckets (kslices slices: fewer
+  // accumulators per thread, two CTAs per SM)
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
+  const int k_off = (int)(blockIdx.z % kslices) * GK;
   constexpr int P = GK + 1;  // odd pitch (doubles): conflict-light row gathers
   const int WA = W + 2 * SD_PADA, WB = W + 2 * SD_PADB;
   double *uA = sm;                      // WA x P : wl_k ul[d, k], zero padded
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(SD_THREADS)
   __shared__ int s_slo[SD_BG + 1];     // bucket starts within the staged list
   __shared__ int s_plo[SD_BG];         // first candidate copy of each bucket
   const int nb = *nbp;
-  const int b0 = blockIdx.z * SD_BG;
+  const int b0 = (int)(blockIdx.z / kslices) * SD_BG;
   if (b0 >= nb) return;
   const int nbk = min(SD_BG, nb - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -502,9 +506,10 @@ __global__ void __launch_bounds__(SD_THREADS)
   for (int e = tid; e < (WA + WB) * P; e += SD_THREADS) uA[e] = 0.0;  // k >= Rs rows stay zero
   __syncthreads();
   for (int e = tid; e < Rs * W; e += SD_THREADS) {  // coalesced read of ul (W x Rs)
-    const int d = e / Rs, k = e - (e / Rs) * Rs;
+    const int d = e / Rs, k = e - (e / Rs) * Rs - k_off;
+    if (k < 0 || k >= GK) continue;
     const double u = ul[e];
-    uA[(d + SD_PADA) * P + k] = wl[k] * u;
+    uA[(d + SD_PADA) * P + k] = wl[k + k_off] * u;
     uB[(d + SD_PADB) * P + k] = u;
   }
   const int64_t yw = y0 + warp * 8;
@@ -593,10 +598,11 @@ __global__ void __launch_bounds__(SD_THREADS)
           for (int jj = 0; jj < 2; ++jj) {
             const int64_t x2 = yw + 2 * kq + jj;
             if (x2 < n) {
-              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
+              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * G + k_off;
 #pragma unroll
               for (int k = 0; k < GK; k += 2)
-                *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
+                if (k_off + k < G)
+                  *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
             }
           }
         }
@@ -615,10 +621,10 @@ __global__ void __launch_bounds__(SD_THREADS)
       for (int jj = 0; jj < 2; ++jj) {
         const int64_t x2 = yw + 2 * kq + jj;
         if (x2 < n) {
-          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
+          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * G + k_off;
 #pragma unroll
           for (int k = 0; k < GK; k += 2)
-            *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
+            if (k_off + k < G) *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
         }
       }
     }
@@ -684,6 +690,53 @@ __global__ void __launch_bounds__(256)
 // always stages the same 2-column pair slot of a chunk, and a cursor walked
 // identically by every thread maps the slot to its source column.
 // nbp == NULL: Tucker columns only.
+// Row-block term table: for GEMM row block rb (BM consecutive (x1, x2) rows of
+// the plane range) and bucket b, kr[rb * ldk + b] = the number of leading
+// terms that can be nonzero anywhere in that row block = kofd[d12] with d12
+// the smallest Chebyshev (x1, x2) distance from the block to a copy of the
+// bucket (0: no copy within gamma).  With the x3 distance of the GEMM's
+// column tile this gives each (row block, column tile, bucket) its term
+// count: the narrow terms only matter next to their copies in all three
+// coordinates.  Copies of a bucket are c2-sorted: binary search of the x2
+// window, scan of the candidates.
+__global__ void k_rowblock_terms(const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+                                 const int32_t *__restrict__ bstart,
+                                 const int32_t *__restrict__ nbp, const int *__restrict__ kofd,
+                                 int gamma, int64_t n, int64_t x1_lo, int64_t rows, int BM,
+                                 int64_t nrb, int64_t ldk, uint8_t *__restrict__ kr) {
+  const int nb = *nbp;
+  const int64_t total = nrb * ldk;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rb = e / ldk;
+    const int b = (int)(e - rb * ldk);
+    if (b >= nb) continue;
+    const int64_t r0 = rb * BM, r1 = min(r0 + BM, rows) - 1;
+    const int64_t xa = x1_lo + r0 / n, xb = x1_lo + r1 / n;
+    const int64_t ya = xa == xb ? r0 % n : 0, yb = xa == xb ? r1 % n : n - 1;
+    int l = bstart[b], h = bstart[b + 1];
+    const int p_hi = h;
+    while (l < h) {
+      const int m = (l + h) >> 1;
+      if (c2[m] < ya - gamma) l = m + 1; else h = m;
+    }
+    int64_t best = (int64_t)gamma + 1;
+    for (int p = l; p < p_hi; ++p) {
+      const int64_t y = c2[p];
+      if (y > yb + gamma) break;
+      const int64_t x = c1[p];
+      const int64_t dx = x < xa ? xa - x : (x > xb ? x - xb : 0);
+      const int64_t dy = y < ya ? ya - y : (y > yb ? y - yb : 0);
+      const int64_t d = max(dx, dy);
+      if (d < best) {
+        best = d;
+        if (d == 0) break;
+      }
+    }
+    kr[e] = (uint8_t)(best <= gamma ? kofd[best] : 0);
+  }
+}
+
 constexpr int PLANE_SEGS = 1024;  // segments per column tile (1 + occupied x3 in the band)
 
 template <bool ACC>
@@ -691,7 +744,8 @@ __global__ void __launch_bounds__(TilePlane::THREADS)
     k_gemm_plane(const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                  int64_t ldb, double *__restrict__ C, int64_t ldc, int64_t M, int64_t N,
                  int64_t r3p, int64_t G, const int32_t *__restrict__ bc3,
-                 const int32_t *__restrict__ nbp, int gamma, const int *__restrict__ kofd) {
+                 const int32_t *__restrict__ nbp, int gamma, const int *__restrict__ kofd,
+                 const uint8_t *__restrict__ kr, int64_t ldk) {
   using T = TilePlane;
   constexpr int CH = T::BK / 2;                  // 2-column pair slots per chunk row
   static_assert(T::THREADS % CH == 0, "pair slot must be fixed per thread");
@@ -744,6 +798,7 @@ __global__ void __launch_bounds__(TilePlane::THREADS)
       const int64_t s3 = bc3[bi];
       const int64_t d = max((int64_t)0, max(n0 - s3, s3 - top));
       K = d <= gamma ? kofd[d] : 0;
+      if (kr) K = min(K, (int)kr[blockIdx.y * ldk + bi]);
     }
     int tot, ptot;
     const int pos = block_exclusive_scan(K > 0 ? 1 : 0, s_wsum, &tot);
@@ -1090,7 +1145,7 @@ using namespace rsb;
 
 // ============================================================== C ABI
 template <int GK>
-static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int gamma,
+static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int G, int gamma,
                                const int32_t *c1, const int32_t *c2, const double *zq,
                                const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                                int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
@@ -1101,26 +1156,28 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int g
   cudaError_t e = cudaFuncSetAttribute((const void *)k_short_dmma<GK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_dmma smem: %s", cudaGetErrorString(e));
+  const int kslices = (G + GK - 1) / GK;
   dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
-            (unsigned)ceil_div(nb_max, SD_BG));
-  k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, GK, gamma, c1, c2, zq, bstart, nb_dev,
-                                                  n, x1_lo, planes, A, lda, col0);
+            (unsigned)(ceil_div(nb_max, SD_BG) * kslices));
+  k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, G, gamma, c1, c2, zq, bstart, nb_dev,
+                                                  n, x1_lo, planes, A, lda, col0, kslices);
   return check_launch("short_dmma");
 }
 
-// one instantiation per even row width G = R_s rounded up to even
+// one instantiation per even term-slice width: G = R_s rounded up to even;
+// G <= 14 in one slice, wider in two (<= ~126 registers: two CTAs per SM)
 static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, int gamma,
                              const int32_t *c1, const int32_t *c2, const double *zq,
                              const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                              int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
                              int64_t col0, cudaStream_t s) {
-  switch (G) {
-#define RS_SD(R)                                                                              \
-  case R:                                                                                     \
-    return launch_short_dmma_t<R>(ul, wl, Rs, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
+  const int GK = G <= 14 ? G : (int)round_up((G + 1) / 2, 2);
+  switch (GK) {
+#define RS_SD(R)                                                                                \
+  case R:                                                                                       \
+    return launch_short_dmma_t<R>(ul, wl, Rs, G, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
                                   x1_lo, planes, A, lda, col0, s);
-    RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14) RS_SD(16) RS_SD(18)
-    RS_SD(20) RS_SD(22) RS_SD(24)
+    RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14)
 #undef RS_SD
   }
   return fail(RS_ERR_UNSUPPORTED, "short_dmma: R_s=%d exceeds 24", Rs);
@@ -1418,7 +1475,10 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
   // Yt (planes x r3p x r2p) | V2p (n x r2p)
   int64_t y = with_long ? round_up((planes * rp * rp + n * rp) * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, TilePlane::BN);
-  int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256);  // ranges | kofd
+  // ranges | kofd | row-block term table (uint8, row blocks x buckets)
+  int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256) +
+               (with_short ? round_up(ceil_div(planes * n, TilePlane::BM) * round_up(nb_max, 16), 256)
+                           : 0);
   *offB = a;
   *offY = a + b;
   *offR = a + b + y;
@@ -1522,9 +1582,15 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                            with_short ? nb_dev : nullptr, r3p, G, stream);
   }
   int *kofd = (int *)((char *)ranges + round_up(ntiles * 4 * 8, 256));
+  const int64_t nrb = ceil_div(planes * n, TilePlane::BM), ldk = round_up(nb_max, 16);
+  uint8_t *kr = (uint8_t *)((char *)kofd + round_up((n + 1) * 4, 256));
   if (with_short) {
     k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
     if ((st = check_launch("term_prefix"))) return st;
+    k_rowblock_terms<<<grid_for(nrb * ldk, 256), 256, 0, s>>>(
+        c1, c2, bstart, nb_dev, kofd, (int)gamma, n, x1_lo, planes * n, TilePlane::BM, nrb, ldk,
+        kr);
+    if ((st = check_launch("rowblock_terms"))) return st;
   }
   dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
   {
@@ -1533,11 +1599,13 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     if (accumulate) {
       if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<true>))) return st;
       k_gemm_plane<true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd);
+          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd,
+          with_short ? kr : nullptr, ldk);
     } else {
       if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<false>))) return st;
       k_gemm_plane<false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd);
+          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd,
+          with_short ? kr : nullptr, ldk);
     }
   }
   return check_launch("plane_gemm");
