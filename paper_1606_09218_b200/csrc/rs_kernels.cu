@@ -471,18 +471,14 @@ constexpr int SD_PADA = SD_TX1;  // plane offsets stay within [-TX1, W + TX1)
 constexpr int SD_PADB = SD_TX2;  // row offsets stay within [-TX2, W + TX2)
 
 template <int GK>
-__global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
+__global__ void __launch_bounds__(SD_THREADS)
     k_short_dmma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
-                 double *__restrict__ A, int64_t lda, int64_t col0, int kslices) {
-  // G: bucket stride of A (R_s rounded up to even); this CTA builds the term
-  // slice [k_off, k_off + GK) of its buckets (kslices slices: fewer
-  // accumulators per thread, two CTAs per SM)
+                 double *__restrict__ A, int64_t lda, int64_t col0) {
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
-  const int k_off = (int)(blockIdx.z % kslices) * GK;
   constexpr int P = GK + 1;  // odd pitch (doubles): conflict-light row gathers
   const int WA = W + 2 * SD_PADA, WB = W + 2 * SD_PADB;
   double *uA = sm;                      // WA x P : wl_k ul[d, k], zero padded
@@ -496,7 +492,7 @@ __global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
   __shared__ int s_slo[SD_BG + 1];     // bucket starts within the staged list
   __shared__ int s_plo[SD_BG];         // first candidate copy of each bucket
   const int nb = *nbp;
-  const int b0 = (int)(blockIdx.z / kslices) * SD_BG;
+  const int b0 = blockIdx.z * SD_BG;
   if (b0 >= nb) return;
   const int nbk = min(SD_BG, nb - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -506,10 +502,9 @@ __global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
   for (int e = tid; e < (WA + WB) * P; e += SD_THREADS) uA[e] = 0.0;  // k >= Rs rows stay zero
   __syncthreads();
   for (int e = tid; e < Rs * W; e += SD_THREADS) {  // coalesced read of ul (W x Rs)
-    const int d = e / Rs, k = e - (e / Rs) * Rs - k_off;
-    if (k < 0 || k >= GK) continue;
+    const int d = e / Rs, k = e - (e / Rs) * Rs;
     const double u = ul[e];
-    uA[(d + SD_PADA) * P + k] = wl[k + k_off] * u;
+    uA[(d + SD_PADA) * P + k] = wl[k] * u;
     uB[(d + SD_PADB) * P + k] = u;
   }
   const int64_t yw = y0 + warp * 8;
@@ -598,11 +593,10 @@ __global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
           for (int jj = 0; jj < 2; ++jj) {
             const int64_t x2 = yw + 2 * kq + jj;
             if (x2 < n) {
-              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * G + k_off;
+              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
 #pragma unroll
               for (int k = 0; k < GK; k += 2)
-                if (k_off + k < G)
-                  *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
+                *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
             }
           }
         }
@@ -621,10 +615,10 @@ __global__ void __launch_bounds__(SD_THREADS, (GK <= 14 ? 2 : 1))
       for (int jj = 0; jj < 2; ++jj) {
         const int64_t x2 = yw + 2 * kq + jj;
         if (x2 < n) {
-          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * G + k_off;
+          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
 #pragma unroll
           for (int k = 0; k < GK; k += 2)
-            if (k_off + k < G) *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
+            *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
         }
       }
     }
@@ -1145,7 +1139,7 @@ using namespace rsb;
 
 // ============================================================== C ABI
 template <int GK>
-static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int G, int gamma,
+static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int gamma,
                                const int32_t *c1, const int32_t *c2, const double *zq,
                                const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                                int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
@@ -1156,28 +1150,26 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int G
   cudaError_t e = cudaFuncSetAttribute((const void *)k_short_dmma<GK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_dmma smem: %s", cudaGetErrorString(e));
-  const int kslices = (G + GK - 1) / GK;
   dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
-            (unsigned)(ceil_div(nb_max, SD_BG) * kslices));
-  k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, G, gamma, c1, c2, zq, bstart, nb_dev,
-                                                  n, x1_lo, planes, A, lda, col0, kslices);
+            (unsigned)ceil_div(nb_max, SD_BG));
+  k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, GK, gamma, c1, c2, zq, bstart, nb_dev,
+                                                  n, x1_lo, planes, A, lda, col0);
   return check_launch("short_dmma");
 }
 
-// one instantiation per even term-slice width: G = R_s rounded up to even;
-// G <= 14 in one slice, wider in two (<= ~126 registers: two CTAs per SM)
+// one instantiation per even row width G = R_s rounded up to even
 static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, int gamma,
                              const int32_t *c1, const int32_t *c2, const double *zq,
                              const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                              int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
                              int64_t col0, cudaStream_t s) {
-  const int GK = G <= 14 ? G : (int)round_up((G + 1) / 2, 2);
-  switch (GK) {
-#define RS_SD(R)                                                                                \
-  case R:                                                                                       \
-    return launch_short_dmma_t<R>(ul, wl, Rs, G, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
+  switch (G) {
+#define RS_SD(R)                                                                              \
+  case R:                                                                                     \
+    return launch_short_dmma_t<R>(ul, wl, Rs, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
                                   x1_lo, planes, A, lda, col0, s);
-    RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14)
+    RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14) RS_SD(16) RS_SD(18)
+    RS_SD(20) RS_SD(22) RS_SD(24)
 #undef RS_SD
   }
   return fail(RS_ERR_UNSUPPORTED, "short_dmma: R_s=%d exceeds 24", Rs);
