@@ -305,12 +305,16 @@ def main():
     dp = rt.DeviceParticles(pos_d, q_d, system.box)
     out_shape = (max(x1_hi - x1_lo, 1), n, n)
 
+    # two output slabs used in turn (a serving loop's reused result buffers)
+    slabs = [torch.empty(out_shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+
     def step(particles):
-        step.last = None   # free the previous grid before the next prefetch allocates
+        step.i = getattr(step, "i", -1) + 1
         # public API: build_rs (short-range planes prefetched on a side stream,
         # overlapping the long-range reduction) + dense_rs of this rank's slab
         res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi),
-                          group=dist.group.WORLD if world > 1 else None)
+                          group=dist.group.WORLD if world > 1 else None,
+                          prefetch_out=slabs[step.i % 2])
         g = rt.dense_rs(res.rs, limit=1 << 62, device=True, x1_range=(x1_lo, x1_hi))
         step.last = g
         return res
@@ -322,6 +326,7 @@ def main():
     L = nat.lib()
     for i in range(max(args.warmup, 8)):
         L.rs_prof_enable(1 if i >= max(args.warmup, 8) - 2 else 0)
+        flush.fill_(i & 0xFF)   # as in the timed loop (its kernel module loads lazily)
         res = step(dp)
     L.rs_prof_enable(0)
     torch.cuda.synchronize()
@@ -343,8 +348,24 @@ def main():
     gc.collect()
     if not os.environ.get("BENCH_GC"):
         gc.disable()
+    verbose = bool(os.environ.get("BENCH_VERBOSE"))
+    if os.environ.get("BENCH_VERBOSE") == "3":
+        torch.cuda.memory._record_memory_history(max_entries=100000)
+    if verbose:
+        mallocs0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
+        host_t, mallocs_t = [], []
     with ClockSampler(local) as clk:
         for i in range(args.steps):
+            if verbose:
+                if os.environ.get("BENCH_VERBOSE") == "2":
+                    mallocs_t.append(torch.cuda.memory_stats().get("num_device_alloc", 0))
+                from paper_1606_09218_b200 import assembly as _asm
+                if _asm._TRACE is not None:
+                    if i == 1:
+                        tr0 = list(_asm._TRACE)
+                    _asm._TRACE.clear()
+                    _asm._mark("step")
+                host_t.append(time.perf_counter())
             flush.fill_(i & 0xFF)
             ev[i][0].record()
             step(dp)
@@ -355,8 +376,25 @@ def main():
     barrier()
     t_steps = [a.elapsed_time(b) for a, b in ev]
     t_mean = float(np.mean(t_steps)) / 1e3
-    if os.environ.get("BENCH_VERBOSE"):
+    if verbose:
         print("step ms:", " ".join(f"{t:.3f}" for t in t_steps), file=sys.stderr)
+        print("host ms:", " ".join(f"{1e3 * (b - a):.3f}" for a, b in zip(host_t[:-1], host_t[1:])),
+              file=sys.stderr)
+        if "tr0" in locals():
+            print("step-0 host trace:", " ".join(f"{a}->{b}:{1e6 * (tb - ta):.0f}us" for (a, ta), (b, tb)
+                                                  in zip(tr0[:-1], tr0[1:])), file=sys.stderr)
+        print("cudaMalloc per step:", [b - a for a, b in zip(mallocs_t[:-1], mallocs_t[1:])],
+              file=sys.stderr)
+        if os.environ.get("BENCH_VERBOSE") == "3":
+            for tr in torch.cuda.memory._snapshot()["device_traces"]:
+                for e in tr:
+                    if e["action"] in ("segment_alloc", "segment_map"):
+                        print(e["action"], e["size"], e.get("stream"), file=sys.stderr)
+                        for f in e["frames"][:14]:
+                            print("   ", f["filename"].split("/")[-1], f["line"], f["name"],
+                                  file=sys.stderr)
+        print("cudaMalloc calls in the timed region:",
+              torch.cuda.memory_stats().get("num_device_alloc", 0) - mallocs0, file=sys.stderr)
     gemm_ms, gemm_n = nat.prof_query("gemm_short")
     prof = {k: nat.prof_query(k) for k in ("gemm_short", "gemm_tucker", "gemm_plane", "short_rows",
                                           "topeig", "syrk", "core", "shift_project")}

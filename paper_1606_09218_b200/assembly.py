@@ -324,10 +324,15 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     _mark("f_buf")
     pf = (None, None, 0, 0, 0, 0, None, None, 0, None, 0, 0, None)
     if prefetch is not None:
-        plan, lo, hi, groups = prefetch
+        plan, lo, hi, groups, out = prefetch
         side = _side_stream()
         rs = int(plan.local.rank)
-        out = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
+        if out is None:
+            out = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
+        elif (tuple(out.shape) != (hi - lo, n, n) or out.dtype != torch.float64
+              or not out.is_cuda or not out.is_contiguous()):
+            raise DomainError(f"prefetch_out must be a contiguous float64 CUDA tensor of shape "
+                              f"{(hi - lo, n, n)}")
         out.record_stream(side)
         L = nat.lib()
         if L.rs_short_method(n, count, plan.gamma, rs) == nat.SHORT_L0:
@@ -522,14 +527,17 @@ def _side_stream():
 
 
 def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
-             prefetch_groups: int = 1) -> AssemblyResult:
+             prefetch_groups: int = 1, prefetch_out=None) -> AssemblyResult:
     """Reference ``build_rs`` (``assembly.py:187-279``) on the device.
 
     Extensions: ``prefetch_dense`` (see :func:`_build_rs`); ``group`` (a
     ``torch.distributed`` group: particle-sharded histograms/core);
     ``prefetch_groups`` splits the prefetched planes into that many groups
     finished one by one, so a host-returning :func:`dense_rs` starts the
-    device->host copy of the first planes while later ones are computed."""
+    device->host copy of the first planes while later ones are computed;
+    ``prefetch_out`` (a float64 CUDA tensor of the slab's shape) receives the
+    prefetched grid instead of a fresh allocation (a serving loop's reused
+    output buffer)."""
     if not prefetch_dense:
         return _build_rs(system, cfg, False, group)
     torch = nat._torch()
@@ -538,7 +546,8 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
     chain.wait_stream(user)
     chain.wait_stream(_stream("side"))   # earlier prefetches may still read recycled memory
     with torch.cuda.stream(chain):
-        res = _build_rs(system, cfg, prefetch_dense, group, max(1, int(prefetch_groups)))
+        res = _build_rs(system, cfg, prefetch_dense, group, max(1, int(prefetch_groups)),
+                        prefetch_out)
     user.wait_stream(chain)
     return res
 
@@ -563,7 +572,7 @@ _SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "140"))
 
 
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
-              prefetch_groups: int = 1) -> AssemblyResult:
+              prefetch_groups: int = 1, prefetch_out=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
 
     ``system`` may be a reference-style :class:`ParticleSystem` /
@@ -585,7 +594,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         if plan0.local.rank > 0:
             lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
                                                             int(prefetch_dense[1]))
-            fused = (plan0, lo, hi, prefetch_groups)
+            fused = (plan0, lo, hi, prefetch_groups, prefetch_out)
     ds, collision = _as_device_system(system, grid, fused)
     if cfg.sigma is not None:
         sigma = float(cfg.sigma)

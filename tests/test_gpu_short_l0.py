@@ -142,3 +142,19 @@ def test_grouped_prefetch_to_host(method, rng_, cuda, golden, monkeypatch):
     assert host.shape == ((n, n, n) if rng_ is None else (hi - lo, n, n))
     assert np.max(np.abs(host.reshape(full.shape) - full)) <= AGREE_TOL * scale
     assert ref.shape[0] == hi - lo
+
+
+def test_prefetch_into_caller_buffer(cuda, golden):
+    """build_rs(prefetch_out=buf): the grid lands in the caller's buffer."""
+    torch = cuda
+    system, cfg, _ = case_inputs("C2")
+    n = cfg.grid.n
+    buf = torch.full((n, n, n), float("nan"), dtype=torch.float64, device="cuda")
+    res = rt.build_rs(system, cfg, prefetch_dense=True, prefetch_out=buf)
+    grid = rt.dense_rs(res.rs, limit=1 << 40, device=True)
+    assert grid.data_ptr() == buf.data_ptr()
+    ref = assemble_grid(res.rs.long, res.rs.short)
+    scale = golden["case_C2"]["grid_max_abs"]
+    assert float((grid - ref).abs().max()) <= AGREE_TOL * scale
+    with pytest.raises(rt.DomainError):
+        rt.build_rs(system, cfg, prefetch_dense=True, prefetch_out=buf[:10])
