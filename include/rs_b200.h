@@ -191,6 +191,11 @@ int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32
                          const int32_t *bc3, const int32_t *nb_dev, int64_t x1_lo,
                          int64_t x1_hi, int accumulate, double *out, void *stream);
 
+/* L2 read bandwidth probe: every CTA streams the first `bytes` of buf (sized
+ * to fit in L2) `iters` times with L1-bypassing loads (the roofline of
+ * rs_assemble_short_l0; time it with events on `stream`). */
+int rs_l2_probe(const double *buf, int64_t bytes, int64_t iters, double *out, void *stream);
+
 /* Bucket layout of the short-range copies from the x3 occupancy counts
  * cnt3 (n): bc3 (capacity n), bstart (capacity n+1), *nb (device int). */
 int rs_short_layout(const int32_t *cnt3, int64_t n, int32_t *bstart, int32_t *bc3,

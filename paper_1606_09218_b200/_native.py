@@ -60,6 +60,7 @@ SIGNATURES = {
                                   _ptr, _ptr, _i64, _ptr]),
     "rs_short_layout": (_i32, [_ptr, _i64, _ptr, _ptr, _ptr, _ptr]),
     "rs_short_method": (_i32, [_i64, _i64, _i64, _i64]),
+    "rs_l2_probe": (_i32, [_ptr, _i64, _i64, _ptr, _ptr]),
     "rs_short_l0_bytes": (_i64, [_i64]),
     "rs_short_l0_table": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr]),
     "rs_assemble_short_l0": (_i32, [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i64,

@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as nat
 from .errors import ConfigError, DomainError, ResolutionError
-from .formats import CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
+from .formats import tucker_accumulate, CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
     short_layout, storage_report, to_device, to_host, trusted_cct
 from .parallel import particle_shard, sharded_sum
 from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
@@ -40,7 +40,7 @@ from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effe
     project_kernel, split_rank, split_tensor
 from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, top_eig_supported, \
     SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eig_desc_batched, eps_rank, rhosvd_error_bound, shift_histograms, \
-    shifted_core, shifted_grams, side_svd, top_eig, truncated_spectra, truncated_spectrum, tucker_to_canonical
+    shifted_core, shifted_grams, side_svd, top_eig, rank_rule_fast, truncated_spectrum, tucker_to_canonical
 
 
 @dataclass(frozen=True)
@@ -568,7 +568,7 @@ def _mark(label: str) -> None:
 
 
 # SMs of the side stream's partition (0: ordinary stream on the whole device)
-_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "140"))
+_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "128"))
 
 
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
@@ -749,18 +749,25 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                     raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
         ranks, values, tails, zs, from_top = [], [], [], [], []
         if use_top:
-            spectra3 = truncated_spectra(packed[:3 * b].reshape(3, b), packed[3 * b:3 * b + 3], n,
-                                         cfg.reduction.eps, forced, limit, iters)
+            fast3 = rank_rule_fast(packed[:3 * b].tolist(), packed[3 * b:3 * b + 3].tolist(), n,
+                                   cfg.reduction.eps, forced, limit, iters)
         for l in range(3):
             fr = forced[l] if forced is not None else None
             r = None
             top = False
             if use_top:
-                r, sv, tail, total = spectra3[l]
+                r, tail_r, total = fast3[l]
                 if r is not None and fr is not None and fr > b:
                     r = None
                 Ul = U[l] if r is not None else None
                 top = r is not None
+                if top:   # spectrum arrays are not needed on this path
+                    ranks.append(int(r))
+                    values.append(None)
+                    tails.append((tail_r, total))
+                    zs.append(Ul)
+                    from_top.append(True)
+                    continue
             if r is None:
                 bb = min(n - n % 2, TOPEIG_MAX_BLOCK if b >= 48 else 2 * b)
                 if b and bb > b and top_eig_supported(n, bb):
@@ -843,7 +850,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
             buf.record_stream(cur)
             if pre["groups"] is None:
                 cur.wait_event(pre["ev"])
-                assemble_grid(tucker, None, lo, hi, out=buf, accumulate=True)
+                tucker_accumulate(tucker, lo, hi, buf)
                 done = torch.cuda.Event()
                 done.record(cur)
                 short._cache["prefetch"] = dict(pre, ev=done, complete=True)
@@ -853,8 +860,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                 for g, ev in enumerate(gev):
                     g0, g1 = g * grp, min(hi - lo, (g + 1) * grp)
                     cur.wait_event(ev)
-                    assemble_grid(tucker, None, lo + g0, lo + g1, out=buf[g0:g1],
-                                  accumulate=True)
+                    tucker_accumulate(tucker, lo + g0, lo + g1, buf[g0:g1])
                     done = torch.cuda.Event()
                     done.record(cur)
                     dones.append(done)

@@ -85,6 +85,32 @@ inline int check_launch(const char *what) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when the (function,
+// device) has not been raised to `bytes` yet: the driver call costs
+// microseconds on the launch-bound build path
+inline cudaError_t smem_attr(const void *fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<const void *> fns;
+  static std::vector<int> devs, sizes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t i = 0;
+  for (; i < fns.size(); ++i)
+    if (fns[i] == fn && devs[i] == dev) break;
+  if (i < fns.size() && sizes[i] >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  if (i < fns.size()) {
+    sizes[i] = bytes;
+  } else {
+    fns.push_back(fn);
+    devs.push_back(dev);
+    sizes.push_back(bytes);
+  }
+  return cudaSuccess;
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -238,10 +238,10 @@ static int launch_jacobi(const double *T, int nmat, double *evals, double *Vt, s
                          cudaStream_t s) {
   const size_t need = (size_t)(2 * B * (B + 1) + B) * 8 + (size_t)((B - 1) * B + 1) * 4;
   const size_t smem = std::max(need, reserve);
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_jacobi<B>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr((const void *)k_jacobi<B>, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
-  k_jacobi<B><<<(unsigned)nmat, JAC_THREADS, smem, s>>>(T, evals, Vt, 16);
+  static const int sweeps = getenv("RSB200_JACOBI_SWEEPS") ? atoi(getenv("RSB200_JACOBI_SWEEPS")) : 16;
+  k_jacobi<B><<<(unsigned)nmat, JAC_THREADS, smem, s>>>(T, evals, Vt, sweeps);
   return check_launch("jacobi");
 }
 
@@ -337,9 +337,7 @@ static int gemm_batched_t(const double *A, int64_t lda, int64_t sA, const double
                           int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t M, int64_t N,
                           int64_t K, int nb, cudaStream_t s) {
   if (T::SMEM_BYTES > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_gemm_nt_batched<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         T::SMEM_BYTES);
+    cudaError_t e = smem_attr((const void *)k_gemm_nt_batched<T>, T::SMEM_BYTES);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
   }
   dim3 grid((unsigned)ceil_div(N, T::BN), (unsigned)ceil_div(M, T::BM), (unsigned)nb);
@@ -397,8 +395,7 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   size_t orth_smem = std::max<size_t>((size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8, reserve);
   const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
   if (orth_smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(orth_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)orth_smem);
+    cudaError_t e = smem_attr(orth_fn, (int)orth_smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth smem: %s", cudaGetErrorString(e));
   }
   // Y = Q G (rows), orth

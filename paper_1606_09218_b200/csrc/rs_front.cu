@@ -395,8 +395,7 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
   RS_REQUIRE(r2 <= 1024, "rs_back: r2 = %lld exceeds the H kernel's block", (long long)r2);
   const int threads = (int)round_up(r2, 32);
   const size_t smem = (size_t)CH_CHUNK * (r2 + CH_TA) * 8;
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_core_h,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr((const void *)k_core_h, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
   k_core_h<<<dim3((unsigned)ceil_div(r1, CH_TA), (unsigned)nq), threads, smem, s>>>(
       TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq, bstart, H, ldH);

@@ -1122,7 +1122,7 @@ inline int grid_for(int64_t total, int threads) { return (int)grid_blocks(total,
 template <class T>
 int set_smem(const void *fn) {
   cudaError_t e =
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+      smem_attr(fn, T::SMEM_BYTES);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
   return RS_OK;
 }
@@ -1147,8 +1147,7 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int g
   const int W = 2 * gamma + 1;
   const size_t smem = (size_t)(GK + 1) * (2 * W + 2 * SD_PADA + 2 * SD_PADB) * 8 +
                       (SD_THREADS + 4) * (8 + 4 + 4 + 4) + 32 * 4;
-  cudaError_t e = cudaFuncSetAttribute((const void *)k_short_dmma<GK>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr((const void *)k_short_dmma<GK>, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_dmma smem: %s", cudaGetErrorString(e));
   dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
             (unsigned)ceil_div(nb_max, SD_BG));
@@ -1359,8 +1358,7 @@ int rs_shift_project(const double *Z, int64_t ldz, int64_t n, int64_t r, const d
              "rs_shift_project: bad shape (table must have 2n rows, n_shift <= n)");
   size_t smem = (size_t)(n + SP_SHIFTS + SP_ICH * 32) * 8;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_shift_project,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_attr((const void *)k_shift_project, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
   }
   RS_REQUIRE(ldz == r, "rs_shift_project: Z must be contiguous (ldz == r)");
@@ -1381,8 +1379,7 @@ int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3, int6
              "rs_shift_project3: bad shape");
   size_t smem = (size_t)(n + SP_SHIFTS + SP_ICH * 32) * 8;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_shift_project,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_attr((const void *)k_shift_project, (int)smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
   }
   Proj3 pj{{Z1, Z2, Z3}, {TT1, TT2, TT3}, {r1, r2, r3}};

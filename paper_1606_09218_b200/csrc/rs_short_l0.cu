@@ -314,3 +314,30 @@ int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// L2 read-bandwidth probe (the roofline of the dense-L0 gather): every CTA
+// streams a `bytes`-long buffer that fits in L2 with 8-byte .cg loads (L1
+// bypassed), `iters` times; bench.py times it with CUDA events.
+namespace rsb {
+namespace {
+__global__ void __launch_bounds__(256) k_l2_probe(const double *__restrict__ buf, int64_t n,
+                                                  int iters, double *__restrict__ out) {
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t start = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    for (int64_t e = start; e < n; e += stride) acc += __ldcg(buf + e);
+    start = (start + 7919 * 32) % stride;  // shift the CTA -> address map between passes
+  }
+  if (acc == 1.2345e300) out[0] = acc;  // keeps the loads alive
+}
+}  // namespace
+}  // namespace rsb
+
+extern "C" int rs_l2_probe(const double *buf, int64_t bytes, int64_t iters, double *out,
+                           void *stream) {
+  RS_REQUIRE(buf && out && bytes >= 8 && iters >= 1, "rs_l2_probe: bad arguments");
+  k_l2_probe<<<148 * 8, 256, 0, as_stream(stream)>>>(buf, bytes / 8, (int)iters, out);
+  return check_launch("l2_probe");
+}

@@ -571,8 +571,7 @@ int rs_tc8_gemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb, i
              "rs_tc8_gemm_s8: bad shape");
   constexpr int BN = 64;
   const size_t smem = 2 * (size_t)(tc8::BM + BN) * tc8::BK + 1024;
-  cudaError_t e = cudaFuncSetAttribute((const void *)tc8::k_gemm_s8<BN>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr((const void *)tc8::k_gemm_s8<BN>, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "tc8 smem: %s", cudaGetErrorString(e));
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, tc8::BM));
   tc8::k_gemm_s8<BN><<<grid, tc8::THREADS, smem, as_stream(stream)>>>(A, lda, B, ldb, C, ldc, M, N,
@@ -667,8 +666,7 @@ int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, 
   if ((st = check_launch("oz_ranges"))) return st;
   dim3 grid((unsigned)ntn, (unsigned)ceil_div(M, tc8::BM));
   auto go = [&](auto kern, int smem) -> int {
-    cudaError_t e = cudaFuncSetAttribute((const void *)kern,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = smem_attr((const void *)kern, smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "oz smem: %s", cudaGetErrorString(e));
     kern<<<grid, tc8::THREADS, smem, s>>>(SA, Mp * ldk, SB, Np * ldk, ksteps, ea, eb, rg, nr, C,
                                           ldc, M, N);

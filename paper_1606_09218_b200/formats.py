@@ -508,6 +508,40 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
     return out
 
 
+def tucker_accumulate(long: TuckerTensor, x1_lo: int, x1_hi: int, out,
+                      workspace_bytes: int = _ASSEMBLE_WORKSPACE, workspace_slot: str = "assemble"):
+    """``out[x1 - x1_lo] += Tucker(long)[x1]`` for x1 in [x1_lo, x1_hi): the
+    long-only case of :func:`assemble_grid` with the argument marshalling cut
+    to one cached plan (it runs on build_rs's critical path)."""
+    n = long.mode_sizes[0]
+    r1, r2, r3 = long.ranks
+    planes = x1_hi - x1_lo
+    flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
+    L = nat.lib()
+    rmax = max(r1, r2, r3)
+    key = (n, planes, rmax, 0, 0, flags, workspace_bytes)
+    plan = _ASM_PLANS.get(key)
+    if plan is None:
+        one = L.rs_assemble_workspace_bytes(n, 1, rmax, 0, 0, flags)
+        per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, 0, 0, flags) - one
+        chunk = max(1, min(planes, (workspace_bytes - (one - per_plane)) // max(per_plane, 1)))
+        plan = _ASM_PLANS[key] = (chunk, L.rs_assemble_workspace_bytes(n, chunk, rmax, 0, 0,
+                                                                        flags))
+    chunk = plan[0]
+    ws = nat.Workspace.get(plan[1], workspace_slot)
+    core, (v1, v2, v3) = long.core, long.factors
+    cp, p1_, p2_, p3_ = core.data_ptr(), v1.data_ptr(), v2.data_ptr(), v3.data_ptr()
+    wp, wn, st = ws.data_ptr(), ws.numel(), nat.stream_ptr()
+    base, pstride = out.data_ptr(), n * n * 8
+    for p0 in range(x1_lo, x1_hi, chunk):
+        p1 = min(x1_hi, p0 + chunk)
+        nat.check(L.rs_assemble_planes(cp, r1, r2, r3, p1_, p2_, p3_, n, None, None, 0, 0, None,
+                                       None, None, None, None, None, 0, p0, p1, flags,
+                                       base + (p0 - x1_lo) * pstride, wp, wn, st),
+                  "rs_assemble_planes")
+    return out
+
+
 def dense_cct(short: CCT, limit: int = MAX_DENSE_ELEMENTS, device: bool = False):
     """Dense short-range sum (``formats.py:432-445``): windows clipped at the faces."""
     _guard_dense(short.mode_sizes, limit)

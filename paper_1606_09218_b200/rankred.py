@@ -26,6 +26,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Optional
 
+import math
+
 import numpy as np
 
 from . import _native as nat
@@ -470,6 +472,48 @@ def truncated_spectra(thetas: np.ndarray, traces, n: int, eps, forced=None, limi
                 out.append((None, s, tail, total))
                 continue
         out.append((r, s, tail, total))
+    return out
+
+
+def rank_rule_fast(thetas, traces, n: int, eps, forced=None, limit=None,
+                   iters: int = TOPEIG_ITERS):
+    """:func:`truncated_spectra` without the spectra arrays, in plain Python
+    floats (a few dozen values per mode; this sits between the eigen block's
+    synchronisation and the core launch).  Returns (rank or None, tail at the
+    rank, total) per mode."""
+    out = []
+    m = len(traces)
+    b = len(thetas) // m
+    for l in range(m):
+        th = [x if x > 0.0 else 0.0 for x in thetas[l * b:(l + 1) * b]]
+        tot_th = float(np.sum(np.asarray(th)))   # same order as truncated_spectrum
+        rem = max(float(traces[l]) - tot_th, 0.0) if b < n else 0.0
+        total = tot_th + rem
+        tails = [0.0] * b
+        acc = 0.0
+        for k in range(b - 1, -1, -1):
+            acc += th[k]
+            tails[k] = acc + rem
+        if forced is not None and forced[l] is not None:
+            r = int(forced[l])
+        elif total == 0.0:
+            r = 1
+        else:
+            thr = eps * total
+            r = next((k for k in range(b) if tails[k] <= thr), -1)
+            if r < 0:
+                out.append((None, 0.0, total))
+                continue
+            r = max(r, 1)
+        if limit is not None:
+            r = min(r, limit)
+        if b < n:
+            lam_r = th[r - 1] if 0 < r <= b else 0.0
+            if (r >= b or lam_r <= 0.0 or th[0] <= 0.0 or
+                    1e2 * (th[b - 1] / lam_r) ** iters * math.sqrt(lam_r / th[0]) > 1e-11):
+                out.append((None, 0.0, total))
+                continue
+        out.append((r, tails[r] if r < b else 0.0, total))
     return out
 
 

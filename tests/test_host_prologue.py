@@ -146,3 +146,24 @@ def test_truncated_spectra_matches_scalar_rule():
                 assert got[l][3] == ref[3]
     z = truncated_spectra(np.zeros((1, b)), [0.0], n, 1e-6, None, 200, 2)
     assert z[0][0] == truncated_spectrum(np.zeros(b), 0.0, n, 1e-6, None, 200, 2)[0]
+
+
+def test_rank_rule_fast_matches_scalar_rule():
+    import numpy as np
+    from paper_1606_09218_b200.rankred import rank_rule_fast, truncated_spectrum
+
+    rng = np.random.default_rng(4)
+    n, b = 256, 24
+    for trial in range(40):
+        decay = rng.uniform(0.2, 3.0)
+        th = np.sort(np.exp(-decay * np.arange(b)) * rng.uniform(0.5, 1.5, b))[::-1]
+        tr = th.sum() * (1 + rng.uniform(0, 1e-6))
+        for eps in (1e-6, 1e-8, 1e-12):
+            for forced in (None, (5,)):
+                got = rank_rule_fast(th.tolist(), [tr], n, eps, forced, 200, 2)[0]
+                ref = truncated_spectrum(th, tr, n, eps, None if forced is None else forced[0],
+                                         200, 2)
+                assert got[0] == ref[0]
+                if ref[0] is not None:
+                    assert got[1] == (float(ref[2][ref[0]]) if ref[0] < b else 0.0)
+                    assert got[2] == ref[3]

@@ -31,5 +31,5 @@ for _ in range(reps):
     torch.cuda.synchronize()
 pr.disable()
 st = io.StringIO()
-pstats.Stats(pr, stream=st).sort_stats("cumulative").print_stats(45)
+pstats.Stats(pr, stream=st).sort_stats("tottime").print_stats(40)
 print(st.getvalue()[:9000])
