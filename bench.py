@@ -181,12 +181,12 @@ def reference_assembly_time(name, stride, repeats=1):
     return best
 
 
-def _ncu_traffic(name):
+def _ncu_traffic(name, kernel="gemm_short"):
     """dram read+write bytes per launch of the dominant kernel from the
     committed ncu --set full summary (profiles/), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
-            return json.load(fh)[name]["gemm_short"]["dram_bytes_per_launch"]
+            return json.load(fh)[name][kernel]["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
 
@@ -247,6 +247,24 @@ def measure_dgemm_peak(torch):
     del a, b
     torch.cuda.empty_cache()
     return 2 * n ** 3 / t / 1e12
+
+
+def measure_l2_peak(torch, nat):
+    """L2 read bandwidth (GB/s): rs_l2_probe streaming a 32 MiB buffer 200
+    times from 1184 CTAs with L1-bypassing loads, CUDA events."""
+    buf = torch.ones(4 << 20, dtype=torch.float64, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    L = nat.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        nat.check(L.rs_l2_probe(buf.data_ptr(), buf.numel() * 8, 20, out.data_ptr(), st), "probe")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nat.check(L.rs_l2_probe(buf.data_ptr(), buf.numel() * 8, 200, out.data_ptr(), st), "probe")
+    e1.record()
+    torch.cuda.synchronize()
+    return buf.numel() * 8 * 200 / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def term_supports(ul, wl, gamma, drop=1e-18):
@@ -314,6 +332,7 @@ def main():
         # overlapping the long-range reduction) + dense_rs of this rank's slab
         res = rt.build_rs(particles, cfg, prefetch_dense=(x1_lo, x1_hi),
                           group=dist.group.WORLD if world > 1 else None,
+                          prefetch_groups=int(os.environ.get("BENCH_GROUPS", "1")),
                           prefetch_out=slabs[step.i % 2])
         g = rt.dense_rs(res.rs, limit=1 << 62, device=True, x1_range=(x1_lo, x1_hi))
         step.last = g
@@ -396,8 +415,10 @@ def main():
         print("cudaMalloc calls in the timed region:",
               torch.cuda.memory_stats().get("num_device_alloc", 0) - mallocs0, file=sys.stderr)
     gemm_ms, gemm_n = nat.prof_query("gemm_short")
+    l0_ms, l0_n = nat.prof_query("short_l0")
     prof = {k: nat.prof_query(k) for k in ("gemm_short", "gemm_tucker", "gemm_plane", "short_rows",
-                                          "topeig", "syrk", "core", "shift_project")}
+                                          "short_l0", "tucker_f", "topeig", "syrk", "core",
+                                          "shift_project")}
     tt = torch.tensor([t_mean], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -467,6 +488,32 @@ def main():
                 lo_x, hi_x = t0 - g, min(n - 1, t0 + 63) + g
                 keff.append(np.count_nonzero((bc3 >= lo_x) & (bc3 <= hi_x)))
         exec_flops = 2.0 * n * n * 64 * float(np.sum(keff))
+        if gemm_n:   # short range on the plane GEMM (FP64 tensor cores)
+            roof = {"bound": "tensor",
+                    "kernel": "k_gemm_plane short-range plane GEMM (gemm_short)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": _ncu_traffic(name),
+                    "peak_source": "cuBLAS DGEMM 8192^3 measured live (fp64; "
+                                   "MEASURED_PEAKS.json has no FP64 entry)",
+                    "algorithmic_flops_per_step": alg_flops,
+                    "executed_flops_upper_bound_per_step": exec_flops,
+                    "avg_launch_ms": gemm_avg_s * 1e3}
+        else:        # low overlap: dense-L0 gather, bound by L2 reads (8 B per pair)
+            l2 = measure_l2_peak(torch, nat)
+            l0_avg_s = l0_ms / max(l0_n, 1) / 1e3
+            alg_bytes = 8.0 * P * slab_frac / (max(l0_n, 1) / args.steps)
+            ach = alg_bytes / l0_avg_s / 1e9 if l0_n else None
+            roof = {"bound": "l2", "kernel": "k_short_l0 dense-L0 gather (short_l0)",
+                    "achieved": ach, "peak": l2, "unit": "GB/s",
+                    "frac": (ach / l2) if ach else None,
+                    "traffic": _ncu_traffic(name, "short_l0"),
+                    "peak_source": "rs_l2_probe: 32 MiB L2-resident buffer, L1-bypassing "
+                                   "8-byte loads, measured live",
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "note": "one 8-byte L0 read per (grid point, covering copy) pair; the "
+                            "grid store (8 B per point) goes to HBM",
+                    "avg_launch_ms": l0_avg_s * 1e3}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             stride = max(1, m["N"] // 400)   # ~10-30 s of CPU work
@@ -501,18 +548,7 @@ def main():
                     "h2d_bytes_per_step": int(pos_h.numel() * 8 + q_h.numel() * 8),
                     "d2h_bytes_per_step": int(out_h.numel() * 8), "ms_per_step": t_e2e * 1e3},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor",
-                         "kernel": "k_gemm_nt<TilePlane> short-range plane GEMM (gemm_short)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": _ncu_traffic(name),
-                         "peak_source": "cuBLAS DGEMM 8192^3 measured live (fp64; "
-                                        "MEASURED_PEAKS.json has no FP64 entry)",
-                         "algorithmic_flops_per_step": alg_flops,
-                         "executed_flops_per_step": exec_flops,
-                         "executed_tflops": exec_flops * slab_frac / launches_per_step /
-                         gemm_avg_s / 1e12 if gemm_n else None,
-                         "avg_launch_ms": gemm_avg_s * 1e3},
+            "roofline": roof,
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "cpu_baseline": cpu,
         }

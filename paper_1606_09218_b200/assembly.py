@@ -38,7 +38,7 @@ from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_
     snap_to_grid
 from .quadrature import RadialKernel, ReferenceCanonical, build_quadrature, effective_support, \
     project_kernel, split_rank, split_tensor
-from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, ReductionConfig, top_eig_supported, \
+from .rankred import TOPEIG_BLOCK, TOPEIG_ITERS, TOPEIG_MAX_BLOCK, TOPEIG_WIDE_BLOCK, ReductionConfig, top_eig_supported, \
     SvdSpectrum, _trusted_tucker, c2t_als, eig_desc, eig_desc_batched, eps_rank, rhosvd_error_bound, shift_histograms, \
     shifted_core, shifted_grams, side_svd, top_eig, rank_rule_fast, truncated_spectrum, tucker_to_canonical
 
@@ -709,6 +709,12 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
         # straight to the full (cuSOLVER) spectrum instead of escalating twice
         use_top = top_eig_supported(n, b) and eps_ >= 1e-7
+        if eps_ < 1e-7 and n >= 512 and forced is None:
+            # wide Ritz block (C5: rank 132 at eps 1e-8): subspace iteration +
+            # cuSOLVER on the b x b Rayleigh quotient instead of three full
+            # n x n syevd; the convergence rule falls back to them per mode
+            b = min(n - n % 2, TOPEIG_WIDE_BLOCK)
+            use_top = top_eig_supported(n, b)
         # two subspace iterations: one already gives grid parity (1e-10) at
         # eps >= 1e-6, but point values / energies (1e-12) need the second
         iters = TOPEIG_ITERS

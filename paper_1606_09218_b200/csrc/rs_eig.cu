@@ -245,6 +245,18 @@ static int launch_jacobi(const double *T, int nmat, double *evals, double *Vt, s
   return check_launch("jacobi");
 }
 
+// cuSOLVER order (ascending values, eigenvectors as rows) -> the Jacobi
+// kernel's (descending values, rows of Vt descending); one block per matrix
+__global__ void k_flip_eig(const double *__restrict__ ev_asc, const double *__restrict__ V,
+                           int b, double *__restrict__ evals, double *__restrict__ Vt) {
+  const int64_t m = blockIdx.x;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int j = e / b, k = e - (e / b) * b;
+    Vt[(m * b + j) * b + k] = V[(m * b + (b - 1 - j)) * b + k];
+  }
+  for (int j = threadIdx.x; j < b; j += blockDim.x) evals[m * b + j] = ev_asc[m * b + b - 1 - j];
+}
+
 // U[m][j][i] = sum_k Vt[m][j][k] Q[m][k][i]   (b x b times b x n, per matrix)
 __global__ void k_ritz(const double *__restrict__ Vt, const double *__restrict__ Q, int b, int64_t n,
                        int nmat, double *__restrict__ U) {
@@ -367,15 +379,33 @@ using namespace rsb;
 
 extern "C" {
 
+int64_t rs_eigh_workspace_bytes(int64_t m, int64_t n);
+int rs_eigh(double *G, int64_t m, int64_t n, double *evals, void *work, int64_t work_bytes,
+            void *stream);
+}  // extern "C"
+namespace rsb {
+int64_t orth_qr_workspace_bytes(int64_t m, int64_t b, int64_t n);
+int orth_qr(double *Y, int64_t m, int64_t b, int64_t n, void *work, int64_t work_bytes,
+            cudaStream_t s);
+}  // namespace rsb
+extern "C" {
+
 int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b) {
-  // Q, Y (nmat*b*n each), T (nmat*b*b), Vt (nmat*b*b)
-  return (2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024;
+  // Q, Y (nmat*b*n each), T (nmat*b*b), Vt (nmat*b*b); b > 96: + ascending
+  // Ritz values (nmat*b) + cuSOLVER workspace for the b x b Rayleigh quotients
+  int64_t base = (2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024;
+  if (b > 96) {
+    const int64_t e = rs_eigh_workspace_bytes(nmat, b), q = orth_qr_workspace_bytes(nmat, b, n);
+    if (e < 0 || q < 0) return -1;
+    base += round_up(nmat * b * 8, 256) + std::max(e, q);
+  }
+  return base;
 }
 
 int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters, double *evals,
               double *U, double *trace, void *work, int64_t work_bytes, void *stream) {
-  RS_REQUIRE(nmat >= 1 && n >= 2 && b >= 2 && b <= n && b % 2 == 0 && b <= 96 && iters >= 1,
-             "rs_topeig: bad sizes (need 2 <= b <= min(n, 96), b even)");
+  RS_REQUIRE(nmat >= 1 && n >= 2 && b >= 2 && b <= n && b % 2 == 0 && b <= 512 && iters >= 1,
+             "rs_topeig: bad sizes (need 2 <= b <= min(n, 512), b even)");
   RS_REQUIRE(n % 2 == 0, "rs_topeig: n must be even");
   if (work_bytes < rs_topeig_workspace_bytes(nmat, n, b))
     return fail(RS_ERR_CAPACITY, "rs_topeig: workspace too small");
@@ -401,6 +431,13 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // Y = Q G (rows), orth
   for (int64_t it = 0; it < iters; ++it) {
     if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
+    if (b > 96) {  // wide block: Householder QR (cuSOLVER), one thread/stream per matrix
+      char *qw = (char *)work + round_up((2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024, 256) +
+                 round_up(nmat * b * 8, 256);
+      if ((st = orth_qr(Y, nmat, b, n, qw, work_bytes - (qw - (char *)work), s))) return st;
+      std::swap(Q, Y);
+      continue;
+    }
     if (q_smem)
       k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
     else
@@ -411,7 +448,15 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // Rayleigh-Ritz: W = Q G (into Y), T = W Q^T
   if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
   if ((st = gemm_batched(Y, n, b * n, Q, n, b * n, T, b, b * b, b, b, n, (int)nmat, s))) return st;
-  switch (b) {
+  if (b > 96) {  // Rayleigh quotients too large for the shared-memory Jacobi: cuSOLVER
+    double *ev_asc = Vt + nmat * b * b;
+    char *ew = (char *)work + round_up((2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024, 256) +
+               round_up(nmat * b * 8, 256);
+    const int64_t ebytes = work_bytes - (ew - (char *)work);
+    if ((st = rs_eigh(T, nmat, b, ev_asc, ew, ebytes, stream))) return st;
+    k_flip_eig<<<(unsigned)nmat, 256, 0, s>>>(ev_asc, T, (int)b, evals, Vt);
+    if ((st = check_launch("flip eig"))) return st;
+  } else switch (b) {
     case 16: st = launch_jacobi<16>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 24: st = launch_jacobi<24>(T, (int)nmat, evals, Vt, reserve, s); break;
     case 32: st = launch_jacobi<32>(T, (int)nmat, evals, Vt, reserve, s); break;
@@ -544,3 +589,76 @@ int rs_eigh(double *G, int64_t m, int64_t n, double *evals, void *work, int64_t 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// Orthonormal basis of the b rows of each (b x n) block by Householder QR
+// (cuSOLVER geqrf + orgqr on the column-major n x b view), one host thread
+// and stream per matrix: the wide Ritz blocks (b = 192 at C5) where the
+// one-CTA CGS2 kernel costs ~86 ms per pass.
+namespace rsb {
+
+int64_t orth_qr_workspace_bytes(int64_t m, int64_t b, int64_t n) {
+  EighCtx *c = nullptr;
+  if (m < 1 || b < 1 || n < b || eigh_ctx(&c)) return -1;
+  int l1 = 0, l2 = 0;
+  if (cusolverDnDgeqrf_bufferSize(c->h[0], (int)n, (int)b, nullptr, (int)n, &l1) !=
+          CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr_bufferSize(c->h[0], (int)n, (int)b, (int)b, nullptr, (int)n, nullptr,
+                                  &l2) != CUSOLVER_STATUS_SUCCESS)
+    return -1;
+  const int64_t lw = std::max(l1, l2);
+  return m * (round_up((lw + b) * 8, 256) + 256);
+}
+
+int orth_qr(double *Y, int64_t m, int64_t b, int64_t n, void *work, int64_t work_bytes,
+            cudaStream_t s) {
+  EighCtx *c = nullptr;
+  int st;
+  if ((st = eigh_ctx(&c))) return st;
+  int l1 = 0, l2 = 0;
+  if (cusolverDnDgeqrf_bufferSize(c->h[0], (int)n, (int)b, Y, (int)n, &l1) !=
+          CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr_bufferSize(c->h[0], (int)n, (int)b, (int)b, Y, (int)n, nullptr, &l2) !=
+          CUSOLVER_STATUS_SUCCESS)
+    return fail(RS_ERR_CUDA, "orth_qr: bufferSize");
+  const int lw = std::max(l1, l2);
+  const int64_t per = round_up(((int64_t)lw + b) * 8, 256) + 256;
+  if (work_bytes < m * per) return fail(RS_ERR_CAPACITY, "orth_qr: workspace too small");
+  if (cudaEventRecord(c->fork, s) != cudaSuccess) return fail(RS_ERR_CUDA, "orth_qr: fork");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int64_t i0 = 0; i0 < m; i0 += EIGH_SLOTS) {
+    const int k = (int)std::min<int64_t>(EIGH_SLOTS, m - i0);
+    int rc[EIGH_SLOTS] = {0, 0, 0};
+    std::thread th[EIGH_SLOTS];
+    for (int j = 0; j < k; ++j) {
+      th[j] = std::thread([&, j] {
+        const int64_t i = i0 + j;
+        cudaSetDevice(dev);
+        double *A = Y + i * b * n;  // rows of the row-major b x n block = columns of n x b
+        double *w = (double *)((char *)work + i * per);
+        double *tau = w + lw;
+        int *info = (int *)((char *)work + i * per + per - 256);
+        if (cudaStreamWaitEvent(c->s[j], c->fork, 0) != cudaSuccess) { rc[j] = 1; return; }
+        if (cusolverDnDgeqrf(c->h[j], (int)n, (int)b, A, (int)n, tau, w, lw, info) !=
+            CUSOLVER_STATUS_SUCCESS) { rc[j] = 2; return; }
+        if (cusolverDnDorgqr(c->h[j], (int)n, (int)b, (int)b, A, (int)n, tau, w, lw, info) !=
+            CUSOLVER_STATUS_SUCCESS) { rc[j] = 3; return; }
+        if (cudaEventRecord(c->join[j], c->s[j]) != cudaSuccess) rc[j] = 4;
+      });
+    }
+    for (int j = 0; j < k; ++j) th[j].join();
+    for (int j = 0; j < k; ++j) {
+      if (rc[j]) return fail(RS_ERR_CUDA, "orth_qr: step %d failed on matrix %lld", rc[j],
+                             (long long)(i0 + j));
+      g_launches.fetch_add(2, std::memory_order_relaxed);
+      if (cudaStreamWaitEvent(s, c->join[j], 0) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "orth_qr: join");
+    }
+    if (i0 + EIGH_SLOTS < m && cudaEventRecord(c->fork, s) != cudaSuccess)
+      return fail(RS_ERR_CUDA, "orth_qr: fork");
+  }
+  return RS_OK;
+}
+
+}  // namespace rsb

@@ -368,13 +368,15 @@ def shifted_grams(table_dev, n: int, w_long_abs, c):
 
 TOPEIG_BLOCK = 24
 TOPEIG_MAX_BLOCK = 96
+TOPEIG_WIDE_BLOCK = 192   # eps < 1e-7 on large grids (C5: rank 132)
 TOPEIG_ITERS = 2
 TOPEIG_SMEM_DOUBLES = 220 * 1024 // 8 - 2
 
 
 def top_eig_supported(n: int, b: int) -> bool:
-    """Block sizes rs_topeig accepts (Jacobi on the b x b Ritz matrix in smem)."""
-    return b in (16, 24, 32, 48, 64, 96) and b <= n
+    """Block sizes rs_topeig accepts (Jacobi on the b x b Ritz matrix in smem up
+    to 96, cuSOLVER on it above)."""
+    return (b in (16, 24, 32, 48, 64, 96) or (b % 32 == 0 and 96 < b <= 512)) and b <= n
 
 
 def top_eig(G, b: int, iters: int = TOPEIG_ITERS):

@@ -86,7 +86,7 @@ def test_sum_dd_matches_fsum(nat, cuda):
     assert got == math.fsum(v)
 
 
-@pytest.mark.parametrize("n,b", [(256, 64), (96, 32), (512, 96), (32, 32), (256, 24), (100, 24), (512, 32)])
+@pytest.mark.parametrize("n,b", [(256, 64), (96, 32), (512, 96), (32, 32), (256, 24), (100, 24), (512, 32), (1024, 192)])
 def test_topeig_graded_spectrum(nat, cuda, n, b):
     """Block subspace iteration + Jacobi vs the known eigensystem of a graded
     PSD matrix (the spectral shape of the RS side-matrix Grams)."""

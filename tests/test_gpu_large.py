@@ -39,11 +39,18 @@ def test_grid_planes(large):
     name, case, p, idx, core, zs, ranks, res = large
     ul, wl = orc.local_window(p["table"], p["w"], case["split_index"], p["gamma"])
     L0 = orc.local_dense(ul, wl)
+    # BASELINE's bound is relative to the grid max-norm; the edge planes (x=1,
+    # n-1) hold values ~1e-6 of it, so the scale is the max over all checked
+    # planes (interior planes included), never a single near-empty plane
+    pairs = []
     for x in PLANES[name]:
         t = np.einsum("abc,a,jb,lc->jl", core, zs[0][x], zs[1], zs[2], optimize=True)
         ref = t + orc.dense_cct_c(L0, p["gamma"], idx, case["charges"], case["n"], x, x + 1)[0]
         got = rt.dense_rs(res.rs, limit=1 << 62, x1_range=(x, x + 1))[0]
-        assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref)), (name, x)
+        pairs.append((x, got, ref))
+    scale = max(float(np.max(np.abs(ref))) for _, _, ref in pairs)
+    for x, got, ref in pairs:
+        assert np.max(np.abs(got - ref)) <= 1e-10 * scale, (name, x)
 
 
 def test_point_values_energy_forces(large):
