@@ -230,6 +230,17 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------- GPU arm
+def _hbm_peak():
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the
+    profiling guide's fallback."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                               "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy test)"
+    except (OSError, KeyError, ValueError):
+        return 6539.0, "fallback 6539 GB/s (B200_PROFILING.md)"
+
+
 def measure_dgemm_peak(torch):
     n = 8192
     a = torch.randn(n, n, dtype=torch.float64, device="cuda")
@@ -514,6 +525,32 @@ def main():
                     "note": "one 8-byte L0 read per (grid point, covering copy) pair; the "
                             "grid store (8 B per point) goes to HBM",
                     "avg_launch_ms": l0_avg_s * 1e3}
+        # the two other kernels the north star names: the Tucker part of the slab
+        # (HBM: read + write 8 B per point when accumulating into the prefetched
+        # short-range slab) and the shift Gram (FP64 tensor cores)
+        hbm = _hbm_peak()
+        secondary = {}
+        t_ms, t_n = prof["gemm_tucker"]
+        if t_n:
+            t_avg = t_ms / t_n / 1e3
+            tb = 16.0 * (x1_hi - x1_lo) * n * n / (t_n / args.steps)
+            secondary["tucker"] = {
+                "bound": "hbm", "kernel": ("k_tucker_apply" if r3 <= 24 else "k_gemm_plane<true>")
+                + " Tucker part accumulated into the slab (gemm_tucker)",
+                "achieved": tb / t_avg / 1e9, "peak": hbm[0], "unit": "GB/s",
+                "frac": tb / t_avg / 1e9 / hbm[0], "peak_source": hbm[1],
+                "algorithmic_bytes_per_launch": tb, "avg_launch_ms": t_avg * 1e3}
+        s_ms, s_n = prof["syrk"]
+        if s_n:
+            s_avg = s_ms / s_n / 1e3
+            R_l = int(plan.w_long_abs.shape[0])
+            gf = 3.0 * n * (n + 1) * (n * R_l) / (s_n / args.steps)
+            secondary["gram"] = {
+                "bound": "tensor", "kernel": "k_syrk_part shift-Gram SYRK on DMMA (syrk)",
+                "achieved": gf / s_avg / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "frac": gf / s_avg / 1e12 / peak,
+                "note": "3 modes x n(n+1) K with the shift-merged K = n R_l",
+                "algorithmic_flops_per_launch": gf, "avg_launch_ms": s_avg * 1e3}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             stride = max(1, m["N"] // 400)   # ~10-30 s of CPU work
@@ -549,6 +586,7 @@ def main():
                     "d2h_bytes_per_step": int(out_h.numel() * 8), "ms_per_step": t_e2e * 1e3},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "secondary_rooflines": secondary,
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "cpu_baseline": cpu,
         }

@@ -127,6 +127,20 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
               double *evals, double *U, double *trace, void *work, int64_t work_bytes,
               void *stream);
 
+/* The long-range chain up to the host's rank decision in ONE call, enqueued
+ * right behind rs_front on the same stream: rs_gram_shifted (hist = the
+ * front's shift histograms) -> rs_topeig (3 modes, block b) -> packed
+ * [evals (3b) | trace (3) | dmax | duplicate-node key | occupied x3 count]
+ * (3b + 6 doubles) into packed_dev and then into pinned packed_host, and the
+ * cudaEvent_t `done` recorded; the host waits on `done` only.  nb may be NULL.
+ * Reference: rankred.py:82-148 (side Gram, eigh, eps-rank inputs). */
+int rs_chain_eig(const double *table, int64_t ld_table, int64_t n, int64_t R,
+                 const double *hist, const double *wabs, double *G, void *gram_work,
+                 int64_t gram_work_bytes, int64_t b, int64_t iters, double *evals,
+                 double *U, double *trace, void *eig_work, int64_t eig_work_bytes,
+                 const double *dmax, const int64_t *dup_key, const int32_t *nb,
+                 double *packed_dev, double *packed_host, void *done, void *stream);
+
 /* The three modes of rs_shift_project in one launch (Z_l contiguous n x r_l). */
 int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3,
                       int64_t r1, int64_t r2, int64_t r3, int64_t n,

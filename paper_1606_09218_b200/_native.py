@@ -75,6 +75,9 @@ SIGNATURES = {
     "rs_front": (_i32, [_ptr, _ptr, _i64, ctypes.c_double, _i64, _ptr, _i64, _ptr,
                         _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64, _ptr, _i32,
                         _i64, _ptr]),
+    "rs_chain_eig": (_i32, [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _i64, _i64, _i64,
+                            _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
+                            _ptr]),
     "rs_back_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64, _i64]),
     "rs_back": (_i32, [_ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64,
                        _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,

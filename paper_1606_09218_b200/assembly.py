@@ -308,7 +308,7 @@ def _short_ws_bytes(n: int, planes: int, nb_max: int, rs: int) -> int:
     return v
 
 
-def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
+def _front_system(positions, charges, box, grid: Grid3, prefetch=None, chain=None):
     """Snap, node sort, bucket-ordered copies, shift histograms and the
     short-range bucket table in one native call (``rs_front``), no sync.
     ``prefetch = (plan, lo, hi)`` also enqueues the short-range planes
@@ -353,6 +353,9 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     nat.check(nat.lib().rs_front(pos.data_ptr(), z.data_ptr(), count, grid.h, n, buf.data_ptr(),
                                  buf.numel(), nat.stream_ptr(), *pf), "rs_front")
     _mark("f_call")
+    if chain is not None:   # Gram -> top-b eigenpairs -> packed D2H, right behind the front
+        chain_out = _launch_chain(chain, buf.data_ptr(), o, n)
+        _mark("f_chain")
     if prefetch is not None:
         ev = torch.cuda.Event()
         ev.record(side)
@@ -375,7 +378,57 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None):
     if prefetch is not None:
         ds._cache["front"]["prefetch"] = dict(lo=lo, hi=hi, buf=out, ev=ev, complete=False,
                                               groups=(grp, gev) if gev else None)
+    if chain is not None:
+        ds._cache["chain"] = chain_out
     return ds, prep["dup_key"]
+
+
+_CHAIN_BUFS: dict = {}
+
+
+def _chain_buffers(n: int, b: int, R_l: int):
+    """Pooled device outputs (G, evals, U, trace, packed), pinned packed copy
+    and the completion event of :func:`_launch_chain`, per (device, n, b).
+    Reuse is stream-ordered: every consumer of a previous call's buffers runs
+    on the chain stream before the next call's kernels, and the host reads the
+    pinned vector before it enqueues the next call."""
+    torch = nat._torch()
+    dev = torch.cuda.current_device()
+    key = (dev, n, b, R_l)
+    ent = _CHAIN_BUFS.get(key)
+    if ent is None:
+        L = nat.lib()
+        m = 3 * n * n + 3 * b + 3 * b * n + 3 + (3 * b + 6)
+        flat = torch.empty(m, dtype=torch.float64, device="cuda")
+        o = [0, 3 * n * n, 3 * n * n + 3 * b, 3 * n * n + 3 * b + 3 * b * n,
+             3 * n * n + 3 * b + 3 * b * n + 3]
+        host = torch.empty(3 * b + 6, dtype=torch.float64, pin_memory=True)
+        ev = torch.cuda.Event()
+        ev.record()   # materialise the cudaEvent_t
+        ent = _CHAIN_BUFS[key] = dict(
+            G=flat[o[0]:o[1]].view(3, n, n), evals=flat[o[1]:o[2]].view(3, b),
+            U=flat[o[2]:o[3]].view(3, b, n), trace=flat[o[3]:o[4]], packed=flat[o[4]:],
+            host=host, host_np=host.numpy(), ev=ev,
+            gws=nat.Workspace.get(L.rs_gram_shifted_workspace_bytes(n, R_l), "syrk"),
+            ews=nat.Workspace.get(L.rs_topeig_workspace_bytes(3, n, b), "topeig"))
+    return ent
+
+
+def _launch_chain(chain, base: int, o, n: int):
+    """``rs_chain_eig`` on the front's histograms (current stream)."""
+    plan, b, iters = chain
+    R_l = int(plan.w_long_abs.shape[0])
+    ent = _chain_buffers(n, b, R_l)
+    L = nat.lib()
+    nat.check(L.rs_chain_eig(plan.table_dev.data_ptr(), plan.table_dev.shape[1], n, R_l,
+                             base + o[11], plan.w_long_abs.data_ptr(), ent["G"].data_ptr(),
+                             ent["gws"].data_ptr(), ent["gws"].numel(), b, iters,
+                             ent["evals"].data_ptr(), ent["U"].data_ptr(),
+                             ent["trace"].data_ptr(), ent["ews"].data_ptr(), ent["ews"].numel(),
+                             base + o[10] + 8, base + o[10], base + o[15],
+                             ent["packed"].data_ptr(), ent["host"].data_ptr(),
+                             ent["ev"].cuda_event, nat.stream_ptr()), "rs_chain_eig")
+    return ent
 
 
 _GROUP_EVENTS: dict = {}
@@ -403,7 +456,7 @@ def _collision_flag(ds, n: int):
     return _node_sort(ds, n)["dup_key"]
 
 
-def _as_device_system(system, grid: Grid3, prefetch=None):
+def _as_device_system(system, grid: Grid3, prefetch=None, chain=None):
     """Accept the reference's types or :class:`DeviceParticles`.  ``prefetch``
     (plan, lo, hi) rides along with the native front when the input is snapped
     here."""
@@ -412,7 +465,8 @@ def _as_device_system(system, grid: Grid3, prefetch=None):
             raise ConfigError("particle system snapped to a different grid")
         return system, None
     if isinstance(system, DeviceParticles):
-        return _front_system(system.positions, system.charges, system.box, grid, prefetch)
+        return _front_system(system.positions, system.charges, system.box, grid, prefetch,
+                             chain)
     if isinstance(system, IndexedParticleSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
@@ -426,7 +480,8 @@ def _as_device_system(system, grid: Grid3, prefetch=None):
         ds._cache["host"] = system
         return ds, None
     if isinstance(system, ParticleSystem):
-        return _front_system(system.positions, system.charges, system.box, grid, prefetch)
+        return _front_system(system.positions, system.charges, system.box, grid, prefetch,
+                             chain)
     raise ConfigError(f"expected a particle system, got {type(system).__name__}")
 
 
@@ -571,6 +626,39 @@ def _mark(label: str) -> None:
 _SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "128"))
 
 
+# the Gram + eigen block enqueued by the front call (RSB200_CHAIN=0: from _build_rs)
+_CHAIN = os.environ.get("RSB200_CHAIN", "1") == "1"
+
+
+def _world(group) -> int:
+    if group is None:
+        return 1
+    import torch.distributed as dist
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def _eig_block(cfg: AssemblyConfig, n: int):
+    """Ritz block of the eigen-truncation: (b, use_top, iters, eps, forced ranks)."""
+    # block size: the numerical rank of the long-part Grams grows as eps shrinks
+    eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
+    b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 64)
+    forced = cfg.reduction.ranks
+    if forced is not None:
+        b = min(n - n % 2, max(b, max(forced) + 16 + (max(forced) % 2)))
+    # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
+    # straight to the full (cuSOLVER) spectrum instead of escalating twice
+    use_top = top_eig_supported(n, b) and eps_ >= 1e-7
+    if eps_ < 1e-7 and n >= 512 and forced is None:
+        # wide Ritz block (C5: rank 132 at eps 1e-8): subspace iteration +
+        # cuSOLVER on the b x b Rayleigh quotient instead of three full
+        # n x n syevd; the convergence rule falls back to them per mode
+        b = min(n - n % 2, TOPEIG_WIDE_BLOCK)
+        use_top = top_eig_supported(n, b)
+    # two subspace iterations: one already gives grid parity (1e-10) at
+    # eps >= 1e-6, but point values / energies (1e-12) need the second
+    return b, use_top, TOPEIG_ITERS, eps_, forced
+
+
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
               prefetch_groups: int = 1, prefetch_out=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
@@ -595,7 +683,14 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
             lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
                                                             int(prefetch_dense[1]))
             fused = (plan0, lo, hi, prefetch_groups, prefetch_out)
-    ds, collision = _as_device_system(system, grid, fused)
+    chain = None
+    if (cfg.split_index is not None and cfg.long_format == "tucker"
+            and cfg.reduction.max_sweeps == 0 and _CHAIN and _world(group) == 1
+            and isinstance(system, (DeviceParticles, ParticleSystem))):
+        b_, top_, it_, _, _ = _eig_block(cfg, n)
+        if top_:
+            chain = (plan_for(cfg, int(cfg.split_index)), b_, it_)
+    ds, collision = _as_device_system(system, grid, fused, chain)
     if cfg.sigma is not None:
         sigma = float(cfg.sigma)
     elif ds.count >= 2:
@@ -699,27 +794,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         # shift histograms -> per-mode Grams on DMMA -> top-b eigenpairs, then
         # ONE synchronisation for everything the host must decide on
         _mark("prefetch")
-        G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
-        # block size: the numerical rank of the long-part Grams grows as eps shrinks
-        eps_ = cfg.reduction.eps if cfg.reduction.eps is not None else 1e-12
-        b = min(n - n % 2, TOPEIG_BLOCK if eps_ >= 1e-6 else 64)
-        forced = cfg.reduction.ranks
-        if forced is not None:
-            b = min(n - n % 2, max(b, max(forced) + 16 + (max(forced) % 2)))
-        # eps < 1e-7 pushes the numerical rank past the largest Ritz block: go
-        # straight to the full (cuSOLVER) spectrum instead of escalating twice
-        use_top = top_eig_supported(n, b) and eps_ >= 1e-7
-        if eps_ < 1e-7 and n >= 512 and forced is None:
-            # wide Ritz block (C5: rank 132 at eps 1e-8): subspace iteration +
-            # cuSOLVER on the b x b Rayleigh quotient instead of three full
-            # n x n syevd; the convergence rule falls back to them per mode
-            b = min(n - n % 2, TOPEIG_WIDE_BLOCK)
-            use_top = top_eig_supported(n, b)
-        # two subspace iterations: one already gives grid parity (1e-10) at
-        # eps >= 1e-6, but point values / energies (1e-12) need the second
-        iters = TOPEIG_ITERS
+        b, use_top, iters, eps_, forced = _eig_block(cfg, n)
         full = None
-        if use_top:
+        chained = ds._cache.get("chain")
+        if chained is not None:   # Gram + eigen block already enqueued by the front
+            G, evals, U, trace = chained["G"], chained["evals"], chained["U"], chained["trace"]
+        else:
+            G = shifted_grams(plan.table_dev, n, plan.w_long_abs, hist)
+        if chained is not None:
+            pass
+        elif use_top:
             _mark("grams")
             evals, U, trace = top_eig(G, b, iters)
         else:
@@ -731,14 +815,20 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         if prefetch_pending:  # short-range planes behind the latency-bound eigen block
             launch_prefetch()
             prefetch_pending = False
-        parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
-        if full is not None:
-            parts.append(full[0].reshape(-1))
-        if front is not None:  # occupied x3 values: sizes the bucket-K core
-            nb_view = front["buf"][front["nb"] - front["buf"].data_ptr():][:4].view(torch.int32)
-            parts.append(nb_view.to(torch.float64))
+        if chained is None:
+            parts = [evals.reshape(-1), trace, prep["dmax"], collision.to(torch.float64)]
+            if full is not None:
+                parts.append(full[0].reshape(-1))
+            if front is not None:  # occupied x3 values: sizes the bucket-K core
+                nb_view = front["buf"][front["nb"] - front["buf"].data_ptr():][:4].view(
+                    torch.int32)
+                parts.append(nb_view.to(torch.float64))
         _mark("eig_enq")
-        packed = to_host(torch.cat(parts))
+        if chained is not None:
+            chained["ev"].synchronize()
+            packed = chained["host_np"].copy()
+        else:
+            packed = to_host(torch.cat(parts))
         _mark("synced_eig")
         nq_host = int(packed[-1]) if front is not None else 0
         nt_ = 3 * b + (3 if use_top else 0)

@@ -662,3 +662,56 @@ int orth_qr(double *Y, int64_t m, int64_t b, int64_t n, void *work, int64_t work
 }
 
 }  // namespace rsb
+
+// ------------------------------------------------------------------ chain
+// The latency-bound long-range chain up to the host's rank decision in one
+// host call, enqueued right behind rs_front: shift Grams (DMMA) -> top-b
+// eigenpairs -> one packed vector [evals (3 b) | trace (3) | max snap
+// displacement | duplicate-node key | occupied x3 count] copied into pinned
+// host memory, then `done` recorded.  The host waits on `done` only.
+namespace {
+__global__ void k_pack_chain(const double *__restrict__ evals, int64_t ne,
+                             const double *__restrict__ trace, const double *__restrict__ dmax,
+                             const int64_t *__restrict__ dup_key, const int32_t *__restrict__ nb,
+                             double *__restrict__ out) {
+  for (int64_t i = threadIdx.x; i < ne + 6; i += blockDim.x) {
+    double v;
+    if (i < ne) v = evals[i];
+    else if (i < ne + 3) v = trace[i - ne];
+    else if (i == ne + 3) v = *dmax;
+    else if (i == ne + 4) v = (double)*dup_key;
+    else v = nb ? (double)*nb : 0.0;
+    out[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" {
+int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R, const double *c,
+                    const double *wabs, double *G, void *work, int64_t work_bytes, void *stream);
+
+int rs_chain_eig(const double *table, int64_t ld_table, int64_t n, int64_t R, const double *hist,
+                 const double *wabs, double *G, void *gram_work, int64_t gram_work_bytes,
+                 int64_t b, int64_t iters, double *evals, double *U, double *trace,
+                 void *eig_work, int64_t eig_work_bytes, const double *dmax,
+                 const int64_t *dup_key, const int32_t *nb, double *packed_dev,
+                 double *packed_host, void *done, void *stream) {
+  RS_REQUIRE(table && hist && wabs && G && evals && U && trace && dmax && dup_key && packed_dev &&
+                 packed_host && done,
+             "rs_chain_eig: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  int st;
+  if ((st = rs_gram_shifted(table, ld_table, n, R, hist, wabs, G, gram_work, gram_work_bytes,
+                            stream)))
+    return st;
+  if ((st = rs_topeig(G, 3, n, b, iters, evals, U, trace, eig_work, eig_work_bytes, stream)))
+    return st;
+  k_pack_chain<<<1, 128, 0, s>>>(evals, 3 * b, trace, dmax, dup_key, nb, packed_dev);
+  if ((st = check_launch("pack chain"))) return st;
+  cudaError_t e = cudaMemcpyAsync(packed_host, packed_dev, (size_t)(3 * b + 6) * 8,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord((cudaEvent_t)done, s);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "rs_chain_eig: %s", cudaGetErrorString(e));
+  return RS_OK;
+}
+}  // extern "C"

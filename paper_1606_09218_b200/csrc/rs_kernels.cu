@@ -861,6 +861,112 @@ __global__ void __launch_bounds__(TilePlane::THREADS)
   store_tile<T, ACC>(acc, C, ldc, m0, M, n0, N);
 }
 
+// Tucker part of a plane slab for small r3 (HBM-bound: 2 r3 flops per 8-byte
+// store, or per 16 bytes moved when accumulating):
+//   out[g, x3] (+)= sum_c A[g, c] V3[x3, c],   g = (x1 - x1_lo) n + x2,
+// with A = V2 Y_x1 from the batched DMMA stage.  Thread t of the CTA owns the
+// column x3 = blockIdx.y blockDim + t and keeps V3[x3, :] in registers (zero
+// past r3); the CTA stages its TA_ROWS rows of A in shared memory (one
+// coalesced load) and walks them TA_U at a time: the TA_U old values are
+// loaded first (accumulate), then each row is a run of broadcast LDS.128 +
+// FMAs and one coalesced 8-byte store per thread.
+template <int R, int U, bool ACC>
+__global__ void __launch_bounds__(256, (R <= 16 && U <= 4) ? 3 : 2)
+    k_tucker_apply(const double *__restrict__ A, int64_t lda, const double *__restrict__ V3,
+                   int r3, int64_t n, int64_t rows, int rows_cta, double *__restrict__ out) {
+  extern __shared__ __align__(16) double sA[];
+  const int64_t x3 = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  const bool col = x3 < n;
+  const int64_t g0 = (int64_t)blockIdx.x * rows_cta;
+  const int64_t g1 = min(g0 + rows_cta, rows);
+  // software pipeline: the old values of batch b + 1 are in flight while
+  // batch b is computed and stored; the first batch is requested before the
+  // A rows are staged
+  double nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    nxt[u] = (ACC && col && g0 + u < g1) ? __ldcs(out + (g0 + u) * n + x3) : 0.0;
+  for (int e = threadIdx.x; e < rows_cta * R; e += blockDim.x) {
+    const int r = e / R, c = e - r * R;
+    sA[e] = (g0 + r < g1 && c < r3) ? __ldg(A + (g0 + r) * lda + c) : 0.0;
+  }
+  double v[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) v[c] = (col && c < r3) ? __ldg(V3 + x3 * r3 + c) : 0.0;
+  __syncthreads();
+  if (!col) return;
+  for (int64_t gb = g0; gb < g1; gb += U) {
+    double acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = nxt[u];
+    if (ACC) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        nxt[u] = (gb + U + u < g1) ? __ldcs(out + (gb + U + u) * n + x3) : 0.0;
+    }
+    const double *a0 = sA + (gb - g0) * R;
+#pragma unroll
+    for (int c = 0; c < R; c += 2) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double2 ac = *reinterpret_cast<const double2 *>(a0 + u * R + c);
+        acc[u] = fma(ac.y, v[c + 1], fma(ac.x, v[c], acc[u]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (gb + u < g1) __stcs(out + (gb + u) * n + x3, acc[u]);
+  }
+}
+
+// rows per CTA and rows per load batch (RSB200_TA_ROWS / RSB200_TA_U: A/B runs)
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+static const int g_ta_rows = env_int("RSB200_TA_ROWS", 64);
+static const int g_ta_u = env_int("RSB200_TA_U", 4);
+
+template <int R, int U>
+static int launch_tucker_apply_ru(const double *A, int64_t lda, const double *V3, int r3,
+                                  int64_t n, int64_t rows, double *out, bool acc, cudaStream_t s) {
+  const int threads = (int)std::min<int64_t>(256, round_up(n, 32));
+  const int rc = std::max(U, g_ta_rows / U * U);
+  const dim3 grid((unsigned)ceil_div(rows, rc), (unsigned)ceil_div(n, threads));
+  const size_t smem = (size_t)rc * R * 8;
+  if (smem > 48 * 1024) return fail(RS_ERR_UNSUPPORTED, "tucker_apply: %d rows too many", rc);
+  if (acc)
+    k_tucker_apply<R, U, true><<<grid, threads, smem, s>>>(A, lda, V3, r3, n, rows, rc, out);
+  else
+    k_tucker_apply<R, U, false><<<grid, threads, smem, s>>>(A, lda, V3, r3, n, rows, rc, out);
+  return check_launch("tucker_apply");
+}
+
+template <int R>
+static int launch_tucker_apply_r(const double *A, int64_t lda, const double *V3, int r3,
+                                 int64_t n, int64_t rows, double *out, bool acc, cudaStream_t s) {
+  if (g_ta_u >= 16) return launch_tucker_apply_ru<R, 16>(A, lda, V3, r3, n, rows, out, acc, s);
+  if (g_ta_u <= 4) return launch_tucker_apply_ru<R, 4>(A, lda, V3, r3, n, rows, out, acc, s);
+  return launch_tucker_apply_ru<R, 8>(A, lda, V3, r3, n, rows, out, acc, s);
+}
+
+constexpr int TA_MAXR = 32;   // r3 = 40 (C4): the plane GEMM measured faster
+
+static bool tucker_apply_ok(int64_t r3, int64_t n) {
+  return r3 >= 1 && r3 <= TA_MAXR && n >= 2 && n % 2 == 0;
+}
+
+static int launch_tucker_apply(const double *A, int64_t lda, const double *V3, int r3, int64_t n,
+                               int64_t rows, double *out, bool acc, cudaStream_t s) {
+  switch ((r3 + 7) / 8) {
+    case 1: return launch_tucker_apply_r<8>(A, lda, V3, r3, n, rows, out, acc, s);
+    case 2: return launch_tucker_apply_r<16>(A, lda, V3, r3, n, rows, out, acc, s);
+    case 3: return launch_tucker_apply_r<24>(A, lda, V3, r3, n, rows, out, acc, s);
+    case 4: return launch_tucker_apply_r<32>(A, lda, V3, r3, n, rows, out, acc, s);
+  }
+  return fail(RS_ERR_UNSUPPORTED, "tucker_apply: r3=%d", r3);
+}
+
 // Bt[x3, :] = [V3[x3, :r3], 0 .. r3p, E[(b,k), x3]] with E = ul[x3 - bc3[b] + g, k] in
 // the band (r3 = 0: no Tucker columns; Rs = 0: no short columns).
 __global__ void k_build_bt(const double *__restrict__ V3, int r3, int r3p,
@@ -1451,6 +1557,12 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
 }
 
 // workspace: A (planes*n x lda) | Bt (n x lda) | Y (planes x r2 r3) | ranges
+// RSB200_TUCKER_APPLY=0: the Tucker part through the plane GEMM as before
+static const bool g_tucker_apply = [] {
+  const char *e = getenv("RSB200_TUCKER_APPLY");
+  return !(e && e[0] == '0');
+}();
+
 static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int64_t nb_max,
                        int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
                        int64_t *offY, int64_t *offR, int64_t *total) {
@@ -1552,6 +1664,12 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
+  const int slices0 = (flags >> 8) & 0xF;
+  if (with_long && !with_short && !slices0 && g_tucker_apply && tucker_apply_ok(r3, n)) {
+    // small r3: the HBM-bound row kernel instead of the plane GEMM
+    ProfScope ps(s, "gemm_tucker");
+    return launch_tucker_apply(A, lda, V3, (int)r3, n, planes * n, out, accumulate, s);
+  }
   k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(with_long ? V3 : nullptr,
                                                      with_long ? (int)r3 : 0, (int)r3p, ul,
                                                      with_short ? (int)Rs : 0, (int)G, (int)gamma,
