@@ -89,26 +89,61 @@ __global__ void k_gather(const double *__restrict__ table, int64_t ld_table, int
   }
 }
 
-// Shift-merged Gram operands of the three modes in one launch:
-// X[l][i][s*R + k] = sqrt(c[l][s]) |w_k| T[(s + i)*ld + k]   (s < n, k < R)
+// Occupied shifts of each mode (c[l][s] != 0), ascending: list[l][j], and the
+// Gram's K per mode kdev[l] = count * R.  One block per mode, fixed-order scan.
+__global__ void __launch_bounds__(1024)
+    k_shift_list(const double *__restrict__ c, int64_t n, int64_t R, int32_t *__restrict__ list,
+                 int32_t *__restrict__ kdev) {
+  __shared__ int32_t wocc[32];
+  __shared__ int32_t carry;
+  const int l = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t x = base + tid;
+    const int32_t occ = (x < n && c[l * n + x] != 0.0) ? 1 : 0;
+    int32_t so = occ;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, so, o);
+      if (lane >= o) so += t;
+    }
+    if (lane == 31) wocc[warp] = so;
+    __syncthreads();
+    int32_t po = carry;
+    for (int w = 0; w < warp; ++w) po += wocc[w];
+    if (occ) list[l * n + po + so - 1] = (int32_t)x;
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry = po + so;
+    __syncthreads();
+  }
+  if (tid == 0) kdev[l] = (int32_t)(carry * R);
+}
+
+// Shift-merged Gram operands of the three modes in one launch, occupied
+// shifts only (empty shifts are zero columns of the reference's A):
+// X[l][i][j*R + k] = sqrt(c[l][s]) |w_k| T[(s + i)*ld + k],  s = list[l][j]
 __global__ void k_gram_operands(const double *__restrict__ table, int64_t ld_table, int64_t n,
                                 int64_t R, const double *__restrict__ c,
-                                const double *__restrict__ wabs, double *__restrict__ X,
+                                const double *__restrict__ wabs, const int32_t *__restrict__ list,
+                                const int32_t *__restrict__ kdev, double *__restrict__ X,
                                 int64_t ldx) {
-  const int64_t cols = n * R;
   const int64_t total = 3 * n * ldx;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l = e / (n * ldx), rem = e - l * n * ldx;
     const int64_t i = rem / ldx, col = rem - i * ldx;
-    double v = 0.0;
-    if (col < cols) {
-      const int64_t sft = col / R, k = col - sft * R;
-      const double cs = c[l * n + sft];
-      if (cs != 0.0) v = sqrt(cs) * wabs[k] * table[(sft + i) * ld_table + k];
-    }
-    X[e] = v;
+    if (col >= kdev[l]) continue;   // never read by the SYRK
+    const int64_t j = col / R, k = col - j * R;
+    const int64_t sft = list[l * n + j];
+    X[e] = sqrt(c[l * n + sft]) * wabs[k] * table[(sft + i) * ld_table + k];
   }
+}
+
+// effective K slices of a mode with K = kl columns: at least 64 columns each
+__device__ __forceinline__ void syrk_slices(int64_t kl, int64_t sp_max, int64_t &sp, int64_t &ks) {
+  sp = min(sp_max, max((int64_t)1, (kl + 63) / 64));
+  ks = ((kl + sp - 1) / sp + 15) / 16 * 16;
 }
 
 // ============================================================ GEMM kernels
@@ -149,11 +184,18 @@ __device__ __forceinline__ void tri_decode(int64_t t, int64_t &bi, int64_t &bj) 
 // Lower-triangle Gram tiles, one K slice per blockIdx.y, partials to `part`.
 __global__ void __launch_bounds__(TileSyrk::THREADS)
     k_syrk_part(const double *__restrict__ A, int64_t lda, int64_t n, int64_t K, int64_t kslice,
-                double *__restrict__ part, int64_t a_stride, int64_t part_stride) {
+                double *__restrict__ part, int64_t a_stride, int64_t part_stride,
+                const int32_t *__restrict__ kdev) {
   using T = TileSyrk;
   extern __shared__ __align__(16) double smem[];
   A += blockIdx.z * a_stride;
   part += blockIdx.z * part_stride;
+  if (kdev) {  // K known on the device only: re-slice it over the first sp splits
+    int64_t sp;
+    K = kdev[blockIdx.z];
+    syrk_slices(K, gridDim.y, sp, kslice);
+    if (blockIdx.y >= sp) return;
+  }
   int64_t bi, bj;
   tri_decode(blockIdx.x, bi, bj);
   const int64_t k_lo = (int64_t)blockIdx.y * kslice;
@@ -166,11 +208,16 @@ __global__ void __launch_bounds__(TileSyrk::THREADS)
 }
 
 __global__ void k_syrk_reduce(const double *__restrict__ part, int64_t splits, int64_t ntiles,
-                              int64_t n, double *__restrict__ G, int64_t part_stride) {
+                              int64_t n, double *__restrict__ G, int64_t part_stride,
+                              const int32_t *__restrict__ kdev) {
   using T = TileSyrk;
   const int64_t per = T::BM * T::BN;
   part += blockIdx.z * part_stride;
   G += blockIdx.z * n * n;
+  if (kdev) {
+    int64_t ks;
+    syrk_slices(kdev[blockIdx.z], splits, splits, ks);
+  }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntiles * per;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e / per, loc = e - t * per;
@@ -476,7 +523,8 @@ __global__ void __launch_bounds__(SD_THREADS)
                  int gamma, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
-                 double *__restrict__ A, int64_t lda, int64_t col0) {
+                 double *__restrict__ A, int64_t lda, int64_t col0,
+                 const int *__restrict__ kofd) {
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
   constexpr int P = GK + 1;  // odd pitch (doubles): conflict-light row gathers
@@ -488,6 +536,7 @@ __global__ void __launch_bounds__(SD_THREADS)
   int *sc2 = sc1 + SD_THREADS + 4;
   int *sbk = sc2 + SD_THREADS + 4;     // staged copy -> local bucket
   int *wsum = sbk + SD_THREADS + 4;    // 32
+  int *skofd = wsum + 32;              // gamma + 1: terms alive at (x1, x2) distance d
   __shared__ int s_bst[SD_BG + 1];     // bucket offsets in the candidate list
   __shared__ int s_slo[SD_BG + 1];     // bucket starts within the staged list
   __shared__ int s_plo[SD_BG];         // first candidate copy of each bucket
@@ -500,6 +549,7 @@ __global__ void __launch_bounds__(SD_THREADS)
   const int64_t x1l0 = (int64_t)blockIdx.y * SD_TX1;
   const int64_t X0 = x1_lo + x1l0;
   for (int e = tid; e < (WA + WB) * P; e += SD_THREADS) uA[e] = 0.0;  // k >= Rs rows stay zero
+  for (int d = tid; d <= gamma; d += SD_THREADS) skofd[d] = kofd ? kofd[d] : GK;
   __syncthreads();
   for (int e = tid; e < Rs * W; e += SD_THREADS) {  // coalesced read of ul (W x Rs)
     const int d = e / Rs, k = e - (e / Rs) * Rs;
@@ -581,10 +631,24 @@ __global__ void __launch_bounds__(SD_THREADS)
         // slots past the bucket's end carry z = 0
         const int q = q0 + kq;
         const double z = q < q_hi ? szq[q] : 0.0;
-        const double *pa = uA + ((int)(X0 + ar - sc1[q]) + gamma + SD_PADA) * P;
-        const double *pb = uB + ((int)(yw + ar - sc2[q]) + gamma + SD_PADB) * P;
+        const int a1 = sc1[q], a2 = sc2[q];
+        const double *pa = uA + ((int)(X0 + ar - a1) + gamma + SD_PADA) * P;
+        const double *pb = uB + ((int)(yw + ar - a2) + gamma + SD_PADB) * P;
+        // terms alive for this warp's 8 planes x 8 rows: kofd at the Chebyshev
+        // distance of each of the 4 copies, max over them (warp-uniform); the
+        // narrow terms of far copies are below RS_TERM_DROP there
+        int kw = 0;
+        if (q < q_hi) {
+          const int dx = max(0, max((int)X0 - a1, a1 - (int)X0 - (SD_TX1 - 1)));
+          const int dy = max(0, max((int)yw - a2, a2 - (int)yw - 7));
+          const int d = max(dx, dy);
+          kw = d <= gamma ? skofd[d] : 0;
+        }
+        kw = max(kw, __shfl_xor_sync(0xffffffffu, kw, 1));
+        kw = max(kw, __shfl_xor_sync(0xffffffffu, kw, 2));
 #pragma unroll
-        for (int k = 0; k < GK; ++k) dmma_884(acc[k], z * pa[k], pb[k]);
+        for (int k = 0; k < GK; ++k)
+          if (k < kw) dmma_884(acc[k], z * pa[k], pb[k]);
       }
       if (s_bst[j + 1] <= cend) {  // bucket complete: store its G-wide row segments
         const int64_t x1l = x1l0 + ar;
@@ -1249,16 +1313,16 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int g
                                const int32_t *c1, const int32_t *c2, const double *zq,
                                const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                                int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
-                               int64_t col0, cudaStream_t s) {
+                               int64_t col0, const int *kofd, cudaStream_t s) {
   const int W = 2 * gamma + 1;
   const size_t smem = (size_t)(GK + 1) * (2 * W + 2 * SD_PADA + 2 * SD_PADB) * 8 +
-                      (SD_THREADS + 4) * (8 + 4 + 4 + 4) + 32 * 4;
+                      (SD_THREADS + 4) * (8 + 4 + 4 + 4) + 32 * 4 + (size_t)(gamma + 1) * 4;
   cudaError_t e = smem_attr((const void *)k_short_dmma<GK>, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_dmma smem: %s", cudaGetErrorString(e));
   dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
             (unsigned)ceil_div(nb_max, SD_BG));
   k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, GK, gamma, c1, c2, zq, bstart, nb_dev,
-                                                  n, x1_lo, planes, A, lda, col0);
+                                                  n, x1_lo, planes, A, lda, col0, kofd);
   return check_launch("short_dmma");
 }
 
@@ -1267,12 +1331,12 @@ static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, 
                              const int32_t *c1, const int32_t *c2, const double *zq,
                              const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                              int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
-                             int64_t col0, cudaStream_t s) {
+                             int64_t col0, const int *kofd, cudaStream_t s) {
   switch (G) {
 #define RS_SD(R)                                                                              \
   case R:                                                                                     \
     return launch_short_dmma_t<R>(ul, wl, Rs, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
-                                  x1_lo, planes, A, lda, col0, s);
+                                  x1_lo, planes, A, lda, col0, kofd, s);
     RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14) RS_SD(16) RS_SD(18)
     RS_SD(20) RS_SD(22) RS_SD(24)
 #undef RS_SD
@@ -1398,11 +1462,11 @@ int rs_syrk(const double *A, int64_t lda, int64_t n, int64_t K, double *G, void 
   {
     ProfScope ps(s, "syrk");
       k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp), TileSyrk::THREADS, TileSyrk::SMEM_BYTES, s>>>(
-        A, lda, n, K, ks, part, 0, 0);
+        A, lda, n, K, ks, part, 0, 0, nullptr);
   }
   if ((st = check_launch("rs_syrk part"))) return st;
   int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
-  k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G, 0);
+  k_syrk_reduce<<<grid_for(tot, 256), 256, 0, s>>>(part, sp, ntp, n, G, 0, nullptr);
   return check_launch("rs_syrk reduce");
 }
 
@@ -1411,7 +1475,8 @@ int64_t rs_gram_shifted_workspace_bytes(int64_t n, int64_t R) {
   int64_t ks;
   const int64_t sp = syrk_splits(n, ldx, &ks);
   const int64_t nt = ceil_div(n, TileSyrk::BM);
-  return round_up(3 * n * ldx * 8, 256) + 3 * sp * (nt * (nt + 1) / 2) * TileSyrk::BM * TileSyrk::BN * 8;
+  return round_up(3 * n * ldx * 8, 256) + 3 * sp * (nt * (nt + 1) / 2) * TileSyrk::BM * TileSyrk::BN * 8 +
+         round_up(3 * n * 4, 256) + 256;
 }
 
 int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R, const double *c,
@@ -1426,20 +1491,27 @@ int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R,
   const int64_t part_stride = sp * ntp * TileSyrk::BM * TileSyrk::BN;
   double *X = (double *)work;
   double *part = (double *)((char *)work + round_up(3 * n * ldx * 8, 256));
+  int32_t *list = (int32_t *)((char *)part + 3 * part_stride * 8);
+  int32_t *kdev = (int32_t *)((char *)list + round_up(3 * n * 4, 256));
   cudaStream_t s = as_stream(stream);
   int st;
-  k_gram_operands<<<grid_for(3 * n * ldx, 256), 256, 0, s>>>(table, ld_table, n, R, c, wabs, X,
-                                                              ldx);
+  // occupied shifts only: K per mode = (#occupied shifts) R instead of n R
+  // (C2: 50 of 256 shifts, C5: 363 of 2048), known on the device
+  k_shift_list<<<3, 1024, 0, s>>>(c, n, R, list, kdev);
+  if ((st = check_launch("shift list"))) return st;
+  k_gram_operands<<<grid_for(3 * n * ldx, 256), 256, 0, s>>>(table, ld_table, n, R, c, wabs, list,
+                                                              kdev, X, ldx);
   if ((st = check_launch("gram operands"))) return st;
   if ((st = set_smem<TileSyrk>((const void *)k_syrk_part))) return st;
   {
     ProfScope ps(s, "syrk");
     k_syrk_part<<<dim3((unsigned)ntp, (unsigned)sp, 3), TileSyrk::THREADS, TileSyrk::SMEM_BYTES,
-                  s>>>(X, ldx, n, ldx, ks, part, n * ldx, part_stride);
+                  s>>>(X, ldx, n, ldx, ks, part, n * ldx, part_stride, kdev);
   }
   if ((st = check_launch("gram syrk"))) return st;
   const int64_t tot = ntp * TileSyrk::BM * TileSyrk::BN;
-  k_syrk_reduce<<<dim3(grid_for(tot, 256), 1, 3), 256, 0, s>>>(part, sp, ntp, n, G, part_stride);
+  k_syrk_reduce<<<dim3(grid_for(tot, 256), 1, 3), 256, 0, s>>>(part, sp, ntp, n, G, part_stride,
+                                                                kdev);
   return check_launch("gram reduce");
 }
 
@@ -1563,6 +1635,12 @@ static const bool g_tucker_apply = [] {
   return !(e && e[0] == '0');
 }();
 
+// RSB200_ROW_CUT=0: the row builder computes every term of every copy
+static const bool g_row_cut = [] {
+  const char *e = getenv("RSB200_ROW_CUT");
+  return !(e && e[0] == '0');
+}();
+
 static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int64_t nb_max,
                        int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
                        int64_t *offY, int64_t *offR, int64_t *total) {
@@ -1657,10 +1735,16 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                               (int)planes, s)))
       return st;
   }
+  const int64_t ntiles0 = ceil_div(n, TilePlane::BN);
+  int *kofd = (int *)((char *)ranges + round_up(ntiles0 * 4 * 8, 256));
   if (with_short) {
+    // per-distance live-term counts: the row builder's and the GEMM's term cuts
+    k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
+    if ((st = check_launch("term_prefix"))) return st;
     ProfScope ps(s, "short_rows");
     if ((st = launch_short_dmma(ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, nb_dev,
-                                nb_max, n, x1_lo, planes, A, lda, r3p, s)))
+                                nb_max, n, x1_lo, planes, A, lda, r3p,
+                                g_row_cut ? kofd : nullptr, s)))
       return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
@@ -1688,12 +1772,9 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                            accumulate ? 1 : 0, wb + oz_off, tot - oz_off,
                            with_short ? nb_dev : nullptr, r3p, G, stream);
   }
-  int *kofd = (int *)((char *)ranges + round_up(ntiles * 4 * 8, 256));
   const int64_t nrb = ceil_div(planes * n, TilePlane::BM), ldk = round_up(nb_max, 16);
   uint8_t *kr = (uint8_t *)((char *)kofd + round_up((n + 1) * 4, 256));
   if (with_short) {
-    k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
-    if ((st = check_launch("term_prefix"))) return st;
     k_rowblock_terms<<<grid_for(nrb * ldk, 256), 256, 0, s>>>(
         c1, c2, bstart, nb_dev, kofd, (int)gamma, n, x1_lo, planes * n, TilePlane::BM, nrb, ldk,
         kr);
