@@ -282,6 +282,33 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
             const int32_t *bstart, const int32_t *bc3, const int32_t *nb,
             int64_t nq /* occupied x3 values if known on the host, else 0 */);
 
+/* rs_back, then (after `wait_event`, a cudaEvent_t, when not NULL) the
+ * Tucker part of planes [x1_lo, x1_hi) accumulated into `out` (the
+ * prefetched short-range slab, (x1_hi - x1_lo) x n x n) by rs_assemble_planes
+ * in chunks of `chunk` planes with `asm_work`: build_rs's post-rank device
+ * work in one call.  Reference: rankred.py:151-177, formats.py:173-176. */
+int rs_back_tucker(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+                   const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+                   const double *z, const double *w, int64_t count, double *Z1, double *Z2,
+                   double *Z3, double *core, void *work, int64_t work_bytes, void *stream,
+                   const int32_t *c1, const int32_t *c2, const double *zq,
+                   const int32_t *bstart, const int32_t *bc3, const int32_t *nb,
+                   int64_t nq_host, double *out, int64_t x1_lo, int64_t x1_hi,
+                   int64_t chunk, void *asm_work, int64_t asm_work_bytes,
+                   void *wait_event);
+
+/* eps-rank rule on top-b Ritz values (host function, no device work), for m
+ * modes: thetas (m x b, descending), traces (m); forced = NULL or m ranks
+ * (> 0 forces); limit > 0 caps the rank.  rank_out[l] = -1 when the block is
+ * too small / not converged to decide (convergence test
+ * 1e2 (theta_{b-1}/theta_{r-1})^iters sqrt(theta_{r-1}/theta_0) <= 1e-11).
+ * tail_out = sum of the eigenvalues beyond the rank (+ the uncaptured trace),
+ * total_out = the captured sum + the uncaptured trace.  Reference:
+ * rankred.py:129-148 (_eps_rank: smallest r with tail <= eps * total). */
+int rs_rank_rule(const double *thetas, const double *traces, int64_t m, int64_t b, int64_t n,
+                 double eps, const int64_t *forced, int64_t limit, int64_t iters,
+                 int64_t *rank_out, double *tail_out, double *total_out);
+
 /* ---- SM partitions ------------------------------------------------------
  * A non-blocking stream whose kernels run on a fixed subset of >= `sms` SMs
  * (green context, created once per (device, sms)); *sms_out = its SM count.

@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as nat
 from .errors import ConfigError, DomainError, ResolutionError
-from .formats import tucker_accumulate, CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
+from .formats import tucker_accumulate, tucker_plan, CCT, CanonicalTensor, RSCanonical, RSTucker, assemble_grid, is_device, \
     short_layout, storage_report, to_device, to_host, trusted_cct
 from .parallel import particle_shard, sharded_sum
 from .particles import Grid3, IndexedParticleSystem, ParticleSystem, separation_distance, \
@@ -637,6 +637,31 @@ def _world(group) -> int:
     return dist.get_world_size(group) if dist.is_initialized() else 1
 
 
+_RANK_BUF: dict = {}
+
+
+def _rank_rule(packed, b: int, n: int, eps, forced, limit, iters):
+    """``rank_rule_fast`` through ``rs_rank_rule`` (C, same arithmetic):
+    [(rank or None, tail at the rank, total)] per mode."""
+    import ctypes
+    buf = _RANK_BUF.get(0)
+    if buf is None:
+        buf = _RANK_BUF[0] = ((ctypes.c_int64 * 3)(), (ctypes.c_double * 3)(),
+                              (ctypes.c_double * 3)(), (ctypes.c_int64 * 3)())
+    ro, to, so, fo = buf
+    fptr = None
+    if forced is not None:
+        for l in range(3):
+            fo[l] = int(forced[l]) if forced[l] is not None else 0
+        fptr = ctypes.addressof(fo)
+    base = packed.ctypes.data
+    nat.check(nat.lib().rs_rank_rule(base, base + 8 * 3 * b, 3, b, n, float(eps), fptr,
+                                     int(limit) if limit is not None else 0, iters,
+                                     ctypes.addressof(ro), ctypes.addressof(to),
+                                     ctypes.addressof(so)), "rs_rank_rule")
+    return [(ro[l] if ro[l] > 0 else None, to[l], so[l]) for l in range(3)]
+
+
 def _eig_block(cfg: AssemblyConfig, n: int):
     """Ritz block of the eigen-truncation: (b, use_top, iters, eps, forced ranks)."""
     # block size: the numerical rank of the long-part Grams grows as eps shrinks
@@ -845,8 +870,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                     raise ConfigError(f"requested rank {r} exceeds min(n, R) = {limit}")
         ranks, values, tails, zs, from_top = [], [], [], [], []
         if use_top:
-            fast3 = rank_rule_fast(packed[:3 * b].tolist(), packed[3 * b:3 * b + 3].tolist(), n,
-                                   cfg.reduction.eps, forced, limit, iters)
+            fast3 = _rank_rule(packed, b, n, cfg.reduction.eps, forced, limit, iters)
         for l in range(3):
             fr = forced[l] if forced is not None else None
             r = None
@@ -894,6 +918,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         ranks = tuple(ranks)
         _mark("d2h")
         core = None
+        fused_tucker = False
         if world == 1:
             # factors + projections + core in one native call (bucket-K core)
             r1, r2, r3 = ranks
@@ -913,15 +938,32 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
             ws = nat.Workspace.get(L.rs_back_workspace_bytes(n, r1, r2, r3, ds.count,
                                                              int(plan.w_long.shape[0]), nq_host),
                                    "core")
-            nat.check(L.rs_back(Ub.data_ptr(), bu, n, r1, r2, r3, plan.table_dev.data_ptr(),
-                                plan.table_dev.shape[1], int(plan.w_long.shape[0]),
-                                nat.ptr(starts), z.data_ptr(), plan.w_long.data_ptr(), ds.count,
-                                zs[0].data_ptr(), zs[1].data_ptr(), zs[2].data_ptr(),
-                                core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr(),
-                                *((prep["c1"], prep["c2"], prep["zq"], front["bstart"],
-                                   front["bc3"], front["nb"]) if front is not None
-                                  else (None,) * 6), nq_host),
-                      "rs_back")
+            back_args = (Ub.data_ptr(), bu, n, r1, r2, r3, plan.table_dev.data_ptr(),
+                         plan.table_dev.shape[1], int(plan.w_long.shape[0]),
+                         nat.ptr(starts), z.data_ptr(), plan.w_long.data_ptr(), ds.count,
+                         zs[0].data_ptr(), zs[1].data_ptr(), zs[2].data_ptr(),
+                         core.data_ptr(), ws.data_ptr(), ws.numel(), nat.stream_ptr(),
+                         *((prep["c1"], prep["c2"], prep["zq"], front["bstart"],
+                            front["bc3"], front["nb"]) if front is not None
+                           else (None,) * 6), nq_host)
+            pre0 = short._cache.get("prefetch") if cfg.long_format == "tucker" else None
+            if (pre0 is not None and _TUCKER_IN_BUILD and pre0["groups"] is None
+                    and not pre0["complete"]):
+                # back + the Tucker part of the prefetched slab in one call
+                lo, hi, buf = pre0["lo"], pre0["hi"], pre0["buf"]
+                chunk, wsb = tucker_plan(n, hi - lo, max(ranks))
+                aws = nat.Workspace.get(wsb, "assemble")
+                cur = torch.cuda.current_stream()
+                buf.record_stream(cur)
+                nat.check(L.rs_back_tucker(*back_args, buf.data_ptr(), lo, hi, chunk,
+                                           aws.data_ptr(), aws.numel(), pre0["ev"].cuda_event),
+                          "rs_back_tucker")
+                done = torch.cuda.Event()
+                done.record(cur)
+                short._cache["prefetch"] = dict(pre0, ev=done, complete=True)
+                fused_tucker = True
+            else:
+                nat.check(L.rs_back(*back_args), "rs_back")
             _mark("back_enq")
         else:
             zs = [zl[:r].T.contiguous() for zl, r in zip(zs, ranks)]
@@ -938,7 +980,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         _mark("tucker_obj")
         long_raw = None
         pre = short._cache.get("prefetch") if cfg.long_format == "tucker" else None
-        if pre is not None and _TUCKER_IN_BUILD:
+        if pre is not None and _TUCKER_IN_BUILD and not fused_tucker:
             # finish the prefetched slab here: the Tucker part is enqueued right
             # behind the core, before the host packages the result
             lo, hi, buf = pre["lo"], pre["hi"], pre["buf"]

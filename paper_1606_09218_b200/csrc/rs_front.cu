@@ -7,6 +7,10 @@
 // (the shift regrouping behind the histograms).
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "rs_common.cuh"
 
 using namespace rsb;
@@ -404,5 +408,119 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
       TT3, (int)r3, n, (int)R, bc3, nb, nq, T3, ldH);
   if ((st = check_launch("core_t3"))) return st;
   return rs_gemm_nt(H, ldH, T3, ldH, core, r3, r1 * r2, r3, ldH, stream);
+}
+
+/* rs_back, then (after `wait_event` when given) the Tucker part of planes
+ * [x1_lo, x1_hi) accumulated into `out` (the prefetched short-range slab) in
+ * chunks of `chunk` planes: the post-synchronisation device work of build_rs
+ * in one host call.  Reference: rankred.py:151-177 + formats.py:173-176. */
+int rs_back_tucker(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+                   const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+                   const double *z, const double *w, int64_t count, double *Z1, double *Z2,
+                   double *Z3, double *core, void *work, int64_t work_bytes, void *stream,
+                   const int32_t *c1, const int32_t *c2, const double *zq,
+                   const int32_t *bstart, const int32_t *bc3, const int32_t *nb, int64_t nq_host,
+                   double *out, int64_t x1_lo, int64_t x1_hi, int64_t chunk, void *asm_work,
+                   int64_t asm_work_bytes, void *wait_event) {
+  RS_REQUIRE(out && asm_work && 0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n && chunk >= 1,
+             "rs_back_tucker: bad slab arguments");
+  int st = rs_back(U, b, n, r1, r2, r3, table, ld_table, R, starts, z, w, count, Z1, Z2, Z3, core,
+                   work, work_bytes, stream, c1, c2, zq, bstart, bc3, nb, nq_host);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  if (wait_event && cudaStreamWaitEvent(s, (cudaEvent_t)wait_event, 0) != cudaSuccess)
+    return fail(RS_ERR_CUDA, "rs_back_tucker: wait");
+  const int flags = RS_ASM_LONG | RS_ASM_ACCUMULATE;
+  for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += chunk) {
+    const int64_t p1 = std::min<int64_t>(x1_hi, p0 + chunk);
+    if ((st = rs_assemble_planes(core, r1, r2, r3, Z1, Z2, Z3, n, nullptr, nullptr, 0, 0, nullptr,
+                                 nullptr, nullptr, nullptr, nullptr, nullptr, 0, p0, p1, flags,
+                                 out + (p0 - x1_lo) * n * n, asm_work, asm_work_bytes, stream)))
+      return st;
+  }
+  return RS_OK;
+}
+}  // extern "C"
+
+// ------------------------------------------------------------ rank rule
+// Host-side eps-rank of the top-b Ritz values (rankred.truncated_spectrum /
+// rank_rule_fast in C: it sits between the eigen block's synchronisation and
+// the back launch).  Reference: rankred.py:129-148 (_eps_rank).
+namespace {
+// numpy's float64 add.reduce of a contiguous vector: pairwise sum (8
+// accumulators up to 128 elements, halves above)
+double np_pairwise(const double *a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+double np_sum(const double *a, int64_t n) {
+  return n <= 0 ? 0.0 : np_pairwise(a, n);
+}
+}  // namespace
+
+extern "C" {
+int rs_rank_rule(const double *thetas, const double *traces, int64_t m, int64_t b, int64_t n,
+                 double eps, const int64_t *forced, int64_t limit, int64_t iters,
+                 int64_t *rank_out, double *tail_out, double *total_out) {
+  RS_REQUIRE(thetas && traces && m >= 1 && b >= 1 && b <= 4096 && rank_out && tail_out &&
+                 total_out,
+             "rs_rank_rule: bad arguments");
+  std::vector<double> th((size_t)b), tails((size_t)b);
+  for (int64_t l = 0; l < m; ++l) {
+    for (int64_t k = 0; k < b; ++k) th[k] = thetas[l * b + k] > 0.0 ? thetas[l * b + k] : 0.0;
+    const double tot_th = np_sum(th.data(), b);
+    const double rem = b < n ? std::max(traces[l] - tot_th, 0.0) : 0.0;
+    const double total = tot_th + rem;
+    double acc = 0.0;
+    for (int64_t k = b - 1; k >= 0; --k) {
+      acc += th[k];
+      tails[k] = acc + rem;
+    }
+    total_out[l] = total;
+    rank_out[l] = -1;
+    tail_out[l] = 0.0;
+    int64_t r;
+    if (forced && forced[l] > 0) {
+      r = forced[l];
+    } else if (total == 0.0) {
+      r = 1;
+    } else {
+      const double thr = eps * total;
+      r = -1;
+      for (int64_t k = 0; k < b; ++k)
+        if (tails[k] <= thr) {
+          r = k;
+          break;
+        }
+      if (r < 0) continue;
+      r = std::max<int64_t>(r, 1);
+    }
+    if (limit > 0) r = std::min(r, limit);
+    if (b < n) {
+      const double lam_r = (0 < r && r <= b) ? th[r - 1] : 0.0;
+      if (r >= b || lam_r <= 0.0 || th[0] <= 0.0 ||
+          1e2 * std::pow(th[b - 1] / lam_r, (double)iters) * std::sqrt(lam_r / th[0]) > 1e-11)
+        continue;
+    }
+    rank_out[l] = r;
+    tail_out[l] = r < b ? tails[r] : 0.0;
+  }
+  return RS_OK;
 }
 }  // extern "C"

@@ -508,6 +508,21 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
     return out
 
 
+def tucker_plan(n: int, planes: int, rmax: int, workspace_bytes: int = _ASSEMBLE_WORKSPACE):
+    """(planes per chunk, workspace bytes) of a Tucker-only accumulate."""
+    flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
+    key = (n, planes, rmax, 0, 0, flags, workspace_bytes)
+    plan = _ASM_PLANS.get(key)
+    if plan is None:
+        L = nat.lib()
+        one = L.rs_assemble_workspace_bytes(n, 1, rmax, 0, 0, flags)
+        per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, 0, 0, flags) - one
+        chunk = max(1, min(planes, (workspace_bytes - (one - per_plane)) // max(per_plane, 1)))
+        plan = _ASM_PLANS[key] = (chunk, L.rs_assemble_workspace_bytes(n, chunk, rmax, 0, 0,
+                                                                        flags))
+    return plan
+
+
 def tucker_accumulate(long: TuckerTensor, x1_lo: int, x1_hi: int, out,
                       workspace_bytes: int = _ASSEMBLE_WORKSPACE, workspace_slot: str = "assemble"):
     """``out[x1 - x1_lo] += Tucker(long)[x1]`` for x1 in [x1_lo, x1_hi): the
@@ -518,17 +533,8 @@ def tucker_accumulate(long: TuckerTensor, x1_lo: int, x1_hi: int, out,
     planes = x1_hi - x1_lo
     flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
     L = nat.lib()
-    rmax = max(r1, r2, r3)
-    key = (n, planes, rmax, 0, 0, flags, workspace_bytes)
-    plan = _ASM_PLANS.get(key)
-    if plan is None:
-        one = L.rs_assemble_workspace_bytes(n, 1, rmax, 0, 0, flags)
-        per_plane = L.rs_assemble_workspace_bytes(n, 2, rmax, 0, 0, flags) - one
-        chunk = max(1, min(planes, (workspace_bytes - (one - per_plane)) // max(per_plane, 1)))
-        plan = _ASM_PLANS[key] = (chunk, L.rs_assemble_workspace_bytes(n, chunk, rmax, 0, 0,
-                                                                        flags))
-    chunk = plan[0]
-    ws = nat.Workspace.get(plan[1], workspace_slot)
+    chunk, wsb = tucker_plan(n, planes, max(r1, r2, r3), workspace_bytes)
+    ws = nat.Workspace.get(wsb, workspace_slot)
     core, (v1, v2, v3) = long.core, long.factors
     cp, p1_, p2_, p3_ = core.data_ptr(), v1.data_ptr(), v2.data_ptr(), v3.data_ptr()
     wp, wn, st = ws.data_ptr(), ws.numel(), nat.stream_ptr()
