@@ -175,6 +175,11 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3,
 #define RS_ASM_LONG 1
 #define RS_ASM_SHORT 2
 #define RS_ASM_ACCUMULATE 4
+/* long part only, split in two calls on the same workspace: RS_ASM_F_ONLY
+ * computes the per-plane Tucker operands A = V2 (core x1 V1[x1]) and returns;
+ * RS_ASM_F_READY skips that stage (A already in the workspace) */
+#define RS_ASM_F_ONLY 16
+#define RS_ASM_F_READY 32
 /* plane GEMM as Ozaki-split FP64 with s int8 slices (tcgen05 kind::i8), s in 6..8 */
 #define RS_ASM_OZ(s) ((s) << 8)
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax,

@@ -951,7 +951,8 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                     and not pre0["complete"]):
                 # back + the Tucker part of the prefetched slab in one call
                 lo, hi, buf = pre0["lo"], pre0["hi"], pre0["buf"]
-                chunk, wsb = tucker_plan(n, hi - lo, max(ranks))
+                # one chunk (operands of the whole slab, formed before the wait)
+                chunk, wsb = tucker_plan(n, hi - lo, max(ranks), workspace_bytes=1 << 62)
                 aws = nat.Workspace.get(wsb, "assemble")
                 cur = torch.cuda.current_stream()
                 buf.record_stream(cur)

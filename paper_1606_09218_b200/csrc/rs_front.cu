@@ -428,9 +428,18 @@ int rs_back_tucker(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2
                    work, work_bytes, stream, c1, c2, zq, bstart, bc3, nb, nq_host);
   if (st) return st;
   cudaStream_t s = as_stream(stream);
+  int flags = RS_ASM_LONG | RS_ASM_ACCUMULATE;
+  if (chunk >= x1_hi - x1_lo) {
+    // one chunk: the Tucker operands do not depend on the short-range planes,
+    // so they are formed before the wait (C5: 24 ms that overlap the prefetch)
+    if ((st = rs_assemble_planes(core, r1, r2, r3, Z1, Z2, Z3, n, nullptr, nullptr, 0, 0, nullptr,
+                                 nullptr, nullptr, nullptr, nullptr, nullptr, 0, x1_lo, x1_hi,
+                                 flags | RS_ASM_F_ONLY, out, asm_work, asm_work_bytes, stream)))
+      return st;
+    flags |= RS_ASM_F_READY;
+  }
   if (wait_event && cudaStreamWaitEvent(s, (cudaEvent_t)wait_event, 0) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_back_tucker: wait");
-  const int flags = RS_ASM_LONG | RS_ASM_ACCUMULATE;
   for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += chunk) {
     const int64_t p1 = std::min<int64_t>(x1_hi, p0 + chunk);
     if ((st = rs_assemble_planes(core, r1, r2, r3, Z1, Z2, Z3, n, nullptr, nullptr, 0, 0, nullptr,

@@ -463,6 +463,20 @@ __global__ void k_tucker_yt(const double *__restrict__ core, int r1, int r2, int
   }
 }
 
+// coreT[(c r2p + b) r1p + a] = core[a, b, c] (zero-padded): the B operand of
+// Yt[x1, (c, b)] = sum_a V1[x1, a] core[a, b, c] as one DMMA GEMM (large ranks)
+__global__ void k_core_t(const double *__restrict__ core, int r1, int r2, int r3, int r1p,
+                         int r2p, int r3p, double *__restrict__ coreT) {
+  const int64_t total = (int64_t)r3p * r2p * r1p;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(e % r1p);
+    const int64_t q = e / r1p;
+    const int b = (int)(q % r2p), c = (int)(q / r2p);
+    coreT[e] = (a < r1 && b < r2 && c < r3) ? core[((int64_t)a * r2 + b) * r3 + c] : 0.0;
+  }
+}
+
 // V2p = V2 (n x r2) with columns zero-padded to r2p (16-byte aligned K rows)
 __global__ void k_pad_cols(const double *__restrict__ V, int64_t n, int r, int rp,
                            double *__restrict__ Vp) {
@@ -1651,8 +1665,8 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
   int64_t a = round_up(planes * n * *lda * 8, 256);
   int64_t b = round_up(n * *lda * 8, 256);
   const int64_t rp = round_up(std::max<int64_t>(rmax, 1), 2);
-  // Yt (planes x r3p x r2p) | V2p (n x r2p)
-  int64_t y = with_long ? round_up((planes * rp * rp + n * rp) * 8, 256) : 0;
+  // Yt (planes x r3p x r2p) | V2p (n x r2p) | V1p (n x r1p) | coreT (r3p r2p x r1p)
+  int64_t y = with_long ? round_up((planes * rp * rp + 2 * n * rp + rp * rp * rp) * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, TilePlane::BN);
   // ranges | kofd | row-block term table (uint8, row blocks x buckets)
   int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256) +
@@ -1720,14 +1734,28 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   int64_t *ranges = (int64_t *)(wb + oR);
   cudaStream_t s = as_stream(stream);
   int st;
-  if (with_long) {
+  const bool f_only = with_long && !with_short && (flags & RS_ASM_F_ONLY);
+  const bool f_ready = with_long && !with_short && (flags & RS_ASM_F_READY);
+  if (with_long && !f_ready) {
     ProfScope ps(s, "tucker_f");
     const int64_t rp = round_up(rmax, 2), r2p = round_up(r2, 2);
     double *Yt = Y;
     double *V2p = Yt + planes * rp * rp;
-    k_tucker_yt<<<grid_for(planes * r3p * r2p, 256), 256, 0, s>>>(
-        core, (int)r1, (int)r2, (int)r3, V1, x1_lo, (int)r2p, (int)r3p, planes, Yt);
-    if ((st = check_launch("tucker_yt"))) return st;
+    if (r1 * r2 * r3 >= 32768) {  // large ranks (C4, C5): Yt as one DMMA GEMM over r1
+      const int64_t r1p = round_up(r1, 2);
+      double *V1p = V2p + n * rp, *coreT = V1p + n * rp;
+      k_pad_cols<<<grid_for(n * r1p, 256), 256, 0, s>>>(V1, n, (int)r1, (int)r1p, V1p);
+      k_core_t<<<grid_for(r3p * r2p * r1p, 256), 256, 0, s>>>(core, (int)r1, (int)r2, (int)r3,
+                                                              (int)r1p, (int)r2p, (int)r3p, coreT);
+      if ((st = check_launch("tucker core_t"))) return st;
+      if ((st = rs_gemm_nt(V1p + x1_lo * r1p, r1p, coreT, r1p, Yt, r3p * r2p, planes, r3p * r2p,
+                           r1p, stream)))
+        return st;
+    } else {
+      k_tucker_yt<<<grid_for(planes * r3p * r2p, 256), 256, 0, s>>>(
+          core, (int)r1, (int)r2, (int)r3, V1, x1_lo, (int)r2p, (int)r3p, planes, Yt);
+      if ((st = check_launch("tucker_yt"))) return st;
+    }
     k_pad_cols<<<grid_for(n * r2p, 256), 256, 0, s>>>(V2, n, (int)r2, (int)r2p, V2p);
     if ((st = check_launch("pad_cols"))) return st;
     // per plane: A[x1l][x2, c] = V2p[x2, :] . Yt[x1l][c, :]  (DMMA, batched over planes)
@@ -1748,6 +1776,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
+  if (f_only) return RS_OK;
   const int slices0 = (flags >> 8) & 0xF;
   if (with_long && !with_short && !slices0 && g_tucker_apply && tucker_apply_ok(r3, n)) {
     // small r3: the HBM-bound row kernel instead of the plane GEMM
