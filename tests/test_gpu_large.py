@@ -75,3 +75,31 @@ def test_point_values_energy_forces(large):
     fref = np.array([orc.force_fd(idx, case["charges"], p["table"], p["w"], case["split_index"], h,
                                   int(j)) for j in sel[:20]])
     assert np.max(np.abs(f - fref)) <= 1e-9 * np.max(np.abs(fref))
+
+
+def test_prefetch_path_planes(large):
+    """The serving path at full size: short planes prefetched by the native
+    front on the side partition, the Gram + eigen block chained behind the
+    front (rs_chain_eig), the rank rule in C, and back + Tucker accumulate in
+    one call (rs_back_tucker: operands formed before the prefetch wait; the
+    HBM row kernel for r3 <= 32, the plane GEMM above)."""
+    import torch
+    name, case, p, idx, core, zs, ranks, res = large
+    system, cfg = configs.system(name), configs.assembly_config(name)
+    dp = rt.DeviceParticles(torch.tensor(system.positions, device="cuda"),
+                            torch.tensor(system.charges, device="cuda"), system.box)
+    resp = rt.build_rs(dp, cfg, prefetch_dense=True)
+    assert resp.report["tucker_ranks"] == list(ranks)
+    g = rt.dense_rs(resp.rs, limit=1 << 62, device=True)
+    ul, wl = orc.local_window(p["table"], p["w"], case["split_index"], p["gamma"])
+    L0 = orc.local_dense(ul, wl)
+    pairs = []
+    for x in PLANES[name]:
+        t = np.einsum("abc,a,jb,lc->jl", core, zs[0][x], zs[1], zs[2], optimize=True)
+        ref = t + orc.dense_cct_c(L0, p["gamma"], idx, case["charges"], case["n"], x, x + 1)[0]
+        pairs.append((x, g[x].cpu().numpy(), ref))
+    del g
+    torch.cuda.empty_cache()
+    scale = max(float(np.max(np.abs(ref))) for _, _, ref in pairs)
+    for x, got, ref in pairs:
+        assert np.max(np.abs(got - ref)) <= 1e-10 * scale, (name, x)
