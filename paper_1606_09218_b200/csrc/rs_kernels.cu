@@ -531,6 +531,7 @@ constexpr int SD_BG = 8;     // buckets per CTA
 constexpr int SD_PADA = SD_TX1;  // plane offsets stay within [-TX1, W + TX1)
 constexpr int SD_PADB = SD_TX2;  // row offsets stay within [-TX2, W + TX2)
 
+// (two CTAs per SM at R_s <= 14 -- 128 registers -- measured no faster)
 template <int GK>
 __global__ void __launch_bounds__(SD_THREADS)
     k_short_dmma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int G,
