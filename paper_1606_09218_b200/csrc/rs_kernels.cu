@@ -149,6 +149,10 @@ __device__ __forceinline__ void syrk_slices(int64_t kl, int64_t sp_max, int64_t 
 // ============================================================ GEMM kernels
 using TilePlane = Tile<128, 64, 32, 32, 3>;  // plane GEMM / generic NT GEMM
 using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
+// narrow x3 tiles for the short-range plane GEMM: the per-term bands add the
+// tile width to every term's support, so narrow terms cost ~half with BN = 32
+using TilePlaneN = Tile<128, 32, 32, 32, 3>;
+constexpr int PLANE_MIN_BN = 32;  // sizes the per-column-tile workspace tables
 
 // C[m0.., n0..] = sum over the K ranges of this column tile of A B^T.
 // ranges: per column tile, nr (lo, hi) pairs; NULL => single range [0, K).
@@ -525,6 +529,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total
 // straddles two passes keeps its accumulators.  Window factors are gathered
 // from shared memory with clamped indices and a validity mask.
 constexpr int SD_THREADS = 256;
+constexpr int RB_ROWS = 128;  // row block of the plane GEMM's term table (TilePlane::BM)
 constexpr int SD_TX1 = 8;    // planes per tile (MMA m)
 constexpr int SD_TX2 = 64;   // rows per tile (8 warps x MMA n)
 constexpr int SD_BG = 8;     // buckets per CTA
@@ -539,7 +544,7 @@ __global__ void __launch_bounds__(SD_THREADS)
                  const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                  const int32_t *__restrict__ nbp, int64_t n, int64_t x1_lo, int64_t planes,
                  double *__restrict__ A, int64_t lda, int64_t col0,
-                 const int *__restrict__ kofd) {
+                 const int *__restrict__ kofd, const uint8_t *__restrict__ kr, int64_t ldk) {
   extern __shared__ double sm[];
   const int W = 2 * gamma + 1;
   constexpr int P = GK + 1;  // odd pitch (doubles): conflict-light row gathers
@@ -672,10 +677,14 @@ __global__ void __launch_bounds__(SD_THREADS)
           for (int jj = 0; jj < 2; ++jj) {
             const int64_t x2 = yw + 2 * kq + jj;
             if (x2 < n) {
-              double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
+              const int64_t g = x1l * n + x2;
+              // only the terms the plane GEMM reads for this row block
+              const int kst = kr ? (int)kr[(g / RB_ROWS) * ldk + b0 + j] : GK;
+              double *dst = A + g * lda + col0 + (int64_t)(b0 + j) * GK;
 #pragma unroll
               for (int k = 0; k < GK; k += 2)
-                *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
+                if (k < kst)
+                  *reinterpret_cast<double2 *>(dst + k) = make_double2(acc[k][jj], acc[k + 1][jj]);
             }
           }
         }
@@ -694,10 +703,12 @@ __global__ void __launch_bounds__(SD_THREADS)
       for (int jj = 0; jj < 2; ++jj) {
         const int64_t x2 = yw + 2 * kq + jj;
         if (x2 < n) {
-          double *dst = A + (x1l * n + x2) * lda + col0 + (int64_t)(b0 + j) * GK;
+          const int64_t g = x1l * n + x2;
+          const int kst = kr ? (int)kr[(g / RB_ROWS) * ldk + b0 + j] : GK;
+          double *dst = A + g * lda + col0 + (int64_t)(b0 + j) * GK;
 #pragma unroll
           for (int k = 0; k < GK; k += 2)
-            *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
+            if (k < kst) *reinterpret_cast<double2 *>(dst + k) = make_double2(0.0, 0.0);
         }
       }
     }
@@ -812,14 +823,13 @@ __global__ void k_rowblock_terms(const int32_t *__restrict__ c1, const int32_t *
 
 constexpr int PLANE_SEGS = 1024;  // segments per column tile (1 + occupied x3 in the band)
 
-template <bool ACC>
-__global__ void __launch_bounds__(TilePlane::THREADS)
+template <class T, bool ACC>
+__global__ void __launch_bounds__(T::THREADS)
     k_gemm_plane(const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                  int64_t ldb, double *__restrict__ C, int64_t ldc, int64_t M, int64_t N,
                  int64_t r3p, int64_t G, const int32_t *__restrict__ bc3,
                  const int32_t *__restrict__ nbp, int gamma, const int *__restrict__ kofd,
                  const uint8_t *__restrict__ kr, int64_t ldk) {
-  using T = TilePlane;
   constexpr int CH = T::BK / 2;                  // 2-column pair slots per chunk row
   static_assert(T::THREADS % CH == 0, "pair slot must be fixed per thread");
   constexpr int ROWS_PER_PASS = T::THREADS / CH;
@@ -1328,7 +1338,8 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int g
                                const int32_t *c1, const int32_t *c2, const double *zq,
                                const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                                int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
-                               int64_t col0, const int *kofd, cudaStream_t s) {
+                               int64_t col0, const int *kofd, const uint8_t *kr, int64_t ldk,
+                               cudaStream_t s) {
   const int W = 2 * gamma + 1;
   const size_t smem = (size_t)(GK + 1) * (2 * W + 2 * SD_PADA + 2 * SD_PADB) * 8 +
                       (SD_THREADS + 4) * (8 + 4 + 4 + 4) + 32 * 4 + (size_t)(gamma + 1) * 4;
@@ -1337,7 +1348,8 @@ static int launch_short_dmma_t(const double *ul, const double *wl, int Rs, int g
   dim3 grid((unsigned)ceil_div(n, SD_TX2), (unsigned)ceil_div(planes, SD_TX1),
             (unsigned)ceil_div(nb_max, SD_BG));
   k_short_dmma<GK><<<grid, SD_THREADS, smem, s>>>(ul, wl, Rs, GK, gamma, c1, c2, zq, bstart, nb_dev,
-                                                  n, x1_lo, planes, A, lda, col0, kofd);
+                                                  n, x1_lo, planes, A, lda, col0, kofd, kr,
+                                                  ldk);
   return check_launch("short_dmma");
 }
 
@@ -1346,12 +1358,13 @@ static int launch_short_dmma(const double *ul, const double *wl, int Rs, int G, 
                              const int32_t *c1, const int32_t *c2, const double *zq,
                              const int32_t *bstart, const int32_t *nb_dev, int64_t nb_max,
                              int64_t n, int64_t x1_lo, int64_t planes, double *A, int64_t lda,
-                             int64_t col0, const int *kofd, cudaStream_t s) {
+                             int64_t col0, const int *kofd, const uint8_t *kr, int64_t ldk,
+                             cudaStream_t s) {
   switch (G) {
 #define RS_SD(R)                                                                              \
   case R:                                                                                     \
     return launch_short_dmma_t<R>(ul, wl, Rs, gamma, c1, c2, zq, bstart, nb_dev, nb_max, n, \
-                                  x1_lo, planes, A, lda, col0, kofd, s);
+                                  x1_lo, planes, A, lda, col0, kofd, kr, ldk, s);
     RS_SD(2) RS_SD(4) RS_SD(6) RS_SD(8) RS_SD(10) RS_SD(12) RS_SD(14) RS_SD(16) RS_SD(18)
     RS_SD(20) RS_SD(22) RS_SD(24)
 #undef RS_SD
@@ -1644,6 +1657,12 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
 }
 
 // workspace: A (planes*n x lda) | Bt (n x lda) | Y (planes x r2 r3) | ranges
+// x3 tile width of the short-range plane GEMM (RSB200_PLANE_BN = 32 or 64)
+static const int g_plane_bn = [] {
+  const char *e = getenv("RSB200_PLANE_BN");
+  return (e && atoi(e) == 32) ? 32 : 64;
+}();
+
 // RSB200_TUCKER_APPLY=0: the Tucker part through the plane GEMM as before
 static const bool g_tucker_apply = [] {
   const char *e = getenv("RSB200_TUCKER_APPLY");
@@ -1668,7 +1687,7 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
   const int64_t rp = round_up(std::max<int64_t>(rmax, 1), 2);
   // Yt (planes x r3p x r2p) | V2p (n x r2p) | V1p (n x r1p) | coreT (r3p r2p x r1p)
   int64_t y = with_long ? round_up((planes * rp * rp + 2 * n * rp + rp * rp * rp) * 8, 256) : 0;
-  int64_t ntiles = ceil_div(n, TilePlane::BN);
+  int64_t ntiles = ceil_div(n, PLANE_MIN_BN);
   // ranges | kofd | row-block term table (uint8, row blocks x buckets)
   int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256) +
                (with_short ? round_up(ceil_div(planes * n, TilePlane::BM) * round_up(nb_max, 16), 256)
@@ -1764,16 +1783,26 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                               (int)planes, s)))
       return st;
   }
-  const int64_t ntiles0 = ceil_div(n, TilePlane::BN);
+  const int64_t ntiles0 = ceil_div(n, PLANE_MIN_BN);
   int *kofd = (int *)((char *)ranges + round_up(ntiles0 * 4 * 8, 256));
+  const int64_t nrb = ceil_div(planes * n, TilePlane::BM), ldk = round_up(nb_max, 16);
+  uint8_t *kr = (uint8_t *)((char *)kofd + round_up((n + 1) * 4, 256));
+  const int slices = (flags >> 8) & 0xF;
   if (with_short) {
-    // per-distance live-term counts: the row builder's and the GEMM's term cuts
+    // per-distance live-term counts and the row-block term table: the row
+    // builder's and the GEMM's term cuts (the builder stores only the terms
+    // the GEMM reads; the Ozaki path reads whole bands, so it gets them all)
     k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
     if ((st = check_launch("term_prefix"))) return st;
+    k_rowblock_terms<<<grid_for(nrb * ldk, 256), 256, 0, s>>>(
+        c1, c2, bstart, nb_dev, kofd, (int)gamma, n, x1_lo, planes * n, TilePlane::BM, nrb, ldk,
+        kr);
+    if ((st = check_launch("rowblock_terms"))) return st;
     ProfScope ps(s, "short_rows");
     if ((st = launch_short_dmma(ul, wl, (int)Rs, (int)G, (int)gamma, c1, c2, zq, bstart, nb_dev,
                                 nb_max, n, x1_lo, planes, A, lda, r3p,
-                                g_row_cut ? kofd : nullptr, s)))
+                                g_row_cut ? kofd : nullptr,
+                                (g_row_cut && !slices) ? kr : nullptr, ldk, s)))
       return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
@@ -1790,7 +1819,6 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                                                      bc3, with_short ? nb_dev : nullptr, n, Bt, lda);
   if ((st = check_launch("build_bt"))) return st;
   const int64_t ntiles = ceil_div(n, TilePlane::BN);
-  const int slices = (flags >> 8) & 0xF;
   if (slices) {  // Ozaki-split FP64 on the int8 tensor cores (same tiles, same K ranges)
     k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
         bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
@@ -1802,28 +1830,25 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                            accumulate ? 1 : 0, wb + oz_off, tot - oz_off,
                            with_short ? nb_dev : nullptr, r3p, G, stream);
   }
-  const int64_t nrb = ceil_div(planes * n, TilePlane::BM), ldk = round_up(nb_max, 16);
-  uint8_t *kr = (uint8_t *)((char *)kofd + round_up((n + 1) * 4, 256));
-  if (with_short) {
-    k_rowblock_terms<<<grid_for(nrb * ldk, 256), 256, 0, s>>>(
-        c1, c2, bstart, nb_dev, kofd, (int)gamma, n, x1_lo, planes * n, TilePlane::BM, nrb, ldk,
-        kr);
-    if ((st = check_launch("rowblock_terms"))) return st;
-  }
-  dim3 grid((unsigned)ntiles, (unsigned)ceil_div(planes * n, TilePlane::BM));
+
   {
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int32_t *nbs = with_short ? nb_dev : nullptr;
-    if (accumulate) {
-      if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<true>))) return st;
-      k_gemm_plane<true><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd,
-          with_short ? kr : nullptr, ldk);
+    const uint8_t *krp = with_short ? kr : nullptr;
+    if (with_short && !with_long && g_plane_bn == 32) {
+      using T = TilePlaneN;
+      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
+      if ((st = set_smem<T>((const void *)fn))) return st;
+      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
+                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
     } else {
-      if ((st = set_smem<TilePlane>((const void *)k_gemm_plane<false>))) return st;
-      k_gemm_plane<false><<<grid, TilePlane::THREADS, TilePlane::SMEM_BYTES, s>>>(
-          A, lda, Bt, lda, out, n, planes * n, n, r3p, G, bc3, nbs, (int)gamma, kofd,
-          with_short ? kr : nullptr, ldk);
+      using T = TilePlane;
+      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
+      if ((st = set_smem<T>((const void *)fn))) return st;
+      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
+                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
     }
   }
   return check_launch("plane_gemm");
