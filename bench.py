@@ -531,15 +531,24 @@ def main():
         hbm = _hbm_peak()
         secondary = {}
         t_ms, t_n = prof["gemm_tucker"]
-        if t_n:
+        if t_n and r3 <= 32:   # k_tucker_apply: 2 r3 flops per 16 bytes moved -> HBM
             t_avg = t_ms / t_n / 1e3
             tb = 16.0 * (x1_hi - x1_lo) * n * n / (t_n / args.steps)
             secondary["tucker"] = {
-                "bound": "hbm", "kernel": ("k_tucker_apply" if r3 <= 24 else "k_gemm_plane<true>")
-                + " Tucker part accumulated into the slab (gemm_tucker)",
+                "bound": "hbm", "kernel": "k_tucker_apply Tucker part accumulated into the slab "
+                                          "(gemm_tucker)",
                 "achieved": tb / t_avg / 1e9, "peak": hbm[0], "unit": "GB/s",
                 "frac": tb / t_avg / 1e9 / hbm[0], "peak_source": hbm[1],
                 "algorithmic_bytes_per_launch": tb, "avg_launch_ms": t_avg * 1e3}
+        elif t_n:              # large r3 (C4, C5): the plane GEMM, FP64-bound
+            t_avg = t_ms / t_n / 1e3
+            tf = 2.0 * r3 * (x1_hi - x1_lo) * n * n / (t_n / args.steps)
+            secondary["tucker"] = {
+                "bound": "tensor", "kernel": "k_gemm_plane<true> Tucker part accumulated into "
+                                             "the slab (gemm_tucker)",
+                "achieved": tf / t_avg / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "frac": tf / t_avg / 1e12 / peak, "note": "2 r3 flops per grid point",
+                "algorithmic_flops_per_launch": tf, "avg_launch_ms": t_avg * 1e3}
         s_ms, s_n = prof["syrk"]
         if s_n:
             s_avg = s_ms / s_n / 1e3

@@ -180,6 +180,9 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3,
  * RS_ASM_F_READY skips that stage (A already in the workspace) */
 #define RS_ASM_F_ONLY 16
 #define RS_ASM_F_READY 32
+/* the per-distance term table (first (n+1) ints of the workspace) is already
+ * filled for this plan (ul, wl, Rs, gamma) */
+#define RS_ASM_KOFD_READY 64
 /* plane GEMM as Ozaki-split FP64 with s int8 slices (tcgen05 kind::i8), s in 6..8 */
 #define RS_ASM_OZ(s) ((s) << 8)
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax,

@@ -325,7 +325,7 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None, chain=Non
     pf = (None, None, 0, 0, 0, 0, None, None, 0, None, 0, 0, None)
     if prefetch is not None:
         plan, lo, hi, groups, out = prefetch
-        side = _side_stream()
+        side = _side_stream(n)
         rs = int(plan.local.rank)
         if out is None:
             out = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")
@@ -548,37 +548,53 @@ class AssemblyResult:
 _STREAMS: dict = {}
 
 
-def _stream(kind: str):
+def _stream(kind: str, sms: int = 0):
     """Per-device internal streams: "side" (lowest priority) carries the
-    prefetched short-range planes, "chain" (highest priority) the
-    latency-bound long-range reduction, so its small kernels are scheduled
-    ahead of the big plane GEMM's blocks."""
+    prefetched short-range planes, on an SM partition of ``sms`` SMs when
+    > 0; "chain" (highest priority) the latency-bound long-range reduction,
+    so its small kernels are scheduled ahead of the big plane GEMM's blocks."""
     torch = nat._torch()
     dev = torch.cuda.current_device()
-    st = _STREAMS.get((dev, kind))
+    st = _STREAMS.get((dev, kind, sms))
     if st is None:
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
             else (0, -1)
-        if kind == "side" and _SIDE_SMS > 0:
+        if kind == "side" and sms > 0:
             # the wide short-range kernels on an SM partition (green context):
             # the SMs outside it stay free for the latency-bound chain
             import ctypes
             ptr, got = ctypes.c_void_p(), ctypes.c_int()
-            if nat.lib().rs_partition_stream(min(_SIDE_SMS, _device_sms(dev)), int(lo),
+            if nat.lib().rs_partition_stream(min(sms, _device_sms(dev)), int(lo),
                                              ctypes.byref(ptr), ctypes.byref(got)) == 0:
                 st = torch.cuda.ExternalStream(ptr.value, device=dev)
         if st is None:
             st = torch.cuda.Stream(device=dev, priority=(hi if kind == "chain" else lo))
-        _STREAMS[(dev, kind)] = st
+        _STREAMS[(dev, kind, sms)] = st
     return st
+
+
+def _side_sms(n: int) -> int:
+    """SMs of the short-range side partition: the chain's latency-bound
+    kernels need ~20 free SMs at C2 (measured best: 128); at n >= 512 the
+    short part dominates the step and takes 140 (C4 227 -> 215 ms, C5 284 ->
+    270 ms against 128).  RSB200_SIDE_SMS overrides (0: ordinary stream)."""
+    if _SIDE_SMS is not None:
+        return _SIDE_SMS
+    return 128 if n <= 256 else 140
+
+
+def _side_streams():
+    torch = nat._torch()
+    dev = torch.cuda.current_device()
+    return [st for (d, kind, _), st in _STREAMS.items() if d == dev and kind == "side"]
 
 
 def _device_sms(dev: int) -> int:
     return nat._torch().cuda.get_device_properties(dev).multi_processor_count
 
 
-def _side_stream():
-    return _stream("side")
+def _side_stream(n: int):
+    return _stream("side", _side_sms(n))
 
 
 def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
@@ -599,7 +615,8 @@ def build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
     user = torch.cuda.current_stream()
     chain = _stream("chain")
     chain.wait_stream(user)
-    chain.wait_stream(_stream("side"))   # earlier prefetches may still read recycled memory
+    for side in _side_streams():   # earlier prefetches may still read recycled memory
+        chain.wait_stream(side)
     with torch.cuda.stream(chain):
         res = _build_rs(system, cfg, prefetch_dense, group, max(1, int(prefetch_groups)),
                         prefetch_out)
@@ -623,7 +640,7 @@ def _mark(label: str) -> None:
 
 
 # SMs of the side stream's partition (0: ordinary stream on the whole device)
-_SIDE_SMS = int(os.environ.get("RSB200_SIDE_SMS", "128"))
+_SIDE_SMS = int(os.environ["RSB200_SIDE_SMS"]) if os.environ.get("RSB200_SIDE_SMS") else None
 
 
 # the Gram + eigen block enqueued by the front call (RSB200_CHAIN=0: from _build_rs)
@@ -793,7 +810,7 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         lo, hi = (0, n) if prefetch_dense is True else (int(prefetch_dense[0]),
                                                         int(prefetch_dense[1]))
         main = torch.cuda.current_stream()
-        side = _side_stream()
+        side = _side_stream(n)
         side.wait_stream(main)
         with torch.cuda.stream(side):
             buf = torch.empty((hi - lo, n, n), dtype=torch.float64, device="cuda")

@@ -36,6 +36,9 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                        void *stream);
 }
 
+extern "C" int rsb_asm_term_prefix(const double *ul, const double *wl, int Rs, int gamma,
+                                   void *work, cudaStream_t s);
+
 namespace {
 
 enum Slot {
@@ -140,6 +143,12 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
   cudaGetDevice(&dev);
   if (!ev[dev & 63] && cudaEventCreateWithFlags(&ev[dev & 63], cudaEventDisableTiming) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_front: event");
+  const bool l0_path = rs_short_method(n, count, gamma, Rs) == RS_SHORT_L0;
+  if (!l0_path) {  // plan-only term table: ahead of the wait, overlapping the front
+    if (work_bytes < (int64_t)((n + 1) * 4))
+      return fail(RS_ERR_CAPACITY, "rs_front: workspace too small");
+    if ((st = rsb_asm_term_prefix(ul, wl, (int)Rs, (int)gamma, work, as_stream(side)))) return st;
+  }
   if (cudaEventRecord(ev[dev & 63], s) != cudaSuccess ||
       cudaStreamWaitEvent(as_stream(side), ev[dev & 63], 0) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_front: stream dependency");
@@ -156,7 +165,7 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
       return fail(RS_ERR_CUDA, "rs_front: group event");
     return RS_OK;
   };
-  if (rs_short_method(n, count, gamma, Rs) == RS_SHORT_L0) {  // dense-L0 gather, L0 in `work`
+  if (l0_path) {  // dense-L0 gather, L0 in `work`
     if (work_bytes < rs_short_l0_bytes(gamma))
       return fail(RS_ERR_CAPACITY, "rs_front: workspace %lld < L0 %lld", (long long)work_bytes,
                   (long long)rs_short_l0_bytes(gamma));
@@ -175,7 +184,7 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
     return RS_OK;
   }
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(n, count));
-  const int flags = RS_ASM_SHORT | RS_ASM_OZ(oz_slices);
+  const int flags = RS_ASM_SHORT | RS_ASM_OZ(oz_slices) | RS_ASM_KOFD_READY;
   const int64_t one = rs_assemble_workspace_bytes(n, 1, 1, nb_max, Rs, flags);
   const int64_t per = rs_assemble_workspace_bytes(n, 2, 1, nb_max, Rs, flags) - one;
   const int64_t chunk = std::max<int64_t>(

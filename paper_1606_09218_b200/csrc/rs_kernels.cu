@@ -152,6 +152,8 @@ using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
 // narrow x3 tiles for the short-range plane GEMM: the per-term bands add the
 // tile width to every term's support, so narrow terms cost ~half with BN = 32
 using TilePlaneN = Tile<128, 32, 32, 32, 3>;
+// wide x3 tiles: fewer column tiles re-read each D row block (A traffic ~ tiles x (BN + 2 gamma))
+using TilePlaneW = Tile<128, 128, 32, 32, 3>;
 constexpr int PLANE_MIN_BN = 32;  // sizes the per-column-tile workspace tables
 
 // C[m0.., n0..] = sum over the K ranges of this column tile of A B^T.
@@ -1660,8 +1662,17 @@ int rs_core(const double *TT1, const double *TT2, const double *TT3, int64_t r1,
 // x3 tile width of the short-range plane GEMM (RSB200_PLANE_BN = 32 or 64)
 static const int g_plane_bn = [] {
   const char *e = getenv("RSB200_PLANE_BN");
-  return (e && atoi(e) == 32) ? 32 : 64;
+  return (e && (atoi(e) == 32 || atoi(e) == 128)) ? atoi(e) : 64;
 }();
+
+// (internal, not part of the ABI header) the per-distance live-term table at
+// offset 0 of an rs_assemble_planes workspace (depends on the plan only:
+// rs_front fills it before its wait on the front)
+int rsb_asm_term_prefix(const double *ul, const double *wl, int Rs, int gamma, void *work,
+                        cudaStream_t s) {
+  k_term_prefix<<<1, 256, 0, s>>>(ul, wl, Rs, gamma, (int *)work);
+  return check_launch("term_prefix");
+}
 
 // RSB200_TUCKER_APPLY=0: the Tucker part through the plane GEMM as before
 static const bool g_tucker_apply = [] {
@@ -1676,8 +1687,8 @@ static const bool g_row_cut = [] {
 }();
 
 static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int64_t nb_max,
-                       int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offB,
-                       int64_t *offY, int64_t *offR, int64_t *total) {
+                       int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offA,
+                       int64_t *offB, int64_t *offY, int64_t *offR, int64_t *total) {
   const bool with_long = flags & RS_ASM_LONG, with_short = (flags & RS_ASM_SHORT) && Rs > 0;
   *r3p = with_long ? round_up(std::max<int64_t>(r3, 1), 2) : 0;
   *G = round_up(std::max<int64_t>(Rs, 1), 2);
@@ -1688,22 +1699,25 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
   // Yt (planes x r3p x r2p) | V2p (n x r2p) | V1p (n x r1p) | coreT (r3p r2p x r1p)
   int64_t y = with_long ? round_up((planes * rp * rp + 2 * n * rp + rp * rp * rp) * 8, 256) : 0;
   int64_t ntiles = ceil_div(n, PLANE_MIN_BN);
-  // ranges | kofd | row-block term table (uint8, row blocks x buckets)
-  int64_t rr = round_up(ntiles * 4 * 8, 256) + round_up((n + 1) * 4, 256) +
+  // kofd first (fixed offset 0 for every plane count: rs_front fills it ahead
+  // of the chunks) | A | Bt | Y | ranges | row-block term table (uint8)
+  const int64_t k0 = round_up((n + 1) * 4, 256);
+  int64_t rr = round_up(ntiles * 4 * 8, 256) +
                (with_short ? round_up(ceil_div(planes * n, TilePlane::BM) * round_up(nb_max, 16), 256)
                            : 0);
-  *offB = a;
-  *offY = a + b;
-  *offR = a + b + y;
-  *total = a + b + y + rr;
+  *offA = k0;
+  *offB = k0 + a;
+  *offY = k0 + a + b;
+  *offR = k0 + a + b + y;
+  *total = k0 + a + b + y + rr;
   const int slices = (flags >> 8) & 0xF;
   if (slices) *total += round_up(rs_oz_workspace_bytes(planes * n, n, *lda, slices), 256);
 }
 
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t nb_max,
                                     int64_t Rs, int flags) {
-  int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
+  int64_t lda, r3p, G, oA, oB, oY, oR, tot;
+  asm_layout(n, planes, rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
   return tot;
 }
 
@@ -1731,7 +1745,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(Rs >= 0 && Rs <= SR_MAXR, "rs_assemble_planes: Rs=%lld exceeds %d", (long long)Rs,
              SR_MAXR);
   RS_REQUIRE(gamma >= 0 && gamma < n, "rs_assemble_planes: bad gamma");
-  RS_REQUIRE(1 + TilePlane::BN + 2 * gamma < PLANE_SEGS,
+  RS_REQUIRE(1 + TilePlaneW::BN + 2 * gamma < PLANE_SEGS,
              "rs_assemble_planes: gamma=%lld too wide for the plane GEMM's segment list",
              (long long)gamma);
   RS_REQUIRE(!with_short || (c1 && c2 && zq && bstart && bc3 && nb_dev && ul && wl),
@@ -1739,8 +1753,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   RS_REQUIRE(with_long || with_short || accumulate, "rs_assemble_planes: nothing to do");
   const int64_t planes = x1_hi - x1_lo;
   const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
-  int64_t lda, r3p, G, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oB, &oY, &oR, &tot);
+  int64_t lda, r3p, G, oA, oB, oY, oR, tot;
+  asm_layout(n, planes, rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
   if (work_bytes < tot)
     return fail(RS_ERR_CAPACITY, "rs_assemble_planes: workspace %lld < %lld",
                 (long long)work_bytes, (long long)tot);
@@ -1748,7 +1762,7 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     return RS_OK;
   }
   char *wb = (char *)work;
-  double *A = (double *)wb;
+  double *A = (double *)(wb + oA);
   double *Bt = (double *)(wb + oB);
   double *Y = (double *)(wb + oY);
   int64_t *ranges = (int64_t *)(wb + oR);
@@ -1784,16 +1798,18 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       return st;
   }
   const int64_t ntiles0 = ceil_div(n, PLANE_MIN_BN);
-  int *kofd = (int *)((char *)ranges + round_up(ntiles0 * 4 * 8, 256));
+  int *kofd = (int *)wb;
   const int64_t nrb = ceil_div(planes * n, TilePlane::BM), ldk = round_up(nb_max, 16);
-  uint8_t *kr = (uint8_t *)((char *)kofd + round_up((n + 1) * 4, 256));
+  uint8_t *kr = (uint8_t *)((char *)ranges + round_up(ntiles0 * 4 * 8, 256));
   const int slices = (flags >> 8) & 0xF;
   if (with_short) {
     // per-distance live-term counts and the row-block term table: the row
     // builder's and the GEMM's term cuts (the builder stores only the terms
     // the GEMM reads; the Ozaki path reads whole bands, so it gets them all)
-    k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
-    if ((st = check_launch("term_prefix"))) return st;
+    if (!(flags & RS_ASM_KOFD_READY)) {
+      k_term_prefix<<<1, 256, 0, s>>>(ul, wl, (int)Rs, (int)gamma, kofd);
+      if ((st = check_launch("term_prefix"))) return st;
+    }
     k_rowblock_terms<<<grid_for(nrb * ldk, 256), 256, 0, s>>>(
         c1, c2, bstart, nb_dev, kofd, (int)gamma, n, x1_lo, planes * n, TilePlane::BM, nrb, ldk,
         kr);
@@ -1835,7 +1851,14 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int32_t *nbs = with_short ? nb_dev : nullptr;
     const uint8_t *krp = with_short ? kr : nullptr;
-    if (with_short && !with_long && g_plane_bn == 32) {
+    if (with_short && !with_long && g_plane_bn == 128) {
+      using T = TilePlaneW;
+      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
+      if ((st = set_smem<T>((const void *)fn))) return st;
+      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
+                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+    } else if (with_short && !with_long && g_plane_bn == 32) {
       using T = TilePlaneN;
       dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
       auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
