@@ -13,12 +13,14 @@ for r in csv.DictReader(io.StringIO(txt)):
     if r.get("Metric Name") != "gpu__time_duration.sum":
         continue
     name = r["Kernel Name"].split("(")[0].replace("void ", "")[:70]
-    if any(x in name for x in ("gemm", "fill", "l2_probe")) and not name.startswith("rsb::") \
-            and "k_" not in name:
+    # our kernels (rsb::, the anonymous-namespace k_* ones, the CUB node sort);
+    # torch's L2-flush fill and the DGEMM/L2 peak probes are not part of the step
+    if not (name.startswith("rsb::") or "::k_" in name or name.startswith("k_")
+            or name.startswith("cub::")) or "l2_probe" in name:
         continue
     v = float(r["Metric Value"])
     unit = r["Metric Unit"]
-    v = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+    v = v / 1e3 if unit in ("nsecond", "ns") else (v * 1e3 if unit in ("msecond", "ms") else v)
     tot[name] += v
     cnt[name] += 1
 S = sum(tot.values())
