@@ -154,6 +154,8 @@ using TileSyrk = Tile<64, 64, 32, 32, 3>;    // Gram (square tiles)
 using TilePlaneN = Tile<128, 32, 32, 32, 3>;
 // wide x3 tiles: fewer column tiles re-read each D row block (A traffic ~ tiles x (BN + 2 gamma))
 using TilePlaneW = Tile<128, 128, 32, 32, 3>;
+using TilePlane4 = Tile<128, 64, 32, 32, 4>;   // deeper cp.async ring
+using TilePlaneM = Tile<128, 64, 64, 32, 3>;   // 64x32 warp tiles (fewer LDS per DMMA)
 constexpr int PLANE_MIN_BN = 32;  // sizes the per-column-tile workspace tables
 
 // C[m0.., n0..] = sum over the K ranges of this column tile of A B^T.
@@ -1674,6 +1676,17 @@ int rsb_asm_term_prefix(const double *ul, const double *wl, int Rs, int gamma, v
   return check_launch("term_prefix");
 }
 
+// short-range plane GEMM tile variant (RSB200_PLANE_TILE: 0 default, 1 four
+// stages, 2 64x32 warp tiles) -- A/B measurements
+static const int g_plane_tile = [] {
+  const char *e = getenv("RSB200_PLANE_TILE");
+  return e && *e ? atoi(e) : 2;   // 64x32 warp tiles: C2 GEMM -4 %, C3 -6 %, C4 -5 %
+}();
+static const int g_tucker_tile = [] {
+  const char *e = getenv("RSB200_TUCKER_TILE");
+  return e && *e ? atoi(e) : 0;
+}();
+
 // RSB200_TUCKER_APPLY=0: the Tucker part through the plane GEMM as before
 static const bool g_tucker_apply = [] {
   const char *e = getenv("RSB200_TUCKER_APPLY");
@@ -1851,7 +1864,22 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int32_t *nbs = with_short ? nb_dev : nullptr;
     const uint8_t *krp = with_short ? kr : nullptr;
-    if (with_short && !with_long && g_plane_bn == 128) {
+    if (with_short && !with_long && g_plane_tile == 1) {
+      using T = TilePlane4;
+      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
+      if ((st = set_smem<T>((const void *)fn))) return st;
+      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
+                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+    } else if ((with_short && !with_long && g_plane_tile == 2) ||
+               (with_long && !with_short && g_tucker_tile == 2)) {
+      using T = TilePlaneM;
+      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
+      if ((st = set_smem<T>((const void *)fn))) return st;
+      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
+                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+    } else if (with_short && !with_long && g_plane_bn == 128) {
       using T = TilePlaneW;
       dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
       auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
