@@ -390,11 +390,18 @@ int orth_qr(double *Y, int64_t m, int64_t b, int64_t n, void *work, int64_t work
 }  // namespace rsb
 extern "C" {
 
+// the one-CTA CGS2 kernel keeps the block in shared memory up to ~200 KB; a
+// larger block (C3/C4: 64 x 512/1024) re-reads it from L2 for every row and
+// costs ~2.5 ms per pass at C3, where Householder QR (cuSOLVER) is faster
+static bool orth_by_qr(int64_t n, int64_t b) {
+  return b > 96 || (size_t)(n + b + 32 + b * n) * 8 > 200 * 1024;
+}
+
 int64_t rs_topeig_workspace_bytes(int64_t nmat, int64_t n, int64_t b) {
   // Q, Y (nmat*b*n each), T (nmat*b*b), Vt (nmat*b*b); b > 96: + ascending
   // Ritz values (nmat*b) + cuSOLVER workspace for the b x b Rayleigh quotients
   int64_t base = (2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024;
-  if (b > 96) {
+  if (orth_by_qr(n, b)) {
     const int64_t e = rs_eigh_workspace_bytes(nmat, b), q = orth_qr_workspace_bytes(nmat, b, n);
     if (e < 0 || q < 0) return -1;
     base += round_up(nmat * b * 8, 256) + std::max(e, q);
@@ -431,7 +438,7 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // Y = Q G (rows), orth
   for (int64_t it = 0; it < iters; ++it) {
     if ((st = gemm_batched(Q, n, b * n, G, n, n * n, Y, n, b * n, b, n, n, (int)nmat, s))) return st;
-    if (b > 96) {  // wide block: Householder QR (cuSOLVER), one thread/stream per matrix
+    if (orth_by_qr(n, b)) {  // wide / large block: Householder QR (cuSOLVER), one thread/stream per matrix
       char *qw = (char *)work + round_up((2 * nmat * b * n + 2 * nmat * b * b) * 8 + 1024, 256) +
                  round_up(nmat * b * 8, 256);
       if ((st = orth_qr(Y, nmat, b, n, qw, work_bytes - (qw - (char *)work), s))) return st;
