@@ -125,6 +125,147 @@ __global__ void __launch_bounds__(ORTH_THREADS)
     for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
 }
 
+// CGS2 with the block in shared memory and the normalisation of row i-1
+// folded into row i's first projection: row i is projected on the
+// unnormalised v_{i-1} (coefficient (v_{i-1}.x)/|v_{i-1}|^2) while the same
+// reduction pass yields |v_{i-1}|^2 and |x|^2, and v_{i-1} is scaled in the
+// update phase -- 4 barriers per row instead of 10.  A collapsed row (norm
+// <= 1e-13 of its input norm) is redone from pseudo-random directions exactly
+// as in k_orth_rows (same seeds), then the current row restarts.
+__device__ void orth_dots(const double *__restrict__ Qs, const double *__restrict__ x, int nd,
+                          int i, int64_t n, double *__restrict__ coef) {
+  // coef[j] = q_j . x (j < i); coef[i] = x . x; coef[i + 1] = q_{i-1} . q_{i-1} (nd = i + 2)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int j = warp; j < nd; j += nwarps) {
+    const double *a = j < i ? Qs + (int64_t)j * n : (j == i ? x : Qs + (int64_t)(i - 1) * n);
+    const double *c = j <= i ? x : a;
+    double d = 0.0;
+    for (int64_t e = lane; e < n; e += 32) d = fma(a[e], c[e], d);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) coef[j] = d;
+  }
+}
+
+// rows < r normalised; row r regenerated from pseudo-random directions until
+// it survives CGS2 (at most 3 attempts, as k_orth_rows), then normalised
+__device__ void orth_row_redo(double *__restrict__ Qs, int r, int64_t n, uint64_t seed,
+                              double *__restrict__ coef, double *__restrict__ red) {
+  double *v = Qs + (int64_t)r * n;
+  double nrm = 0.0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x)
+      v[e] = hash_unit(seed + 7919 * (attempt + 1), (uint64_t)(r * n + e));
+    __syncthreads();
+    double ss = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+    const double nrm0 = sqrt(block_sum(ss, red));
+    for (int pass = 0; pass < 2; ++pass) {
+      orth_dots(Qs, v, r, r, n, coef);
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+        double a = v[e];
+        for (int j = 0; j < r; ++j) a -= coef[j] * Qs[(int64_t)j * n + e];
+        v[e] = a;
+      }
+      __syncthreads();
+    }
+    ss = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += v[e] * v[e];
+    nrm = sqrt(block_sum(ss, red));
+    if (nrm > 1e-13 * nrm0 && nrm > 0.0) break;
+  }
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v[e] *= inv;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(ORTH_THREADS)
+    k_orth_rows_fused(double *__restrict__ Qall, int b, int64_t n, int64_t stride,
+                      uint64_t seed) {
+  extern __shared__ double sm[];
+  double *coef = sm;            // b + 8
+  double *red = coef + b + 8;   // 32
+  double *Qs = red + 32;        // b * n
+  double *Qg = Qall + blockIdx.x * stride;
+  for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qs[e] = Qg[e];
+  __syncthreads();
+  bool pending = false;  // row i-1 orthogonalised but not yet normalised
+  double nrm0_prev = 0.0;
+  for (int i = 0; i < b; ++i) {
+    double *v = Qs + (int64_t)i * n;
+    orth_dots(Qs, v, pending ? i + 2 : i + 1, i, n, coef);
+    __syncthreads();
+    double cprev = 0.0, inv_prev = 1.0;
+    if (pending) {
+      const double pp = coef[i + 1], nprev = sqrt(pp);
+      if (!(nprev > 1e-13 * nrm0_prev && nprev > 0.0)) {  // row i-1 collapsed (uniform)
+        __syncthreads();
+        orth_row_redo(Qs, i - 1, n, seed, coef, red);
+        pending = false;
+        --i;          // redo row i with row i-1 normalised
+        continue;
+      }
+      cprev = coef[i - 1] / pp;
+      inv_prev = 1.0 / nprev;
+    }
+    const double nrm0 = sqrt(coef[i]);
+    const int jn = pending ? i - 1 : i;  // rows already normalised
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+      double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int j = 0;
+      for (; j + 4 <= jn; j += 4) {
+        a0 -= coef[j] * Qs[(int64_t)j * n + e];
+        a1 -= coef[j + 1] * Qs[(int64_t)(j + 1) * n + e];
+        a2 -= coef[j + 2] * Qs[(int64_t)(j + 2) * n + e];
+        a3 -= coef[j + 3] * Qs[(int64_t)(j + 3) * n + e];
+      }
+      for (; j < jn; ++j) a0 -= coef[j] * Qs[(int64_t)j * n + e];
+      if (pending) {
+        double *qp = Qs + (int64_t)(i - 1) * n + e;
+        const double q = *qp;
+        a1 -= cprev * q;
+        *qp = q * inv_prev;
+      }
+      v[e] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    if (i > 0) {  // second projection (all previous rows normalised now)
+      orth_dots(Qs, v, i, i, n, coef);
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+        double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= i; j += 4) {
+          a0 -= coef[j] * Qs[(int64_t)j * n + e];
+          a1 -= coef[j + 1] * Qs[(int64_t)(j + 1) * n + e];
+          a2 -= coef[j + 2] * Qs[(int64_t)(j + 2) * n + e];
+          a3 -= coef[j + 3] * Qs[(int64_t)(j + 3) * n + e];
+        }
+        for (; j < i; ++j) a0 -= coef[j] * Qs[(int64_t)j * n + e];
+        v[e] = (a0 + a1) + (a2 + a3);
+      }
+      __syncthreads();
+    }
+    pending = true;
+    nrm0_prev = nrm0;
+  }
+  // the last row's norm
+  double ss = 0.0;
+  const double *vl = Qs + (int64_t)(b - 1) * n;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) ss += vl[e] * vl[e];
+  const double nl = sqrt(block_sum(ss, red));
+  if (!(nl > 1e-13 * nrm0_prev && nl > 0.0)) {
+    __syncthreads();
+    orth_row_redo(Qs, b - 1, n, seed, coef, red);
+  } else {
+    const double inv = 1.0 / nl;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) Qs[(int64_t)(b - 1) * n + e] *= inv;
+    __syncthreads();
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qg[e] = Qs[e];
+}
+
 // Parallel cyclic Jacobi on the B x B symmetric T (shared memory), one CTA per
 // matrix.  Each round rotates B/2 disjoint pairs (round-robin table built once
 // in shared memory); the rotations are computed by B/2 threads, then
@@ -390,6 +531,12 @@ int orth_qr(double *Y, int64_t m, int64_t b, int64_t n, void *work, int64_t work
 }  // namespace rsb
 extern "C" {
 
+// RSB200_ORTH_FUSED=0: the 10-barrier-per-row CGS2 kernel
+static const bool g_orth_fused = [] {
+  const char *e = getenv("RSB200_ORTH_FUSED");
+  return !(e && e[0] == '0');
+}();
+
 // the one-CTA CGS2 kernel keeps the block in shared memory up to ~200 KB; a
 // larger block (C3/C4: 64 x 512/1024) re-reads it from L2 for every row and
 // costs ~2.5 ms per pass at C3, where Householder QR (cuSOLVER) is faster
@@ -430,7 +577,9 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
   // request near the limit) so concurrent plane-GEMM blocks cannot co-reside
   const size_t reserve = 200 * 1024;
   size_t orth_smem = std::max<size_t>((size_t)(n + b + 32 + (q_smem ? b * n : 0)) * 8, reserve);
-  const void *orth_fn = q_smem ? (const void *)k_orth_rows<true> : (const void *)k_orth_rows<false>;
+  const void *orth_fn = q_smem ? (g_orth_fused ? (const void *)k_orth_rows_fused
+                                               : (const void *)k_orth_rows<true>)
+                               : (const void *)k_orth_rows<false>;
   if (orth_smem > 48 * 1024) {
     cudaError_t e = smem_attr(orth_fn, (int)orth_smem);
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "orth smem: %s", cudaGetErrorString(e));
@@ -445,7 +594,10 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
       std::swap(Q, Y);
       continue;
     }
-    if (q_smem)
+    if (q_smem && g_orth_fused)
+      k_orth_rows_fused<<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n,
+                                                                        777 + it);
+    else if (q_smem)
       k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
     else
       k_orth_rows<false><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
