@@ -89,19 +89,30 @@ __global__ void k_gather(const double *__restrict__ table, int64_t ld_table, int
   }
 }
 
-// Occupied shifts of each mode (c[l][s] != 0), ascending: list[l][j], and the
-// Gram's K per mode kdev[l] = count * R.  One block per mode, fixed-order scan.
-__global__ void __launch_bounds__(1024)
-    k_shift_list(const double *__restrict__ c, int64_t n, int64_t R, int32_t *__restrict__ list,
-                 int32_t *__restrict__ kdev) {
-  __shared__ int32_t wocc[32];
+// Shift-merged Gram operands of the three modes in one launch, occupied
+// shifts only (empty shifts are zero columns of the reference's A):
+// X[l][i][j*R + k] = sqrt(c[l][s]) |w_k| T[(s + i)*ld + k],  s = j-th occupied
+// shift.  The shift list is built per block: block (i, l) scans
+// the occupancy of mode l's histogram (fixed order, so every block of the
+// mode gets the same list), then writes row i of X_l over the occupied shifts
+// only; block (0, l) publishes kdev[l] = (occupied shifts) R, the K the
+// SYRK re-slices in-kernel (C2: 50 of 256 shifts occupied).
+__global__ void __launch_bounds__(256)
+    k_gram_operands_rows(const double *__restrict__ table, int64_t ld_table, int64_t n,
+                         int64_t R, const double *__restrict__ c,
+                         const double *__restrict__ wabs, int32_t *__restrict__ kdev,
+                         double *__restrict__ X, int64_t ldx) {
+  extern __shared__ int32_t s_list[];  // n
+  __shared__ int32_t wocc[8];
   __shared__ int32_t carry;
-  const int l = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i = blockIdx.x;
+  const int l = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double *cl = c + (int64_t)l * n;
   if (tid == 0) carry = 0;
   __syncthreads();
   for (int64_t base = 0; base < n; base += blockDim.x) {
     const int64_t x = base + tid;
-    const int32_t occ = (x < n && c[l * n + x] != 0.0) ? 1 : 0;
+    const int32_t occ = (x < n && cl[x] != 0.0) ? 1 : 0;
     int32_t so = occ;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -112,31 +123,18 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     int32_t po = carry;
     for (int w = 0; w < warp; ++w) po += wocc[w];
-    if (occ) list[l * n + po + so - 1] = (int32_t)x;
+    if (occ) s_list[po + so - 1] = (int32_t)x;
     __syncthreads();
     if (tid == blockDim.x - 1) carry = po + so;
     __syncthreads();
   }
-  if (tid == 0) kdev[l] = (int32_t)(carry * R);
-}
-
-// Shift-merged Gram operands of the three modes in one launch, occupied
-// shifts only (empty shifts are zero columns of the reference's A):
-// X[l][i][j*R + k] = sqrt(c[l][s]) |w_k| T[(s + i)*ld + k],  s = list[l][j]
-__global__ void k_gram_operands(const double *__restrict__ table, int64_t ld_table, int64_t n,
-                                int64_t R, const double *__restrict__ c,
-                                const double *__restrict__ wabs, const int32_t *__restrict__ list,
-                                const int32_t *__restrict__ kdev, double *__restrict__ X,
-                                int64_t ldx) {
-  const int64_t total = 3 * n * ldx;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = e / (n * ldx), rem = e - l * n * ldx;
-    const int64_t i = rem / ldx, col = rem - i * ldx;
-    if (col >= kdev[l]) continue;   // never read by the SYRK
+  const int64_t cols = (int64_t)carry * R;
+  if (i == 0 && tid == 0) kdev[l] = (int32_t)cols;
+  double *xr = X + ((int64_t)l * n + i) * ldx;
+  for (int64_t col = tid; col < cols; col += blockDim.x) {
     const int64_t j = col / R, k = col - j * R;
-    const int64_t sft = list[l * n + j];
-    X[e] = sqrt(c[l * n + sft]) * wabs[k] * table[(sft + i) * ld_table + k];
+    const int64_t sft = s_list[j];
+    xr[col] = sqrt(cl[sft]) * wabs[k] * table[(sft + i) * ld_table + k];
   }
 }
 
@@ -1523,16 +1521,13 @@ int rs_gram_shifted(const double *table, int64_t ld_table, int64_t n, int64_t R,
   const int64_t part_stride = sp * ntp * TileSyrk::BM * TileSyrk::BN;
   double *X = (double *)work;
   double *part = (double *)((char *)work + round_up(3 * n * ldx * 8, 256));
-  int32_t *list = (int32_t *)((char *)part + 3 * part_stride * 8);
-  int32_t *kdev = (int32_t *)((char *)list + round_up(3 * n * 4, 256));
+  int32_t *kdev = (int32_t *)((char *)part + 3 * part_stride * 8);
   cudaStream_t s = as_stream(stream);
   int st;
   // occupied shifts only: K per mode = (#occupied shifts) R instead of n R
   // (C2: 50 of 256 shifts, C5: 363 of 2048), known on the device
-  k_shift_list<<<3, 1024, 0, s>>>(c, n, R, list, kdev);
-  if ((st = check_launch("shift list"))) return st;
-  k_gram_operands<<<grid_for(3 * n * ldx, 256), 256, 0, s>>>(table, ld_table, n, R, c, wabs, list,
-                                                              kdev, X, ldx);
+  k_gram_operands_rows<<<dim3((unsigned)n, 3), 256, (size_t)n * 4, s>>>(table, ld_table, n, R, c,
+                                                                        wabs, kdev, X, ldx);
   if ((st = check_launch("gram operands"))) return st;
   if ((st = set_smem<TileSyrk>((const void *)k_syrk_part))) return st;
   {
