@@ -162,3 +162,26 @@ def test_oz_gemm_fp64(nat, cuda, M, N, K, slices):
     scale = np.abs(a).max(1)[:, None] * np.abs(b).max(1)[None, :]
     err = np.abs(C.cpu().numpy() - ref) / scale
     assert err.max() <= 4 * K * 2.0 ** (-7 * slices + 1), err.max()
+
+
+@pytest.mark.parametrize("n,b,rank", [(256, 24, 5), (96, 32, 1), (200, 16, 12), (64, 24, 0)])
+def test_topeig_rank_deficient(nat, cuda, n, b, rank):
+    """Exactly rank-deficient Grams (rank < b): the CGS2 block collapses row
+    by row and the restart path (fresh pseudo-random directions) must still
+    return an orthonormal Ritz block, the exact nonzero eigenvalues and zeros."""
+    from paper_1606_09218_b200.rankred import top_eig
+    rng = np.random.default_rng(100 * n + b + rank)
+    q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    lam = np.zeros(n)
+    lam[:rank] = 10.0 ** (-np.arange(rank) / 1.5)
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    ev, U, tr = top_eig(cuda.from_numpy(g[None]).cuda(), b, iters=2)
+    ev, U = ev.cpu().numpy()[0], U.cpu().numpy()[0]
+    assert np.all(np.isfinite(U)) and np.all(np.isfinite(ev))
+    assert np.allclose(U @ U.T, np.eye(b), atol=1e-12)          # orthonormal block
+    assert np.allclose(ev[:rank], lam[:rank], rtol=0, atol=1e-14)
+    assert np.all(np.abs(ev[rank:]) <= 1e-14)
+    if rank:
+        proj = np.abs(U[:rank] @ q[:, :rank])
+        assert np.allclose(np.diag(proj), 1.0, atol=1e-9)
