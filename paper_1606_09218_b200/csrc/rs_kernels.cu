@@ -1677,6 +1677,11 @@ static const int g_plane_tile = [] {
   const char *e = getenv("RSB200_PLANE_TILE");
   return e && *e ? atoi(e) : 2;   // 64x32 warp tiles: C2 GEMM -4 %, C3 -6 %, C4 -5 %
 }();
+// RSB200_PLANE_RBG: row blocks per plane-GEMM launch (0: one launch)
+static const int64_t g_plane_rbg = [] {
+  const char *e = getenv("RSB200_PLANE_RBG");
+  return (int64_t)(e && *e ? atoll(e) : 0);
+}();
 static const int g_tucker_tile = [] {
   const char *e = getenv("RSB200_TUCKER_TILE");
   return e && *e ? atoi(e) : 0;
@@ -1859,42 +1864,35 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int32_t *nbs = with_short ? nb_dev : nullptr;
     const uint8_t *krp = with_short ? kr : nullptr;
-    if (with_short && !with_long && g_plane_tile == 1) {
-      using T = TilePlane4;
-      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
+    auto launch = [&](auto tile) -> int {
+      using T = decltype(tile);
       auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
-      if ((st = set_smem<T>((const void *)fn))) return st;
-      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
-                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+      int e;
+      if ((e = set_smem<T>((const void *)fn))) return e;
+      const int64_t M = planes * n, nrb_all = ceil_div(M, T::BM);
+      // row-block groups: every launch is at most one wave, so the column tiles
+      // of a row block start together and share its D rows in L2
+      const int64_t rbg = g_plane_rbg > 0 ? g_plane_rbg : nrb_all;
+      for (int64_t rb0 = 0; rb0 < nrb_all; rb0 += rbg) {
+        const int64_t m0 = rb0 * T::BM, mg = min(M - m0, rbg * T::BM);
+        dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(mg, T::BM));
+        fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A + m0 * lda, lda, Bt, lda, out + m0 * n, n,
+                                                   mg, n, r3p, G, bc3, nbs, (int)gamma, kofd,
+                                                   krp ? krp + rb0 * ldk : nullptr, ldk);
+      }
+      return 0;
+    };
+    if (with_short && !with_long && g_plane_tile == 1) {
+      if ((st = launch(TilePlane4{}))) return st;
     } else if ((with_short && !with_long && g_plane_tile == 2) ||
                (with_long && !with_short && g_tucker_tile == 2)) {
-      using T = TilePlaneM;
-      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
-      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
-      if ((st = set_smem<T>((const void *)fn))) return st;
-      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
-                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+      if ((st = launch(TilePlaneM{}))) return st;
     } else if (with_short && !with_long && g_plane_bn == 128) {
-      using T = TilePlaneW;
-      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
-      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
-      if ((st = set_smem<T>((const void *)fn))) return st;
-      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
-                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+      if ((st = launch(TilePlaneW{}))) return st;
     } else if (with_short && !with_long && g_plane_bn == 32) {
-      using T = TilePlaneN;
-      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
-      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
-      if ((st = set_smem<T>((const void *)fn))) return st;
-      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
-                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+      if ((st = launch(TilePlaneN{}))) return st;
     } else {
-      using T = TilePlane;
-      dim3 grid((unsigned)ceil_div(n, T::BN), (unsigned)ceil_div(planes * n, T::BM));
-      auto fn = accumulate ? k_gemm_plane<T, true> : k_gemm_plane<T, false>;
-      if ((st = set_smem<T>((const void *)fn))) return st;
-      fn<<<grid, T::THREADS, T::SMEM_BYTES, s>>>(A, lda, Bt, lda, out, n, planes * n, n, r3p, G,
-                                                 bc3, nbs, (int)gamma, kofd, krp, ldk);
+      if ((st = launch(TilePlane{}))) return st;
     }
   }
   return check_launch("plane_gemm");
