@@ -180,7 +180,44 @@ __device__ void orth_row_redo(double *__restrict__ Qs, int r, int64_t n, uint64_
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(ORTH_THREADS)
+// v[e] -= sum_{j < jn} coef[j] Q_j[e] for every e < n, with P threads per
+// element (consecutive lanes) splitting the j sum and combining it by a fixed
+// xor tree; with `pending`, row im1 (= i - 1, unnormalised) is also projected
+// out with coefficient cprev and scaled by inv_prev in the same pass.
+__device__ __forceinline__ void orth_update(double *__restrict__ Qs, double *__restrict__ v,
+                                            const double *__restrict__ coef, int jn, int64_t n,
+                                            int P, bool pending, int im1, double cprev,
+                                            double inv_prev) {
+  const int part = threadIdx.x & (P - 1);
+  const int64_t stride = blockDim.x / P;
+  for (int64_t eb = 0; eb < n; eb += stride) {  // uniform trip count: the shuffles stay converged
+    const int64_t e = eb + threadIdx.x / P;
+    const bool ok = e < n;
+    double a0 = 0.0, a1 = 0.0;
+    if (ok) {
+      int j = part;
+      for (; j + P < jn; j += 2 * P) {
+        a0 -= coef[j] * Qs[(int64_t)j * n + e];
+        a1 -= coef[j + P] * Qs[(int64_t)(j + P) * n + e];
+      }
+      if (j < jn) a0 -= coef[j] * Qs[(int64_t)j * n + e];
+      if (part == 0) {
+        if (pending) {
+          double *qp = Qs + (int64_t)im1 * n + e;
+          const double q = *qp;
+          a1 -= cprev * q;
+          *qp = q * inv_prev;
+        }
+        a0 += v[e];
+      }
+    }
+    double a = a0 + a1;
+    for (int o = 1; o < P; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (ok && part == 0) v[e] = a;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
     k_orth_rows_fused(double *__restrict__ Qall, int b, int64_t n, int64_t stride,
                       uint64_t seed) {
   extern __shared__ double sm[];
@@ -190,6 +227,9 @@ __global__ void __launch_bounds__(ORTH_THREADS)
   double *Qg = Qall + blockIdx.x * stride;
   for (int64_t e = threadIdx.x; e < (int64_t)b * n; e += blockDim.x) Qs[e] = Qg[e];
   __syncthreads();
+  // threads per element in the projection updates (power of two, <= 8)
+  int P = 1;
+  while (P < 8 && (int64_t)blockDim.x >= 2 * P * n) P <<= 1;
   bool pending = false;  // row i-1 orthogonalised but not yet normalised
   double nrm0_prev = 0.0;
   for (int i = 0; i < b; ++i) {
@@ -211,40 +251,12 @@ __global__ void __launch_bounds__(ORTH_THREADS)
     }
     const double nrm0 = sqrt(coef[i]);
     const int jn = pending ? i - 1 : i;  // rows already normalised
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-      double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int j = 0;
-      for (; j + 4 <= jn; j += 4) {
-        a0 -= coef[j] * Qs[(int64_t)j * n + e];
-        a1 -= coef[j + 1] * Qs[(int64_t)(j + 1) * n + e];
-        a2 -= coef[j + 2] * Qs[(int64_t)(j + 2) * n + e];
-        a3 -= coef[j + 3] * Qs[(int64_t)(j + 3) * n + e];
-      }
-      for (; j < jn; ++j) a0 -= coef[j] * Qs[(int64_t)j * n + e];
-      if (pending) {
-        double *qp = Qs + (int64_t)(i - 1) * n + e;
-        const double q = *qp;
-        a1 -= cprev * q;
-        *qp = q * inv_prev;
-      }
-      v[e] = (a0 + a1) + (a2 + a3);
-    }
+    orth_update(Qs, v, coef, jn, n, P, pending, i - 1, cprev, inv_prev);
     __syncthreads();
     if (i > 0) {  // second projection (all previous rows normalised now)
       orth_dots(Qs, v, i, i, n, coef);
       __syncthreads();
-      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-        double a0 = v[e], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int j = 0;
-        for (; j + 4 <= i; j += 4) {
-          a0 -= coef[j] * Qs[(int64_t)j * n + e];
-          a1 -= coef[j + 1] * Qs[(int64_t)(j + 1) * n + e];
-          a2 -= coef[j + 2] * Qs[(int64_t)(j + 2) * n + e];
-          a3 -= coef[j + 3] * Qs[(int64_t)(j + 3) * n + e];
-        }
-        for (; j < i; ++j) a0 -= coef[j] * Qs[(int64_t)j * n + e];
-        v[e] = (a0 + a1) + (a2 + a3);
-      }
+      orth_update(Qs, v, coef, i, n, P, false, 0, 0.0, 1.0);
       __syncthreads();
     }
     pending = true;
@@ -273,7 +285,9 @@ __global__ void __launch_bounds__(ORTH_THREADS)
 // single phase.  B is a template parameter so every index computation is a
 // constant shift/mask.  Outputs eigenvalues sorted descending and the
 // matching eigenvectors as rows of Vt.
-constexpr int JAC_THREADS = 256;
+// launch bound; RSB200_JACOBI_THREADS = 256 or 512 (default: one pass per
+// rotation round at B = 24; C3 topeig 2.64 -> 2.47 ms, C2 0.367 -> 0.36 ms)
+constexpr int JAC_THREADS = 512;
 
 template <int B>
 __global__ void __launch_bounds__(JAC_THREADS)
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(JAC_THREADS)
         rs[i] = s;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < HALF * HALF + HALF * B; e += JAC_THREADS) {
+      for (int e = threadIdx.x; e < HALF * HALF + HALF * B; e += blockDim.x) {
         if (e < HALF * HALF) {
           const int i = e / HALF, j = e % HALF;
           const double ci = rc[i], si = rs[i], cj = rc[j], sj = rs[j];
@@ -382,7 +396,11 @@ static int launch_jacobi(const double *T, int nmat, double *evals, double *Vt, s
   cudaError_t e = smem_attr((const void *)k_jacobi<B>, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "jacobi smem: %s", cudaGetErrorString(e));
   static const int sweeps = getenv("RSB200_JACOBI_SWEEPS") ? atoi(getenv("RSB200_JACOBI_SWEEPS")) : 16;
-  k_jacobi<B><<<(unsigned)nmat, JAC_THREADS, smem, s>>>(T, evals, Vt, sweeps);
+  static const int threads = [] {
+    const char *e = getenv("RSB200_JACOBI_THREADS");
+    return e && atoi(e) == 256 ? 256 : JAC_THREADS;
+  }();
+  k_jacobi<B><<<(unsigned)nmat, threads, smem, s>>>(T, evals, Vt, sweeps);
   return check_launch("jacobi");
 }
 
@@ -536,6 +554,14 @@ static const bool g_orth_fused = [] {
   const char *e = getenv("RSB200_ORTH_FUSED");
   return !(e && e[0] == '0');
 }();
+// threads of the fused CGS2 CTA (RSB200_ORTH_THREADS = 256, 512 or 1024): the
+// extra warps take one dot product each and split the projection sums.  1024
+// measured no faster (C2 topeig 0.366 -> 0.39 ms, C3 equal): 256 stays.
+static const int g_orth_threads = [] {
+  const char *e = getenv("RSB200_ORTH_THREADS");
+  const int t = e && *e ? atoi(e) : 256;
+  return (t == 512 || t == 1024) ? t : 256;
+}();
 
 // the one-CTA CGS2 kernel keeps the block in shared memory up to ~200 KB; a
 // larger block (C3/C4: 64 x 512/1024) re-reads it from L2 for every row and
@@ -595,8 +621,8 @@ int rs_topeig(const double *G, int64_t nmat, int64_t n, int64_t b, int64_t iters
       continue;
     }
     if (q_smem && g_orth_fused)
-      k_orth_rows_fused<<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n,
-                                                                        777 + it);
+      k_orth_rows_fused<<<(unsigned)nmat, g_orth_threads, orth_smem, s>>>(Y, (int)b, n, b * n,
+                                                                          777 + it);
     else if (q_smem)
       k_orth_rows<true><<<(unsigned)nmat, ORTH_THREADS, orth_smem, s>>>(Y, (int)b, n, b * n, 777 + it);
     else
