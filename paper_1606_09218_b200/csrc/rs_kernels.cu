@@ -3,6 +3,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "rs_common.cuh"
 #include "rs_dmma.cuh"
@@ -821,6 +822,137 @@ __global__ void k_rowblock_terms(const int32_t *__restrict__ c1, const int32_t *
     }
     kr[e] = (uint8_t)(best <= gamma ? kofd[best] : 0);
   }
+}
+
+// Tucker-only plane GEMM with the A row block resident in shared memory:
+//   C[g, x3] (+)= sum_{c < K} A[g, c] Bt[x3, c]   (K = r3p <= TR_KMAX)
+// One 256-thread CTA per 128-row block walks ALL column tiles of 64: A (128 x
+// K) is staged once, the Bt chunks of every (tile, 16-column K chunk) stream
+// through one cp.async ring that never drains between tiles, and the old C
+// values of a tile are requested into registers when its first chunk starts
+// (their latency hides under the tile's MMAs), so neither the K-loop
+// prologue nor the read-modify-write epilogue stalls the DMMA pipe per tile.
+// With K ~ 132 (C5) these two bubbles cost the per-tile kernel ~40 % of peak.
+namespace tr {
+constexpr int BN = 64, BK = 16, LDB = BK + 4, STAGES = 3;
+constexpr int WM = 32, WN = 32, WARPS_N = BN / WN, MT = WM / 8, NT = WN / 8;
+constexpr int KMAX = 176;
+__host__ __device__ constexpr int threads(int bm) { return (bm / WM) * WARPS_N * 32; }
+__host__ __device__ constexpr int lda_s(int kc) { return kc * BK + 4; }  // = 4 mod 16: conflict-free fragments
+__host__ __device__ constexpr int smem_bytes(int bm, int kc) {
+  return (bm * lda_s(kc) + STAGES * BN * LDB) * 8;
+}
+}  // namespace tr
+
+// BM = 128: 8 warps, one CTA per SM; BM = 64: 4 warps, two CTAs per SM
+template <int BM, bool ACC>
+__global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
+    k_tucker_gemm_res(const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int64_t M, int64_t N,
+                      int K) {
+  using namespace tr;
+  constexpr int THREADS = threads(BM);
+  extern __shared__ __align__(16) double smem[];
+  const int KC = (K + BK - 1) / BK, LDA = lda_s(KC);
+  double *sA = smem;
+  double *sB = smem + BM * LDA;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int ntiles = (int)((N + BN - 1) / BN);
+  const int total = ntiles * KC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
+  const int gid = lane >> 2, tig = lane & 3;
+  // resident A block (zero past K and past M), first commit group with chunk 0
+  for (int e = threadIdx.x; e < BM * (KC * BK / 2); e += THREADS) {
+    const int r = e / (KC * BK / 2), kk = 2 * (e - r * (KC * BK / 2));
+    const int64_t g = m0 + r;
+    const bool ok = g < M && kk < K;
+    const int bytes = ok ? (kk + 1 < K ? 16 : 8) : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                     smem_addr(sA + r * LDA + kk)),
+                 "l"(ok ? A + g * lda + kk : A), "r"(bytes));
+  }
+  auto load_b = [&](int c) {
+    const int t = c / KC, kc = c - t * KC;
+    double *st = sB + (c % STAGES) * BN * LDB;
+#pragma unroll
+    for (int e0 = 0; e0 < BN * BK / 2; e0 += THREADS) {
+      const int e = e0 + threadIdx.x;
+      const int r = e / (BK / 2), kk = kc * BK + 2 * (e % (BK / 2));
+      const int64_t g = (int64_t)t * BN + r;
+      const bool ok = g < N && kk < K;
+      const int bytes = ok ? (kk + 1 < K ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                       smem_addr(st + r * LDB + 2 * (e % (BK / 2)))),
+                   "l"(ok ? B + g * ldb + kk : B), "r"(bytes));
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < total) load_b(s);
+    cp_async_commit();
+  }
+  double acc[MT][NT][2], cold[MT][NT][2];
+  for (int c = 0; c < total; ++c) {
+    const int t = c / KC, kc = c - t * KC;
+    if (kc == 0) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+          cold[i][j][0] = cold[i][j][1] = 0.0;
+          if (ACC) {
+            const int64_t r = m0 + wm0 + i * 8 + gid, col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
+            if (r < M && col + 1 < N) {
+              const double2 o = __ldcs(reinterpret_cast<const double2 *>(C + r * ldc + col));
+              cold[i][j][0] = o.x;
+              cold[i][j][1] = o.y;
+            } else if (r < M && col < N) {
+              cold[i][j][0] = __ldcs(C + r * ldc + col);
+            }
+          }
+        }
+    }
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (c + STAGES - 1 < total) load_b(c + STAGES - 1);
+    cp_async_commit();
+    const double *st = sB + (c % STAGES) * BN * LDB;
+    const int kv = min(BK, K - kc * BK);  // the last chunk: only its live 4-column steps
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if (kk >= kv) break;  // uniform across the CTA
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = sA[(wm0 + i * 8 + gid) * LDA + kc * BK + kk + tig];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = st[(wn0 + j * 8 + gid) * LDB + kk + tig];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_884(acc[i][j], a[i], b[j]);
+    }
+    if (kc == KC - 1) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int64_t r = m0 + wm0 + i * 8 + gid;
+        if (r >= M) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int64_t col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
+          double *p = C + r * ldc + col;
+          const double v0 = acc[i][j][0] + cold[i][j][0], v1 = acc[i][j][1] + cold[i][j][1];
+          if (col + 1 < N) {
+            __stcs(reinterpret_cast<double2 *>(p), make_double2(v0, v1));
+          } else if (col < N) {
+            __stcs(p, v0);
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
 }
 
 constexpr int PLANE_SEGS = 1024;  // segments per column tile (1 + occupied x3 in the band)
@@ -1677,6 +1809,15 @@ static const int g_plane_tile = [] {
   const char *e = getenv("RSB200_PLANE_TILE");
   return e && *e ? atoi(e) : 2;   // 64x32 warp tiles: C2 GEMM -4 %, C3 -6 %, C4 -5 %
 }();
+// RSB200_TUCKER_RES=0: the Tucker-only plane GEMM as one CTA per (row block,
+// column tile) instead of the A-resident kernel
+// (RSB200_TUCKER_RES=128: 128-row blocks, one CTA per SM; default 64-row
+// blocks, two CTAs per SM: C4 Tucker 7.18 -> 4.67 ms, C5 109.8 -> 99.7 ms)
+static const int g_tucker_res = [] {
+  const char *e = getenv("RSB200_TUCKER_RES");
+  if (e && e[0] == '0') return 0;
+  return e && atoi(e) == 128 ? 128 : 64;
+}();
 // RSB200_PLANE_RBG: row blocks per plane-GEMM launch (0: one launch)
 static const int64_t g_plane_rbg = [] {
   const char *e = getenv("RSB200_PLANE_RBG");
@@ -1882,8 +2023,28 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       }
       return 0;
     };
-    if (with_short && !with_long && g_plane_tile == 1) {
+    if (with_long && !with_short && g_tucker_res && r3p <= tr::KMAX && n % 2 == 0) {
+      // A-resident Tucker GEMM: one CTA per 128-row block over all column tiles
+      const int kc = (int)ceil_div(r3p, (int64_t)tr::BK);
+      auto go = [&](auto bm_c) -> int {
+        constexpr int BM = decltype(bm_c)::value;
+        const int smem = tr::smem_bytes(BM, kc);
+        auto fn = accumulate ? k_tucker_gemm_res<BM, true> : k_tucker_gemm_res<BM, false>;
+        cudaError_t e = smem_attr((const void *)fn, smem);
+        if (e != cudaSuccess)
+          return fail(RS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        fn<<<(unsigned)ceil_div(planes * n, (int64_t)BM), tr::threads(BM), smem, s>>>(
+            A, lda, Bt, lda, out, n, planes * n, n, (int)r3p);
+        return 0;
+      };
+      if ((st = g_tucker_res == 128 ? go(std::integral_constant<int, 128>{})
+                                    : go(std::integral_constant<int, 64>{})))
+        return st;
+    } else if ((with_short && !with_long && g_plane_tile == 1) ||
+        (with_long && !with_short && g_tucker_tile == 1)) {
       if ((st = launch(TilePlane4{}))) return st;
+    } else if (with_long && !with_short && g_tucker_tile == 3) {
+      if ((st = launch(TilePlaneW{}))) return st;
     } else if ((with_short && !with_long && g_plane_tile == 2) ||
                (with_long && !with_short && g_tucker_tile == 2)) {
       if ((st = launch(TilePlaneM{}))) return st;
