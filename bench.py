@@ -544,8 +544,8 @@ def main():
             t_avg = t_ms / t_n / 1e3
             tf = 2.0 * r3 * (x1_hi - x1_lo) * n * n / (t_n / args.steps)
             secondary["tucker"] = {
-                "bound": "tensor", "kernel": "k_gemm_plane<true> Tucker part accumulated into "
-                                             "the slab (gemm_tucker)",
+                "bound": "tensor", "kernel": "k_tucker_gemm_res<64, true> A-resident Tucker "
+                                             "GEMM accumulated into the slab (gemm_tucker)",
                 "achieved": tf / t_avg / 1e12, "peak": peak, "unit": "TFLOP/s",
                 "frac": tf / t_avg / 1e12 / peak, "note": "2 r3 flops per grid point",
                 "algorithmic_flops_per_launch": tf, "avg_launch_ms": t_avg * 1e3}

@@ -2,7 +2,7 @@
 # Round profiling pass (run on the GPU box from the repo root): bench lines,
 # reference arm, launch list and ncu --set full captures of the top kernels.
 # Numbers printed by runs under ncu are never bench values.
-TAG=${TAG:-r01d}
+TAG=${TAG:-r01f}
 O=gpurun_out
 python bench.py > $O/${TAG}_bench_C2.json 2> $O/${TAG}_bench_C2.err
 for c in C3 C4 C5; do
@@ -18,9 +18,9 @@ RSB200_SIDE_SMS=0 timeout 900 ncu --set full --clock-control none --import-sourc
   python bench.py --steps 1 --warmup 8 --no-cpu-baseline > $O/${TAG}_ncu_c2.log 2>&1
 for c in C3 C4; do
   RSB200_SIDE_SMS=0 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_gemm_plane|k_short_dmma" -s 12 -c 2 -f -o $O/${TAG}_full_$c \
+    -k regex:"k_gemm_plane|k_short_dmma|k_tucker_gemm_res" -s 12 -c 3 -f -o $O/${TAG}_full_$c \
     python bench.py --config $c --steps 1 --warmup 8 --no-cpu-baseline > $O/${TAG}_ncu_$c.log 2>&1
 done
 RSB200_SIDE_SMS=0 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_short_l0|k_gemm_plane" -s 8 -c 2 -f -o $O/${TAG}_full_C5 \
+  -k regex:"k_short_l0|k_gemm_plane|k_tucker_gemm_res" -s 8 -c 2 -f -o $O/${TAG}_full_C5 \
   python bench.py --config C5 --steps 1 --warmup 8 --no-cpu-baseline > $O/${TAG}_ncu_C5.log 2>&1
