@@ -213,6 +213,23 @@ int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32
                          const int32_t *bc3, const int32_t *nb_dev, int64_t x1_lo,
                          int64_t x1_hi, int accumulate, double *out, void *stream);
 
+/* Single-pass grid store of the low-overlap regime (formats.py:448-453,
+ * dense_rs = TuckerTensor.dense + dense_cct, the short part by the dense-L0
+ * gather): out[((x1-x1_lo)*n + x2)*n + x3] = Tucker[x] + sum_p zq_p L0[x - c_p + gamma]
+ * for x1 in [x1_lo, x1_hi), every grid value stored once.  The per-plane
+ * Tucker operands must have been formed on `work` by
+ * rs_assemble_planes(RS_ASM_LONG | RS_ASM_F_ONLY) for planes [a_lo, a_hi)
+ * containing [x1_lo, x1_hi) (same ranks, same workspace).  Bitwise equal to
+ * rs_assemble_short_l0 followed by the accumulating Tucker pass.
+ * rs_fused_l0_supported: 1 when the kernel handles (n, r3, gamma). */
+int rs_assemble_fused_l0(int64_t r1, int64_t r2, int64_t r3, const double *V3, int64_t n,
+                         const double *L0, int64_t gamma, const int32_t *c1, const int32_t *c2,
+                         const double *zq, const int32_t *bstart, const int32_t *bc3,
+                         const int32_t *nb_dev, int64_t a_lo, int64_t a_hi, int64_t x1_lo,
+                         int64_t x1_hi, double *out, void *work, int64_t work_bytes,
+                         void *stream);
+int rs_fused_l0_supported(int64_t n, int64_t r3, int64_t gamma);
+
 /* L2 read bandwidth probe: every CTA streams the first `bytes` of buf (sized
  * to fit in L2) `iters` times with L1-bypassing loads (the roofline of
  * rs_assemble_short_l0; time it with events on `stream`). */

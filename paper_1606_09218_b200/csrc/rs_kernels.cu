@@ -7,6 +7,7 @@
 
 #include "rs_common.cuh"
 #include "rs_dmma.cuh"
+#include "rs_fused.cuh"
 
 namespace rsb {
 thread_local char g_err[512] = "";
@@ -893,61 +894,75 @@ __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
     cp_async_commit();
   }
   double acc[MT][NT][2], cold[MT][NT][2];
-  for (int c = 0; c < total; ++c) {
-    const int t = c / KC, kc = c - t * KC;
-    if (kc == 0) {
+  // S k-steps of 4 columns of one staged chunk, fragments of step s+1 loaded
+  // while the DMMAs of step s issue (the LDS latency off the tensor pipe)
+  auto mma_steps = [&](const double *st, int kc, auto steps_c) {
+    constexpr int S = decltype(steps_c)::value;
+    double a[2][MT], b[2][NT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) a[0][i] = sA[(wm0 + i * 8 + gid) * LDA + kc * BK + tig];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) b[0][j] = st[(wn0 + j * 8 + gid) * LDB + tig];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (s + 1 < S) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          a[(s + 1) & 1][i] = sA[(wm0 + i * 8 + gid) * LDA + kc * BK + 4 * (s + 1) + tig];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[(s + 1) & 1][j] = st[(wn0 + j * 8 + gid) * LDB + 4 * (s + 1) + tig];
+      }
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          acc[i][j][0] = acc[i][j][1] = 0.0;
-          cold[i][j][0] = cold[i][j][1] = 0.0;
-          if (ACC) {
-            const int64_t r = m0 + wm0 + i * 8 + gid, col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
-            if (r < M && col + 1 < N) {
-              const double2 o = __ldcs(reinterpret_cast<const double2 *>(C + r * ldc + col));
-              cold[i][j][0] = o.x;
-              cold[i][j][1] = o.y;
-            } else if (r < M && col < N) {
-              cold[i][j][0] = __ldcs(C + r * ldc + col);
-            }
+        for (int j = 0; j < NT; ++j) dmma_884(acc[i][j], a[s & 1][i], b[s & 1][j]);
+    }
+  };
+  const int ksteps_last = (K - (KC - 1) * BK + 3) / 4;  // live 4-column steps of the last chunk
+  int c = 0;
+  for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        acc[i][j][0] = acc[i][j][1] = 0.0;
+        cold[i][j][0] = cold[i][j][1] = 0.0;
+        if (ACC) {
+          const int64_t r = m0 + wm0 + i * 8 + gid, col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
+          if (r < M && col + 1 < N) {
+            const double2 o = __ldcs(reinterpret_cast<const double2 *>(C + r * ldc + col));
+            cold[i][j][0] = o.x;
+            cold[i][j][1] = o.y;
+          } else if (r < M && col < N) {
+            cold[i][j][0] = __ldcs(C + r * ldc + col);
           }
         }
+      }
+    for (int kc = 0; kc < KC; ++kc, ++c) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      if (c + STAGES - 1 < total) load_b(c + STAGES - 1);
+      cp_async_commit();
+      const double *st = sB + (c % STAGES) * BN * LDB;
+      const int ks = kc == KC - 1 ? ksteps_last : 4;
+      if (ks == 4) mma_steps(st, kc, std::integral_constant<int, 4>{});
+      else if (ks == 3) mma_steps(st, kc, std::integral_constant<int, 3>{});
+      else if (ks == 2) mma_steps(st, kc, std::integral_constant<int, 2>{});
+      else mma_steps(st, kc, std::integral_constant<int, 1>{});
     }
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    if (c + STAGES - 1 < total) load_b(c + STAGES - 1);
-    cp_async_commit();
-    const double *st = sB + (c % STAGES) * BN * LDB;
-    const int kv = min(BK, K - kc * BK);  // the last chunk: only its live 4-column steps
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      if (kk >= kv) break;  // uniform across the CTA
-      double a[MT], b[NT];
+    for (int i = 0; i < MT; ++i) {
+      const int64_t r = m0 + wm0 + i * 8 + gid;
+      if (r >= M) continue;
 #pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = sA[(wm0 + i * 8 + gid) * LDA + kc * BK + kk + tig];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = st[(wn0 + j * 8 + gid) * LDB + kk + tig];
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma_884(acc[i][j], a[i], b[j]);
-    }
-    if (kc == KC - 1) {
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int64_t r = m0 + wm0 + i * 8 + gid;
-        if (r >= M) continue;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int64_t col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
-          double *p = C + r * ldc + col;
-          const double v0 = acc[i][j][0] + cold[i][j][0], v1 = acc[i][j][1] + cold[i][j][1];
-          if (col + 1 < N) {
-            __stcs(reinterpret_cast<double2 *>(p), make_double2(v0, v1));
-          } else if (col < N) {
-            __stcs(p, v0);
-          }
+      for (int j = 0; j < NT; ++j) {
+        const int64_t col = (int64_t)t * BN + wn0 + j * 8 + tig * 2;
+        double *p = C + r * ldc + col;
+        const double v0 = acc[i][j][0] + cold[i][j][0], v1 = acc[i][j][1] + cold[i][j][1];
+        if (col + 1 < N) {
+          __stcs(reinterpret_cast<double2 *>(p), make_double2(v0, v1));
+        } else if (col < N) {
+          __stcs(p, v0);
         }
       }
     }
@@ -2057,6 +2072,43 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     }
   }
   return check_launch("plane_gemm");
+}
+
+int rs_assemble_fused_l0(int64_t r1, int64_t r2, int64_t r3, const double *V3, int64_t n,
+                         const double *L0, int64_t gamma, const int32_t *c1, const int32_t *c2,
+                         const double *zq, const int32_t *bstart, const int32_t *bc3,
+                         const int32_t *nb_dev, int64_t a_lo, int64_t a_hi, int64_t x1_lo,
+                         int64_t x1_hi, double *out, void *work, int64_t work_bytes,
+                         void *stream) {
+  RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && V3 && L0 && c1 && c2 && zq && bstart && bc3 &&
+                 nb_dev && out && work,
+             "rs_assemble_fused_l0: bad arguments");
+  RS_REQUIRE(0 <= a_lo && a_lo <= x1_lo && x1_lo < x1_hi && x1_hi <= a_hi && a_hi <= n,
+             "rs_assemble_fused_l0: plane range [%lld, %lld) outside the formed operands "
+             "[%lld, %lld)", (long long)x1_lo, (long long)x1_hi, (long long)a_lo, (long long)a_hi);
+  // the workspace layout of the RS_ASM_F_ONLY call that formed A for [a_lo, a_hi)
+  const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
+  int64_t lda, r3p, G, oA, oB, oY, oR, tot;
+  asm_layout(n, a_hi - a_lo, rmax, r3, 0, 0, RS_ASM_LONG | RS_ASM_ACCUMULATE, &lda, &r3p, &G, &oA,
+             &oB, &oY, &oR, &tot);
+  if (work_bytes < tot)
+    return fail(RS_ERR_CAPACITY, "rs_assemble_fused_l0: workspace %lld < %lld",
+                (long long)work_bytes, (long long)tot);
+  RS_REQUIRE(fused_l0_supported(n, r3p, gamma), "rs_assemble_fused_l0: unsupported shape");
+  char *wb = (char *)work;
+  const double *A = (const double *)(wb + oA) + (x1_lo - a_lo) * n * lda;
+  double *Bt = (double *)(wb + oB);
+  cudaStream_t s = as_stream(stream);
+  k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(V3, (int)r3, (int)r3p, nullptr, 0, 2, 0,
+                                                     nullptr, nullptr, n, Bt, lda);
+  int st;
+  if ((st = check_launch("build_bt"))) return st;
+  return launch_fused_l0(A, lda, Bt, lda, r3p, L0, gamma, n, c1, c2, zq, bstart, bc3, nb_dev,
+                         x1_lo, x1_hi, out, s);
+}
+
+int rs_fused_l0_supported(int64_t n, int64_t r3, int64_t gamma) {
+  return fused_l0_supported(n, round_up(std::max<int64_t>(r3, 1), 2), gamma) ? 1 : 0;
 }
 
 int rs_eval_tucker(const double *core, int64_t r1, int64_t r2, int64_t r3, const double *V1,

@@ -7,18 +7,21 @@
 // separable form, paying 2 R_s flops per (point, occupied x3 bucket) on the
 // FP64 tensor cores.  When the mean window overlap is low (C5: 15 copies per
 // grid point, 363 occupied x3 values) that is ~50x the 2 flops per (point,
-// copy) pair; here every pair is one 8-byte L0 read (L2-resident: W^3 doubles,
-// 33 MB at W = 161, loaded with an L2 evict_last policy) and one DFMA, and
-// every grid point is stored once (streaming store).  Roofline: L2 load
-// bandwidth, 8 B per pair.
+// copy) pair; here every pair is one 8-byte L0 read (L2-resident, loaded with
+// an L2 evict_last policy; two x3 neighbours per 16-byte load from the pair
+// table of rs_l0.cuh, 17 MB at W = 161) and one DFMA, and every grid point is
+// stored once (streaming 16-byte stores).  Roofline: L2 load bandwidth, 8 B
+// per pair.
 //
-// A CTA owns an 8 (x1) x 16 (x2) x 128 (x3) output tile.  Its candidate copies
+// A CTA owns an 8 (x1) x 16 (x2) x 128 (x3) output tile; lane l of a warp owns
+// the x3 pairs (2l, 2l + 1) and (64 + 2l, 65 + 2l) of two rows.  Its candidate copies
 // are found from the x3-bucket layout of rs_front (bucket range by binary
 // search over bc3, x2 window by binary search inside each c2-sorted bucket,
 // x1 filter by an order-preserving block scan) and staged in shared memory;
 // the accumulation then runs plane by plane with the candidates in bucket
 // order, so results are deterministic.
 #include "rs_common.cuh"
+#include "rs_l0.cuh"
 
 #include <algorithm>
 #include <stdlib.h>
@@ -29,8 +32,8 @@ namespace {
 
 constexpr int L0_T1 = 8;                  // x1 planes per tile
 constexpr int L0_T2 = 16;                 // x2 rows per tile (8 warps x 2)
-constexpr int L0_J = 4;                   // x3 points per lane
-constexpr int L0_T3 = 32 * L0_J;          // x3 columns per tile
+constexpr int L0_J = 2;                   // x3 pairs per lane
+constexpr int L0_T3 = 64 * L0_J;          // x3 columns per tile
 constexpr int L0_THREADS = 256;
 constexpr int L0_CAP = 1024;              // staged candidates per flush
 
@@ -55,45 +58,35 @@ __device__ __forceinline__ int l0_block_scan(int v, int *wsum, int *total) {
   return base + x - v;
 }
 
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-// predicated L0 load: 0.0 (and no memory access) when !ok
-__device__ __forceinline__ double ld_l0_pred(const double *p, bool ok, uint64_t pol) {
-  double v = 0.0;
-  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
-      " @q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n}"
-      : "+d"(v)
-      : "l"(p), "r"((int)ok), "l"(pol));
-  return v;
-}
-
-// L0[(a W + b) W + c] = sum_k wl[k] ul[a,k] ul[b,k] ul[c,k]   (ul: W x Rs)
+// P[par][da][b][j] (rs_l0.cuh): sum_k wl[k] ul[g+da,k] ul[b,k] ul[c,k], c = j - 2 + par
 __global__ void k_build_l0(const double *__restrict__ ul, const double *__restrict__ wl, int Rs,
-                           int W, double *__restrict__ L0) {
-  const int64_t tot = (int64_t)W * W * W;
+                           int gamma, double *__restrict__ P) {
+  const int W = 2 * gamma + 1;
+  const int64_t tot = l0_pair_doubles(gamma);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ab = e / W;
-    const int c = (int)(e - ab * W);
-    const int a = (int)(ab / W), b = (int)(ab - (int64_t)a * W);
+    const int64_t row = e / L0_PITCH;
+    const int j = (int)(e - row * L0_PITCH);
+    const int b = (int)(row % W);
+    const int64_t pda = row / W;
+    const int par = (int)(pda / (gamma + 1));
+    const int a = gamma + (int)(pda - (int64_t)par * (gamma + 1));
+    const int c = j - 2 + par;
     double s = 0.0;
-    for (int k = 0; k < Rs; ++k) s += wl[k] * ul[a * Rs + k] * ul[b * Rs + k] * ul[c * Rs + k];
-    L0[e] = s;
+    if (c >= 0 && c < W)
+      for (int k = 0; k < Rs; ++k) s += wl[k] * ul[a * Rs + k] * ul[b * Rs + k] * ul[c * Rs + k];
+    P[e] = s;
   }
 }
 
 template <int UNROLL, int MINB>
 __global__ void __launch_bounds__(L0_THREADS, MINB)
-    k_short_l0(const double *__restrict__ L0, int W, int gamma, int64_t n,
+    k_short_l0(const double *__restrict__ P, int W, int gamma, int64_t n,
                const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp, int64_t x1_lo,
                int64_t x1_hi, int accumulate, double *__restrict__ out) {
-  __shared__ int s_c1[L0_CAP], s_c2[L0_CAP], s_c3[L0_CAP];
+  __shared__ int s_c1[L0_CAP], s_c2[L0_CAP], s_cg[L0_CAP];  // s_cg = X3 + gamma - c3
   __shared__ double s_z[L0_CAP];
   __shared__ int s_lo[L0_THREADS], s_off[L0_THREADS], s_b3[L0_THREADS];
   __shared__ int wsum[L0_THREADS / 32];
@@ -124,45 +117,49 @@ __global__ void __launch_bounds__(L0_THREADS, MINB)
   }
   __syncthreads();
   const int blo = s_br[0], bhi = s_br[1];
-  const uint64_t pol = l2_evict_last_policy();
-  // thread -> (2 rows, J columns)
+  const uint64_t pol = l0_evict_last();
+  // thread -> (2 rows, J column pairs)
   const int64_t xr0 = X2 + 2 * warp;
-  const uint64_t Wu = (uint64_t)W;
   int len = 0;
   bool first = !accumulate;
   auto flush = [&]() {
     for (int64_t x1 = X1; x1 < x1e; ++x1) {
-      double acc[2][L0_J];
+      double2 acc[2][L0_J];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int64_t x2 = xr0 + r;
 #pragma unroll
         for (int j = 0; j < L0_J; ++j) {
-          const int64_t x3 = X3 + lane + 32 * j;
-          acc[r][j] = (!first && x2 < x2e && x3 < x3e)
-                          ? __ldcs(out + ((x1 - x1_lo) * n + x2) * n + x3)
-                          : 0.0;
+          const int64_t x3 = X3 + 64 * j + 2 * lane;
+          acc[r][j] = make_double2(0.0, 0.0);
+          if (!first && x2 < x2e && x3 < x3e)   // n even: x3 + 1 < x3e too
+            acc[r][j] = __ldcs(reinterpret_cast<const double2 *>(
+                out + ((x1 - x1_lo) * n + x2) * n + x3));
         }
       }
       // branch-free body (validity as load predicates) so consecutive
-      // candidates' loads are in flight together
+      // candidates' loads are in flight together; the two rows and two
+      // column pairs of a lane are immediate offsets off one address
 #pragma unroll UNROLL
       for (int e = 0; e < len; ++e) {
-        const int a = (int)(x1 - s_c1[e]) + gamma;
-        const bool av = (unsigned)a < (unsigned)W;
+        const int da = abs((int)(x1 - s_c1[e]));
+        const int cg = s_cg[e];
         const double z = s_z[e];
-        const int c0 = (int)(X3 + lane - s_c3[e]) + gamma;
+        const int b0 = (int)xr0 - s_c2[e] + gamma;
+        const int cl = cg + 2 * lane;
+        const int par = cg & 1;
+        const bool ok0 = da <= gamma && (unsigned)(cl + 1) <= (unsigned)W;
+        const bool ok1 = da <= gamma && (unsigned)(cl + 65) <= (unsigned)W;
+        const double *p = P + l0_off(par, min(da, gamma), b0, cl, gamma);
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-          const int b = (int)(xr0 + r - s_c2[e]) + gamma;
-          const bool rv = av && (unsigned)b < (unsigned)W;
-          const double *row = L0 + ((uint64_t)(rv ? a : 0) * Wu + (uint64_t)(rv ? b : 0)) * Wu;
-#pragma unroll
-          for (int j = 0; j < L0_J; ++j) {
-            const int c = c0 + 32 * j;
-            const double v = ld_l0_pred(row + c, rv && (unsigned)c < (unsigned)W, pol);
-            acc[r][j] = fma(z, v, acc[r][j]);
-          }
+          const bool rv = (unsigned)(b0 + r) < (unsigned)W;
+          const double2 v0 = l0_ld2(p + r * L0_PITCH, rv && ok0, pol);
+          const double2 v1 = l0_ld2(p + r * L0_PITCH + 64, rv && ok1, pol);
+          acc[r][0].x = fma(z, v0.x, acc[r][0].x);
+          acc[r][0].y = fma(z, v0.y, acc[r][0].y);
+          acc[r][1].x = fma(z, v1.x, acc[r][1].x);
+          acc[r][1].y = fma(z, v1.y, acc[r][1].y);
         }
       }
 #pragma unroll
@@ -171,8 +168,9 @@ __global__ void __launch_bounds__(L0_THREADS, MINB)
         if (x2 >= x2e) continue;
 #pragma unroll
         for (int j = 0; j < L0_J; ++j) {
-          const int64_t x3 = X3 + lane + 32 * j;
-          if (x3 < x3e) __stcs(out + ((x1 - x1_lo) * n + x2) * n + x3, acc[r][j]);
+          const int64_t x3 = X3 + 64 * j + 2 * lane;
+          if (x3 < x3e)
+            __stcs(reinterpret_cast<double2 *>(out + ((x1 - x1_lo) * n + x2) * n + x3), acc[r][j]);
         }
       }
     }
@@ -231,7 +229,7 @@ __global__ void __launch_bounds__(L0_THREADS, MINB)
       if (cov) {
         s_c1[len + pos] = c1[p];
         s_c2[len + pos] = c2[p];
-        s_c3[len + pos] = s_b3[k];
+        s_cg[len + pos] = (int)(X3 + gamma) - s_b3[k];
         s_z[len + pos] = zq[p];
       }
       len += t2;
@@ -266,19 +264,18 @@ int rs_short_method(int64_t n, int64_t count, int64_t gamma, int64_t Rs) {
   const double ov = (double)count * (w / n) * (w / n) * (w / n);
   // L0 reads 8 B per (point, copy) from L2; the plane GEMM pays 2 R_s flops
   // per (point, occupied x3 bucket), so the gather wins at low overlap
-  return ov <= 64.0 ? RS_SHORT_L0 : RS_SHORT_GEMM;
+  return (ov <= 64.0 && l0_gamma_ok(gamma) && n % 2 == 0) ? RS_SHORT_L0 : RS_SHORT_GEMM;
 }
 
-int64_t rs_short_l0_bytes(int64_t gamma) {
-  const int64_t W = 2 * gamma + 1;
-  return W * W * W * 8;
-}
+int64_t rs_short_l0_bytes(int64_t gamma) { return l0_pair_doubles(gamma) * 8; }
 
 int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t gamma, double *L0,
                       void *stream) {
   RS_REQUIRE(ul && wl && L0 && Rs >= 1 && gamma >= 0, "rs_short_l0_table: bad arguments");
-  const int64_t W = 2 * gamma + 1;
-  k_build_l0<<<grid_blocks(W * W * W), 256, 0, as_stream(stream)>>>(ul, wl, (int)Rs, (int)W, L0);
+  RS_REQUIRE(l0_gamma_ok(gamma), "rs_short_l0_table: gamma=%lld exceeds the pair table",
+             (long long)gamma);
+  k_build_l0<<<grid_blocks(l0_pair_doubles(gamma)), 256, 0, as_stream(stream)>>>(ul, wl, (int)Rs,
+                                                                              (int)gamma, L0);
   return check_launch("short_l0_table");
 }
 
@@ -291,6 +288,9 @@ int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32
   RS_REQUIRE(n >= 1 && gamma >= 0 && 0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n,
              "rs_assemble_short_l0: bad plane range");
   RS_REQUIRE(2 * gamma + 1 <= 46340, "rs_assemble_short_l0: gamma too large");
+  RS_REQUIRE(n % 2 == 0, "rs_assemble_short_l0: n must be even");
+  RS_REQUIRE(l0_gamma_ok(gamma), "rs_assemble_short_l0: gamma=%lld exceeds the pair table",
+             (long long)gamma);
   dim3 grid((unsigned)ceil_div(n, L0_T3), (unsigned)ceil_div(n, L0_T2),
             (unsigned)ceil_div(x1_hi - x1_lo, L0_T1));
   RS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "rs_assemble_short_l0: grid too large");
@@ -302,12 +302,12 @@ int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32
       L0, (int)(2 * gamma + 1), (int)gamma, n, c1, c2, zq, bstart, bc3, nb_dev, x1_lo, x1_hi, \
       accumulate ? 1 : 0, out)
   switch (var) {  // RSB200_L0_VARIANT: tuning experiments (unroll, min CTAs per SM)
-    case 1: RS_L0_LAUNCH(2, 1); break;
-    case 2: RS_L0_LAUNCH(4, 1); break;
+    case 1: RS_L0_LAUNCH(2, 2); break;
+    case 2: RS_L0_LAUNCH(4, 2); break;
     case 3: RS_L0_LAUNCH(2, 4); break;
-    case 4: RS_L0_LAUNCH(8, 2); break;
-    case 5: RS_L0_LAUNCH(4, 4); break;
-    default: RS_L0_LAUNCH(4, 3); break;
+    case 4: RS_L0_LAUNCH(2, 3); break;
+    case 5: RS_L0_LAUNCH(4, 3); break;
+    default: RS_L0_LAUNCH(4, 4); break;  // C5 slab: 10.2 ms vs 10.6 (4, 3), 10.8 (2, 4)
   }
 #undef RS_L0_LAUNCH
   return check_launch("short_l0");

@@ -24,6 +24,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Optional
 
+import os
+
 import numpy as np
 
 from . import _native as nat
@@ -305,16 +307,35 @@ class CCT:
         return lay
 
 
+    def l0_supported(self) -> bool:
+        """The dense-L0 gathers fold L0 in x1 and x2: they need the local
+        factors symmetric about the window centre (always true for
+        ``assemble_short``'s window of the doubled table)."""
+        v = self._cache.get("l0_sym")
+        if v is None:
+            u = np.asarray(to_host(self.local.factors[0]))
+            g = self.gamma
+            v = self._cache["l0_sym"] = bool(u.shape[0] == 2 * g + 1 and 2 * g + 4 <= 256
+                                             and np.array_equal(u[g:], u[g::-1]))
+        return v
+
     def l0_table(self):
-        """Dense local tensor L0 (W^3, device) for the low-overlap gather,
-        built on the device from the normalised factors and cached per CCT
-        (``formats.py:432``: ``local.dense()``)."""
+        """Dense local tensor L0 for the low-overlap gather (``formats.py:432``:
+        ``local.dense()``), built on the device from the normalised factors and
+        cached per CCT, in the x1-folded two-copy pair layout of
+        ``csrc/rs_l0.cuh``: ``P[par, |a-g|, b, c + 2 - par] = L0[a, b, c]``
+        (zero margins), shape ``(2, g+1, 2g+1, 256)``."""
         t = self._cache.get("l0")
         if t is None:
             torch = nat._torch()
             lay = self.device_layout()
-            w = 2 * self.gamma + 1
-            t = torch.empty((w, w, w), dtype=torch.float64, device=lay["ul"].device)
+            if not self.l0_supported():
+                raise DomainError("the dense-L0 gather needs local factors symmetric about "
+                                  "the window centre")
+            g = self.gamma
+            t = torch.empty((2, g + 1, 2 * g + 1, 256), dtype=torch.float64,
+                            device=lay["ul"].device)
+            assert t.numel() * 8 == nat.lib().rs_short_l0_bytes(g)
             nat.check(nat.lib().rs_short_l0_table(nat.ptr(lay["ul"]), nat.ptr(lay["wl"]),
                                                   self.local.rank, self.gamma, t.data_ptr(),
                                                   nat.stream_ptr()), "rs_short_l0_table")
@@ -456,9 +477,16 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
     have_short = short is not None and short.local.rank > 0 and short.count > 0
     L = nat.lib()
     if have_short and L.rs_short_method(n, short.count, short.gamma,
-                                        short.local.rank) == nat.SHORT_L0:
-        # low window overlap: Tucker planes by the plane GEMM, then the short
-        # part as a dense-L0 gather on top (rs_assemble_short_l0)
+                                        short.local.rank) == nat.SHORT_L0 \
+            and short.l0_supported() and n % 2 == 0:
+        # low window overlap: the short part is a dense-L0 gather.  With a long
+        # part and no accumulation, both go through ONE pass that stores every
+        # grid value once (rs_assemble_fused_l0); otherwise the Tucker planes by
+        # the plane GEMM, then the gather on top (rs_assemble_short_l0)
+        if (long is not None and not accumulate and _FUSED_L0
+                and L.rs_fused_l0_supported(n, long.ranks[2], short.gamma)):
+            return _assemble_fused_l0(long, short, x1_lo, x1_hi, out, workspace_bytes,
+                                      workspace_slot)
         if long is not None:
             assemble_grid(long, None, x1_lo, x1_hi, out=out, accumulate=accumulate,
                           workspace_bytes=workspace_bytes, workspace_slot=workspace_slot)
@@ -505,6 +533,37 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
             nat.ptr(wl), rs, gamma, nat.ptr(c1), nat.ptr(c2), nat.ptr(zq), nat.ptr(bstart),
             nat.ptr(bc3), nat.ptr(nb), nb_max, p0, p1, flags, dst.data_ptr(), ws.data_ptr(),
             ws.numel(), stream), "rs_assemble_planes")
+    return out
+
+
+_FUSED_L0 = os.environ.get("RSB200_FUSED", "1") == "1"
+
+
+def _assemble_fused_l0(long: TuckerTensor, short: CCT, x1_lo: int, x1_hi: int, out,
+                       workspace_bytes: int, workspace_slot: str):
+    """Tucker + dense-L0 short part in one pass per chunk of planes: the
+    per-plane Tucker operands (``RS_ASM_F_ONLY``), then ``rs_assemble_fused_l0``."""
+    n = long.mode_sizes[0]
+    r1, r2, r3 = long.ranks
+    L = nat.lib()
+    chunk, wsb = tucker_plan(n, x1_hi - x1_lo, max(r1, r2, r3), workspace_bytes)
+    ws = nat.Workspace.get(wsb, workspace_slot)
+    core, (v1, v2, v3) = long.core, long.factors
+    lay = short.device_layout()
+    l0 = short.l0_table()
+    stream = nat.stream_ptr()
+    for p0 in range(x1_lo, x1_hi, chunk):
+        p1 = min(x1_hi, p0 + chunk)
+        nat.check(L.rs_assemble_planes(
+            core.data_ptr(), r1, r2, r3, v1.data_ptr(), v2.data_ptr(), v3.data_ptr(), n, None,
+            None, 0, 0, None, None, None, None, None, None, 0, p0, p1,
+            nat.ASM_LONG | nat.ASM_ACCUMULATE | nat.ASM_F_ONLY, out[p0 - x1_lo].data_ptr(),
+            ws.data_ptr(), ws.numel(), stream), "rs_assemble_planes")
+        nat.check(L.rs_assemble_fused_l0(
+            r1, r2, r3, v3.data_ptr(), n, nat.ptr(l0), short.gamma, nat.ptr(lay["c1"]),
+            nat.ptr(lay["c2"]), nat.ptr(lay["zq"]), nat.ptr(lay["bstart"]), nat.ptr(lay["bc3"]),
+            nat.ptr(lay["nb"]), p0, p1, p0, p1, out[p0 - x1_lo].data_ptr(), ws.data_ptr(),
+            ws.numel(), stream), "rs_assemble_fused_l0")
     return out
 
 

@@ -59,11 +59,20 @@ def test_l0_table_vs_oracle(cuda):
     system, cfg, _ = case_inputs("C2")
     res = rt.build_rs(system, cfg)
     sh = res.rs.short
-    l0 = sh.l0_table().cpu().numpy()
+    P = sh.l0_table().cpu().numpy()
     ul = np.asarray(sh.local.factors[0])
     ref = orc.local_dense(ul, np.asarray(sh.local.weights))
-    assert l0.shape == ref.shape
-    assert np.max(np.abs(l0 - ref)) <= 1e-14 * np.max(np.abs(ref))
+    # unfold the pair table: L0[a, b, c] = P[par, |a-g|, b, c + 2 - par]
+    g = sh.gamma
+    w = 2 * g + 1
+    fa = np.abs(np.arange(w) - g)
+    for par in (0, 1):
+        l0 = P[par][fa][:, :, 2 - par:2 - par + w]
+        assert l0.shape == ref.shape
+        assert np.max(np.abs(l0 - ref)) <= 1e-14 * np.max(np.abs(ref))
+    # zero margins: a 16-byte pair straddling the window edge reads zeros
+    assert not P[0][..., :2].any() and not P[0][..., 2 + w:].any()
+    assert not P[1][..., :1].any() and not P[1][..., 1 + w:].any()
 
 
 @pytest.mark.parametrize("name", ["tiny_newton", "tiny_yukawa", "C1", "C2"])
