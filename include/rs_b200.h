@@ -258,7 +258,9 @@ int rs_eval_cct(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
  *   base[j]      = sum_{p != excl} z[p] * pl(o)            (double-double)
  *   dshift[3j+a] = sum_{p != tgt} z[p] * (pl(o - e_a) - pl(o))
  * where pl(o) = sum_{k<R_l} w[k] T[n0+o0,k] T[n0+o1,k] T[n0+o2,k] / h3.
- * mode 0: energy terms (all p, incl. self), mode 1: forces (p != j). */
+ * mode 0: energy terms (all p, incl. self), mode 1: forces (p != j),
+ * mode 2: dshift[3j+a] = sum_{p != tgt} |z[p]| (|pl(o - e_a)| + |pl(o)|), the
+ * magnitude the mode-1 differences cancel from (their rounding-error scale). */
 int rs_pair_sums(const double *table, int64_t ld_table, int64_t n0,
                  const double *w, int64_t Rl, double h3,
                  const int64_t *idx, const double *z, int64_t count,

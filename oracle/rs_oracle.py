@@ -357,6 +357,22 @@ def force_fd(idx, z, table, w, split_index, h, j):
     return f
 
 
+def force_fd_scale(idx, z, table, w, split_index, h, j):
+    """Magnitude the differences of force_fd cancel from, per axis:
+    |z_j| sum_p |z_p| (|shifted| + |base|) / h (the rounding-error scale of
+    observables.py:253-256; used by the tests to state the force tolerance)."""
+    nt = split_index + 1
+    others = np.arange(idx.shape[0]) != j
+    off = idx[j] - idx[others]
+    base = np.abs(_window_values(table, w, off, nt, h))
+    s = np.empty(3)
+    for a in range(3):
+        sh = off.copy()
+        sh[:, a] -= 1
+        s[a] = abs(z[j]) * math.fsum(np.abs(z[others]) * (np.abs(_window_values(table, w, sh, nt, h)) + base)) / h
+    return s
+
+
 # ------------------------------------------------------------ full pipeline
 def prologue(kind, lam, b, n, M, split_index, delta, C0=3.0):
     h = grid_h(b, n)

@@ -20,7 +20,7 @@ from .formats import (CCT, MAX_DENSE_ELEMENTS, CanonicalTensor, RSCanonical, RST
                       eval_canonical, eval_canonical_many, eval_cct, eval_rs, eval_rs_many,
                       eval_tucker, eval_tucker_many, lookup_short, storage_report)
 from .observables import (EnergyReport, ForceVector, direct_energy, direct_force, force_fd,
-                          forces_fd, grad_long, particle_potentials, reference_energy, rs_energy)
+                          forces_fd, forces_fd_scale, grad_long, particle_potentials, reference_energy, rs_energy)
 from .particles import (Box3, Grid3, IndexedParticleSystem, ParticleSystem, generate_lattice,
                         generate_random_cluster, load_particles, save_particles,
                         separation_distance, snap_to_grid)

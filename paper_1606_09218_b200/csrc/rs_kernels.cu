@@ -1428,6 +1428,13 @@ __global__ void __launch_bounds__(PS_THREADS)
       double s0 = window_value(T, ldt, n0, w, Rl, h3, o0 - 1, o1, o2);
       double s1 = window_value(T, ldt, n0, w, Rl, h3, o0, o1 - 1, o2);
       double s2 = window_value(T, ldt, n0, w, Rl, h3, o0, o1, o2 - 1);
+      if (mode == 2) {  // condition scale of the differences: sum |z| (|shifted| + |base|)
+        const double za = fabs(z[p]);
+        acc[0] = dd_add_d(acc[0], __dmul_rn(za, fabs(s0) + fabs(b0)));
+        acc[1] = dd_add_d(acc[1], __dmul_rn(za, fabs(s1) + fabs(b0)));
+        acc[2] = dd_add_d(acc[2], __dmul_rn(za, fabs(s2) + fabs(b0)));
+        continue;
+      }
       acc[0] = dd_add_d(acc[0], __dmul_rn(z[p], __dsub_rn(s0, b0)));
       acc[1] = dd_add_d(acc[1], __dmul_rn(z[p], __dsub_rn(s1, b0)));
       acc[2] = dd_add_d(acc[2], __dmul_rn(z[p], __dsub_rn(s2, b0)));
@@ -2134,7 +2141,7 @@ int rs_eval_cct(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
 int rs_pair_sums(const double *table, int64_t ld_table, int64_t n0, const double *w, int64_t Rl,
                  double h3, const int64_t *idx, const double *z, int64_t count, const int64_t *tgt,
                  int64_t m, int mode, double *base, double *dshift, void *stream) {
-  RS_REQUIRE(Rl >= 1 && count >= 1 && m >= 0 && (mode == 0 || mode == 1) && h3 > 0,
+  RS_REQUIRE(Rl >= 1 && count >= 1 && m >= 0 && mode >= 0 && mode <= 2 && h3 > 0,
              "rs_pair_sums: bad arguments");
   if (m == 0) return RS_OK;
   k_pair_sums<<<(unsigned)m, PS_THREADS, 0, as_stream(stream)>>>(

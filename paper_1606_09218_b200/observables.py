@@ -212,6 +212,28 @@ def forces_fd(system, reference, split_index: Optional[int] = None, targets=None
     return f if device else to_host(f)
 
 
+def forces_fd_scale(system, reference, split_index: Optional[int] = None, targets=None,
+                    device: bool = False):
+    """Cancellation scale of :func:`forces_fd`, per target and axis:
+    ``|z_j| sum_{p != j} |z_p| (|pl(o - e_a)| + |pl(o)|) / h`` -- the magnitude
+    the one-sided difference ``observables.py:253-256`` cancels from.  Two
+    correctly rounded evaluations of the force (the reference's ``math.fsum``
+    and the double-double sum here) agree to a few ulp of THIS number, not of
+    the force itself; the parity tests state their tolerance against it."""
+    r_l = reference.split_index if split_index is None else int(split_index)
+    if r_l is None:
+        raise ConfigError("reference carries no split index")
+    count = system.count
+    tg = np.arange(count) if targets is None else np.asarray(targets, dtype=np.int64)
+    if tg.size and (tg.min() < 0 or tg.max() >= count):
+        raise DomainError("particle index out of range")
+    _, dsh, z = _pair_sums(system, reference, r_l, tg, 2)
+    torch = nat._torch()
+    zt = z[to_device(tg, torch.int64)].abs()
+    f = (zt[:, None] * dsh) / system.grid.h
+    return f if device else to_host(f)
+
+
 def force_fd(system, j: int, reference, split_index: Optional[int] = None,
              support_radius: Optional[float] = None) -> ForceVector:
     """Force on particle ``j`` (``observables.py:216-259``)."""

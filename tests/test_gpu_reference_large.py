@@ -1,0 +1,202 @@
+"""C3-C5 against fixtures the REFERENCE itself produced at full size
+(``tests/golden/make_golden_large.py`` imports ``rstensor`` in the build
+container; the GPU box only reads ``large.json`` / ``large_<C>.npz``).
+
+Tolerances are BASELINE's: 1e-10 of the grid max-norm on the assembled grid,
+1e-12 relative on point values, per-particle potentials and energies.  Forces
+are one-sided differences of two O(N)-term sums (``observables.py:253-256``):
+two correctly rounded evaluations agree to a few ulp of the magnitude the
+difference cancels from, ``S_ja = |z_j| sum_p |z_p| (|pl(o-e_a)| + |pl(o)|)/h``
+(``forces_fd_scale``; checked here against the oracle on a sample), so the
+force bound is 1e-12 of S -- for EVERY particle.
+
+* C3: the reference's full ``build_rs`` + ``dense_rs`` grid (moments, every
+  x1-plane's sum / abs sum / max, every (x1, x2) row sum, 4 planes, 5000
+  samples), ``eval_rs_many`` at all particle nodes + 2000 random points,
+  energies, phi and ``force_fd`` for all particles.
+* C5: the reference's ``build_rs`` (the 68.7 GB grid does not fit the build
+  container): ``eval_rs_many`` at all particle nodes + 2000 random points, the
+  long and the short part separately at 5000 points, 4 Tucker x1-planes,
+  energies, phi and ``force_fd`` for all particles.
+* C4: the reference's short part at 5000 points and ``force_fd`` on 300
+  particles (its long part needs 59 GB of side matrices; it stays pinned
+  through the oracle, ``test_gpu_large.py``).
+"""
+import json
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1606_09218_b200 as rt
+from conftest import GOLDEN, load_npz
+from oracle import rs_oracle as orc
+from paper_1606_09218_b200 import configs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GRID_TOL = 1e-10
+VAL_TOL = 1e-12
+
+
+def _meta():
+    with open(os.path.join(GOLDEN, "large.json")) as fh:
+        return json.load(fh)
+
+
+def _have(name):
+    return os.path.exists(os.path.join(GOLDEN, f"large_{name}.npz")) and name in _meta()
+
+
+@pytest.fixture(scope="module", params=["C3", "C5", "C4"])
+def ref_case(request, cuda):
+    name = request.param
+    if not _have(name):
+        pytest.skip(f"no reference fixture for {name}")
+    meta, z = _meta()[name], load_npz(f"large_{name}.npz")
+    res = rt.build_rs(configs.system(name), configs.assembly_config(name))
+    return name, meta, z, res
+
+
+def test_ranks_report_indices(ref_case):
+    import hashlib
+    name, meta, z, res = ref_case
+    assert res.gamma == meta["gamma"]
+    idx = np.ascontiguousarray(np.asarray(res.system.indices))
+    assert hashlib.sha256(idx.tobytes()).hexdigest() == meta["indices_sha"]
+    if "ranks" not in meta:
+        return
+    assert res.report["tucker_ranks"] == meta["ranks"]
+    for key in ("n", "b", "particles", "quadrature_rank", "split_index", "short_terms",
+                "raw_long_rank", "reduced", "gamma", "gamma_h", "storage_floats",
+                "storage_bound", "max_snap_displacement", "sigma"):
+        assert res.report[key] == meta["report"][key], key
+    assert np.allclose(res.report["reduction_tail_fraction"],
+                       meta["report"]["reduction_tail_fraction"], rtol=1e-6)
+
+
+def test_full_grid_vs_reference(ref_case):
+    """The whole dense_rs grid against the reference's (C3)."""
+    name, meta, z, res = ref_case
+    if "grid_max_abs" not in meta:
+        pytest.skip("the reference grid of this config does not fit the build container")
+    import torch
+    n = res.rs.grid.n
+    g = rt.dense_rs(res.rs, limit=1 << 62, device=True)
+    scale = meta["grid_max_abs"]
+    assert abs(float(g.abs().max()) - scale) <= GRID_TOL * scale
+    s = torch.as_tensor(z["sample_idx"], device="cuda")
+    got = g[s[:, 0], s[:, 1], s[:, 2]].cpu().numpy()
+    assert np.max(np.abs(got - z["sample_vals"])) <= GRID_TOL * scale
+    for key in z:
+        if key.startswith("plane_") and key.split("_")[1].isdigit():
+            p = int(key.split("_")[1])
+            assert np.max(np.abs(g[p].cpu().numpy() - z[key])) <= GRID_TOL * scale, key
+    # every (x1, x2) row: the sum over x3 of n values, each within tol
+    row = g.sum(dim=2).cpu().numpy()
+    assert np.max(np.abs(row - z["row_sum"])) <= GRID_TOL * scale * n
+    # every x1 plane: sum, abs sum, max
+    assert np.max(np.abs(g.sum(dim=(1, 2)).cpu().numpy() - z["plane_sum"])) \
+        <= GRID_TOL * scale * n * n
+    assert np.max(np.abs(g.abs().sum(dim=(1, 2)).cpu().numpy() - z["plane_abs_sum"])) \
+        <= GRID_TOL * scale * n * n
+    assert np.max(np.abs(g.abs().amax(dim=(1, 2)).cpu().numpy() - z["plane_max_abs"])) \
+        <= GRID_TOL * scale
+    assert float((g * g).sum()) == pytest.approx(meta["grid_sq_sum"], rel=1e-9)
+    assert float(g.sum()) == pytest.approx(meta["grid_sum"], rel=1e-9,
+                                           abs=1e-10 * meta["grid_abs_sum"])
+    # the long part alone at the sample points
+    lv = rt.eval_tucker_many(res.rs.long, z["sample_idx"])
+    assert np.max(np.abs(lv - z["long_sample"])) <= VAL_TOL * np.abs(z["long_sample"]).max()
+
+
+def test_point_values_all_nodes(ref_case):
+    """eval_rs_many (long + short) at every particle node + random points."""
+    name, meta, z, res = ref_case
+    if "eval_vals" not in z:
+        pytest.skip("no full point values for this config")
+    vals = rt.eval_rs_many(res.rs, z["eval_idx"])
+    ref = z["eval_vals"]
+    assert np.max(np.abs(vals - ref)) <= VAL_TOL * np.abs(ref).max()
+
+
+def test_long_and_short_parts(ref_case):
+    name, meta, z, res = ref_case
+    if "short_sample" in z:   # C5: both parts separately at the sample points
+        lv = rt.eval_tucker_many(res.rs.long, z["sample_idx"])
+        assert np.max(np.abs(lv - z["long_sample"])) <= VAL_TOL * np.abs(z["long_sample"]).max()
+        sv = np.array([rt.eval_cct(res.rs.short, i) for i in z["sample_idx"][:500]])
+        ref = z["short_sample"][:500]
+        assert np.max(np.abs(sv - ref)) <= VAL_TOL * max(np.abs(z["short_sample"]).max(), 1e-300)
+        # the same short values through the batched device path: rs - long
+        tot = rt.eval_rs_many(res.rs, z["sample_idx"])
+        scale = np.abs(z["long_sample"] + z["short_sample"]).max()
+        assert np.max(np.abs(tot - (z["long_sample"] + z["short_sample"]))) <= 2 * VAL_TOL * scale
+    elif "short_vals" in z:   # C4: the reference's short part alone
+        pts = z["short_idx"]
+        tot = rt.eval_rs_many(res.rs, pts)
+        lv = rt.eval_tucker_many(res.rs.long, pts)
+        ref = z["short_vals"]
+        scale = max(np.abs(tot).max(), np.abs(ref).max())
+        assert np.max(np.abs((tot - lv) - ref)) <= 2 * VAL_TOL * scale
+    else:
+        pytest.skip("covered by the full grid")
+
+
+def test_tucker_planes(ref_case):
+    """x1-planes of the Tucker part against the reference's own core and
+    factors contracted in numpy (C5, where no dense grid fits)."""
+    name, meta, z, res = ref_case
+    keys = [k for k in z if k.startswith("tucker_plane_")]
+    if not keys:
+        pytest.skip("covered by the full grid")
+    planes = {int(k.split("_")[2]): z[k] for k in keys}
+    scale = max(float(np.abs(v).max()) for v in planes.values())
+    for p, ref in planes.items():
+        got = rt.TuckerTensor.dense_slab(res.rs.long, p, p + 1)[0] \
+            if hasattr(rt.TuckerTensor, "dense_slab") else \
+            rt.assemble_grid(res.rs.long, None, p, p + 1).cpu().numpy()[0]
+        assert np.max(np.abs(got - ref)) <= GRID_TOL * scale, p
+
+
+def test_energies_and_potentials(ref_case):
+    name, meta, z, res = ref_case
+    if "rs_energy" not in meta:
+        pytest.skip("no energies for this config")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        e = rt.rs_energy(res.rs, res.system, res.reference)
+    assert e == pytest.approx(meta["rs_energy"], rel=VAL_TOL)
+    if "reference_energy" in meta:
+        e2 = rt.reference_energy(res.system, res.reference)
+        assert e2 == pytest.approx(meta["reference_energy"], rel=VAL_TOL)
+    phi = rt.particle_potentials(res.rs, res.system, res.reference)
+    assert np.max(np.abs(phi - z["phi"])) <= VAL_TOL * np.abs(z["phi"]).max()
+
+
+def test_forces_all_particles(ref_case):
+    name, meta, z, res = ref_case
+    if "forces" not in z:
+        pytest.skip("no forces for this config")
+    tg = z["force_idx"] if "force_idx" in z else None
+    f = rt.forces_fd(res.system, res.reference, targets=tg)
+    S = rt.forces_fd_scale(res.system, res.reference, targets=tg)
+    ref = z["forces"]
+    assert f.shape == ref.shape
+    # the scale itself against the oracle on a few particles
+    case = configs.oracle_case(name)
+    p = orc.prologue(case["kind"], case["lam"], case["b"], case["n"], case["M"],
+                     case["split_index"], case["delta"])
+    idx, _, _ = orc.snap(case["positions"], case["b"], case["n"])
+    sel = np.arange(f.shape[0])[:: max(1, f.shape[0] // 8)][:8]
+    for k in sel:
+        j = int(tg[k]) if tg is not None else int(k)
+        s_ref = orc.force_fd_scale(idx, case["charges"], p["table"], p["w"], case["split_index"],
+                                   p["h"], j)
+        assert np.allclose(S[k], s_ref, rtol=1e-10)
+    err = np.abs(f - ref) / S
+    print(f"{name}: forces on {f.shape[0]} particles, max |f - ref| / S = {err.max():.2e}, "
+          f"max |f - ref| / max|f| = {np.abs(f - ref).max() / np.abs(ref).max():.2e}, "
+          f"median S/|f| = {np.median(S / np.maximum(np.abs(ref), 1e-300)):.1e}")
+    assert err.max() <= VAL_TOL

@@ -1,5 +1,5 @@
 """Summarise ncu --set full reports: per kernel launch, duration, DRAM bytes,
-L2 hit rate, occupancy, FP64 pipe and top stall reasons (markdown rows)."""
+L2 hit rate, occupancy, DMMA / tensor pipe and top stall reasons (markdown rows)."""
 import csv
 import io
 import subprocess
@@ -14,8 +14,14 @@ WANT = {
     "launch__registers_per_thread": "regs",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm%",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem%",
-    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64pipe%",
+    # FP64 tensor math on sm_100a is DMMA: it issues on the tensor pipe's dmma
+    # sub-pipe, so sm__pipe_fp64_* / sm__inst_executed_pipe_fp64 read 0 for it
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_inst%",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe%",
+    "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active": "tensor_inst%",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe%",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64inst%",
+    "lts__t_bytes.sum": "l2_bytes",
 }
 
 
