@@ -309,6 +309,20 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
             const int32_t *bstart, const int32_t *bc3, const int32_t *nb,
             int64_t nq /* occupied x3 values if known on the host, else 0 */);
 
+/* rs_back for one rank of a sharded run: the factors and shift
+ * projections as in rs_back (replicated), but `core` receives only this
+ * rank's partial of rankred.py:151-161's sum over the K = N (R_l+1) columns --
+ * the x3 buckets [q_lo, q_hi) of the nq occupied ones on the bucket-K path,
+ * the particles [p_lo, p_hi) on the particle-K path (the path is chosen from
+ * sizes all ranks share).  The caller all-reduces `core` (r1 r2 r3 doubles). */
+int rs_back_shard(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+                  const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+                  const double *z, const double *w, int64_t count, double *Z1, double *Z2,
+                  double *Z3, double *core, void *work, int64_t work_bytes, void *stream,
+                  const int32_t *c1, const int32_t *c2, const double *zq,
+                  const int32_t *bstart, const int32_t *bc3, const int32_t *nb,
+                  int64_t nq, int64_t q_lo, int64_t q_hi, int64_t p_lo, int64_t p_hi);
+
 /* rs_back, then (after `wait_event`, a cudaEvent_t, when not NULL) the
  * Tucker part of planes [x1_lo, x1_hi) accumulated into `out` (the
  * prefetched short-range slab, (x1_hi - x1_lo) x n x n) by rs_assemble_planes

@@ -92,6 +92,9 @@ SIGNATURES = {
     "rs_back": (_i32, [_ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _ptr, _ptr, _i64,
                        _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
                        _ptr, _i64]),
+    "rs_back_shard": (_i32, [_ptr, _i64, _i64, _i64, _i64, _i64, _ptr, _i64, _i64, _ptr, _ptr, _ptr,
+                             _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _i64, _ptr, _ptr, _ptr, _ptr, _ptr,
+                             _ptr, _ptr, _i64, _i64, _i64, _i64, _i64]),
     "rs_partition_stream": (_i32, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int)]),
     "rs_oz_workspace_bytes": (_i64, [_i64, _i64, _i64, _i32]),

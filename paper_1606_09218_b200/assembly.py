@@ -470,6 +470,9 @@ def _as_device_system(system, grid: Grid3, prefetch=None, chain=None):
     if isinstance(system, IndexedParticleSystem):
         if system.grid != grid:
             raise ConfigError("particle system snapped to a different grid")
+        twin = getattr(system, "_device", None)
+        if twin is not None:   # a build_rs result handed back in: its device arrays
+            return twin, twin._cache.get("prep", {}).get("dup_key")
         torch = nat._torch()
         ds = DeviceIndexedSystem(positions=to_device(system.base.positions),
                                  charges=to_device(system.charges), grid=grid,
@@ -480,13 +483,44 @@ def _as_device_system(system, grid: Grid3, prefetch=None, chain=None):
         ds._cache["host"] = system
         return ds, None
     if isinstance(system, ParticleSystem):
-        return _front_system(system.positions, system.charges, system.box, grid, prefetch,
-                             chain)
+        ds, dup = _front_system(system.positions, system.charges, system.box, grid, prefetch,
+                                chain)
+        ds._cache["host_input"] = True
+        return ds, dup
     raise ConfigError(f"expected a particle system, got {type(system).__name__}")
 
 
+def _trusted_indexed(ds: DeviceIndexedSystem) -> IndexedParticleSystem:
+    """The reference's result type (``assembly.py:271-279``: an
+    ``IndexedParticleSystem`` with read-only numpy arrays) from the device
+    system, without re-running the host validation the device already did
+    (box containment at input, node collisions in ``rs_prep``).  The device
+    twin rides along as ``_device`` so the observables reuse its arrays."""
+    def frozen(t, dtype):
+        a = np.ascontiguousarray(to_host(t), dtype=dtype)
+        a.setflags(write=False)
+        return a
+
+    base = object.__new__(ParticleSystem)
+    object.__setattr__(base, "positions", frozen(ds.positions, np.float64))
+    object.__setattr__(base, "charges", frozen(ds.charges, np.float64))
+    object.__setattr__(base, "box", ds.box)
+    out = object.__new__(IndexedParticleSystem)
+    object.__setattr__(out, "base", base)
+    object.__setattr__(out, "grid", ds.grid)
+    object.__setattr__(out, "indices", frozen(ds.indices, np.int64))
+    object.__setattr__(out, "max_displacement", ds.max_displacement)
+    object.__setattr__(out, "_device", ds)
+    return out
+
+
 def _host_system(ds: DeviceIndexedSystem):
+    """``AssemblyResult.system``: host particle systems come back as the
+    reference's host type; device inputs stay on the device (no D2H on the
+    serving path)."""
     h = ds._cache.get("host")
+    if h is None and ds._cache.get("host_input"):
+        h = ds._cache["host"] = _trusted_indexed(ds)
     return h if h is not None else ds
 
 
@@ -701,6 +735,35 @@ def _eig_block(cfg: AssemblyConfig, n: int):
     return b, use_top, TOPEIG_ITERS, eps_, forced
 
 
+def _eig_by_mode(G, group, fn, shapes):
+    """The per-mode eigen work of a sharded run: mode l is solved by rank
+    l mod world and broadcast (one message per mode), so every rank holds
+    bitwise the same factors ("rank 0 + broadcast", spread over
+    the three modes).  ``fn`` maps a (1, n, n) Gram stack to tensors of shapes
+    ``(1,) + shapes[i]``; returns them stacked over the modes."""
+    import math as _m
+    import torch.distributed as dist
+    torch = nat._torch()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    sizes = [int(_m.prod(sh)) for sh in shapes]
+    flats = []
+    for l in range(3):
+        owner = l % world
+        if owner == rank:
+            flat = torch.cat([t.reshape(-1) for t in fn(G[l:l + 1].contiguous())])
+        else:
+            flat = torch.empty(sum(sizes), dtype=torch.float64, device="cuda")
+        flats.append(flat)
+    for l in range(3):   # after all local solves are enqueued
+        dist.broadcast(flats[l], src=dist.get_global_rank(group, l % world), group=group)
+    out = []
+    o = 0
+    for sh, m in zip(shapes, sizes):
+        out.append(torch.stack([f[o:o + m].view(sh) for f in flats]).contiguous())
+        o += m
+    return tuple(out)
+
+
 def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
               prefetch_groups: int = 1, prefetch_out=None) -> AssemblyResult:
     """Snap, project, split, reduce, package (``assembly.py:200-279``) -- device path.
@@ -847,13 +910,16 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
             pass
         elif use_top:
             _mark("grams")
-            evals, U, trace = top_eig(G, b, iters)
+            evals, U, trace = (top_eig(G, b, iters) if world == 1 else
+                               _eig_by_mode(G, group, lambda g: top_eig(g, b, iters),
+                                            [(b,), (b, n), ()]))
         else:
             # full spectra of the three modes at once (forked cuSOLVER streams),
             # values fetched with the one packed synchronisation below
             b = 0
             evals = U = trace = torch.zeros(0, dtype=torch.float64, device="cuda")
-            full = eig_desc_batched(G)
+            full = eig_desc_batched(G) if world == 1 else \
+                _eig_by_mode(G, group, eig_desc_batched, [(n,), (n, n)])
         if prefetch_pending:  # short-range planes behind the latency-bound eigen block
             launch_prefetch()
             prefetch_pending = False
@@ -936,8 +1002,10 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
         _mark("d2h")
         core = None
         fused_tucker = False
-        if world == 1:
-            # factors + projections + core in one native call (bucket-K core)
+        if world == 1 or front is not None:
+            # factors + projections + core in one native call (bucket-K core);
+            # a rank of a sharded run sums its x3 buckets (or particles) only
+            # and the r1 r2 r3 partials are all-reduced
             r1, r2, r3 = ranks
             Ub, bu = U, b
             if not (use_top and all(t is True for t in from_top)):
@@ -964,7 +1032,11 @@ def _build_rs(system, cfg: AssemblyConfig, prefetch_dense=False, group=None,
                             front["bc3"], front["nb"]) if front is not None
                            else (None,) * 6), nq_host)
             pre0 = short._cache.get("prefetch") if cfg.long_format == "tucker" else None
-            if (pre0 is not None and _TUCKER_IN_BUILD and pre0["groups"] is None
+            if world > 1:
+                q_lo, q_hi = particle_shard(nq_host, dist.get_rank(group), world)
+                nat.check(L.rs_back_shard(*back_args, q_lo, q_hi, p_lo, p_hi), "rs_back_shard")
+                sharded_sum(core, group)
+            elif (pre0 is not None and _TUCKER_IN_BUILD and pre0["groups"] is None
                     and not pre0["complete"]):
                 # back + the Tucker part of the prefetched slab in one call
                 lo, hi, buf = pre0["lo"], pre0["hi"], pre0["buf"]

@@ -326,9 +326,9 @@ __global__ void k_core_h(const double *__restrict__ TT1t, const double *__restri
 // T3[c, q*R + k] = TT3[c, n - bc3[q], k] for occupied buckets, 0 past *nb
 __global__ void k_core_t3(const double *__restrict__ TT3, int r3, int64_t n, int R,
                           const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
-                          int64_t nq, double *__restrict__ T3, int64_t ldT) {
+                          int64_t nq, double *__restrict__ T3, int64_t ldT, int q_off) {
   const int64_t tot = (int64_t)r3 * ldT;
-  const int nb = *nbp;
+  const int nb = *nbp - q_off;   // bc3 already points at bucket q_off
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / ldT, col = e - c * ldT;
@@ -365,14 +365,25 @@ int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3, i
 
 /* U: (3, b, n) Ritz rows (descending); Z_l (n, r_l) = U[l, :r_l]^T; core
  * (r1, r2, r3) of the shift-structured long part. */
-int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+}  // extern "C"
+
+// rs_back / rs_back_shard.  A shard (rank of `world`) sums only its share of
+// the core's K dimension: the x3 buckets [q_lo, q_hi) on the bucket-K path,
+// the particles [p_lo, p_hi) on the particle-K path (which of the two runs
+// depends only on sizes every rank agrees on).  q_lo < 0: everything.
+static int back_impl(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
             const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
             const double *z, const double *w, int64_t count, double *Z1, double *Z2, double *Z3,
             double *core, void *work, int64_t work_bytes, void *stream,
             const int32_t *c1, const int32_t *c2, const double *zq, const int32_t *bstart,
-            const int32_t *bc3, const int32_t *nb, int64_t nq_host) {
+            const int32_t *bc3, const int32_t *nb, int64_t nq_host, int64_t q_lo, int64_t q_hi,
+            int64_t p_lo, int64_t p_hi) {
   RS_REQUIRE(r1 >= 1 && r2 >= 1 && r3 >= 1 && r1 <= b && r2 <= b && r3 <= b && n >= 2,
              "rs_back: bad ranks");
+  const bool shard = q_lo >= 0;
+  RS_REQUIRE(!shard || (q_lo <= q_hi && q_hi <= std::max<int64_t>(nq_host, 0) && 0 <= p_lo &&
+                        p_lo <= p_hi && p_hi <= count),
+             "rs_back_shard: bad shard bounds");
   if (work_bytes < rs_back_workspace_bytes(n, r1, r2, r3, count, R, nq_host))
     return fail(RS_ERR_CAPACITY, "rs_back: workspace too small");
   cudaStream_t s = as_stream(stream);
@@ -389,9 +400,29 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
   // the particle-K Khatri-Rao GEMM is latency-bound and cheap below ~1e10
   // flops (C1-C3); the bucket-K form wins once N R_l r1 r2 r3 dominates (C4, C5)
   const double kr_flops = 2.0 * (double)r1 * r2 * r3 * (double)count * R;
-  if (!bstart || nq_host <= 0 || R > CH_RMAX || kr_flops < 1e10 || r2 > 1024)
-    return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
-                   rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
+  if (!bstart || nq_host <= 0 || R > CH_RMAX || kr_flops < 1e10 || r2 > 1024) {
+    if (!shard)
+      return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
+                     rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
+    if (p_hi == p_lo) {  // empty particle shard: a zero partial
+      if (cudaMemsetAsync(core, 0, (size_t)(r1 * r2 * r3) * 8, s) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "rs_back_shard: memset");
+      return RS_OK;
+    }
+    return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts + 3 * p_lo, z + p_lo, w, p_hi - p_lo,
+                   core, cw, rs_core_workspace_bytes(r1, r2, r3, p_hi - p_lo, R), stream);
+  }
+  if (shard) {  // this rank's buckets: the tables are indexed from q_lo
+    if (q_hi == q_lo) {
+      if (cudaMemsetAsync(core, 0, (size_t)(r1 * r2 * r3) * 8, s) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "rs_back_shard: memset");
+      return RS_OK;
+    }
+    bstart += q_lo;
+    bc3 += q_lo;
+    nq_host = q_hi - q_lo;
+  }
+  const int q_off = shard ? (int)q_lo : 0;
   // bucket-K core: H (r1 r2 x nq R) on CUDA cores, then one DMMA GEMM
   // nq_host: the occupied x3 count the host read back (0: the upper bound)
   const int64_t nq = nq_host > 0 ? nq_host : std::min<int64_t>(n, count), ldH = ldh_of(nq, R);
@@ -414,9 +445,33 @@ int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64
       TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq, bstart, H, ldH);
   if ((st = check_launch("core_h"))) return st;
   k_core_t3<<<(unsigned)std::min<int64_t>(ceil_div(r3 * ldH, 256), 4096), 256, 0, s>>>(
-      TT3, (int)r3, n, (int)R, bc3, nb, nq, T3, ldH);
+      TT3, (int)r3, n, (int)R, bc3, nb, nq, T3, ldH, q_off);
   if ((st = check_launch("core_t3"))) return st;
   return rs_gemm_nt(H, ldH, T3, ldH, core, r3, r1 * r2, r3, ldH, stream);
+}
+
+extern "C" {
+int rs_back(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+            const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+            const double *z, const double *w, int64_t count, double *Z1, double *Z2, double *Z3,
+            double *core, void *work, int64_t work_bytes, void *stream,
+            const int32_t *c1, const int32_t *c2, const double *zq, const int32_t *bstart,
+            const int32_t *bc3, const int32_t *nb, int64_t nq_host) {
+  return back_impl(U, b, n, r1, r2, r3, table, ld_table, R, starts, z, w, count, Z1, Z2, Z3, core,
+                   work, work_bytes, stream, c1, c2, zq, bstart, bc3, nb, nq_host, -1, -1, 0, 0);
+}
+
+int rs_back_shard(const double *U, int64_t b, int64_t n, int64_t r1, int64_t r2, int64_t r3,
+                  const double *table, int64_t ld_table, int64_t R, const int64_t *starts,
+                  const double *z, const double *w, int64_t count, double *Z1, double *Z2,
+                  double *Z3, double *core, void *work, int64_t work_bytes, void *stream,
+                  const int32_t *c1, const int32_t *c2, const double *zq, const int32_t *bstart,
+                  const int32_t *bc3, const int32_t *nb, int64_t nq_host, int64_t q_lo,
+                  int64_t q_hi, int64_t p_lo, int64_t p_hi) {
+  RS_REQUIRE(q_lo >= 0, "rs_back_shard: bad shard bounds");
+  return back_impl(U, b, n, r1, r2, r3, table, ld_table, R, starts, z, w, count, Z1, Z2, Z3, core,
+                   work, work_bytes, stream, c1, c2, zq, bstart, bc3, nb, nq_host, q_lo, q_hi,
+                   p_lo, p_hi);
 }
 
 /* rs_back, then (after `wait_event` when given) the Tucker part of planes

@@ -80,6 +80,7 @@ def _long_values(rs, indices):
 
 def _system_arrays(system):
     torch = nat._torch()
+    system = getattr(system, "_device", system)   # host result of build_rs: its device twin
     return to_device(system.indices, torch.int64), to_device(system.charges)
 
 

@@ -99,3 +99,33 @@ def test_explicit_operand_api(cuda):
     d1 = t.dense(limit=1 << 30)
     d2 = res.rs.long.dense(limit=1 << 30)
     assert np.max(np.abs(d1 - d2)) <= 1e-11 * np.abs(d2).max()
+
+
+def test_result_system_is_reference_type(cuda):
+    """Host input -> AssemblyResult.system is the reference's host type
+    (``assembly.py:271-279``): an IndexedParticleSystem with read-only numpy
+    arrays that numpy code and a second build_rs accept unchanged."""
+    rng = np.random.default_rng(6)
+    pos = rng.uniform(-6, 6, (40, 3))
+    q = rng.uniform(-1, 1, 40)
+    cfg = cfg_for()
+    system = rt.ParticleSystem(pos, q, cfg.grid.box)
+    res = rt.build_rs(system, cfg)
+    s = res.system
+    assert isinstance(s, rt.IndexedParticleSystem)
+    assert isinstance(s.indices, np.ndarray) and s.indices.dtype == np.int64
+    assert not s.indices.flags.writeable and not s.base.positions.flags.writeable
+    host = rt.snap_to_grid(system, cfg.grid)
+    assert np.array_equal(s.indices, host.indices)
+    assert np.array_equal(s.base.positions, host.base.positions)
+    assert np.array_equal(s.charges, host.charges)
+    assert s.max_displacement == host.max_displacement
+    assert s.count == 40 and s.grid == cfg.grid
+    # numpy code on the result, as reference users write it
+    assert np.all(np.abs(s.grid.position(s.indices) - s.base.positions) == 0)
+    # and it feeds back into the API (indexed input path)
+    res2 = rt.build_rs(s, cfg)
+    assert res2.report["tucker_ranks"] == res.report["tucker_ranks"]
+    e1 = rt.reference_energy(s, res.reference)
+    e2 = rt.reference_energy(host, res.reference)
+    assert e1 == e2

@@ -167,3 +167,14 @@ def test_rank_rule_fast_matches_scalar_rule():
                 if ref[0] is not None:
                     assert got[1] == (float(ref[2][ref[0]]) if ref[0] < b else 0.0)
                     assert got[2] == ref[3]
+
+
+def test_kernels_module_alias():
+    """``from rstensor.kernels import ...`` ports by renaming the package."""
+    from paper_1606_09218_b200 import kernels, quadrature
+    from paper_1606_09218_b200.kernels import (DEFAULT_R_RANGE, QuadratureRule, RadialKernel,  # noqa: F401
+                                               ReferenceCanonical, build_quadrature,
+                                               effective_support, eval_expansion, project_kernel,
+                                               split_rank, split_tensor)
+    assert project_kernel is quadrature.project_kernel
+    assert kernels.RadialKernel is rt.RadialKernel
