@@ -204,10 +204,26 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3,
  * forces one).  Reference: formats.py:423-445 (dense_cct). */
 #define RS_SHORT_GEMM 0
 #define RS_SHORT_L0 1
+#define RS_SHORT_MMA 2
 int rs_short_method(int64_t n, int64_t count, int64_t gamma, int64_t Rs);
 int64_t rs_short_l0_bytes(int64_t gamma);
 int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
                       double *L0, void *stream);
+/* (a13) dense_cct, formats.py:423-445, as ONE fused FP64 tensor-core kernel
+ * (RS_SHORT_MMA): per 8 x 16 x 64 output tile a GEMM over (x3 bucket, term)
+ * columns whose A fragments are formed in registers from shared-memory staged
+ * 1-D factors (outer products summed over the bucket's copies near the tile)
+ * and whose B fragments are gathered from the same table; nothing but the
+ * grid goes to HBM.  work: rs_short_mma_workspace_bytes(gamma).  flags:
+ * RS_ASM_ACCUMULATE adds to `out`; RS_ASM_KOFD_READY: the per-distance term
+ * table at offset 0 of `work` is already filled. */
+int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs);
+int64_t rs_short_mma_workspace_bytes(int64_t gamma);
+int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
+                          int64_t n, const int32_t *c1, const int32_t *c2, const double *zq,
+                          const int32_t *bstart, const int32_t *bc3, const int32_t *nb_dev,
+                          int64_t x1_lo, int64_t x1_hi, int flags, double *out, void *work,
+                          int64_t work_bytes, void *stream);
 int rs_assemble_short_l0(const double *L0, int64_t gamma, int64_t n, const int32_t *c1,
                          const int32_t *c2, const double *zq, const int32_t *bstart,
                          const int32_t *bc3, const int32_t *nb_dev, int64_t x1_lo,

@@ -65,6 +65,10 @@ SIGNATURES = {
                                     _ptr, _ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _i64,
                                     _ptr]),
     "rs_fused_l0_supported": (_i32, [_i64, _i64, _i64]),
+    "rs_short_mma_supported": (_i32, [_i64, _i64, _i64]),
+    "rs_short_mma_workspace_bytes": (_i64, [_i64]),
+    "rs_assemble_short_mma": (_i32, [_ptr, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr,
+                                     _ptr, _i64, _i64, _i32, _ptr, _ptr, _i64, _ptr]),
     "rs_short_l0_bytes": (_i64, [_i64]),
     "rs_short_l0_table": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr]),
     "rs_assemble_short_l0": (_i32, [_ptr, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr, _i64,
@@ -166,7 +170,7 @@ def stream_ptr() -> int:
 
 ASM_LONG, ASM_SHORT, ASM_ACCUMULATE = 1, 2, 4
 ASM_F_ONLY, ASM_F_READY, ASM_KOFD_READY = 16, 32, 64
-SHORT_GEMM, SHORT_L0 = 0, 1   # rs_short_method: plane GEMM or dense-L0 gather
+SHORT_GEMM, SHORT_L0, SHORT_MMA = 0, 1, 2   # rs_short_method: plane GEMM, dense-L0 gather, fused DMMA
 # short-range plane GEMM as Ozaki-split FP64 on the int8 tensor cores with this
 # many slices (0: FP64 DMMA); RSB200_OZ_SLICES overrides
 OZ_SLICES = int(os.environ.get("RSB200_OZ_SLICES", "0"))

@@ -143,7 +143,8 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
   cudaGetDevice(&dev);
   if (!ev[dev & 63] && cudaEventCreateWithFlags(&ev[dev & 63], cudaEventDisableTiming) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_front: event");
-  const bool l0_path = rs_short_method(n, count, gamma, Rs) == RS_SHORT_L0;
+  const int method = rs_short_method(n, count, gamma, Rs);
+  const bool l0_path = method == RS_SHORT_L0;
   if (!l0_path) {  // plan-only term table: ahead of the wait, overlapping the front
     if (work_bytes < (int64_t)((n + 1) * 4))
       return fail(RS_ERR_CAPACITY, "rs_front: workspace too small");
@@ -178,6 +179,19 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
                                      (const int32_t *)P(F_BSTART), (const int32_t *)P(F_BC3),
                                      (const int32_t *)P(F_NB), p0, p1, 0,
                                      out + (p0 - x1_lo) * n * n, side)) ||
+          (st = mark(p1)))
+        return st;
+    }
+    return RS_OK;
+  }
+  if (method == RS_SHORT_MMA) {  // fused tensor-core kernel, term table at work[0]
+    for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += grp) {
+      const int64_t p1 = std::min<int64_t>(x1_hi, p0 + grp);
+      if ((st = rs_assemble_short_mma(ul, wl, Rs, gamma, n, (const int32_t *)P(F_C1),
+                                      (const int32_t *)P(F_C2), (const double *)P(F_ZQ),
+                                      (const int32_t *)P(F_BSTART), (const int32_t *)P(F_BC3),
+                                      (const int32_t *)P(F_NB), p0, p1, RS_ASM_KOFD_READY,
+                                      out + (p0 - x1_lo) * n * n, work, work_bytes, side)) ||
           (st = mark(p1)))
         return st;
     }

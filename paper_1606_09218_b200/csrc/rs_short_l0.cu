@@ -240,11 +240,12 @@ __global__ void __launch_bounds__(L0_THREADS, MINB)
   if (len > 0 || first) flush();
 }
 
-int short_l0_env() {  // RSB200_SHORT=gemm|l0 forces a method (tests, tuning)
+int short_l0_env() {  // RSB200_SHORT=gemm|l0|mma forces a method (tests, tuning)
   const char *e = getenv("RSB200_SHORT");
   if (!e) return -1;
-  if (!strcmp(e, "l0")) return 1;
-  if (!strcmp(e, "gemm")) return 0;
+  if (!strcmp(e, "mma")) return RS_SHORT_MMA;
+  if (!strcmp(e, "l0")) return RS_SHORT_L0;
+  if (!strcmp(e, "gemm")) return RS_SHORT_GEMM;
   return -1;
 }
 
@@ -258,7 +259,8 @@ extern "C" {
 int rs_short_method(int64_t n, int64_t count, int64_t gamma, int64_t Rs) {
   if (n < 1 || count < 1 || gamma < 0 || Rs < 1) return RS_SHORT_GEMM;
   const int forced = short_l0_env();
-  if (forced >= 0) return forced ? RS_SHORT_L0 : RS_SHORT_GEMM;
+  if (forced == RS_SHORT_MMA && rs_short_mma_supported(n, gamma, Rs)) return RS_SHORT_MMA;
+  if (forced == RS_SHORT_L0 || forced == RS_SHORT_GEMM) return forced;
   // mean number of windows covering a grid point (clipped at the grid)
   const double w = (double)std::min<int64_t>(2 * gamma + 1, n);
   const double ov = (double)count * (w / n) * (w / n) * (w / n);

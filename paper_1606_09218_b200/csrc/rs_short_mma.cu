@@ -1,0 +1,423 @@
+// Short-range agglomeration fused onto the FP64 tensor cores
+// (formats.py:423-445, dense_cct):
+//
+//   P_short[x] = sum_p z_p sum_k wl_k ul_k[x1-c1p+g] ul_k[x2-c2p+g] ul_k[x3-c3p+g]
+//
+// Output-stationary: a CTA owns an 8 (x1) x 16 (x2) x 64 (x3) tile and, for it,
+// the GEMM  C[(x1,x2), x3] = sum_col A[(x1,x2), col] B[x3, col]  whose columns
+// are (x3 bucket s, term k) pairs:
+//
+//   A[(x1,x2),(s,k)] = sum_{p in bucket s near the tile} z_p v_k[x1-c1p] v_k[x2-c2p]
+//   B[x3,(s,k)]      = v_k[x3-s],            v_k = cbrt(wl_k) ul_k (zero off the window)
+//
+// Neither operand ever exists in memory.  The per-particle 1-D factors v_k are
+// staged once per CTA in shared memory (k-major, zero margins, pitch = 4 mod 16
+// doubles so the fragment gathers below are bank-conflict free); every lane
+// forms its own mma.m8n8k4 A fragment -- the outer product of the staged
+// factors summed over the bucket's candidate copies, 1 DMUL + 2 DFMA per copy
+// against the 16 DMMAs (4096 FMAs) the fragment feeds -- and gathers its B
+// fragment straight from the same table.  Warp w owns plane x1 = X0 + w, so
+// the x1 factor is one value per (copy, term) and lane; there is no operand
+// staging, no barrier and no cp.async pipeline inside the K loop.
+//
+// Sparsity (the same 1e-18 drop rule as the plane GEMM's bands, k_term_prefix):
+// a copy contributes term k to a tile only when the tile lies within g_k cells
+// of it in all three coordinates; terms are ordered widest first, so copy p
+// brings its first kofd[Chebyshev distance(tile, p)] terms and a bucket's
+// column count is the maximum over its copies.  Buckets without a copy near
+// the tile cost nothing.
+//
+// Candidates come from rs_front's x3-bucket layout (bucket range by binary
+// search over bc3, x2 window by binary search in the c2-sorted bucket, x1
+// filter + order-preserving block scan), are staged SM_CAP at a time and
+// consumed in bucket order: deterministic.  CTAs are persistent (the factor
+// table is staged once) and take tiles from an atomic counter, x3 fastest.
+// Roofline: FP64 tensor pipe (DMMA); algorithmic work 2 flops per (grid
+// point, covering copy) pair.
+#include "rs_common.cuh"
+#include "rs_dmma.cuh"
+
+#include <algorithm>
+#include <stdlib.h>
+#include <string.h>
+
+extern "C" int rsb_asm_term_prefix(const double *ul, const double *wl, int Rs, int gamma,
+                                   void *work, cudaStream_t s);  // rs_kernels.cu
+
+namespace rsb {
+namespace {
+
+constexpr int SM_T1 = 8;       // x1 planes per tile = warps per CTA
+constexpr int SM_T2 = 16;      // x2 rows per tile (2 MMA row groups)
+constexpr int SM_T3 = 64;      // x3 columns per tile (8 MMA column groups)
+constexpr int SM_THREADS = 256;
+constexpr int SM_PAD = 64;     // zero margin of the factor table, >= every tile edge
+constexpr int SM_CAP = 512;    // staged candidate copies per MMA phase
+constexpr int SM_MAXR = 24;    // largest short rank
+
+__host__ __device__ inline int sm_pitch(int gamma) {
+  int ld = 2 * gamma + 1 + 2 * SM_PAD;
+  while (ld % 16 != 4) ++ld;
+  return ld;
+}
+
+struct SmLayout {
+  int table, pk, z, cb, seg, grp, kofd, total;  // byte offsets
+};
+
+__host__ __device__ inline SmLayout sm_layout(int gamma, int Rs) {
+  SmLayout L;
+  int o = 0;
+  L.table = o; o += Rs * sm_pitch(gamma) * 8;
+  L.z = o;     o += SM_CAP * 8;
+  L.pk = o;    o += SM_CAP * 4;
+  L.cb = o;    o += (SM_CAP + 2) * 4;            // + sentinel, keeps the int2 array 8-aligned
+  L.seg = o;   o += (SM_CAP + 1) * 8;            // int2 per segment (+ sentinel)
+  L.grp = o;   o += 3 * SM_THREADS * 4 + 64;     // per-bucket lo / offset / x3 of a group
+  L.kofd = o;  o += (gamma + 2) * 4;
+  L.total = (o + 15) & ~15;
+  return L;
+}
+
+__device__ __forceinline__ int sm_block_scan(int v, int *wsum, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < SM_THREADS / 32; ++w) {
+    if (w < warp) base += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return base + x - v;
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(SM_THREADS, 2)
+    k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
+                int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+                const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+                const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
+                const int *__restrict__ kofd_g, int64_t x1_lo, int64_t x1_hi,
+                int *__restrict__ counter, double *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const SmLayout L = sm_layout(gamma, Rs);
+  double *ut = (double *)(sm_raw + L.table);
+  double *s_z = (double *)(sm_raw + L.z);
+  int *s_pk = (int *)(sm_raw + L.pk);
+  int *s_cb = (int *)(sm_raw + L.cb);
+  int2 *s_seg = (int2 *)(sm_raw + L.seg);   // .x = first staged copy | columns before << 16
+                                            // .y = column count | (B offset << 8)
+  int *s_lo = (int *)(sm_raw + L.grp);
+  int *s_off = s_lo + SM_THREADS;
+  int *s_b3 = s_off + SM_THREADS;
+  int *skofd = (int *)(sm_raw + L.kofd);
+  __shared__ int wsum[SM_THREADS / 32];
+  __shared__ int s_band[2], s_tile, s_segk[SM_CAP];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int W = 2 * gamma + 1, LD = sm_pitch(gamma);
+  const int nb = *nbp;
+  // x1 tiles sit on absolute multiples of SM_T1, so a slab's values do not
+  // depend on where the slab starts (same candidates, same term cuts, same sums)
+  const int64_t x1_base = x1_lo - x1_lo % SM_T1;
+  const int n3t = (int)((n + SM_T3 - 1) / SM_T3), n2t = (int)((n + SM_T2 - 1) / SM_T2);
+  const int64_t ntiles = (int64_t)n3t * n2t * ((x1_hi - x1_base + SM_T1 - 1) / SM_T1);
+
+  // the factor table, once per CTA: v_k[d] = cbrt(wl_k) ul[d, k] inside the
+  // window, zero in the margins
+  for (int e = tid; e < Rs * LD; e += SM_THREADS) ut[e] = 0.0;
+  for (int d = tid; d <= gamma; d += SM_THREADS) skofd[d] = kofd_g[d];
+  __syncthreads();
+  for (int e = tid; e < Rs * W; e += SM_THREADS) {   // coalesced read of ul (W x Rs)
+    const int d = e / Rs, k = e - d * Rs;
+    ut[k * LD + SM_PAD + d] = cbrt(wl[k]) * ul[e];
+  }
+
+  for (;;) {
+    __syncthreads();   // previous tile done with the staging arrays; table complete
+    if (tid == 0) s_tile = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int t3 = (int)(tile % n3t), t2 = (int)((tile / n3t) % n2t);
+    const int64_t t1 = tile / ((int64_t)n3t * n2t);
+    const int X0 = (int)(x1_base + t1 * SM_T1), Y0 = t2 * SM_T2, Z0 = t3 * SM_T3;
+
+    double acc[2][8][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // one MMA phase over the staged copies [0, len): segments = runs of equal
+    // bucket, column count = max live terms of the run's copies
+    auto flush = [&](int len) {
+      __syncthreads();
+      if (tid == 0) s_cb[len] = -1;
+      for (int i = tid; i < SM_CAP; i += SM_THREADS) s_segk[i] = 0;
+      __syncthreads();
+      int nseg = 0;
+      for (int i0 = 0; i0 < len; i0 += SM_THREADS) {   // segment starts
+        const int i = i0 + tid;
+        const bool start = i < len && (i == 0 || s_cb[i] != s_cb[i - 1]);
+        int tot;
+        const int pos = sm_block_scan(start ? 1 : 0, wsum, &tot);
+        if (start) s_seg[nseg + pos].x = i;
+        nseg += tot;
+      }
+      if (tid == 0) s_seg[nseg].x = len;
+      __syncthreads();
+      for (int i = tid; i < len; i += SM_THREADS) {    // copy -> its segment (binary search)
+        int l = 0, h = nseg;
+        while (h - l > 1) {
+          const int m = (l + h) >> 1;
+          if (s_seg[m].x <= i) l = m; else h = m;
+        }
+        atomicMax(&s_segk[l], s_pk[i] >> 24);
+        if (s_seg[l].x == i) s_seg[l].y = s_cb[i] << 8;   // B offset of the bucket (<= 12 bits)
+      }
+      __syncthreads();
+      int ncol = 0;
+      for (int i0 = 0; i0 < nseg; i0 += SM_THREADS) {  // column prefix
+        const int i = i0 + tid;
+        const int K = i < nseg ? s_segk[i] : 0;
+        int tot;
+        const int pre = sm_block_scan(K, wsum, &tot);
+        if (i < nseg) {
+          s_seg[i].x |= (ncol + pre) << 16;
+          s_seg[i].y |= K;
+        }
+        ncol += tot;
+      }
+      if (tid == 0) s_seg[nseg].x |= ncol << 16;
+      __syncthreads();
+      const int steps = (ncol + 3) >> 2;
+      int si = 0;
+      for (int st = 0; st < steps; ++st) {
+        const int c = 4 * st + tig;
+        double a0 = 0.0, a1 = 0.0, b[8];
+        if (c < ncol) {
+          while ((int)((unsigned)s_seg[si + 1].x >> 16) <= c) ++si;
+          const int2 sg = s_seg[si];
+          const int k = c - (int)((unsigned)sg.x >> 16);
+          const int q_lo = sg.x & 0xFFFF, q_hi = s_seg[si + 1].x & 0xFFFF;
+          const double *uk = ut + k * LD;
+          for (int q = q_lo; q < q_hi; ++q) {
+            const int pk = s_pk[q];
+            if (k < (pk >> 24)) {
+              const double t = s_z[q] * uk[(pk & 0xFFF) + warp];
+              const double *u2 = uk + ((pk >> 12) & 0xFFF) + gid;
+              a0 = fma(t, u2[0], a0);
+              a1 = fma(t, u2[8], a1);
+            }
+          }
+          const double *ub = uk + (sg.y >> 8) + gid;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[j] = ub[8 * j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[j] = 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          dmma_884(acc[0][j], a0, b[j]);
+          dmma_884(acc[1][j], a1, b[j]);
+        }
+      }
+    };
+
+    // candidate copies of this tile, bucket group by bucket group
+    if (tid == 0) {
+      const int lo_x = Z0 - gamma, hi_x = Z0 + SM_T3 - 1 + gamma;
+      int l = 0, h = nb;
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (bc3[m] < lo_x) l = m + 1; else h = m;
+      }
+      s_band[0] = l;
+      h = nb;
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (bc3[m] <= hi_x) l = m + 1; else h = m;
+      }
+      s_band[1] = l;
+    }
+    __syncthreads();
+    const int blo = s_band[0], bhi = s_band[1];
+    const int c1lo = X0 - gamma, c1hi = X0 + SM_T1 - 1 + gamma;
+    const int c2lo = Y0 - gamma, c2hi = Y0 + SM_T2 - 1 + gamma;
+    int len = 0;
+    for (int g = blo; g < bhi; g += SM_THREADS) {
+      const int bi = g + tid;
+      int lo = 0, cnt = 0, b3 = 0;
+      if (bi < bhi) {  // the bucket's copies whose x2 window meets the tile (c2 ascending)
+        const int p_lo = bstart[bi], p_hi = bstart[bi + 1];
+        b3 = bc3[bi];
+        int l = p_lo, h = p_hi;
+        while (l < h) {
+          const int m = (l + h) >> 1;
+          if (c2[m] < c2lo) l = m + 1; else h = m;
+        }
+        lo = l;
+        h = p_hi;
+        while (l < h) {
+          const int m = (l + h) >> 1;
+          if (c2[m] <= c2hi) l = m + 1; else h = m;
+        }
+        cnt = l - lo;
+      }
+      int tot;
+      const int off = sm_block_scan(cnt, wsum, &tot);
+      s_lo[tid] = lo;
+      s_off[tid] = off;
+      s_b3[tid] = b3;
+      const int nbk = min(SM_THREADS, bhi - g);
+      __syncthreads();
+      for (int cs = 0; cs < tot; cs += SM_THREADS) {
+        if (len > SM_CAP - SM_THREADS) {   // uniform
+          flush(len);
+          __syncthreads();
+          len = 0;
+        }
+        const int v = cs + tid;
+        bool cov = false;
+        int pk = 0, bo = 0;
+        double z = 0.0;
+        if (v < tot) {   // last bucket with offset <= v (empty buckets share offsets)
+          int l = 0, h = nbk;
+          while (h - l > 1) {
+            const int m = (l + h) >> 1;
+            if (s_off[m] <= v) l = m; else h = m;
+          }
+          const int p = s_lo[l] + (v - s_off[l]);
+          const int a1 = c1[p];
+          if (a1 >= c1lo && a1 <= c1hi) {
+            const int a2 = c2[p], a3 = s_b3[l];
+            const int d1 = max(0, max(X0 - a1, a1 - (X0 + SM_T1 - 1)));
+            const int d2 = max(0, max(Y0 - a2, a2 - (Y0 + SM_T2 - 1)));
+            const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
+            const int kn = skofd[max(d1, max(d2, d3))];
+            if (kn > 0) {
+              cov = true;
+              z = zq[p];
+              pk = (X0 - a1 + gamma + SM_PAD) | ((Y0 - a2 + gamma + SM_PAD) << 12) | (kn << 24);
+              bo = Z0 - a3 + gamma + SM_PAD;   // B offset: identifies the bucket as well
+            }
+          }
+        }
+        int t2;
+        const int pos = sm_block_scan(cov ? 1 : 0, wsum, &t2);
+        if (cov) {
+          s_pk[len + pos] = pk;
+          s_z[len + pos] = z;
+          s_cb[len + pos] = bo;
+        }
+        len += t2;
+      }
+      __syncthreads();
+    }
+    if (len > 0) flush(len);
+
+    // epilogue: every grid point of the tile is written once
+    const int64_t x1 = X0 + warp;
+    if (x1 >= x1_lo && x1 < x1_hi) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int64_t x2 = Y0 + 8 * i + gid;
+        if (x2 >= n) continue;
+        double *row = out + ((x1 - x1_lo) * n + x2) * n + Z0 + 2 * tig;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t x3 = Z0 + 8 * j + 2 * tig;
+          double v0 = acc[i][j][0], v1 = acc[i][j][1];
+          if (x3 + 1 < n) {
+            double2 *p = reinterpret_cast<double2 *>(row + 8 * j);
+            if (ACC) {
+              const double2 o = __ldcs(p);
+              v0 += o.x;
+              v1 += o.y;
+            }
+            __stcs(p, make_double2(v0, v1));
+          } else if (x3 < n) {
+            if (ACC) v0 += __ldcs(row + 8 * j);
+            __stcs(row + 8 * j, v0);
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+}  // namespace rsb
+
+using namespace rsb;
+
+extern "C" {
+
+int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs) {
+  if (n < 2 || n % 2 || gamma < 0 || Rs < 1 || Rs > SM_MAXR) return 0;
+  if (sm_pitch((int)gamma) >= 4096) return 0;                       // 12-bit table offsets
+  const SmLayout L = sm_layout((int)gamma, (int)Rs);
+  return L.total + 4096 <= 227 * 1024 ? 1 : 0;
+}
+
+int64_t rs_short_mma_workspace_bytes(int64_t gamma) { return round_up((gamma + 2) * 4, 256) + 256; }
+
+/* (a13) dense_cct on planes [x1_lo, x1_hi) by the fused tensor-core kernel.
+ * flags: RS_ASM_ACCUMULATE adds to `out`; RS_ASM_KOFD_READY: the term table at
+ * offset 0 of `work` is already filled (rsb_asm_term_prefix). */
+int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_t gamma, int64_t n,
+                          const int32_t *c1, const int32_t *c2, const double *zq,
+                          const int32_t *bstart, const int32_t *bc3, const int32_t *nb_dev,
+                          int64_t x1_lo, int64_t x1_hi, int flags, double *out, void *work,
+                          int64_t work_bytes, void *stream) {
+  RS_REQUIRE(ul && wl && c1 && c2 && zq && bstart && bc3 && nb_dev && out && work,
+             "rs_assemble_short_mma: bad arguments");
+  RS_REQUIRE(0 <= x1_lo && x1_lo < x1_hi && x1_hi <= n, "rs_assemble_short_mma: bad plane range");
+  RS_REQUIRE(rs_short_mma_supported(n, gamma, Rs),
+             "rs_assemble_short_mma: unsupported shape (n=%lld gamma=%lld Rs=%lld)", (long long)n,
+             (long long)gamma, (long long)Rs);
+  if (work_bytes < rs_short_mma_workspace_bytes(gamma))
+    return fail(RS_ERR_CAPACITY, "rs_assemble_short_mma: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  int st;
+  int *kofd = (int *)work;
+  int *counter = (int *)((char *)work + round_up((gamma + 2) * 4, 256));
+  if (!(flags & RS_ASM_KOFD_READY) &&
+      (st = rsb_asm_term_prefix(ul, wl, (int)Rs, (int)gamma, kofd, s)))
+    return st;
+  if (cudaMemsetAsync(counter, 0, 4, s) != cudaSuccess)
+    return fail(RS_ERR_CUDA, "rs_assemble_short_mma: memset");
+  const SmLayout L = sm_layout((int)gamma, (int)Rs);
+  const bool acc = flags & RS_ASM_ACCUMULATE;
+  auto fn = acc ? k_short_mma<true> : k_short_mma<false>;
+  cudaError_t e = smem_attr((const void *)fn, L.total);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_mma smem: %s", cudaGetErrorString(e));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int per_sm = L.total + 1024 <= 113 * 1024 ? 2 : 1;
+  const int64_t ntiles = ceil_div(n, SM_T3) * ceil_div(n, SM_T2) *
+                         ceil_div(x1_hi - (x1_lo - x1_lo % SM_T1), SM_T1);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  ProfScope ps(s, "short_mma");
+  fn<<<grid, SM_THREADS, L.total, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,
+                                       nb_dev, kofd, x1_lo, x1_hi, counter, out);
+  return check_launch("short_mma");
+}
+
+}  // extern "C"

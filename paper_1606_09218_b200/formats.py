@@ -499,6 +499,22 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
             x1_lo, x1_hi, 1 if (accumulate or long is not None) else 0, out.data_ptr(), stream),
             "rs_assemble_short_l0")
         return out
+    if have_short and L.rs_short_method(n, short.count, short.gamma,
+                                        short.local.rank) == nat.SHORT_MMA:
+        # the fused tensor-core kernel (rs_assemble_short_mma); the Tucker planes,
+        # if any, first, then the short part on top
+        if long is not None:
+            assemble_grid(long, None, x1_lo, x1_hi, out=out, accumulate=accumulate,
+                          workspace_bytes=workspace_bytes, workspace_slot=workspace_slot)
+        lay = short.device_layout()
+        ws = nat.Workspace.get(L.rs_short_mma_workspace_bytes(short.gamma), "short_mma")
+        nat.check(L.rs_assemble_short_mma(
+            nat.ptr(lay["ul"]), nat.ptr(lay["wl"]), short.local.rank, short.gamma, n,
+            nat.ptr(lay["c1"]), nat.ptr(lay["c2"]), nat.ptr(lay["zq"]), nat.ptr(lay["bstart"]),
+            nat.ptr(lay["bc3"]), nat.ptr(lay["nb"]), x1_lo, x1_hi,
+            nat.ASM_ACCUMULATE if (accumulate or long is not None) else 0, out.data_ptr(),
+            ws.data_ptr(), ws.numel(), nat.stream_ptr()), "rs_assemble_short_mma")
+        return out
     if have_short:
         flags |= nat.ASM_SHORT | nat.asm_oz(nat.OZ_SLICES)
         lay = short.device_layout()
