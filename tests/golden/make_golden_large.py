@@ -21,7 +21,8 @@ only reads those files.
   2000 random points, the long part alone and the short part alone
   (``eval_tucker_many`` / ``eval_cct``) at 5000 random points, 4 full
   x1-planes of the Tucker part (``TuckerTensor.dense``'s contraction on the
-  reference's own core and factors, one V1 row at a time), energies, phi and
+  reference's own core and factors, one V1 row at a time; stored as a stride-8
+  subsample plus row sums, column sums and the max), energies, phi and
   ``force_fd`` for EVERY particle (process pool).
 * C4 (the 44 GB of side matrices plus the weighted copy do not fit): the
   reference short part (``assemble_short`` -> ``eval_cct``) at 3000 random
@@ -185,9 +186,14 @@ def run_reduced(name):
     # (formats.py:173-176) on the reference's own core and factors, one row of
     # V1 at a time (the class itself refuses a 1-row factor: rank > mode size)
     v1, v2, v3 = rs.long.factors
+    # (a 2048^2 plane is 33 MB: the fixture keeps a stride-8 subsample, the
+    # row and column sums -- every entry enters two of them -- and the max)
     for p in PLANES[name]:
-        arrays[f"tucker_plane_{p}"] = np.einsum("abc,a,jb,lc->jl", rs.long.core, v1[p], v2, v3,
-                                                optimize=True)
+        t = np.einsum("abc,a,jb,lc->jl", rs.long.core, v1[p], v2, v3, optimize=True)
+        arrays[f"tucker_plane_{p}_sub8"] = np.ascontiguousarray(t[3::8, 5::8])
+        arrays[f"tucker_plane_{p}_rowsum"] = t.sum(axis=1)
+        arrays[f"tucker_plane_{p}_colsum"] = t.sum(axis=0)
+        arrays[f"tucker_plane_{p}_maxabs"] = np.array(np.abs(t).max())
     store(name, meta, arrays)
     del res, rs
     idx_sys = rt.snap_to_grid(ref_system(name), cfg.grid)
