@@ -214,11 +214,11 @@ int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t ga
  * columns whose A fragments are formed in registers from shared-memory staged
  * 1-D factors (outer products summed over the bucket's copies near the tile)
  * and whose B fragments are gathered from the same table; nothing but the
- * grid goes to HBM.  work: rs_short_mma_workspace_bytes(gamma).  flags:
+ * grid goes to HBM.  work: rs_short_mma_workspace_bytes(n, gamma).  flags:
  * RS_ASM_ACCUMULATE adds to `out`; RS_ASM_KOFD_READY: the per-distance term
  * table at offset 0 of `work` is already filled. */
 int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs);
-int64_t rs_short_mma_workspace_bytes(int64_t gamma);
+int64_t rs_short_mma_workspace_bytes(int64_t n, int64_t gamma);
 int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
                           int64_t n, const int32_t *c1, const int32_t *c2, const double *zq,
                           const int32_t *bstart, const int32_t *bc3, const int32_t *nb_dev,

@@ -339,7 +339,7 @@ def _front_system(positions, charges, box, grid: Grid3, prefetch=None, chain=Non
         if method == nat.SHORT_L0:
             wsb = L.rs_short_l0_bytes(plan.gamma)   # the gather needs only L0
         elif method == nat.SHORT_MMA:               # term table + tile counter
-            wsb = max(L.rs_short_mma_workspace_bytes(plan.gamma), (n + 1) * 4)
+            wsb = max(L.rs_short_mma_workspace_bytes(n, plan.gamma), (n + 1) * 4)
         else:
             wsb = _short_ws_bytes(n, hi - lo, max(1, min(n, count)), rs)
         ws = nat.Workspace.get(wsb, "assemble_side")

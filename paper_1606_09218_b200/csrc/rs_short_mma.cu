@@ -62,17 +62,31 @@ __host__ __device__ inline int sm_pitch(int gamma) {
 }
 
 struct SmLayout {
-  int table, pk, z, cb, seg, grp, kofd, total;  // byte offsets
+  int table, rec, cb, kn, seg, grp, kofd, total;  // byte offsets
+};
+
+// one staged candidate copy: charge and the two table offsets of its window
+struct __align__(16) SmRec {
+  double z;
+  int o1, o2;   // X0 - c1 + gamma + PAD,  Y0 - c2 + gamma + PAD
+};
+
+// one segment (= bucket run) of an MMA phase
+struct __align__(16) SmSeg {
+  int q_lo;     // first staged copy
+  int col;      // columns before this segment
+  int K;        // its column count (live terms)
+  int bo;       // B offset Z0 - s + gamma + PAD
 };
 
 __host__ __device__ inline SmLayout sm_layout(int gamma, int Rs) {
   SmLayout L;
   int o = 0;
   L.table = o; o += Rs * sm_pitch(gamma) * 8;
-  L.z = o;     o += SM_CAP * 8;
-  L.pk = o;    o += SM_CAP * 4;
-  L.cb = o;    o += (SM_CAP + 2) * 4;            // + sentinel, keeps the int2 array 8-aligned
-  L.seg = o;   o += (SM_CAP + 1) * 8;            // int2 per segment (+ sentinel)
+  L.rec = o;   o += SM_CAP * 16;
+  L.seg = o;   o += (SM_CAP + 1) * 16;           // + sentinel
+  L.cb = o;    o += (SM_CAP + 4) * 4;            // bucket id (B offset) per staged copy
+  L.kn = o;    o += (SM_CAP + 4) * 4;            // live terms per staged copy
   L.grp = o;   o += 3 * SM_THREADS * 4 + 64;     // per-bucket lo / offset / x3 of a group
   L.kofd = o;  o += (gamma + 2) * 4;
   L.total = (o + 15) & ~15;
@@ -100,28 +114,49 @@ __device__ __forceinline__ int sm_block_scan(int v, int *wsum, int *total) {
   return base + x - v;
 }
 
+// Coarse x2 index of the bucket-ordered copies: y16[b * ldy + j] = first copy p
+// of bucket b (c2 ascending inside a bucket) with c2[p] >= 16 j; the last
+// entry is the bucket's end.  Two lookups replace the two binary searches a
+// tile would run per bucket.
+__global__ void k_x2_index(const int32_t *__restrict__ c2, const int32_t *__restrict__ bstart,
+                           const int32_t *__restrict__ nbp, int ldy, int32_t *__restrict__ y16) {
+  const int nb = *nbp;
+  const int64_t total = (int64_t)nb * ldy;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / ldy), j = (int)(e - (int64_t)b * ldy);
+    int l = bstart[b], h = bstart[b + 1];
+    const int key = 16 * j;
+    while (l < h) {
+      const int m = (l + h) >> 1;
+      if (c2[m] < key) l = m + 1; else h = m;
+    }
+    y16[e] = j == ldy - 1 ? bstart[b + 1] : l;
+  }
+}
+
 template <bool ACC>
 __global__ void __launch_bounds__(SM_THREADS, 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
                 int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                 const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
-                const int *__restrict__ kofd_g, int64_t x1_lo, int64_t x1_hi,
-                int *__restrict__ counter, double *__restrict__ out) {
+                const int *__restrict__ kofd_g, const int32_t *__restrict__ y16, int ldy,
+                int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter,
+                double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const SmLayout L = sm_layout(gamma, Rs);
   double *ut = (double *)(sm_raw + L.table);
-  double *s_z = (double *)(sm_raw + L.z);
-  int *s_pk = (int *)(sm_raw + L.pk);
+  SmRec *s_rec = (SmRec *)(sm_raw + L.rec);
+  SmSeg *s_seg = (SmSeg *)(sm_raw + L.seg);
   int *s_cb = (int *)(sm_raw + L.cb);
-  int2 *s_seg = (int2 *)(sm_raw + L.seg);   // .x = first staged copy | columns before << 16
-                                            // .y = column count | (B offset << 8)
+  int *s_kn = (int *)(sm_raw + L.kn);
   int *s_lo = (int *)(sm_raw + L.grp);
   int *s_off = s_lo + SM_THREADS;
   int *s_b3 = s_off + SM_THREADS;
   int *skofd = (int *)(sm_raw + L.kofd);
   __shared__ int wsum[SM_THREADS / 32];
-  __shared__ int s_band[2], s_tile, s_segk[SM_CAP];
+  __shared__ int s_band[2], s_tile;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -164,64 +199,67 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     auto flush = [&](int len) {
       __syncthreads();
       if (tid == 0) s_cb[len] = -1;
-      for (int i = tid; i < SM_CAP; i += SM_THREADS) s_segk[i] = 0;
       __syncthreads();
-      int nseg = 0;
-      for (int i0 = 0; i0 < len; i0 += SM_THREADS) {   // segment starts
+      int nseg = 0, ncol = 0;
+      for (int i0 = 0; i0 < len; i0 += SM_THREADS) {
         const int i = i0 + tid;
         const bool start = i < len && (i == 0 || s_cb[i] != s_cb[i - 1]);
-        int tot;
-        const int pos = sm_block_scan(start ? 1 : 0, wsum, &tot);
-        if (start) s_seg[nseg + pos].x = i;
-        nseg += tot;
-      }
-      if (tid == 0) s_seg[nseg].x = len;
-      __syncthreads();
-      for (int i = tid; i < len; i += SM_THREADS) {    // copy -> its segment (binary search)
-        int l = 0, h = nseg;
-        while (h - l > 1) {
-          const int m = (l + h) >> 1;
-          if (s_seg[m].x <= i) l = m; else h = m;
+        int K = 0;
+        if (start) {   // the run is short (copies of one bucket near the tile)
+          const int id = s_cb[i];
+          for (int q = i; s_cb[q] == id; ++q) K = max(K, s_kn[q]);
         }
-        atomicMax(&s_segk[l], s_pk[i] >> 24);
-        if (s_seg[l].x == i) s_seg[l].y = s_cb[i] << 8;   // B offset of the bucket (<= 12 bits)
-      }
-      __syncthreads();
-      int ncol = 0;
-      for (int i0 = 0; i0 < nseg; i0 += SM_THREADS) {  // column prefix
-        const int i = i0 + tid;
-        const int K = i < nseg ? s_segk[i] : 0;
-        int tot;
-        const int pre = sm_block_scan(K, wsum, &tot);
-        if (i < nseg) {
-          s_seg[i].x |= (ncol + pre) << 16;
-          s_seg[i].y |= K;
+        int tot;   // one scan for both the segment index (low half) and the column prefix
+        const int pre = sm_block_scan(start ? (K << 12) | 1 : 0, wsum, &tot);
+        if (start) {
+          SmSeg sg;
+          sg.q_lo = i;
+          sg.col = ncol + (pre >> 12);
+          sg.K = K;
+          sg.bo = s_cb[i];
+          s_seg[nseg + (pre & 0xFFF)] = sg;
         }
-        ncol += tot;
+        nseg += tot & 0xFFF;
+        ncol += tot >> 12;
       }
-      if (tid == 0) s_seg[nseg].x |= ncol << 16;
+      if (tid == 0) {
+        SmSeg sg;
+        sg.q_lo = len;
+        sg.col = ncol;
+        sg.K = 0;
+        sg.bo = 0;
+        s_seg[nseg] = sg;
+      }
       __syncthreads();
       const int steps = (ncol + 3) >> 2;
-      int si = 0;
+      int si = -1, seg_end = 0, col0 = 0, q_lo = 0, q_hi = 0, bo = 0;
+      const double *ut1 = ut + warp, *ut2 = ut + gid;
       for (int st = 0; st < steps; ++st) {
         const int c = 4 * st + tig;
         double a0 = 0.0, a1 = 0.0, b[8];
         if (c < ncol) {
-          while ((int)((unsigned)s_seg[si + 1].x >> 16) <= c) ++si;
-          const int2 sg = s_seg[si];
-          const int k = c - (int)((unsigned)sg.x >> 16);
-          const int q_lo = sg.x & 0xFFFF, q_hi = s_seg[si + 1].x & 0xFFFF;
-          const double *uk = ut + k * LD;
-          for (int q = q_lo; q < q_hi; ++q) {
-            const int pk = s_pk[q];
-            if (k < (pk >> 24)) {
-              const double t = s_z[q] * uk[(pk & 0xFFF) + warp];
-              const double *u2 = uk + ((pk >> 12) & 0xFFF) + gid;
-              a0 = fma(t, u2[0], a0);
-              a1 = fma(t, u2[8], a1);
-            }
+          if (c >= seg_end) {   // this lane's column enters a new segment
+            SmSeg sg;
+            do {
+              sg = s_seg[++si];
+              seg_end = sg.col + sg.K;
+            } while (c >= seg_end);
+            col0 = sg.col;
+            q_lo = sg.q_lo;
+            bo = sg.bo;
+            q_hi = s_seg[si + 1].q_lo;
           }
-          const double *ub = uk + (sg.y >> 8) + gid;
+          const int koff = (c - col0) * LD;
+          const double *u1 = ut1 + koff, *u2 = ut2 + koff;
+#pragma unroll 2
+          for (int q = q_lo; q < q_hi; ++q) {
+            const SmRec r = s_rec[q];
+            const double t = r.z * u1[r.o1];
+            const double *w2 = u2 + r.o2;
+            a0 = fma(t, w2[0], a0);
+            a1 = fma(t, w2[8], a1);
+          }
+          const double *ub = u2 + bo;
 #pragma unroll
           for (int j = 0; j < 8; ++j) b[j] = ub[8 * j];
         } else {
@@ -260,21 +298,11 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     for (int g = blo; g < bhi; g += SM_THREADS) {
       const int bi = g + tid;
       int lo = 0, cnt = 0, b3 = 0;
-      if (bi < bhi) {  // the bucket's copies whose x2 window meets the tile (c2 ascending)
-        const int p_lo = bstart[bi], p_hi = bstart[bi + 1];
+      if (bi < bhi) {  // the bucket's copies in the 16-cell x2 blocks the window meets
         b3 = bc3[bi];
-        int l = p_lo, h = p_hi;
-        while (l < h) {
-          const int m = (l + h) >> 1;
-          if (c2[m] < c2lo) l = m + 1; else h = m;
-        }
-        lo = l;
-        h = p_hi;
-        while (l < h) {
-          const int m = (l + h) >> 1;
-          if (c2[m] <= c2hi) l = m + 1; else h = m;
-        }
-        cnt = l - lo;
+        const int32_t *yr = y16 + (int64_t)bi * ldy;
+        lo = yr[max(c2lo, 0) >> 4];
+        cnt = yr[min((c2hi >> 4) + 1, ldy - 1)] - lo;
       }
       int tot;
       const int off = sm_block_scan(cnt, wsum, &tot);
@@ -291,8 +319,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         }
         const int v = cs + tid;
         bool cov = false;
-        int pk = 0, bo = 0;
-        double z = 0.0;
+        int kn = 0, bo = 0;
+        SmRec rec;
         if (v < tot) {   // last bucket with offset <= v (empty buckets share offsets)
           int l = 0, h = nbk;
           while (h - l > 1) {
@@ -300,17 +328,18 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             if (s_off[m] <= v) l = m; else h = m;
           }
           const int p = s_lo[l] + (v - s_off[l]);
-          const int a1 = c1[p];
-          if (a1 >= c1lo && a1 <= c1hi) {
-            const int a2 = c2[p], a3 = s_b3[l];
+          const int a1 = c1[p], a2 = c2[p];
+          if (a1 >= c1lo && a1 <= c1hi && a2 >= c2lo && a2 <= c2hi) {
+            const int a3 = s_b3[l];
             const int d1 = max(0, max(X0 - a1, a1 - (X0 + SM_T1 - 1)));
             const int d2 = max(0, max(Y0 - a2, a2 - (Y0 + SM_T2 - 1)));
             const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
-            const int kn = skofd[max(d1, max(d2, d3))];
+            kn = skofd[max(d1, max(d2, d3))];
             if (kn > 0) {
               cov = true;
-              z = zq[p];
-              pk = (X0 - a1 + gamma + SM_PAD) | ((Y0 - a2 + gamma + SM_PAD) << 12) | (kn << 24);
+              rec.z = zq[p];
+              rec.o1 = X0 - a1 + gamma + SM_PAD;
+              rec.o2 = Y0 - a2 + gamma + SM_PAD;
               bo = Z0 - a3 + gamma + SM_PAD;   // B offset: identifies the bucket as well
             }
           }
@@ -318,8 +347,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         int t2;
         const int pos = sm_block_scan(cov ? 1 : 0, wsum, &t2);
         if (cov) {
-          s_pk[len + pos] = pk;
-          s_z[len + pos] = z;
+          s_rec[len + pos] = rec;
+          s_kn[len + pos] = kn;
           s_cb[len + pos] = bo;
         }
         len += t2;
@@ -367,12 +396,16 @@ extern "C" {
 
 int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs) {
   if (n < 2 || n % 2 || gamma < 0 || Rs < 1 || Rs > SM_MAXR) return 0;
-  if (sm_pitch((int)gamma) >= 4096) return 0;                       // 12-bit table offsets
   const SmLayout L = sm_layout((int)gamma, (int)Rs);
   return L.total + 4096 <= 227 * 1024 ? 1 : 0;
 }
 
-int64_t rs_short_mma_workspace_bytes(int64_t gamma) { return round_up((gamma + 2) * 4, 256) + 256; }
+static int64_t sm_ldy(int64_t n) { return ceil_div(n, 16) + 1; }
+
+// kofd (gamma + 2 ints) | tile counter | x2 index (n buckets x ldy)
+int64_t rs_short_mma_workspace_bytes(int64_t n, int64_t gamma) {
+  return round_up((gamma + 2) * 4, 256) + 256 + round_up(n * sm_ldy(n) * 4, 256);
+}
 
 /* (a13) dense_cct on planes [x1_lo, x1_hi) by the fused tensor-core kernel.
  * flags: RS_ASM_ACCUMULATE adds to `out`; RS_ASM_KOFD_READY: the term table at
@@ -388,7 +421,7 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   RS_REQUIRE(rs_short_mma_supported(n, gamma, Rs),
              "rs_assemble_short_mma: unsupported shape (n=%lld gamma=%lld Rs=%lld)", (long long)n,
              (long long)gamma, (long long)Rs);
-  if (work_bytes < rs_short_mma_workspace_bytes(gamma))
+  if (work_bytes < rs_short_mma_workspace_bytes(n, gamma))
     return fail(RS_ERR_CAPACITY, "rs_assemble_short_mma: workspace too small");
   cudaStream_t s = as_stream(stream);
   int st;
@@ -399,6 +432,10 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
     return st;
   if (cudaMemsetAsync(counter, 0, 4, s) != cudaSuccess)
     return fail(RS_ERR_CUDA, "rs_assemble_short_mma: memset");
+  int32_t *y16 = (int32_t *)((char *)counter + 256);
+  const int ldy = (int)sm_ldy(n);
+  k_x2_index<<<grid_blocks(n * ldy), 256, 0, s>>>(c2, bstart, nb_dev, ldy, y16);
+  if ((st = check_launch("short_mma x2 index"))) return st;
   const SmLayout L = sm_layout((int)gamma, (int)Rs);
   const bool acc = flags & RS_ASM_ACCUMULATE;
   auto fn = acc ? k_short_mma<true> : k_short_mma<false>;
@@ -416,7 +453,7 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
   ProfScope ps(s, "short_mma");
   fn<<<grid, SM_THREADS, L.total, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,
-                                       nb_dev, kofd, x1_lo, x1_hi, counter, out);
+                                       nb_dev, kofd, y16, ldy, x1_lo, x1_hi, counter, out);
   return check_launch("short_mma");
 }
 

@@ -507,7 +507,7 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
             assemble_grid(long, None, x1_lo, x1_hi, out=out, accumulate=accumulate,
                           workspace_bytes=workspace_bytes, workspace_slot=workspace_slot)
         lay = short.device_layout()
-        ws = nat.Workspace.get(L.rs_short_mma_workspace_bytes(short.gamma), "short_mma")
+        ws = nat.Workspace.get(L.rs_short_mma_workspace_bytes(n, short.gamma), "short_mma")
         nat.check(L.rs_assemble_short_mma(
             nat.ptr(lay["ul"]), nat.ptr(lay["wl"]), short.local.rank, short.gamma, n,
             nat.ptr(lay["c1"]), nat.ptr(lay["c2"]), nat.ptr(lay["zq"]), nat.ptr(lay["bstart"]),
