@@ -515,9 +515,10 @@ def main():
               torch.cuda.memory_stats().get("num_device_alloc", 0) - mallocs0, file=sys.stderr)
     gemm_ms, gemm_n = nat.prof_query("gemm_short")
     l0_ms, l0_n = nat.prof_query("short_l0")
-    prof = {k: nat.prof_query(k) for k in ("gemm_short", "gemm_tucker", "gemm_plane", "short_rows",
-                                          "short_l0", "tucker_f", "topeig", "syrk", "core",
-                                          "shift_project")}
+    mma_ms, mma_n = nat.prof_query("short_mma")
+    prof = {k: nat.prof_query(k) for k in ("short_mma", "gemm_short", "gemm_tucker", "gemm_plane",
+                                          "short_rows", "short_l0", "tucker_f", "topeig", "syrk",
+                                          "core", "shift_project")}
     tt = torch.tensor([t_mean], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -587,7 +588,21 @@ def main():
                 lo_x, hi_x = t0 - g, min(n - 1, t0 + 63) + g
                 keff.append(np.count_nonzero((bc3 >= lo_x) & (bc3 <= hi_x)))
         exec_flops = 2.0 * n * n * 64 * float(np.sum(keff))
-        if gemm_n:   # short range on the plane GEMM (FP64 tensor cores)
+        if mma_n:    # short range by the fused tensor-core kernel (the default)
+            mma_avg_s = mma_ms / mma_n / 1e3
+            ach = alg_flops * slab_frac / (mma_n / args.steps) / mma_avg_s / 1e12
+            roof = {"bound": "tensor",
+                    "kernel": "k_short_mma fused short-range agglomeration on DMMA (short_mma)",
+                    "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": _ncu_traffic(name, "short_mma"),
+                    "peak_source": "cuBLAS DGEMM 8192^3 measured live (fp64; "
+                                   "MEASURED_PEAKS.json has no FP64 entry)",
+                    "algorithmic_flops_per_launch": alg_flops * slab_frac / (mma_n / args.steps),
+                    "note": "algorithmic = 2 flops per (grid point, covering copy) pair "
+                            "(SURVEY 8d); the separable form executes more: every (tile, "
+                            "x3 bucket, live term) column is a full 128 x 64 MMA column",
+                    "avg_launch_ms": mma_avg_s * 1e3}
+        elif gemm_n:   # short range on the plane GEMM (FP64 tensor cores)
             roof = {"bound": "tensor",
                     "kernel": "k_gemm_plane short-range plane GEMM (gemm_short)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -652,6 +667,32 @@ def main():
                         f"= {k_occ} (the reference's A A^T has K = N R_l = "
                         f"{host_idx.shape[0] * R_l} columns, equal up to merging equal shifts)",
                 "algorithmic_flops_per_launch": gf, "avg_launch_ms": s_avg * 1e3}
+        # the other outputs BASELINE names for this config (configs[4]: per-particle
+        # potential and forces): timed once, outside the assembly's timed region
+        obs = None
+        if world == 1 and not os.environ.get("BENCH_NO_OBSERVABLES"):
+            def timed(fn, reps=3):
+                fn()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(reps):
+                    fn()
+                b.record()
+                torch.cuda.synchronize()
+                return a.elapsed_time(b) / reps
+            sysd = res.system
+            obs = {"particles": int(m["N"]),
+                   "particle_potentials_ms": timed(lambda: rt.particle_potentials(
+                       res.rs, sysd, res.reference, device=True)),
+                   "eval_rs_many_all_nodes_ms": timed(lambda: rt.eval_rs_many(
+                       res.rs, sysd.indices, device=True)),
+                   "forces_fd_all_particles_ms": timed(lambda: rt.forces_fd(
+                       sysd, res.reference, device=True), reps=1),
+                   "reference_energy_ms": timed(lambda: rt.reference_energy(sysd, res.reference),
+                                                reps=1),
+                   "note": "device results, no host copy; forces_fd / reference_energy are the "
+                           "O(N^2 R_l) windowed pair sums (observables.py:190-259)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             tc, _, det = reference_assembly_time(name, 20.0)   # ~20 s of CPU work
@@ -683,6 +724,7 @@ def main():
             "roofline": roof,
             "secondary_rooflines": secondary,
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "observables": obs,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

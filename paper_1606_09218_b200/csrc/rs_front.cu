@@ -272,34 +272,41 @@ __global__ void k_tt_transpose(const double *__restrict__ TT, int r, int64_t n, 
   }
 }
 
-// Block = (bucket q, CH_TA consecutive a); thread = one b (blockDim >= r2).
-// Per staged chunk of the bucket's copies and per term k: the copies' TT2
-// vectors (all b) and TT1 entries (the block's a) land in shared memory with
-// coalesced loads; every thread accumulates CH_TA x R outputs in registers
-// and finally writes its rows' R-wide segments.
-constexpr int CH_TA = 2;
-__global__ void k_core_h(const double *__restrict__ TT1t, const double *__restrict__ TT2t, int r1,
-                         int r2, int64_t n, int R, const double *__restrict__ w,
-                         const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
-                         const double *__restrict__ zq, const int32_t *__restrict__ bstart,
-                         double *__restrict__ H, int64_t ldH) {
+// Block = (bucket q, CH_TA consecutive a, CH_KG consecutive terms k); thread =
+// one b (blockDim >= r2).  Per staged chunk of the bucket's copies and per
+// term k: the copies' TT2 vectors (all b) and TT1 entries (the block's a) land
+// in shared memory with coalesced loads; every thread accumulates CH_TA x
+// CH_KG outputs in registers and finally writes, per row, one aligned CH_KG-
+// wide segment.  The TT2 panel of a (copy, term) is re-read once per a-tile:
+// 16 a per block instead of 2 cut the L2 traffic of this stage 8x (C5 core
+// 27 -> see DESIGN).
+constexpr int CH_TA = 16;
+constexpr int CH_KG = 4;
+__global__ void __launch_bounds__(256)
+    k_core_h(const double *__restrict__ TT1t, const double *__restrict__ TT2t, int r1,
+             int r2, int64_t n, int R, const double *__restrict__ w,
+             const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
+             const double *__restrict__ zq, const int32_t *__restrict__ bstart,
+             double *__restrict__ H, int64_t ldH) {
   extern __shared__ double sh[];
   double *sY = sh;                          // CH_CHUNK x r2
   double *sX = sh + CH_CHUNK * r2;          // CH_CHUNK x CH_TA
   const int q = blockIdx.y;
   const int a0 = blockIdx.x * CH_TA;
+  const int k0 = blockIdx.z * CH_KG;
   const int bcol = threadIdx.x;
-  double acc[CH_TA][CH_RMAX];
+  double acc[CH_TA][CH_KG];
 #pragma unroll
   for (int u = 0; u < CH_TA; ++u)
 #pragma unroll
-    for (int k = 0; k < CH_RMAX; ++k) acc[u][k] = 0.0;
+    for (int k = 0; k < CH_KG; ++k) acc[u][k] = 0.0;
   const int p_lo = bstart[q], p_hi = bstart[q + 1];
   for (int i0 = p_lo; i0 < p_hi; i0 += CH_CHUNK) {
     const int cnt = min(CH_CHUNK, p_hi - i0);
 #pragma unroll
-    for (int k = 0; k < CH_RMAX; ++k) {
-      if (k < R) {
+    for (int kk = 0; kk < CH_KG; ++kk) {
+      const int k = k0 + kk;
+      if (k < R) {   // uniform
         for (int e = threadIdx.x; e < cnt * r2; e += blockDim.x) {
           const int j = e / r2, t = e - j * r2;
           sY[e] = TT2t[((int64_t)(n - c2[i0 + j]) * R + k) * r2 + t];
@@ -314,8 +321,13 @@ __global__ void k_core_h(const double *__restrict__ TT1t, const double *__restri
         if (bcol < r2) {
           for (int j = 0; j < cnt; ++j) {
             const double y = sY[j * r2 + bcol];
+            const double2 *xs = reinterpret_cast<const double2 *>(sX + j * CH_TA);
 #pragma unroll
-            for (int u = 0; u < CH_TA; ++u) acc[u][k] = fma(sX[j * CH_TA + u], y, acc[u][k]);
+            for (int u = 0; u < CH_TA; u += 2) {
+              const double2 x = xs[u >> 1];
+              acc[u][kk] = fma(x.x, y, acc[u][kk]);
+              acc[u + 1][kk] = fma(x.y, y, acc[u + 1][kk]);
+            }
           }
         }
         __syncthreads();
@@ -327,11 +339,11 @@ __global__ void k_core_h(const double *__restrict__ TT1t, const double *__restri
     for (int u = 0; u < CH_TA; ++u) {
       const int a = a0 + u;
       if (a >= r1) continue;
-      double *dst = H + ((int64_t)a * r2 + bcol) * ldH + (int64_t)q * R;
+      double *dst = H + ((int64_t)a * r2 + bcol) * ldH + (int64_t)q * R + k0;
 #pragma unroll
-      for (int k = 0; k < CH_RMAX; ++k)
-        if (k < R) dst[k] = acc[u][k];
-      if (q == (int)gridDim.y - 1)  // even-K padding column(s)
+      for (int kk = 0; kk < CH_KG; ++kk)
+        if (k0 + kk < R) dst[kk] = acc[u][kk];
+      if (q == (int)gridDim.y - 1 && blockIdx.z == gridDim.z - 1)  // even-K padding column(s)
         for (int64_t c = (int64_t)(q + 1) * R; c < ldH; ++c) H[((int64_t)a * r2 + bcol) * ldH + c] = 0.0;
     }
   }
@@ -414,7 +426,7 @@ static int back_impl(const double *U, int64_t b, int64_t n, int64_t r1, int64_t 
   // the particle-K Khatri-Rao GEMM is latency-bound and cheap below ~1e10
   // flops (C1-C3); the bucket-K form wins once N R_l r1 r2 r3 dominates (C4, C5)
   const double kr_flops = 2.0 * (double)r1 * r2 * r3 * (double)count * R;
-  if (!bstart || nq_host <= 0 || R > CH_RMAX || kr_flops < 1e10 || r2 > 1024) {
+  if (!bstart || nq_host <= 0 || R > CH_RMAX || kr_flops < 1e10 || r2 > 256) {
     if (!shard)
       return rs_core(TT1, TT2, TT3, r1, r2, r3, n, R, starts, z, w, count, core, cw,
                      rs_core_workspace_bytes(r1, r2, r3, count, R), stream);
@@ -450,12 +462,13 @@ static int back_impl(const double *U, int64_t b, int64_t n, int64_t r1, int64_t 
   k_tt_transpose<<<(unsigned)std::min<int64_t>(ceil_div(r2 * n * R, 256), 4096), 256, 0, s>>>(
       TT2, (int)r2, n, (int)R, TT2t);
   if ((st = check_launch("core transpose"))) return st;
-  RS_REQUIRE(r2 <= 1024, "rs_back: r2 = %lld exceeds the H kernel's block", (long long)r2);
+  RS_REQUIRE(r2 <= 256, "rs_back: r2 = %lld exceeds the H kernel's block", (long long)r2);
   const int threads = (int)round_up(r2, 32);
   const size_t smem = (size_t)CH_CHUNK * (r2 + CH_TA) * 8;
   cudaError_t e = smem_attr((const void *)k_core_h, (int)smem);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
-  k_core_h<<<dim3((unsigned)ceil_div(r1, CH_TA), (unsigned)nq), threads, smem, s>>>(
+  k_core_h<<<dim3((unsigned)ceil_div(r1, CH_TA), (unsigned)nq, (unsigned)ceil_div(R, CH_KG)),
+             threads, smem, s>>>(
       TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq, bstart, H, ldH);
   if ((st = check_launch("core_h"))) return st;
   k_core_t3<<<(unsigned)std::min<int64_t>(ceil_div(r3 * ldH, 256), 4096), 256, 0, s>>>(

@@ -30,8 +30,9 @@
 // Candidates come from rs_front's x3-bucket layout (bucket range by binary
 // search over bc3, x2 window by binary search in the c2-sorted bucket, x1
 // filter + order-preserving block scan), are staged SM_CAP at a time and
-// consumed in bucket order: deterministic.  CTAs are persistent (the factor
-// table is staged once) and take tiles from an atomic counter, x3 fastest.
+// consumed in bucket order: deterministic.  CTAs take tiles from an atomic
+// counter, x3 fastest, and retire after a bounded number of them (the factor
+// table is staged once per CTA).
 // Roofline: FP64 tensor pipe (DMMA); algorithmic work 2 flops per (grid
 // point, covering copy) pair.
 #include "rs_common.cuh"
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
                 const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
                 const int *__restrict__ kofd_g, const int32_t *__restrict__ y16, int ldy,
-                int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter,
+                int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter, int tiles_per_cta,
                 double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const SmLayout L = sm_layout(gamma, Rs);
@@ -178,7 +179,10 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     ut[k * LD + SM_PAD + d] = cbrt(wl[k]) * ul[e];
   }
 
-  for (;;) {
+  // a CTA retires after tiles_per_cta tiles: the turnover lets the kernels of a
+  // higher-priority stream (the latency-bound Gram / eigen / core chain) onto
+  // the SMs between two CTAs instead of behind the whole grid
+  for (int done = 0; done < tiles_per_cta; ++done) {
     __syncthreads();   // previous tile done with the staging arrays; table complete
     if (tid == 0) s_tile = atomicAdd(counter, 1);
     __syncthreads();
@@ -450,10 +454,16 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const int per_sm = L.total + 1024 <= 113 * 1024 ? 2 : 1;
   const int64_t ntiles = ceil_div(n, SM_T3) * ceil_div(n, SM_T2) *
                          ceil_div(x1_hi - (x1_lo - x1_lo % SM_T1), SM_T1);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  static const int waves = [] {   // RSB200_MMA_WAVES: CTA generations per SM slot
+    const char *e = getenv("RSB200_MMA_WAVES");
+    return e && atoi(e) > 0 ? atoi(e) : 256;
+  }();
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int tiles_per_cta = (int)std::max<int64_t>(1, ceil_div(ntiles, slots * waves));
+  const unsigned grid = (unsigned)ceil_div(ntiles, tiles_per_cta);
   ProfScope ps(s, "short_mma");
   fn<<<grid, SM_THREADS, L.total, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,
-                                       nb_dev, kofd, y16, ldy, x1_lo, x1_hi, counter, out);
+                                       nb_dev, kofd, y16, ldy, x1_lo, x1_hi, counter, tiles_per_cta, out);
   return check_launch("short_mma");
 }
 

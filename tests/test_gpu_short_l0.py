@@ -46,9 +46,13 @@ def both(res, monkeypatch, **kw):
 def test_method_choice_and_override(monkeypatch):
     L = nat.lib()
     monkeypatch.delenv("RSB200_SHORT", raising=False)
-    assert L.rs_short_method(2048, 31130, 80, 20) == nat.SHORT_L0      # C5: 15 copies / point
-    assert L.rs_short_method(256, 1000, 94, 14) == nat.SHORT_GEMM      # C2: 278
-    assert L.rs_short_method(1024, 100000, 107, 18) == nat.SHORT_GEMM  # C4: 899
+    # default: the fused tensor-core kernel wherever its table fits shared memory
+    assert L.rs_short_method(2048, 31130, 80, 20) == nat.SHORT_MMA
+    assert L.rs_short_method(256, 1000, 94, 14) == nat.SHORT_MMA
+    assert L.rs_short_method(1024, 100000, 107, 18) == nat.SHORT_MMA
+    # beyond it: the L0 gather at low overlap (15 copies / point), else the plane GEMM
+    assert L.rs_short_method(4096, 31130, 700, 20) == nat.SHORT_GEMM   # pair table too wide too
+    assert L.rs_short_method(4096, 100, 120, 30) == nat.SHORT_L0       # Rs beyond the fused kernel
     monkeypatch.setenv("RSB200_SHORT", "l0")
     assert L.rs_short_method(256, 1000, 94, 14) == nat.SHORT_L0
     monkeypatch.setenv("RSB200_SHORT", "gemm")
