@@ -835,26 +835,32 @@ __global__ void k_rowblock_terms(const int32_t *__restrict__ c1, const int32_t *
 // prologue nor the read-modify-write epilogue stalls the DMMA pipe per tile.
 // With K ~ 132 (C5) these two bubbles cost the per-tile kernel ~40 % of peak.
 namespace tr {
-constexpr int BN = 64, BK = 16, LDB = BK + 4, STAGES = 3;
+constexpr int BN = 64;
 constexpr int WM = 32, WN = 32, WARPS_N = BN / WN, MT = WM / 8, NT = WN / 8;
 constexpr int KMAX = 176;
 __host__ __device__ constexpr int threads(int bm) { return (bm / WM) * WARPS_N * 32; }
-__host__ __device__ constexpr int lda_s(int kc) { return kc * BK + 4; }  // = 4 mod 16: conflict-free fragments
-__host__ __device__ constexpr int smem_bytes(int bm, int kc) {
-  return (bm * lda_s(kc) + STAGES * BN * LDB) * 8;
+// row pitch of the resident A block: K rounded up to a k-step, then to 4 mod 16
+// doubles (conflict-free fragment reads)
+__host__ __device__ constexpr int lda_s(int K) {
+  int l = (K + 3) / 4 * 4;
+  while (l % 16 != 4) l += 4;
+  return l;
+}
+__host__ __device__ constexpr int smem_bytes(int bm, int K, int bk, int stages) {
+  return (bm * lda_s(K) + stages * BN * (bk + 4)) * 8;
 }
 }  // namespace tr
 
 // BM = 128: 8 warps, one CTA per SM; BM = 64: 4 warps, two CTAs per SM
-template <int BM, bool ACC>
+template <int BM, bool ACC, int BK, int STAGES>
 __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
     k_tucker_gemm_res(const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int64_t M, int64_t N,
                       int K) {
   using namespace tr;
-  constexpr int THREADS = threads(BM);
+  constexpr int THREADS = threads(BM), LDB = BK + 4;
   extern __shared__ __align__(16) double smem[];
-  const int KC = (K + BK - 1) / BK, LDA = lda_s(KC);
+  const int KC = (K + BK - 1) / BK, LDA = lda_s(K);
   double *sA = smem;
   double *sB = smem + BM * LDA;
   const int64_t m0 = (int64_t)blockIdx.x * BM;
@@ -864,8 +870,8 @@ __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
   const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
   const int gid = lane >> 2, tig = lane & 3;
   // resident A block (zero past K and past M), first commit group with chunk 0
-  for (int e = threadIdx.x; e < BM * (KC * BK / 2); e += THREADS) {
-    const int r = e / (KC * BK / 2), kk = 2 * (e - r * (KC * BK / 2));
+  for (int e = threadIdx.x; e < BM * (LDA / 2); e += THREADS) {
+    const int r = e / (LDA / 2), kk = 2 * (e - r * (LDA / 2));
     const int64_t g = m0 + r;
     const bool ok = g < M && kk < K;
     const int bytes = ok ? (kk + 1 < K ? 16 : 8) : 0;
@@ -873,24 +879,55 @@ __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
                      smem_addr(sA + r * LDA + kk)),
                  "l"(ok ? A + g * lda + kk : A), "r"(bytes));
   }
-  auto load_b = [&](int c) {
-    const int t = c / KC, kc = c - t * KC;
-    double *st = sB + (c % STAGES) * BN * LDB;
+  // Bt chunks are requested strictly in order (tile-major, chunk-minor), so the
+  // loader keeps running state instead of decoding the chunk index: per thread
+  // its SLOTS (row, column-pair) slots are fixed, the source pointers advance by
+  // BK per chunk and by BN rows per tile, and only the last chunk of a tile
+  // (K not a multiple of BK) and the last tile (N not a multiple of BN) take
+  // the predicated path.  (The div/mod version spent ~45 % of the issue slots
+  // of this 2-warps-per-scheduler kernel on addressing.)
+  constexpr int SLOTS = BN * BK / 2 / THREADS;
+  uint32_t sdst[SLOTS];
+  const double *src[SLOTS];
 #pragma unroll
-    for (int e0 = 0; e0 < BN * BK / 2; e0 += THREADS) {
-      const int e = e0 + threadIdx.x;
-      const int r = e / (BK / 2), kk = kc * BK + 2 * (e % (BK / 2));
-      const int64_t g = (int64_t)t * BN + r;
-      const bool ok = g < N && kk < K;
-      const int bytes = ok ? (kk + 1 < K ? 16 : 8) : 0;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
-                       smem_addr(st + r * LDB + 2 * (e % (BK / 2)))),
-                   "l"(ok ? B + g * ldb + kk : B), "r"(bytes));
+  for (int u = 0; u < SLOTS; ++u) {
+    const int e = u * THREADS + threadIdx.x, r = e / (BK / 2), pr = e % (BK / 2);
+    sdst[u] = smem_addr(sB + r * LDB + 2 * pr);
+    src[u] = B + (int64_t)r * ldb + 2 * pr;
+  }
+  int lt = 0, lkc = 0, lst = 0;
+  const bool k_even = (K % BK) == 0;
+  auto load_next = [&]() {
+    const bool fast = (k_even || lkc < KC - 1) && (int64_t)(lt + 1) * BN <= N;
+    const uint32_t soff = (uint32_t)(lst * BN * LDB * 8);
+    if (fast) {
+#pragma unroll
+      for (int u = 0; u < SLOTS; ++u)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst[u] + soff),
+                     "l"(src[u] + lkc * BK));
+    } else {
+#pragma unroll
+      for (int u = 0; u < SLOTS; ++u) {
+        const int e = u * THREADS + threadIdx.x;
+        const int r = e / (BK / 2), kk = lkc * BK + 2 * (e % (BK / 2));
+        const int64_t g = (int64_t)lt * BN + r;
+        const bool ok = g < N && kk < K;
+        const int bytes = ok ? (kk + 1 < K ? 16 : 8) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst[u] + soff),
+                     "l"(ok ? src[u] + lkc * BK : B), "r"(bytes));
+      }
     }
+    if (++lkc == KC) {
+      lkc = 0;
+      ++lt;
+#pragma unroll
+      for (int u = 0; u < SLOTS; ++u) src[u] += (int64_t)BN * ldb;
+    }
+    if (++lst == STAGES) lst = 0;
   };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < total) load_b(s);
+    if (s < total) load_next();
     cp_async_commit();
   }
   double acc[MT][NT][2], cold[MT][NT][2];
@@ -919,7 +956,7 @@ __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
     }
   };
   const int ksteps_last = (K - (KC - 1) * BK + 3) / 4;  // live 4-column steps of the last chunk
-  int c = 0;
+  int c = 0, cst = 0;
   for (int t = 0; t < ntiles; ++t) {
 #pragma unroll
     for (int i = 0; i < MT; ++i)
@@ -941,14 +978,24 @@ __global__ void __launch_bounds__(tr::threads(BM), BM == 64 ? 2 : 1)
     for (int kc = 0; kc < KC; ++kc, ++c) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
-      if (c + STAGES - 1 < total) load_b(c + STAGES - 1);
+      if (c + STAGES - 1 < total) load_next();
       cp_async_commit();
-      const double *st = sB + (c % STAGES) * BN * LDB;
-      const int ks = kc == KC - 1 ? ksteps_last : 4;
-      if (ks == 4) mma_steps(st, kc, std::integral_constant<int, 4>{});
-      else if (ks == 3) mma_steps(st, kc, std::integral_constant<int, 3>{});
-      else if (ks == 2) mma_steps(st, kc, std::integral_constant<int, 2>{});
-      else mma_steps(st, kc, std::integral_constant<int, 1>{});
+      const double *st = sB + cst * BN * LDB;
+      if (++cst == STAGES) cst = 0;
+      const int ks = kc == KC - 1 ? ksteps_last : BK / 4;
+      if (ks == BK / 4) {
+        mma_steps(st, kc, std::integral_constant<int, BK / 4>{});
+      } else {
+        switch (ks) {   // live steps of a tile's last chunk
+          case 1: mma_steps(st, kc, std::integral_constant<int, 1>{}); break;
+          case 2: mma_steps(st, kc, std::integral_constant<int, 2>{}); break;
+          case 3: mma_steps(st, kc, std::integral_constant<int, 3>{}); break;
+          case 4: if constexpr (BK > 16) mma_steps(st, kc, std::integral_constant<int, 4>{}); break;
+          case 5: if constexpr (BK > 16) mma_steps(st, kc, std::integral_constant<int, 5>{}); break;
+          case 6: if constexpr (BK > 16) mma_steps(st, kc, std::integral_constant<int, 6>{}); break;
+          default: if constexpr (BK > 16) mma_steps(st, kc, std::integral_constant<int, 7>{}); break;
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
@@ -2047,17 +2094,30 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
     };
     if (with_long && !with_short && g_tucker_res && r3p <= tr::KMAX && n % 2 == 0) {
       // A-resident Tucker GEMM: one CTA per 128-row block over all column tiles
-      const int kc = (int)ceil_div(r3p, (int64_t)tr::BK);
+      // Bt chunk width x ring depth: 16 columns x 3 stages, or 32 x 2 for short K
+      // (same-job A/B: C5, K = 132: 2.82 vs 2.98 ms per 64 planes; C4, K = 40:
+      // 0.381 vs 0.355 ms); RSB200_TUCKER_BK=16|32 forces one
+      static const int bk_env = [] {
+        const char *e = getenv("RSB200_TUCKER_BK");
+        return e ? atoi(e) : 0;
+      }();
+      const int bk = bk_env == 16 || bk_env == 32 ? bk_env : (r3p <= 64 ? 32 : 16);
       auto go = [&](auto bm_c) -> int {
         constexpr int BM = decltype(bm_c)::value;
-        const int smem = tr::smem_bytes(BM, kc);
-        auto fn = accumulate ? k_tucker_gemm_res<BM, true> : k_tucker_gemm_res<BM, false>;
-        cudaError_t e = smem_attr((const void *)fn, smem);
-        if (e != cudaSuccess)
-          return fail(RS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        fn<<<(unsigned)ceil_div(planes * n, (int64_t)BM), tr::threads(BM), smem, s>>>(
-            A, lda, Bt, lda, out, n, planes * n, n, (int)r3p);
-        return 0;
+        auto run = [&](auto bk_c, auto st_c) -> int {
+          constexpr int BK = decltype(bk_c)::value, STG = decltype(st_c)::value;
+          const int smem = tr::smem_bytes(BM, (int)r3p, BK, STG);
+          auto fn = accumulate ? k_tucker_gemm_res<BM, true, BK, STG>
+                               : k_tucker_gemm_res<BM, false, BK, STG>;
+          cudaError_t e = smem_attr((const void *)fn, smem);
+          if (e != cudaSuccess)
+            return fail(RS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+          fn<<<(unsigned)ceil_div(planes * n, (int64_t)BM), tr::threads(BM), smem, s>>>(
+              A, lda, Bt, lda, out, n, planes * n, n, (int)r3p);
+          return 0;
+        };
+        return bk == 16 ? run(std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{})
+                        : run(std::integral_constant<int, 32>{}, std::integral_constant<int, 2>{});
       };
       if ((st = g_tucker_res == 128 ? go(std::integral_constant<int, 128>{})
                                     : go(std::integral_constant<int, 64>{})))
