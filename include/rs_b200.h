@@ -220,7 +220,8 @@ int rs_short_l0_table(const double *ul, const double *wl, int64_t Rs, int64_t ga
 int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs);
 int64_t rs_short_mma_workspace_bytes(int64_t n, int64_t gamma);
 int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_t gamma,
-                          int64_t n, const int32_t *c1, const int32_t *c2, const double *zq,
+                          int64_t n, int64_t count /* copies: sizes the CTAs' tile batches */,
+                          const int32_t *c1, const int32_t *c2, const double *zq,
                           const int32_t *bstart, const int32_t *bc3, const int32_t *nb_dev,
                           int64_t x1_lo, int64_t x1_hi, int flags, double *out, void *work,
                           int64_t work_bytes, void *stream);

@@ -67,7 +67,7 @@ SIGNATURES = {
     "rs_fused_l0_supported": (_i32, [_i64, _i64, _i64]),
     "rs_short_mma_supported": (_i32, [_i64, _i64, _i64]),
     "rs_short_mma_workspace_bytes": (_i64, [_i64, _i64]),
-    "rs_assemble_short_mma": (_i32, [_ptr, _ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr,
+    "rs_assemble_short_mma": (_i32, [_ptr, _ptr, _i64, _i64, _i64, _i64, _ptr, _ptr, _ptr, _ptr, _ptr,
                                      _ptr, _i64, _i64, _i32, _ptr, _ptr, _i64, _ptr]),
     "rs_short_l0_bytes": (_i64, [_i64]),
     "rs_short_l0_table": (_i32, [_ptr, _ptr, _i64, _i64, _ptr, _ptr]),

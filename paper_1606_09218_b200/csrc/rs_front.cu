@@ -187,7 +187,7 @@ int rs_front(const double *pos, const double *z, int64_t count, double h, int64_
   if (method == RS_SHORT_MMA) {  // fused tensor-core kernel, term table at work[0]
     for (int64_t p0 = x1_lo; p0 < x1_hi; p0 += grp) {
       const int64_t p1 = std::min<int64_t>(x1_hi, p0 + grp);
-      if ((st = rs_assemble_short_mma(ul, wl, Rs, gamma, n, (const int32_t *)P(F_C1),
+      if ((st = rs_assemble_short_mma(ul, wl, Rs, gamma, n, count, (const int32_t *)P(F_C1),
                                       (const int32_t *)P(F_C2), (const double *)P(F_ZQ),
                                       (const int32_t *)P(F_BSTART), (const int32_t *)P(F_BC3),
                                       (const int32_t *)P(F_NB), p0, p1, RS_ASM_KOFD_READY,

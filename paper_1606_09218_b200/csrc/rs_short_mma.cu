@@ -136,6 +136,27 @@ __global__ void k_x2_index(const int32_t *__restrict__ c2, const int32_t *__rest
   }
 }
 
+// explicit shared-space loads (32-bit addresses): the generic-pointer form made
+// the compiler rebuild the shared window base inside the K loop
+__device__ __forceinline__ double sm_lds(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ double sm_lds_at(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+__device__ __forceinline__ void sm_lds_rec(uint32_t a, double &z, int &o1, int &o2) {
+  int lo, hi;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(lo), "=r"(hi), "=r"(o1), "=r"(o2)
+               : "r"(a));
+  z = __hiloint2double(hi, lo);
+}
+
 template <bool ACC>
 __global__ void __launch_bounds__(SM_THREADS, 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
@@ -236,36 +257,50 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
       }
       __syncthreads();
       const int steps = (ncol + 3) >> 2;
-      int si = -1, seg_end = 0, col0 = 0, q_lo = 0, q_hi = 0, bo = 0;
-      const double *ut1 = ut + warp, *ut2 = ut + gid;
+      int si = -1, seg_end = 0, col0 = 0;
+      uint32_t qa_lo = 0, qa_hi = 0, bob = 0;
+      const uint32_t ut_s = smem_addr(ut), rec_s = smem_addr(s_rec), seg_s = smem_addr(s_seg);
+      const uint32_t ut1_s = ut_s + 8 * warp, ut2_s = ut_s + 8 * gid;
+      const int LDb = LD * 8;
       for (int st = 0; st < steps; ++st) {
         const int c = 4 * st + tig;
         double a0 = 0.0, a1 = 0.0, b[8];
         if (c < ncol) {
           if (c >= seg_end) {   // this lane's column enters a new segment
-            SmSeg sg;
+            int q_lo, K, bo, nq;
             do {
-              sg = s_seg[++si];
-              seg_end = sg.col + sg.K;
+              ++si;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(q_lo), "=r"(col0), "=r"(K), "=r"(bo)
+                           : "r"(seg_s + 16 * si));
+              seg_end = col0 + K;
             } while (c >= seg_end);
-            col0 = sg.col;
-            q_lo = sg.q_lo;
-            bo = sg.bo;
-            q_hi = s_seg[si + 1].q_lo;
+            asm volatile("ld.shared.b32 %0, [%1+16];" : "=r"(nq) : "r"(seg_s + 16 * si));
+            qa_lo = rec_s + 16 * q_lo;
+            qa_hi = rec_s + 16 * nq;
+            bob = 8 * bo;
           }
-          const int koff = (c - col0) * LD;
-          const double *u1 = ut1 + koff, *u2 = ut2 + koff;
+          const uint32_t koff = (uint32_t)((c - col0) * LDb);
+          const uint32_t u1 = ut1_s + koff, u2 = ut2_s + koff;
 #pragma unroll 2
-          for (int q = q_lo; q < q_hi; ++q) {
-            const SmRec r = s_rec[q];
-            const double t = r.z * u1[r.o1];
-            const double *w2 = u2 + r.o2;
-            a0 = fma(t, w2[0], a0);
-            a1 = fma(t, w2[8], a1);
+          for (uint32_t qa = qa_lo; qa < qa_hi; qa += 16) {
+            double z;
+            int o1, o2;
+            sm_lds_rec(qa, z, o1, o2);
+            const double t = z * sm_lds(u1 + o1);
+            const uint32_t w2 = u2 + o2;
+            a0 = fma(t, sm_lds(w2), a0);
+            a1 = fma(t, sm_lds_at<64>(w2), a1);
           }
-          const double *ub = u2 + bo;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) b[j] = ub[8 * j];
+          const uint32_t ub = u2 + bob;
+          b[0] = sm_lds(ub);
+          b[1] = sm_lds_at<64>(ub);
+          b[2] = sm_lds_at<128>(ub);
+          b[3] = sm_lds_at<192>(ub);
+          b[4] = sm_lds_at<256>(ub);
+          b[5] = sm_lds_at<320>(ub);
+          b[6] = sm_lds_at<384>(ub);
+          b[7] = sm_lds_at<448>(ub);
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) b[j] = 0.0;
@@ -342,8 +377,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             if (kn > 0) {
               cov = true;
               rec.z = zq[p];
-              rec.o1 = X0 - a1 + gamma + SM_PAD;
-              rec.o2 = Y0 - a2 + gamma + SM_PAD;
+              rec.o1 = 8 * (X0 - a1 + gamma + SM_PAD);   // byte offsets into a table row
+              rec.o2 = 8 * (Y0 - a2 + gamma + SM_PAD);
               bo = Z0 - a3 + gamma + SM_PAD;   // B offset: identifies the bucket as well
             }
           }
@@ -415,7 +450,7 @@ int64_t rs_short_mma_workspace_bytes(int64_t n, int64_t gamma) {
  * flags: RS_ASM_ACCUMULATE adds to `out`; RS_ASM_KOFD_READY: the term table at
  * offset 0 of `work` is already filled (rsb_asm_term_prefix). */
 int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_t gamma, int64_t n,
-                          const int32_t *c1, const int32_t *c2, const double *zq,
+                          int64_t count, const int32_t *c1, const int32_t *c2, const double *zq,
                           const int32_t *bstart, const int32_t *bc3, const int32_t *nb_dev,
                           int64_t x1_lo, int64_t x1_hi, int flags, double *out, void *work,
                           int64_t work_bytes, void *stream) {
@@ -459,7 +494,15 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
     return e && atoi(e) > 0 ? atoi(e) : 256;
   }();
   const int64_t slots = (int64_t)sms * per_sm;
-  const int tiles_per_cta = (int)std::max<int64_t>(1, ceil_div(ntiles, slots * waves));
+  // tiles per CTA: at least ~100 us of work per staged factor table (a tile
+  // costs ~0.3 us per window covering a grid point: C5 ~5 us, C2-C4 ~100 us)
+  // when the launch has that many tiles per SM slot, and no more than
+  // 1/waves of a slot's share, so CTAs keep turning over
+  const double w = (double)std::min<int64_t>(2 * gamma + 1, n);
+  const double ov = std::max(1.0, (double)std::max<int64_t>(count, 1) * (w / n) * (w / n) * (w / n));
+  const int64_t t_min = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)(100.0 / (0.3 * ov))));
+  const int tiles_per_cta = (int)std::max<int64_t>(
+      ceil_div(ntiles, slots * waves), std::min<int64_t>(t_min, ceil_div(ntiles, slots)));
   const unsigned grid = (unsigned)ceil_div(ntiles, tiles_per_cta);
   ProfScope ps(s, "short_mma");
   fn<<<grid, SM_THREADS, L.total, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,

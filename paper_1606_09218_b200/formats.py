@@ -509,7 +509,7 @@ def assemble_grid(long: Optional[TuckerTensor], short: Optional[CCT], x1_lo: int
         lay = short.device_layout()
         ws = nat.Workspace.get(L.rs_short_mma_workspace_bytes(n, short.gamma), "short_mma")
         nat.check(L.rs_assemble_short_mma(
-            nat.ptr(lay["ul"]), nat.ptr(lay["wl"]), short.local.rank, short.gamma, n,
+            nat.ptr(lay["ul"]), nat.ptr(lay["wl"]), short.local.rank, short.gamma, n, short.count,
             nat.ptr(lay["c1"]), nat.ptr(lay["c2"]), nat.ptr(lay["zq"]), nat.ptr(lay["bstart"]),
             nat.ptr(lay["bc3"]), nat.ptr(lay["nb"]), x1_lo, x1_hi,
             nat.ASM_ACCUMULATE if (accumulate or long is not None) else 0, out.data_ptr(),
