@@ -55,6 +55,7 @@ constexpr int SM_THREADS = 256;
 constexpr int SM_PAD = 64;     // zero margin of the factor table, >= every tile edge
 constexpr int SM_CAP = 512;    // staged candidate copies per MMA phase
 constexpr int SM_MAXR = 24;    // largest short rank
+constexpr int SM_MAXT3 = 256;  // x3 tiles per grid row (n <= 16384)
 
 __host__ __device__ inline int sm_pitch(int gamma) {
   int ld = 2 * gamma + 1 + 2 * SM_PAD;
@@ -178,7 +179,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   int *s_b3 = s_off + SM_THREADS;
   int *skofd = (int *)(sm_raw + L.kofd);
   __shared__ int wsum[SM_THREADS / 32];
-  __shared__ int s_band[2], s_tile;
+  __shared__ int s_tile[2];
+  __shared__ int s_bands[2 * SM_MAXT3];   // bucket band [lo, hi) of every x3 tile
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -199,16 +201,35 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     const int d = e / Rs, k = e - d * Rs;
     ut[k * LD + SM_PAD + d] = cbrt(wl[k]) * ul[e];
   }
+  // occupied x3 buckets within gamma of each x3 tile: found once per CTA, all
+  // tiles in parallel (per tile this was ~18 dependent global loads by one
+  // thread with the CTA waiting at a barrier)
+  for (int t3 = tid; t3 < n3t; t3 += SM_THREADS) {
+    const int lo_x = t3 * SM_T3 - gamma, hi_x = t3 * SM_T3 + SM_T3 - 1 + gamma;
+    int l = 0, h = nb;
+    while (l < h) {
+      const int m = (l + h) >> 1;
+      if (bc3[m] < lo_x) l = m + 1; else h = m;
+    }
+    s_bands[2 * t3] = l;
+    h = nb;
+    while (l < h) {
+      const int m = (l + h) >> 1;
+      if (bc3[m] <= hi_x) l = m + 1; else h = m;
+    }
+    s_bands[2 * t3 + 1] = l;
+  }
 
   // a CTA retires after tiles_per_cta tiles: the turnover lets the kernels of a
   // higher-priority stream (the latency-bound Gram / eigen / core chain) onto
   // the SMs between two CTAs instead of behind the whole grid
+  if (tid == 0) s_tile[0] = atomicAdd(counter, 1);
   for (int done = 0; done < tiles_per_cta; ++done) {
     __syncthreads();   // previous tile done with the staging arrays; table complete
-    if (tid == 0) s_tile = atomicAdd(counter, 1);
-    __syncthreads();
-    const int64_t tile = s_tile;
+    const int64_t tile = s_tile[done & 1];
     if (tile >= ntiles) break;
+    // the next tile's index is requested now: the atomic's latency hides under this tile
+    if (tid == 0 && done + 1 < tiles_per_cta) s_tile[(done + 1) & 1] = atomicAdd(counter, 1);
     const int t3 = (int)(tile % n3t), t2 = (int)((tile / n3t) % n2t);
     const int64_t t1 = tile / ((int64_t)n3t * n2t);
     const int X0 = (int)(x1_base + t1 * SM_T1), Y0 = t2 * SM_T2, Z0 = t3 * SM_T3;
@@ -314,23 +335,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     };
 
     // candidate copies of this tile, bucket group by bucket group
-    if (tid == 0) {
-      const int lo_x = Z0 - gamma, hi_x = Z0 + SM_T3 - 1 + gamma;
-      int l = 0, h = nb;
-      while (l < h) {
-        const int m = (l + h) >> 1;
-        if (bc3[m] < lo_x) l = m + 1; else h = m;
-      }
-      s_band[0] = l;
-      h = nb;
-      while (l < h) {
-        const int m = (l + h) >> 1;
-        if (bc3[m] <= hi_x) l = m + 1; else h = m;
-      }
-      s_band[1] = l;
-    }
-    __syncthreads();
-    const int blo = s_band[0], bhi = s_band[1];
+    const int blo = s_bands[2 * t3], bhi = s_bands[2 * t3 + 1];
     const int c1lo = X0 - gamma, c1hi = X0 + SM_T1 - 1 + gamma;
     const int c2lo = Y0 - gamma, c2hi = Y0 + SM_T2 - 1 + gamma;
     int len = 0;
@@ -368,6 +373,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
           }
           const int p = s_lo[l] + (v - s_off[l]);
           const int a1 = c1[p], a2 = c2[p];
+          const double zp = zq[p];   // with the coordinates: one memory round trip, not two
           if (a1 >= c1lo && a1 <= c1hi && a2 >= c2lo && a2 <= c2hi) {
             const int a3 = s_b3[l];
             const int d1 = max(0, max(X0 - a1, a1 - (X0 + SM_T1 - 1)));
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             kn = skofd[max(d1, max(d2, d3))];
             if (kn > 0) {
               cov = true;
-              rec.z = zq[p];
+              rec.z = zp;
               rec.o1 = 8 * (X0 - a1 + gamma + SM_PAD);   // byte offsets into a table row
               rec.o2 = 8 * (Y0 - a2 + gamma + SM_PAD);
               bo = Z0 - a3 + gamma + SM_PAD;   // B offset: identifies the bucket as well
@@ -435,6 +441,7 @@ extern "C" {
 
 int rs_short_mma_supported(int64_t n, int64_t gamma, int64_t Rs) {
   if (n < 2 || n % 2 || gamma < 0 || Rs < 1 || Rs > SM_MAXR) return 0;
+  if (ceil_div(n, SM_T3) > SM_MAXT3) return 0;
   const SmLayout L = sm_layout((int)gamma, (int)Rs);
   return L.total + 4096 <= 227 * 1024 ? 1 : 0;
 }
