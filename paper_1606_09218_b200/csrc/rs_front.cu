@@ -36,6 +36,11 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
                        void *stream);
 }
 
+int rsb_shift_project3_listed(const double *Z1, const double *Z2, const double *Z3, int64_t r1,
+                              int64_t r2, int64_t r3, int64_t n, const double *table,
+                              int64_t ld_table, int64_t R, const int64_t *shift, int64_t count,
+                              double *TT1, double *TT2, double *TT3, void *list_work,
+                              cudaStream_t s);  // rs_kernels.cu
 extern "C" int rsb_asm_term_prefix(const double *ul, const double *wl, int Rs, int gamma,
                                    void *work, cudaStream_t s);
 
@@ -385,7 +390,7 @@ int64_t rs_back_workspace_bytes(int64_t n, int64_t r1, int64_t r2, int64_t r3, i
   const int64_t nq = nq_host > 0 ? nq_host : std::min<int64_t>(n, count), ld = ldh_of(nq, R);
   const int64_t hb = round_up(r1 * r2 * ld * 8, 256) + round_up(r3 * ld * 8, 256) +
                      (r1 + r2) * n * R * 8;
-  return round_up((r1 + r2 + r3) * n * R * 8, 256) +
+  return round_up((r1 + r2 + r3) * n * R * 8, 256) + round_up((6 * n + 8) * 4, 256) +
          std::max<int64_t>(rs_core_workspace_bytes(r1, r2, r3, count, R), hb);
 }
 
@@ -419,10 +424,17 @@ static int back_impl(const double *U, int64_t b, int64_t n, int64_t r1, int64_t 
   int st;
   if ((st = check_launch("rs_back factors"))) return st;
   double *TT1 = (double *)work, *TT2 = TT1 + r1 * n * R, *TT3 = TT2 + r2 * n * R;
-  if ((st = rs_shift_project3(Z1, Z2, Z3, r1, r2, r3, n, table, ld_table, R, n, TT1, TT2, TT3,
-                              stream)))
+  // projections at the occupied shifts only (the core reads no others)
+  char *lw = (char *)work + round_up((r1 + r2 + r3) * n * R * 8, 256);
+  if (n <= 8192) {
+    if ((st = rsb_shift_project3_listed(Z1, Z2, Z3, r1, r2, r3, n, table, ld_table, R, starts,
+                                        count, TT1, TT2, TT3, lw, s)))
+      return st;
+  } else if ((st = rs_shift_project3(Z1, Z2, Z3, r1, r2, r3, n, table, ld_table, R, n, TT1, TT2,
+                                     TT3, stream))) {
     return st;
-  char *cw = (char *)work + round_up((r1 + r2 + r3) * n * R * 8, 256);
+  }
+  char *cw = lw + round_up((6 * n + 8) * 4, 256);
   // the particle-K Khatri-Rao GEMM is latency-bound and cheap below ~1e10
   // flops (C1-C3); the bucket-K form wins once N R_l r1 r2 r3 dominates (C4, C5)
   const double kr_flops = 2.0 * (double)r1 * r2 * r3 * (double)count * R;

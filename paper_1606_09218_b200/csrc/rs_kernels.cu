@@ -299,6 +299,92 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The projections are read only at the shifts the particles occupy (mode l:
+// n - c_l of some particle; C5: ~360 of 2048).  k_shift_flags marks them,
+// k_shift_compact lists them in ascending order (one block per mode), and
+// k_shift_project_list is k_shift_project over 32 consecutive LISTED shifts:
+// its table window spans first..last listed shift + n rows (<= 2n).
+__device__ __forceinline__ int block_exclusive_scan(int v, int *wsum, int *total);
+
+__global__ void k_shift_flags(const int64_t *__restrict__ shift, int64_t count, int64_t n,
+                              int *__restrict__ flags) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 3 * count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sft = shift[e];
+    if (sft >= 0 && sft < n) flags[(e % 3) * n + sft] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    k_shift_compact(const int *__restrict__ flags, int64_t n, int *__restrict__ list,
+                    int *__restrict__ cnt) {
+  __shared__ int wsum[32];
+  const int l = blockIdx.x;
+  int base = 0;
+  for (int64_t s0 = 0; s0 < n; s0 += 1024) {
+    const int64_t sft = s0 + threadIdx.x;
+    const int f = sft < n ? flags[l * n + sft] : 0;
+    int tot;
+    const int pos = block_exclusive_scan(f, wsum, &tot);
+    if (f) list[l * n + base + pos] = (int)sft;
+    base += tot;
+  }
+  if (threadIdx.x == 0) cnt[l] = base;
+}
+
+__global__ void __launch_bounds__(256)
+    k_shift_project_list(Proj3 pj, int64_t n, const double *__restrict__ T, int64_t ld_table,
+                         int64_t R, int64_t n_shift, const int *__restrict__ list,
+                         const int *__restrict__ cnt) {
+  const int l = blockIdx.z;
+  const int m = cnt[l];
+  const int j0 = blockIdx.x * SP_SHIFTS;
+  if (j0 >= m) return;
+  const double *__restrict__ Z = pj.Z[l];
+  double *__restrict__ TT = pj.TT[l];
+  const int64_t r = pj.r[l], ldz = r;
+  extern __shared__ double win[];      // up to 2n, then SP_ICH * 32
+  const int *ls = list + (int64_t)l * n;
+  const int nsh = min(SP_SHIFTS, m - j0);
+  const int64_t s_first = ls[j0], s_last = ls[j0 + nsh - 1];
+  const int64_t len = s_last - s_first + n;
+  double *zs = win + 2 * n;
+  const int64_t k = blockIdx.y;
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+    const int64_t row = s_first + e;
+    win[e] = row < 2 * n ? T[row * ld_table + k] : 0.0;
+  }
+  const int sl = threadIdx.x % SP_SHIFTS, a0 = threadIdx.x / SP_SHIFTS;  // a0 < 8
+  const int64_t sft = sl < nsh ? ls[j0 + sl] : s_first;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t a_base = 0; a_base < r; a_base += 32) {
+    for (int u = 0; u < 4; ++u) acc[u] = 0.0;
+    for (int64_t i0 = 0; i0 < n; i0 += SP_ICH) {
+      const int64_t ni = n - i0 < SP_ICH ? n - i0 : SP_ICH;
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < ni * 32; e += blockDim.x) {
+        int64_t ii = e / 32, aa = a_base + e % 32;
+        zs[e] = aa < r ? Z[(i0 + ii) * ldz + aa] : 0.0;
+      }
+      __syncthreads();
+      const double *w = win + (sft - s_first) + i0;
+      for (int64_t ii = 0; ii < ni; ++ii) {
+        const double wv = w[ii];
+        const double *zr = zs + ii * 32 + a0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(zr[8 * u], wv, acc[u]);
+      }
+    }
+    if (sl < nsh && sft < n_shift) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int64_t a = a_base + a0 + 8 * u;
+        if (a < r) TT[(a * n_shift + sft) * R + k] = acc[u];
+      }
+    }
+  }
+}
+
 // Per-mode shift histograms c[l][s] = sum_{p: n - idx[p][l] == s} z_p^2 and
 // the x3 occupancy counts cnt[x] = #{p: idx[p][2] == x}.  Warp per (mode, s):
 // lanes stride the particles (staged in shared memory, shared by the block's
@@ -1797,6 +1883,37 @@ int rs_shift_project3(const double *Z1, const double *Z2, const double *Z3, int6
   return check_launch("rs_shift_project3");
 }
 
+}  // extern "C"
+
+// (internal) rs_shift_project3 restricted to the shifts in `shift` (count x 3,
+// n - c of the particles); list_work: (6 n + 8) ints.  Entries of TT at other
+// shifts are left untouched (they are never read).
+int rsb_shift_project3_listed(const double *Z1, const double *Z2, const double *Z3, int64_t r1,
+                              int64_t r2, int64_t r3, int64_t n, const double *table,
+                              int64_t ld_table, int64_t R, const int64_t *shift, int64_t count,
+                              double *TT1, double *TT2, double *TT3, void *list_work,
+                              cudaStream_t s) {
+  int *flags = (int *)list_work, *list = flags + 3 * n, *cnt = list + 3 * n;
+  if (cudaMemsetAsync(flags, 0, (size_t)(3 * n) * 4, s) != cudaSuccess)
+    return fail(RS_ERR_CUDA, "shift list: memset");
+  k_shift_flags<<<grid_blocks(3 * count), 256, 0, s>>>(shift, count, n, flags);
+  k_shift_compact<<<3, 1024, 0, s>>>(flags, n, list, cnt);
+  int st;
+  if ((st = check_launch("shift list"))) return st;
+  const size_t smem = (size_t)(2 * n + SP_ICH * 32) * 8;
+  if (smem > 200 * 1024) return fail(RS_ERR_UNSUPPORTED, "shift_project: n too large");
+  cudaError_t e = smem_attr((const void *)k_shift_project_list, (int)smem);
+  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "shift_project smem: %s", cudaGetErrorString(e));
+  Proj3 pj{{Z1, Z2, Z3}, {TT1, TT2, TT3}, {r1, r2, r3}};
+  {
+    ProfScope ps(s, "shift_project");
+    dim3 grid((unsigned)ceil_div(n, SP_SHIFTS), (unsigned)R, 3);
+    k_shift_project_list<<<grid, 256, smem, s>>>(pj, n, table, ld_table, R, n, list, cnt);
+  }
+  return check_launch("shift_project_list");
+}
+
+extern "C" {
 int rs_shift_hist(const int64_t *idx, const double *z, int64_t count, int64_t n, double *c,
                   int32_t *cnt3, void *stream) {
   RS_REQUIRE(count >= 1 && n >= 2, "rs_shift_hist: bad sizes");
