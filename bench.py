@@ -205,12 +205,18 @@ def reference_assembly_time(name, budget_s=8.0):
     zs = [zz[:, :r] for zz, r in zip(zs, ranks)]
     t0 = time.perf_counter()
     pr = [zz.T @ u for zz, u in zip(zs, facs)]
+    t_proj = time.perf_counter() - t0
+    # the core contraction (einsum, 2 r1 r2 r3 flops per column at ~3.5e9 flop/s)
+    # on its own, smaller column sample: ~0.15 budget
+    kc = int(max(4 * nt, min(weights.size, 0.15 * budget_s * 3.5e9 /
+                             (2.0 * ranks[0] * ranks[1] * ranks[2]))))
+    t0 = time.perf_counter()
     core = np.zeros(ranks)
-    for lo in range(0, weights.size, 2048):
-        hi = min(lo + 2048, weights.size)
+    for lo in range(0, kc, 2048):
+        hi = min(lo + 2048, kc)
         core += np.einsum("k,ak,bk,ck->abc", weights[lo:hi], pr[0][:, lo:hi], pr[1][:, lo:hi],
                           pr[2][:, lo:hi], optimize=True)
-    t_core = time.perf_counter() - t0
+    t_core = t_proj + (time.perf_counter() - t0) * weights.size / kc   # scaled to the Gram sample
     del facs, grams, pr
     # Tucker dense on a slab of planes (2 r1 n^3-dominated: ~0.15 budget)
     planes = int(max(1, min(n, 0.15 * budget_s * 5e10 / (2.0 * ranks[0] * n * n + 1))))
@@ -230,6 +236,7 @@ def reference_assembly_time(name, budget_s=8.0):
     total = (t_snap + t_eigh + (t_gram + t_core) * kscale + t_tucker * n / planes
              + t_cct / frac)
     det = dict(measured_s=measured, extrapolated_s=total, gram_particles=int(sub.size),
+               core_columns=kc,
                tucker_planes=planes, cct_stride=cstride, pair_fraction=frac,
                stages_s=dict(snap=t_snap, eigh=t_eigh, gram_x=t_gram * kscale,
                              core_x=t_core * kscale, tucker_x=t_tucker * n / planes,
@@ -242,8 +249,9 @@ def reference_sample_text(name, det, cores):
     return (f"{name} reference pipeline (oracle numpy port of rstensor build_rs + dense_rs; BLAS "
             f"on {cores} threads, dense_cct single-threaded like the reference), EXTRAPOLATED "
             f"per stage from a bounded sample: {det['measured_s']:.1f} s measured -> "
-            f"{det['extrapolated_s']:.1f} s per assembly. Snap + 3 eigh at full size; Gram + core "
-            f"on {det['gram_particles']} particles (x N/sample); Tucker dense on "
+            f"{det['extrapolated_s']:.1f} s per assembly. Snap + 3 eigh at full size; Gram + "
+            f"projections on {det['gram_particles']} particles (x N/sample), the core einsum on "
+            f"{det['core_columns']} of their columns (x columns/sample); Tucker dense on "
             f"{det['tucker_planes']} planes (x n/planes); dense_cct on every "
             f"{det['cct_stride']}-th particle = {det['pair_fraction']:.4f} of the pairs (x 1/that). "
             f"Extrapolated stage seconds: " + ", ".join(f"{k} {v:.2f}" for k, v in st.items()))

@@ -262,7 +262,7 @@ __global__ void k_ritz_to_factors(const double *__restrict__ U, int64_t b, int64
 // with H[(a,b),(q,k)] = sum_{i in bucket q} zq_i w_k TT1[a, n-c1_i, k] TT2[b, n-c2_i, k]
 // and T3[c,(q,k)] = TT3[c, n - x3_q, k]: the K of the core GEMM drops from
 // N R_l (particles x terms) to (occupied x3 values) x R_l.
-constexpr int CH_CHUNK = 32;   // bucket copies staged per pass
+constexpr int CH_CHUNK = 64;   // bucket copies staged per pass (32: C5 core_h 6.9 ms)
 constexpr int CH_RMAX = 24;
 
 // TTt[s][k][a] = TT[a][s][k]: per-(shift, term) vectors contiguous in a
