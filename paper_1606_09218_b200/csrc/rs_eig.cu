@@ -502,6 +502,9 @@ __global__ void __launch_bounds__(T::THREADS)
 
 using TileEig = Tile<64, 64, 32, 32, 3>;
 using TileEigS = Tile<32, 32, 16, 16, 3>;  // skinny Ritz blocks (b <= 32): 4x the CTAs
+// N just above a multiple of 64 (the Tucker operand GEMM at C5: N = r3 = 132 -> 3 x 64 = 192
+// columns computed, 69 % useful): 48-wide tiles (3 x 48 = 144, 92 %)
+using TileEigN48 = Tile<128, 48, 32, 24, 3>;
 
 template <class T>
 static int gemm_batched_t(const double *A, int64_t lda, int64_t sA, const double *B, int64_t ldb,
@@ -522,6 +525,8 @@ static int gemm_batched(const double *A, int64_t lda, int64_t sA, const double *
                         int64_t K, int nb, cudaStream_t s) {
   if (M <= 32 || N <= 32)
     return gemm_batched_t<TileEigS>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
+  if (M >= 256 && 100 * ceil_div(N, 48) * 48 <= 85 * ceil_div(N, 64) * 64)
+    return gemm_batched_t<TileEigN48>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
   return gemm_batched_t<TileEig>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, nb, s);
 }
 
