@@ -56,6 +56,8 @@ constexpr int SM_PAD = 64;     // zero margin of the factor table, >= every tile
 constexpr int SM_CAP = 512;    // staged candidate copies per MMA phase
 constexpr int SM_MAXR = 24;    // largest short rank
 constexpr int SM_MAXT3 = 256;  // x3 tiles per grid row (n <= 16384)
+constexpr int SM_ACH = 16;     // columns per staged A chunk (builder variant)
+constexpr int SM_ALD = 132;    // doubles per A column: 8 planes x 16 rows + 4 (= 4 mod 16)
 
 __host__ __device__ inline int sm_pitch(int gamma) {
   int ld = 2 * gamma + 1 + 2 * SM_PAD;
@@ -64,7 +66,7 @@ __host__ __device__ inline int sm_pitch(int gamma) {
 }
 
 struct SmLayout {
-  int table, rec, cb, kn, seg, grp, kofd, total;  // byte offsets
+  int table, rec, cb, kn, seg, grp, kofd, abuf, total;  // byte offsets
 };
 
 // one staged candidate copy: charge and the two table offsets of its window
@@ -81,7 +83,7 @@ struct __align__(16) SmSeg {
   int bo;       // B offset Z0 - s + gamma + PAD
 };
 
-__host__ __device__ inline SmLayout sm_layout(int gamma, int Rs) {
+__host__ __device__ inline SmLayout sm_layout(int gamma, int Rs, bool build = false) {
   SmLayout L;
   int o = 0;
   L.table = o; o += Rs * sm_pitch(gamma) * 8;
@@ -91,6 +93,8 @@ __host__ __device__ inline SmLayout sm_layout(int gamma, int Rs) {
   L.kn = o;    o += (SM_CAP + 4) * 4;            // live terms per staged copy
   L.grp = o;   o += 3 * SM_THREADS * 4 + 64;     // per-bucket lo / offset / x3 of a group
   L.kofd = o;  o += (gamma + 2) * 4;
+  o = (o + 15) & ~15;
+  L.abuf = o;  o += build ? 2 * SM_ACH * SM_ALD * 8 : 0;   // two A chunks (builder variant)
   L.total = (o + 15) & ~15;
   return L;
 }
@@ -158,7 +162,7 @@ __device__ __forceinline__ void sm_lds_rec(uint32_t a, double &z, int &o1, int &
   z = __hiloint2double(hi, lo);
 }
 
-template <bool ACC>
+template <bool ACC, bool BUILD>
 __global__ void __launch_bounds__(SM_THREADS, 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
                 int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter, int tiles_per_cta,
                 double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  const SmLayout L = sm_layout(gamma, Rs);
+  const SmLayout L = sm_layout(gamma, Rs, BUILD);
   double *ut = (double *)(sm_raw + L.table);
   SmRec *s_rec = (SmRec *)(sm_raw + L.rec);
   SmSeg *s_seg = (SmSeg *)(sm_raw + L.seg);
@@ -277,59 +281,165 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         s_seg[nseg] = sg;
       }
       __syncthreads();
-      const int steps = (ncol + 3) >> 2;
-      int si = -1, seg_end = 0, col0 = 0;
-      uint32_t qa_lo = 0, qa_hi = 0, bob = 0;
-      const uint32_t ut_s = smem_addr(ut), rec_s = smem_addr(s_rec), seg_s = smem_addr(s_seg);
-      const uint32_t ut1_s = ut_s + 8 * warp, ut2_s = ut_s + 8 * gid;
-      const int LDb = LD * 8;
-      for (int st = 0; st < steps; ++st) {
-        const int c = 4 * st + tig;
-        double a0 = 0.0, a1 = 0.0, b[8];
-        if (c < ncol) {
-          if (c >= seg_end) {   // this lane's column enters a new segment
-            int q_lo, K, bo, nq;
-            do {
-              ++si;
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(q_lo), "=r"(col0), "=r"(K), "=r"(bo)
-                           : "r"(seg_s + 16 * si));
-              seg_end = col0 + K;
-            } while (c >= seg_end);
-            asm volatile("ld.shared.b32 %0, [%1+16];" : "=r"(nq) : "r"(seg_s + 16 * si));
-            qa_lo = rec_s + 16 * q_lo;
-            qa_hi = rec_s + 16 * nq;
-            bob = 8 * bo;
+      if constexpr (!BUILD) {
+        const int steps = (ncol + 3) >> 2;
+        int si = -1, seg_end = 0, col0 = 0;
+        uint32_t qa_lo = 0, qa_hi = 0, bob = 0;
+        const uint32_t ut_s = smem_addr(ut), rec_s = smem_addr(s_rec), seg_s = smem_addr(s_seg);
+        const uint32_t ut1_s = ut_s + 8 * warp, ut2_s = ut_s + 8 * gid;
+        const int LDb = LD * 8;
+        for (int st = 0; st < steps; ++st) {
+          const int c = 4 * st + tig;
+          double a0 = 0.0, a1 = 0.0, b[8];
+          if (c < ncol) {
+            if (c >= seg_end) {   // this lane's column enters a new segment
+              int q_lo, K, bo, nq;
+              do {
+                ++si;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(q_lo), "=r"(col0), "=r"(K), "=r"(bo)
+                             : "r"(seg_s + 16 * si));
+                seg_end = col0 + K;
+              } while (c >= seg_end);
+              asm volatile("ld.shared.b32 %0, [%1+16];" : "=r"(nq) : "r"(seg_s + 16 * si));
+              qa_lo = rec_s + 16 * q_lo;
+              qa_hi = rec_s + 16 * nq;
+              bob = 8 * bo;
+            }
+            const uint32_t koff = (uint32_t)((c - col0) * LDb);
+            const uint32_t u1 = ut1_s + koff, u2 = ut2_s + koff;
+  #pragma unroll 2
+            for (uint32_t qa = qa_lo; qa < qa_hi; qa += 16) {
+              double z;
+              int o1, o2;
+              sm_lds_rec(qa, z, o1, o2);
+              const double t = z * sm_lds(u1 + o1);
+              const uint32_t w2 = u2 + o2;
+              a0 = fma(t, sm_lds(w2), a0);
+              a1 = fma(t, sm_lds_at<64>(w2), a1);
+            }
+            const uint32_t ub = u2 + bob;
+            b[0] = sm_lds(ub);
+            b[1] = sm_lds_at<64>(ub);
+            b[2] = sm_lds_at<128>(ub);
+            b[3] = sm_lds_at<192>(ub);
+            b[4] = sm_lds_at<256>(ub);
+            b[5] = sm_lds_at<320>(ub);
+            b[6] = sm_lds_at<384>(ub);
+            b[7] = sm_lds_at<448>(ub);
+          } else {
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = 0.0;
           }
-          const uint32_t koff = (uint32_t)((c - col0) * LDb);
-          const uint32_t u1 = ut1_s + koff, u2 = ut2_s + koff;
-#pragma unroll 2
-          for (uint32_t qa = qa_lo; qa < qa_hi; qa += 16) {
-            double z;
-            int o1, o2;
-            sm_lds_rec(qa, z, o1, o2);
-            const double t = z * sm_lds(u1 + o1);
-            const uint32_t w2 = u2 + o2;
-            a0 = fma(t, sm_lds(w2), a0);
-            a1 = fma(t, sm_lds_at<64>(w2), a1);
+  #pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            dmma_884(acc[0][j], a0, b[j]);
+            dmma_884(acc[1][j], a1, b[j]);
           }
-          const uint32_t ub = u2 + bob;
-          b[0] = sm_lds(ub);
-          b[1] = sm_lds_at<64>(ub);
-          b[2] = sm_lds_at<128>(ub);
-          b[3] = sm_lds_at<192>(ub);
-          b[4] = sm_lds_at<256>(ub);
-          b[5] = sm_lds_at<320>(ub);
-          b[6] = sm_lds_at<384>(ub);
-          b[7] = sm_lds_at<448>(ub);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) b[j] = 0.0;
         }
+      } else {
+        // Builder variant (many copies per bucket: C2-C4).  The 128 A values of a
+        // column, A[(x1,x2)] = sum_p (z_p v_k[x1-c1p]) v_k[x2-c2p], are a rank-(copies)
+        // product P (8 x copies) Q (copies x 16): ONE warp forms them with
+        // mma.m8n8k4 itself (2 DMMAs per 4 copies) from 3 table loads per lane and
+        // 4 copies, instead of every lane of every warp re-reading the copies'
+        // records and x2 factors (8x redundant across the planes, and the shared-
+        // memory bandwidth bound of the per-lane form).  Columns go through a
+        // double-buffered shared A chunk of 16; warp w builds columns 2w, 2w + 1 of
+        // the next chunk, then runs the 4 k-steps of the current one: one barrier
+        // per chunk.
+        const uint32_t ut_s = smem_addr(ut), rec_s = smem_addr(s_rec), seg_s = smem_addr(s_seg);
+        const uint32_t ab_s = smem_addr(sm_raw + L.abuf);
+        const int LDb = LD * 8;
+        const int nchunks = (ncol + SM_ACH - 1) / SM_ACH;
+        int bsi = -1, bseg_end = 0, bcol0 = 0;      // builder cursor (warp-uniform)
+        uint32_t bqa_lo = 0, bqa_hi = 0;
+        auto build = [&](int ch) {
+          const uint32_t buf = ab_s + (uint32_t)((ch & 1) * SM_ACH * SM_ALD * 8);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          dmma_884(acc[0][j], a0, b[j]);
-          dmma_884(acc[1][j], a1, b[j]);
+          for (int u = 0; u < 2; ++u) {
+            const int cl = 2 * warp + u, c = ch * SM_ACH + cl;
+            double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+            if (c < ncol) {
+              if (c >= bseg_end) {
+                int q_lo, K, bo, nq;
+                do {
+                  ++bsi;
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(q_lo), "=r"(bcol0), "=r"(K), "=r"(bo)
+                               : "r"(seg_s + 16 * bsi));
+                  bseg_end = bcol0 + K;
+                } while (c >= bseg_end);
+                asm volatile("ld.shared.b32 %0, [%1+16];" : "=r"(nq) : "r"(seg_s + 16 * bsi));
+                bqa_lo = rec_s + 16 * q_lo;
+                bqa_hi = rec_s + 16 * nq;
+              }
+              const uint32_t ug = ut_s + (uint32_t)((c - bcol0) * LDb) + 8 * gid;
+              for (uint32_t qa = bqa_lo; qa < bqa_hi; qa += 64) {   // 4 copies per step
+                const uint32_t mine = qa + 16 * tig;
+                double z = 0.0;
+                int o1 = 0, o2 = 0;                 // offset 0: the table's zero margin
+                if (mine < bqa_hi) sm_lds_rec(mine, z, o1, o2);
+                const double av = z * sm_lds(ug + o1);
+                const uint32_t w2 = ug + o2;
+                dmma_884(d0, av, sm_lds(w2));
+                dmma_884(d1, av, sm_lds_at<64>(w2));
+              }
+            }
+            // A[col][x1 = gid][x2 = 2 tig .. +1] and [x2 = 8 + 2 tig .. +1]
+            const uint32_t dst = buf + (uint32_t)((cl * SM_ALD + gid * 16 + 2 * tig) * 8);
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(dst), "d"(d0[0]), "d"(d0[1]));
+            asm volatile("st.shared.v2.f64 [%0+64], {%1, %2};" ::"r"(dst), "d"(d1[0]), "d"(d1[1]));
+          }
+        };
+        int si = -1, seg_end = 0, col0 = 0;          // per-lane cursor of the main loop
+        uint32_t bob = 0;
+        const uint32_t ut2_s = ut_s + 8 * gid;
+        if (nchunks > 0) build(0);
+        __syncthreads();
+        for (int ch = 0; ch < nchunks; ++ch) {
+          if (ch + 1 < nchunks) build(ch + 1);
+          const uint32_t buf = ab_s + (uint32_t)((ch & 1) * SM_ACH * SM_ALD * 8) +
+                               (uint32_t)((warp * 16 + gid) * 8);
+#pragma unroll
+          for (int ks = 0; ks < SM_ACH / 4; ++ks) {
+            const int c = ch * SM_ACH + 4 * ks + tig;
+            if (4 * ks + ch * SM_ACH >= ncol) break;   // uniform: no live column in this step
+            const uint32_t ap = buf + (uint32_t)((4 * ks + tig) * SM_ALD * 8);
+            const double a0 = sm_lds(ap), a1 = sm_lds_at<64>(ap);
+            double b[8];
+            if (c < ncol) {
+              if (c >= seg_end) {
+                int q_lo, K, bo;
+                do {
+                  ++si;
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(q_lo), "=r"(col0), "=r"(K), "=r"(bo)
+                               : "r"(seg_s + 16 * si));
+                  seg_end = col0 + K;
+                } while (c >= seg_end);
+                bob = 8 * bo;
+              }
+              const uint32_t ub = ut2_s + (uint32_t)((c - col0) * LDb) + bob;
+              b[0] = sm_lds(ub);
+              b[1] = sm_lds_at<64>(ub);
+              b[2] = sm_lds_at<128>(ub);
+              b[3] = sm_lds_at<192>(ub);
+              b[4] = sm_lds_at<256>(ub);
+              b[5] = sm_lds_at<320>(ub);
+              b[6] = sm_lds_at<384>(ub);
+              b[7] = sm_lds_at<448>(ub);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) b[j] = 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              dmma_884(acc[0][j], a0, b[j]);
+              dmma_884(acc[1][j], a1, b[j]);
+            }
+          }
+          __syncthreads();
         }
       }
     };
@@ -482,9 +592,18 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const int ldy = (int)sm_ldy(n);
   k_x2_index<<<grid_blocks(n * ldy), 256, 0, s>>>(c2, bstart, nb_dev, ldy, y16);
   if ((st = check_launch("short_mma x2 index"))) return st;
-  const SmLayout L = sm_layout((int)gamma, (int)Rs);
+  // many copies per bucket and tile (C2-C4): the DMMA builder variant; few (C5): the
+  // per-lane form.  RSB200_MMA_BUILD=0|1 forces one.
+  const char *benv = getenv("RSB200_MMA_BUILD");   // (read per call: the tests switch it)
+  const int build_env = benv && *benv ? atoi(benv) : -1;
+  const double w0 = (double)std::min<int64_t>(2 * gamma + 1, n);
+  const double ov0 = (double)std::max<int64_t>(count, 1) * (w0 / n) * (w0 / n) * (w0 / n);
+  bool build = build_env >= 0 ? build_env != 0 : ov0 >= 64.0;
+  if (build && sm_layout((int)gamma, (int)Rs, true).total + 4096 > 227 * 1024) build = false;
+  const SmLayout L = sm_layout((int)gamma, (int)Rs, build);
   const bool acc = flags & RS_ASM_ACCUMULATE;
-  auto fn = acc ? k_short_mma<true> : k_short_mma<false>;
+  auto fn = build ? (acc ? k_short_mma<true, true> : k_short_mma<false, true>)
+                  : (acc ? k_short_mma<true, false> : k_short_mma<false, false>);
   cudaError_t e = smem_attr((const void *)fn, L.total);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_mma smem: %s", cudaGetErrorString(e));
   static int sms = 0;

@@ -46,8 +46,10 @@ def test_supported_and_override(monkeypatch):
     assert L.rs_short_method(2048, 31130, 80, 20) == nat.SHORT_MMA
 
 
+@pytest.mark.parametrize("build", ["0", "1"])
 @pytest.mark.parametrize("name", ["tiny_newton", "tiny_yukawa", "C1", "C2"])
-def test_mma_grid_vs_reference(name, cuda, golden, monkeypatch):
+def test_mma_grid_vs_reference(name, build, cuda, golden, monkeypatch):
+    monkeypatch.setenv("RSB200_MMA_BUILD", build)
     system, cfg, _ = case_inputs(name)
     res = rt.build_rs(system, cfg)
     gg, gm = methods(res, monkeypatch)
@@ -60,10 +62,13 @@ def test_mma_grid_vs_reference(name, cuda, golden, monkeypatch):
         assert np.max(np.abs(gm - z["grid"])) <= GRID_TOL * scale
 
 
+@pytest.mark.parametrize("build", ["0", "1"])
 @pytest.mark.parametrize("n,count,seed,kind", [(50, 40, 3, "newton"), (34, 7, 11, "yukawa"),
                                                (130, 300, 2, "newton"), (32, 1, 4, "newton")])
-def test_mma_ragged_sizes_vs_oracle(n, count, seed, kind, cuda, monkeypatch):
-    """n not a multiple of the 8 x 16 x 64 tile; windows clipped at every face."""
+def test_mma_ragged_sizes_vs_oracle(n, count, seed, kind, build, cuda, monkeypatch):
+    """n not a multiple of the 8 x 16 x 64 tile; windows clipped at every face;
+    both A-fragment variants (per-lane outer products / DMMA builder)."""
+    monkeypatch.setenv("RSB200_MMA_BUILD", build)
     system, cfg, c = small(n, count, seed, kind)
     res = rt.build_rs(system, cfg)
     gg, gm = methods(res, monkeypatch)
