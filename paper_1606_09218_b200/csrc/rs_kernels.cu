@@ -1665,7 +1665,7 @@ extern "C" {
 int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                     int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
                     int slices, int accumulate, void *work, int64_t work_bytes,
-                    const int32_t *nb, int64_t r3p, int64_t G, void *stream);
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream, int phase);
 
 int rs_abi_version(void) { return 1; }
 const char *rs_last_error(void) { return g_err; }
@@ -2026,6 +2026,22 @@ static const bool g_row_cut = [] {
   return !(e && e[0] == '0');
 }();
 
+// The Tucker part of the grid at large ranks (96 < r3 <= 160: C5) runs as an
+// Ozaki-split GEMM on the int8 tensor cores (tcgen05, rs_tc8.cu: k_oz_res) instead of
+// the FP64 DMMA kernel: C5 slab of 64 planes 2.77 -> 1.88 ms.  RSB200_TUCKER_OZ=0
+// keeps the DMMA kernel, 6 | 7 sets the slice count.  Explicit slices in `flags` win.
+static int tucker_oz_policy(int flags, int64_t r3, int64_t n) {
+  static const int env = [] {
+    const char *e = getenv("RSB200_TUCKER_OZ");
+    const int v = e && *e ? atoi(e) : 7;
+    return (v == 6 || v == 7) ? v : 0;
+  }();
+  if (((flags >> 8) & 0xF) || !(flags & RS_ASM_LONG) || (flags & RS_ASM_SHORT) || !env) return flags;
+  const int64_t r3p = round_up(std::max<int64_t>(r3, 1), 2);
+  if (r3p > 96 && r3p <= 160 && n >= 256) flags |= env << 8;
+  return flags;
+}
+
 static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int64_t nb_max,
                        int64_t Rs, int flags, int64_t *lda, int64_t *r3p, int64_t *G, int64_t *offA,
                        int64_t *offB, int64_t *offY, int64_t *offR, int64_t *total) {
@@ -2057,7 +2073,8 @@ static void asm_layout(int64_t n, int64_t planes, int64_t rmax, int64_t r3, int6
 int64_t rs_assemble_workspace_bytes(int64_t n, int64_t planes, int64_t rmax, int64_t nb_max,
                                     int64_t Rs, int flags) {
   int64_t lda, r3p, G, oA, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax, rmax, nb_max, Rs, flags, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
+  asm_layout(n, planes, rmax, rmax, nb_max, Rs, tucker_oz_policy(flags, rmax, n), &lda, &r3p, &G,
+             &oA, &oB, &oY, &oR, &tot);
   return tot;
 }
 
@@ -2094,7 +2111,14 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   const int64_t planes = x1_hi - x1_lo;
   const int64_t rmax = std::max<int64_t>(std::max<int64_t>(r1, r2), r3);
   int64_t lda, r3p, G, oA, oB, oY, oR, tot;
-  asm_layout(n, planes, rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
+  {
+    const int pf = tucker_oz_policy(flags, r3, n);
+    asm_layout(n, planes, rmax, r3, nb_max, Rs, pf, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
+    if (pf != flags && work_bytes < tot)   // caller sized the workspace without the slices
+      asm_layout(n, planes, rmax, r3, nb_max, Rs, flags, &lda, &r3p, &G, &oA, &oB, &oY, &oR, &tot);
+    else
+      flags = pf;
+  }
   if (work_bytes < tot)
     return fail(RS_ERR_CAPACITY, "rs_assemble_planes: workspace %lld < %lld",
                 (long long)work_bytes, (long long)tot);
@@ -2162,8 +2186,19 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       return st;
   }
   if (with_short && (st = check_launch("short_rows"))) return st;
-  if (f_only) return RS_OK;
   const int slices0 = (flags >> 8) & 0xF;
+  if (f_only) {
+    if (slices0) {   // Ozaki Tucker GEMM: the operands' exponents and slices belong to this phase
+      k_build_bt<<<grid_for(n * lda, 256), 256, 0, s>>>(V3, (int)r3, (int)r3p, ul, 0, (int)G,
+                                                         (int)gamma, bc3, nullptr, n, Bt, lda);
+      if ((st = check_launch("build_bt"))) return st;
+      ProfScope ps(s, "tucker_f");
+      const int64_t oz_off = tot - round_up(rs_oz_workspace_bytes(planes * n, n, lda, slices0), 256);
+      return rs_oz_gemm_cols(A, lda, Bt, lda, out, n, planes * n, n, lda, nullptr, 2, slices0, 0,
+                             wb + oz_off, tot - oz_off, nullptr, r3p, G, stream, 1);
+    }
+    return RS_OK;
+  }
   if (with_long && !with_short && !slices0 && g_tucker_apply && tucker_apply_ok(r3, n)) {
     // small r3: the HBM-bound row kernel instead of the plane GEMM
     ProfScope ps(s, "gemm_tucker");
@@ -2176,15 +2211,18 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
   if ((st = check_launch("build_bt"))) return st;
   const int64_t ntiles = ceil_div(n, TilePlane::BN);
   if (slices) {  // Ozaki-split FP64 on the int8 tensor cores (same tiles, same K ranges)
-    k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
-        bc3, with_short ? nb_dev : nullptr, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles,
-        ranges);
-    if ((st = check_launch("band_ranges"))) return st;
+    if (with_short) {
+      k_band_ranges<<<(unsigned)ceil_div(ntiles, 128), 128, 0, s>>>(
+          bc3, nb_dev, n, (int)gamma, TilePlane::BN, r3p, (int)G, ntiles, ranges);
+      if ((st = check_launch("band_ranges"))) return st;
+    }
     ProfScope ps(s, with_long && with_short ? "gemm_plane" : (with_short ? "gemm_short" : "gemm_tucker"));
     const int64_t oz_off = tot - round_up(rs_oz_workspace_bytes(planes * n, n, lda, slices), 256);
-    return rs_oz_gemm_cols(A, lda, Bt, lda, out, n, planes * n, n, lda, ranges, 2, slices,
+    // Tucker columns only: one dense K range (ranges = NULL -> the A-resident kernel)
+    return rs_oz_gemm_cols(A, lda, Bt, lda, out, n, planes * n, n, lda,
+                           with_short ? ranges : nullptr, 2, slices,
                            accumulate ? 1 : 0, wb + oz_off, tot - oz_off,
-                           with_short ? nb_dev : nullptr, r3p, G, stream);
+                           with_short ? nb_dev : nullptr, r3p, G, stream, f_ready ? 2 : 3);
   }
 
   {

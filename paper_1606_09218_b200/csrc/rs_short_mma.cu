@@ -162,7 +162,15 @@ __device__ __forceinline__ void sm_lds_rec(uint32_t a, double &z, int &o1, int &
   z = __hiloint2double(hi, lo);
 }
 
-template <bool ACC, bool BUILD>
+// 8-bit mask of the 8-wide x3 blocks j of a tile in which column (bucket s,
+// term k) can be nonzero: |Z0 + 8 j + t - s| <= g_k for some t in [0, 8).
+// e = Z0 - s.  Beyond g_k the term is below the drop threshold (k_term_prefix).
+__device__ __forceinline__ unsigned sm_live_blocks(int e, int g) {
+  const int jlo = max((-e - g) >> 3, 0), jhi = min((g - e) >> 3, 7);
+  return jhi < jlo ? 0u : ((2u << jhi) - 1u) & ~((1u << jlo) - 1u);
+}
+
+template <bool ACC, bool BUILD, bool SKIP>
 __global__ void __launch_bounds__(SM_THREADS, 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
                 int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
                 const int *__restrict__ kofd_g, const int32_t *__restrict__ y16, int ldy,
                 int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter, int tiles_per_cta,
-                double *__restrict__ out) {
+                int one, double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const SmLayout L = sm_layout(gamma, Rs, BUILD);
   double *ut = (double *)(sm_raw + L.table);
@@ -185,6 +193,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   __shared__ int wsum[SM_THREADS / 32];
   __shared__ int s_tile[2];
   __shared__ int s_bands[2 * SM_MAXT3];   // bucket band [lo, hi) of every x3 tile
+  __shared__ int s_gk[SM_MAXR];           // reach g_k of term k (cells), from kofd
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -204,6 +213,12 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   for (int e = tid; e < Rs * W; e += SM_THREADS) {   // coalesced read of ul (W x Rs)
     const int d = e / Rs, k = e - d * Rs;
     ut[k * LD + SM_PAD + d] = cbrt(wl[k]) * ul[e];
+  }
+  if (tid < Rs) {   // g_k = the largest distance at which term k is still kept
+    int g = -1;
+    for (int d = 0; d <= gamma; ++d)
+      if (skofd[d] > tid) g = d;
+    s_gk[tid] = g;
   }
   // occupied x3 buckets within gamma of each x3 tile: found once per CTA, all
   // tiles in parallel (per tile this was ~18 dependent global loads by one
@@ -281,9 +296,10 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         s_seg[nseg] = sg;
       }
       __syncthreads();
+      if (one < 0) ncol = 0;
       if constexpr (!BUILD) {
         const int steps = (ncol + 3) >> 2;
-        int si = -1, seg_end = 0, col0 = 0;
+        int si = -1, seg_end = 0, col0 = 0, e3 = 0;
         uint32_t qa_lo = 0, qa_hi = 0, bob = 0;
         const uint32_t ut_s = smem_addr(ut), rec_s = smem_addr(s_rec), seg_s = smem_addr(s_seg);
         const uint32_t ut1_s = ut_s + 8 * warp, ut2_s = ut_s + 8 * gid;
@@ -291,6 +307,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         for (int st = 0; st < steps; ++st) {
           const int c = 4 * st + tig;
           double a0 = 0.0, a1 = 0.0, b[8];
+          unsigned own = 0;   // x3 blocks of the tile this lane's column reaches
+          uint32_t ub = ut2_s;
           if (c < ncol) {
             if (c >= seg_end) {   // this lane's column enters a new segment
               int q_lo, K, bo, nq;
@@ -305,7 +323,9 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
               qa_lo = rec_s + 16 * q_lo;
               qa_hi = rec_s + 16 * nq;
               bob = 8 * bo;
+              e3 = bo - gamma - SM_PAD;
             }
+            own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : 0xFFu;
             const uint32_t koff = (uint32_t)((c - col0) * LDb);
             const uint32_t u1 = ut1_s + koff, u2 = ut2_s + koff;
   #pragma unroll 2
@@ -318,23 +338,36 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
               a0 = fma(t, sm_lds(w2), a0);
               a1 = fma(t, sm_lds_at<64>(w2), a1);
             }
-            const uint32_t ub = u2 + bob;
-            b[0] = sm_lds(ub);
-            b[1] = sm_lds_at<64>(ub);
-            b[2] = sm_lds_at<128>(ub);
-            b[3] = sm_lds_at<192>(ub);
-            b[4] = sm_lds_at<256>(ub);
-            b[5] = sm_lds_at<320>(ub);
-            b[6] = sm_lds_at<384>(ub);
-            b[7] = sm_lds_at<448>(ub);
-          } else {
-  #pragma unroll
-            for (int j = 0; j < 8; ++j) b[j] = 0.0;
+            ub = u2 + bob;
           }
+          // the step's 4 columns (mostly consecutive terms of one bucket) reach only
+          // some of the tile's 8 x3 blocks: the others' MMAs and B loads are skipped
+          const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : 0xFFu;
+          b[0] = (own & 1u) ? sm_lds(ub) : 0.0;
+          b[1] = (own & 2u) ? sm_lds_at<64>(ub) : 0.0;
+          b[2] = (own & 4u) ? sm_lds_at<128>(ub) : 0.0;
+          b[3] = (own & 8u) ? sm_lds_at<192>(ub) : 0.0;
+          b[4] = (own & 16u) ? sm_lds_at<256>(ub) : 0.0;
+          b[5] = (own & 32u) ? sm_lds_at<320>(ub) : 0.0;
+          b[6] = (own & 64u) ? sm_lds_at<384>(ub) : 0.0;
+          b[7] = (own & 128u) ? sm_lds_at<448>(ub) : 0.0;
   #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            dmma_884(acc[0][j], a0, b[j]);
-            dmma_884(acc[1][j], a1, b[j]);
+            if (SKIP) {
+              // a predicated-off DMMA costs the pipe as much as a live one
+              // (tools/probe_dmma_pred.cu), and ptxas if-converts any plain `if` around
+              // the pair: the trip count `one` (= 1, a kernel argument) keeps the branch
+              if (live & (1u << j)) {
+  #pragma unroll 1
+                for (int r = 0; r < one; ++r) {
+                  dmma_884(acc[0][j], a0, b[j]);
+                  dmma_884(acc[1][j], a1, b[j]);
+                }
+              }
+            } else {
+              dmma_884(acc[0][j], a0, b[j]);
+              dmma_884(acc[1][j], a1, b[j]);
+            }
           }
         }
       } else {
@@ -392,7 +425,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             asm volatile("st.shared.v2.f64 [%0+64], {%1, %2};" ::"r"(dst), "d"(d1[0]), "d"(d1[1]));
           }
         };
-        int si = -1, seg_end = 0, col0 = 0;          // per-lane cursor of the main loop
+        int si = -1, seg_end = 0, col0 = 0, e3 = 0;  // per-lane cursor of the main loop
         uint32_t bob = 0;
         const uint32_t ut2_s = ut_s + 8 * gid;
         if (nchunks > 0) build(0);
@@ -408,6 +441,8 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             const uint32_t ap = buf + (uint32_t)((4 * ks + tig) * SM_ALD * 8);
             const double a0 = sm_lds(ap), a1 = sm_lds_at<64>(ap);
             double b[8];
+            unsigned own = 0;
+            uint32_t ub = ut2_s;
             if (c < ncol) {
               if (c >= seg_end) {
                 int q_lo, K, bo;
@@ -419,24 +454,34 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                   seg_end = col0 + K;
                 } while (c >= seg_end);
                 bob = 8 * bo;
+                e3 = bo - gamma - SM_PAD;
               }
-              const uint32_t ub = ut2_s + (uint32_t)((c - col0) * LDb) + bob;
-              b[0] = sm_lds(ub);
-              b[1] = sm_lds_at<64>(ub);
-              b[2] = sm_lds_at<128>(ub);
-              b[3] = sm_lds_at<192>(ub);
-              b[4] = sm_lds_at<256>(ub);
-              b[5] = sm_lds_at<320>(ub);
-              b[6] = sm_lds_at<384>(ub);
-              b[7] = sm_lds_at<448>(ub);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) b[j] = 0.0;
+              own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : 0xFFu;
+              ub = ut2_s + (uint32_t)((c - col0) * LDb) + bob;
             }
+            const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : 0xFFu;
+            b[0] = (own & 1u) ? sm_lds(ub) : 0.0;
+            b[1] = (own & 2u) ? sm_lds_at<64>(ub) : 0.0;
+            b[2] = (own & 4u) ? sm_lds_at<128>(ub) : 0.0;
+            b[3] = (own & 8u) ? sm_lds_at<192>(ub) : 0.0;
+            b[4] = (own & 16u) ? sm_lds_at<256>(ub) : 0.0;
+            b[5] = (own & 32u) ? sm_lds_at<320>(ub) : 0.0;
+            b[6] = (own & 64u) ? sm_lds_at<384>(ub) : 0.0;
+            b[7] = (own & 128u) ? sm_lds_at<448>(ub) : 0.0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              dmma_884(acc[0][j], a0, b[j]);
-              dmma_884(acc[1][j], a1, b[j]);
+              if (SKIP) {
+                if (live & (1u << j)) {
+#pragma unroll 1
+                  for (int r = 0; r < one; ++r) {
+                    dmma_884(acc[0][j], a0, b[j]);
+                    dmma_884(acc[1][j], a1, b[j]);
+                  }
+                }
+              } else {
+                dmma_884(acc[0][j], a0, b[j]);
+                dmma_884(acc[1][j], a1, b[j]);
+              }
             }
           }
           __syncthreads();
@@ -602,9 +647,22 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   if (build && sm_layout((int)gamma, (int)Rs, true).total + 4096 > 227 * 1024) build = false;
   const SmLayout L = sm_layout((int)gamma, (int)Rs, build);
   const bool acc = flags & RS_ASM_ACCUMULATE;
-  auto fn = build ? (acc ? k_short_mma<true, true> : k_short_mma<false, true>)
-                  : (acc ? k_short_mma<true, false> : k_short_mma<false, false>);
-  cudaError_t e = smem_attr((const void *)fn, L.total);
+  // RSB200_MMA_SKIP=1: the MMAs (and B loads) of the 8-wide x3 blocks a step's columns
+  // cannot reach are skipped -- 25 % (C5) / 15 % (C4) fewer DMMAs.  Measured no faster
+  // (C5 75.5 -> 75.1 ms) or slower (C4 113 -> 124 ms): with every DMMA removed the
+  // kernel still takes 56 ms (C5) / 93 ms (C4) (RSB200_MMA_DBG=1) -- operand forming and
+  // the candidate search dominate, not the tensor pipe -- so the default issues them all.
+  const char *senv = getenv("RSB200_MMA_SKIP");
+  const bool skip = senv && senv[0] == '1';
+  auto fn = skip ? (build ? (acc ? k_short_mma<true, true, true> : k_short_mma<false, true, true>)
+                          : (acc ? k_short_mma<true, false, true> : k_short_mma<false, false, true>))
+                 : (build ? (acc ? k_short_mma<true, true, false> : k_short_mma<false, true, false>)
+                          : (acc ? k_short_mma<true, false, false> : k_short_mma<false, false, false>));
+  // RSB200_MMA_PAD_KB: extra dynamic shared memory per CTA (occupancy experiments:
+  // one CTA per SM leaves room for another kernel's CTAs)
+  const char *penv = getenv("RSB200_MMA_PAD_KB");
+  const int smem_bytes = std::min(L.total + (penv ? atoi(penv) * 1024 : 0), 227 * 1024);
+  cudaError_t e = smem_attr((const void *)fn, smem_bytes);
   if (e != cudaSuccess) return fail(RS_ERR_CUDA, "short_mma smem: %s", cudaGetErrorString(e));
   static int sms = 0;
   if (!sms) {
@@ -612,7 +670,7 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int per_sm = L.total + 1024 <= 113 * 1024 ? 2 : 1;
+  const int per_sm = smem_bytes + 1024 <= 113 * 1024 ? 2 : 1;
   const int64_t ntiles = ceil_div(n, SM_T3) * ceil_div(n, SM_T2) *
                          ceil_div(x1_hi - (x1_lo - x1_lo % SM_T1), SM_T1);
   static const int waves = [] {   // RSB200_MMA_WAVES: CTA generations per SM slot
@@ -630,9 +688,12 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const int tiles_per_cta = (int)std::max<int64_t>(
       ceil_div(ntiles, slots * waves), std::min<int64_t>(t_min, ceil_div(ntiles, slots)));
   const unsigned grid = (unsigned)ceil_div(ntiles, tiles_per_cta);
+  // RSB200_MMA_DBG (diagnostics, results wrong): 1 = no DMMA issued, 2 = no K loop at all
+  const char *denv = getenv("RSB200_MMA_DBG");
+  const int one = denv && *denv ? 1 - atoi(denv) : 1;
   ProfScope ps(s, "short_mma");
-  fn<<<grid, SM_THREADS, L.total, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,
-                                       nb_dev, kofd, y16, ldy, x1_lo, x1_hi, counter, tiles_per_cta, out);
+  fn<<<grid, SM_THREADS, smem_bytes, s>>>(ul, wl, (int)Rs, (int)gamma, n, c1, c2, zq, bstart, bc3,
+                                       nb_dev, kofd, y16, ldy, x1_lo, x1_hi, counter, tiles_per_cta, one, out);
   return check_launch("short_mma");
 }
 

@@ -13,6 +13,8 @@
 // slice products are exact in int32, and the fp64 result is recombined with
 // power-of-two scales -- FP64 accuracy at int8 tensor-core throughput.
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -315,7 +317,8 @@ template <int S>
 __global__ void k_oz_slice_t(const double *__restrict__ X, int64_t rows, int64_t rows_pad,
                              int64_t ld, int64_t cols0, const int32_t *__restrict__ nb,
                              int64_t r3p, int64_t G, const int *__restrict__ e,
-                             int8_t *__restrict__ out, int TR, int64_t ksteps, int64_t sstride) {
+                             int8_t *__restrict__ out, int TR, int64_t ksteps, int64_t sstride,
+                             int64_t tstride) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= rows_pad * ksteps * 2) return;
   const int64_t r = t % rows_pad, g = t / rows_pad;
@@ -339,7 +342,9 @@ __global__ void k_oz_slice_t(const double *__restrict__ X, int64_t rows, int64_t
     }
   }
   const int64_t rt = r / TR, rr = r - rt * TR, ks = g >> 1, c = g & 1;
-  const int64_t off = (rt * ksteps + ks) * (int64_t)TR * 32 + rr * 32 + ((c ^ ((rr >> 2) & 1)) << 4);
+  // tstride: bytes between consecutive (row tile, K step) blocks of one slice (TR * 32
+  // when a slice is contiguous, S * TR * 32 when the S slices of a block are interleaved)
+  const int64_t off = (rt * ksteps + ks) * tstride + rr * 32 + ((c ^ ((rr >> 2) & 1)) << 4);
 #pragma unroll
   for (int p = 0; p < S; ++p)
     *reinterpret_cast<uint4 *>(out + p * sstride + off) =
@@ -554,6 +559,357 @@ __global__ void __launch_bounds__(THREADS)
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
+
+// ------------------------------------------------------------------------
+// A-resident, warp-specialised Ozaki GEMM for dense K <= 160 (the Tucker part
+// of the grid at large ranks: C (M x N) (+)= A (M x K) B (N x K)^T, M = planes
+// x n rows, N = n, K = r3).  One persistent CTA per SM:
+//   warp 0 (one thread)  bulk-copies the S slices of a 128-row block of A into
+//                        shared memory once (all K steps: S x 5 x 4 KB), then
+//                        streams the B slices of every 64-column tile through
+//                        a 4-stage ring (S x 2 KB per 32-column K step);
+//   warp 1 (one thread)  issues tcgen05.mma kind::i8 (128 x 64 x 32) into TMEM;
+//   warps 2-9            drain TMEM, recombine in fp64 and update C.
+// TMEM holds S accumulators of 64 columns (one per diagonal p + q = t).  To
+// overlap the drain with the tensor pipe the diagonals are split in two groups
+// -- {0..4} (15 slice products per K step) and {5, 6} (13) -- each computed in
+// its own pass over the tile's K steps: while the MMAs of one group run, the
+// epilogue warps drain the other (group 0 into per-thread fp64 partials, group
+// 1 on top, then one coalesced-by-row update of C).  int32 partial sums are
+// merged pairwise in integers (a_t 2^7 + a_{t+1} fits 31 bits) before the
+// conversion, so a C entry costs 4 conversions and 3 FMAs.
+template <int S>
+struct OzRes {
+  static constexpr int BN = 64, G1 = 5;
+  static constexpr int A_SLICE = BM * 32, B_SLICE = BN * 32;
+  static constexpr int MAXSTEPS = 5;                      // K <= 160
+  static constexpr int A_BYTES = S * MAXSTEPS * A_SLICE;  // 140 KB at S = 7
+  static constexpr int B_STAGE = S * B_SLICE;
+  static constexpr int NSTB = MAXSTEPS;                   // one stage per K step of the tile
+  static constexpr int EPW = 16;                          // epilogue warps: 4 per TMEM lane quarter
+  static constexpr int SMEM = A_BYTES + NSTB * B_STAGE + 1024;
+  static constexpr int THREADS_RES = (2 + EPW) * 32;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(taddr));
+}
+
+// 16 TMEM lanes x 16 columns: thread T holds rows T/4 (v[0], v[1], v[4], v[5]) and T/4 + 8
+// (v[2], v[3], v[6], v[7]), columns 2 (T%4) + {0, 1} (v[0..3]) and 8 + 2 (T%4) + {0, 1}
+// (v[4..7]) -- the accumulator-fragment layout, so 4 lanes cover 64 contiguous bytes of C
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(taddr));
+}
+
+// int32 -> double without the conversion pipe: 2^52 + 2^31 + a is exact
+__device__ __forceinline__ double s32_to_f64(int32_t a) {
+  return __hiloint2double(0x43300000, a ^ (int32_t)0x80000000) - 4503601774854144.0;
+}
+
+__device__ __forceinline__ double pow2_f64(int e) {   // 2^e, e in the normal range
+  return __hiloint2double((e + 1023) << 20, 0);
+}
+
+template <int S>
+__global__ void __launch_bounds__(OzRes<S>::THREADS_RES, 1)
+    k_oz_res(const int8_t *__restrict__ SA, const int8_t *__restrict__ SB, int64_t ksteps, int nsteps, const int *__restrict__ ea,
+             const int *__restrict__ eb, double *__restrict__ C, int64_t ldc, int64_t M,
+             int64_t N, int accumulate) {
+  using Cfg = OzRes<S>;
+  constexpr int NSTB = Cfg::NSTB, G1 = Cfg::G1, BN = Cfg::BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[NSTB], empty[NSTB], a_full, a_empty, acc_full[2],
+      acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSTB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&a_full, 1);
+    mbar_init(&a_empty, 1);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&acc_full[g], 1);
+      mbar_init(&acc_empty[g], Cfg::EPW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const int64_t nrb = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN;
+  const uint32_t a_s = smem_u32(smem), b_s = a_s + Cfg::A_BYTES;
+  // every CTA walks the column tiles from its own start: 148 CTAs on the same B block and
+  // the same C columns at once hot-spot a few L2 slices
+  const int64_t ct0 = ((int64_t)blockIdx.x * 5) % ntn;
+  long long dbg_c0 = 0;
+  unsigned long long dbg_t0 = 0;
+  if ((accumulate >> 4) & 128) {
+    dbg_c0 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+  }
+  const int dbg = accumulate >> 4;   // RSB200_OZ_DBG (diagnostics): 1 no C update, 2 no TMEM drain, 4 no MMA, 8 MMAs wait for nothing, 16 no L2 prefetch of C
+  accumulate &= 1;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------------------------------------- loader
+      uint32_t it = 0, ra = 0;
+      for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ra) {
+        mbar_wait(&a_empty, (ra & 1u) ^ 1u);
+        // A: [K step][slice] blocks of the row tile lie back to back (interleaved slices)
+        mbar_expect_tx(&a_full, (uint32_t)(S * nsteps * Cfg::A_SLICE));
+        for (int ks = 0; ks < nsteps; ++ks)
+          bulk_g2s(a_s + ks * S * Cfg::A_SLICE,
+                   SA + (rb * ksteps + ks) * (int64_t)(S * Cfg::A_SLICE),
+                   (uint32_t)(S * Cfg::A_SLICE), &a_full);
+        for (int64_t ci = 0; ci < ntn; ++ci) {
+          const int64_t ct = (ct0 + ci) % ntn;
+          // B: the S slices of a (column tile, K step) block lie back to back: one copy
+          // (both passes of the tile read them from shared memory: stage = K step)
+          const int8_t *gB = SB + ct * ksteps * (int64_t)Cfg::B_STAGE;
+          for (int ks = 0; ks < nsteps; ++ks) {
+            mbar_wait(&empty[ks], (it & 1u) ^ 1u);
+            mbar_expect_tx(&full[ks], (uint32_t)Cfg::B_STAGE);
+            bulk_g2s(b_s + ks * Cfg::B_STAGE, gB + ks * (int64_t)Cfg::B_STAGE,
+                     (uint32_t)Cfg::B_STAGE, &full[ks]);
+          }
+          ++it;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {   // -------------------------------------------- MMA issuer
+    // The whole warp walks the (warp-uniform) loops and waits; one elected lane issues.
+    // With a single divergent thread the descriptor arithmetic ran on the vector
+    // datapath plus register -> uniform-register moves: ~110 cycles per MMA against the
+    // 48 the 128 x 64 x 32 MMA itself takes.
+    const uint32_t idesc = make_idesc(BM, BN);
+    const uint64_t da0 = make_desc_sw32(a_s), db0 = make_desc_sw32(b_s);
+    uint32_t leader;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(leader));
+    uint32_t ra = 0, ut = 0;
+    for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ra) {
+      mbar_wait(&a_full, ra & 1u);
+      for (int64_t ct = 0; ct < ntn; ++ct, ++ut) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (!(dbg & 8)) mbar_wait(&acc_empty[g], (ut & 1u) ^ 1u);   // (8: free-running MMAs)
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          for (int ks = 0; ks < nsteps; ++ks) {
+            if (g == 0 && !(dbg & 8)) {   // pass 2 finds the K step in place
+              mbar_wait(&full[ks], ut & 1u);
+              asm volatile("tcgen05.fence::after_thread_sync;\n");
+            }
+            const uint64_t dak = da0 + (uint64_t)((ks * S * Cfg::A_SLICE) >> 4);
+            const uint64_t dbk = db0 + (uint64_t)((ks * Cfg::B_STAGE) >> 4);
+            const uint32_t acc0 = ks > 0 ? 1u : 0u;
+            if (leader && !(dbg & 4)) {
+#pragma unroll
+              for (int t = (g ? G1 : 0); t < (g ? S : G1); ++t) {
+#pragma unroll
+                for (int p = 0; p <= t; ++p)
+                  umma_i8(tmem + t * BN, dak + (uint64_t)((p * Cfg::A_SLICE) >> 4),
+                          dbk + (uint64_t)(((t - p) * Cfg::B_SLICE) >> 4), idesc, p > 0 ? 1u : acc0);
+              }
+            }
+            if (leader && g == 1) umma_commit(&empty[ks]);   // the next tile's K step may land
+            __syncwarp();
+          }
+          if (leader) umma_commit(&acc_full[g]);
+          __syncwarp();
+        }
+      }
+      if (leader) umma_commit(&a_empty);
+      __syncwarp();
+    }
+  } else {             // --------------------------------------------- epilogue
+    // 16 warps: warp -> (TMEM lane quarter, 16-column group).  tcgen05.ld 16x256b hands
+    // thread T rows T/4 (+8) and column pairs 2 (T%4) (+8) of a 16 x 16 block, so the
+    // update of C runs as 16-byte accesses, 8 rows x 64 contiguous bytes per instruction,
+    // straight from registers.
+    const int quarter = warp & 3, cg = (warp - 2) >> 2;
+    const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(cg * 16);
+    const int r4 = lane >> 2, c2 = 2 * (lane & 3);
+    const bool vec = !(ldc & 1);
+    uint32_t ut = 0;
+    for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+      const int64_t rbase = rb * BM + quarter * 32 + r4;   // rows rbase + {0, 8, 16, 24}
+      int er[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) er[i] = rbase + 8 * i < M ? ea[rbase + 8 * i] : 0;
+      for (int64_t ci = 0; ci < ntn; ++ci, ++ut) {
+        const int64_t ct = (ct0 + ci) % ntn;
+        const int64_t n0 = ct * BN + cg * 16 + c2;          // columns n0 + {0, 1, 8, 9}
+        int ecol[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t col = n0 + (j & 1) + 8 * (j >> 1);
+          ecol[j] = col < N ? eb[col] : 0;
+        }
+        if (accumulate && !(dbg & (1 | 32 | 16))) {   // old values of the block into L2 (no registers)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (rbase + 8 * i < M) {
+              const double *src = C + (rbase + 8 * i) * ldc + n0;
+              if (n0 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+              if (n0 + 8 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 8));
+            }
+        }
+        // v[h][k]: k = register index of the 16x256b.x2 load of lanes 16 h .. 16 h + 15:
+        // rows (2 h + ((k >> 1) & 1)), column j = (k & 1) + 2 (k >> 2)
+        double v[2][8];
+        mbar_wait(&acc_full[0], ut & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        if (dbg & 2) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[h][k] = 0.0;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t th = tq + ((uint32_t)(16 * h) << 16);
+            uint32_t x[8], y[8];
+            tmem_ld_16x256b_x2(th + 0 * BN, x);
+            tmem_ld_16x256b_x2(th + 1 * BN, y);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              v[h][k] = s32_to_f64((int32_t)x[k] * 128 + (int32_t)y[k]) * 0.0078125;
+            tmem_ld_16x256b_x2(th + 2 * BN, x);
+            tmem_ld_16x256b_x2(th + 3 * BN, y);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              v[h][k] = fma(s32_to_f64((int32_t)x[k] * 128 + (int32_t)y[k]), 0x1p-21, v[h][k]);
+            tmem_ld_16x256b_x2(th + 4 * BN, x);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[h][k] = fma(s32_to_f64((int32_t)x[k]), 0x1p-28, v[h][k]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[0]);
+        mbar_wait(&acc_full[1], ut & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        if (!(dbg & 2)) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t th = tq + ((uint32_t)(16 * h) << 16);
+            uint32_t x[8], y[8];
+            tmem_ld_16x256b_x2(th + 5 * BN, x);
+            if (S > 6) tmem_ld_16x256b_x2(th + 6 * BN, y);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              v[h][k] = fma(s32_to_f64((int32_t)x[k] * 128 + (S > 6 ? (int32_t)y[k] : 0)), 0x1p-42,
+                            v[h][k]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[1]);
+        // C[row, col] (+)= v 2^(ea[row] + eb[col] - 12), v = sum_t acc_t 2^(-7 t); two rows
+        // (one 16-lane half) at a time: 4 x 16 bytes of old values in flight per lane
+        if (!(dbg & 1)) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double o[2][4];
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int64_t grow = rbase + 8 * (2 * h + ii);
+#pragma unroll
+              for (int jp = 0; jp < 2; ++jp) {
+                const int64_t col = n0 + 8 * jp;
+                o[ii][2 * jp] = o[ii][2 * jp + 1] = 0.0;
+                if (accumulate && !(dbg & 32) && grow < M) {   // (32: store only)
+                  const double *src = C + grow * ldc + col;
+                  if (vec && col + 1 < N) {
+                    const double2 t2 = __ldcs(reinterpret_cast<const double2 *>(src));
+                    o[ii][2 * jp] = t2.x;
+                    o[ii][2 * jp + 1] = t2.y;
+                  } else {
+                    if (col < N) o[ii][2 * jp] = __ldcs(src);
+                    if (col + 1 < N) o[ii][2 * jp + 1] = __ldcs(src + 1);
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int i = 2 * h + ii;
+              const int64_t grow = rbase + 8 * i;
+              if (grow >= M) continue;
+#pragma unroll
+              for (int jp = 0; jp < 2; ++jp) {
+                const int64_t col = n0 + 8 * jp;
+                double r[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  // (exponents beyond the normal range are clamped: no physical operand gets there)
+                  const int x = min(max(er[i] + ecol[2 * jp + u] - 12, -1022), 1023);
+                  r[u] = fma(v[h][u + 2 * ii + 4 * jp], pow2_f64(x), o[ii][2 * jp + u]);
+                }
+                double *dst = C + grow * ldc + col;
+                if (dbg & 64) {   // (64: no stores (the values are still formed))
+                  if (r[0] + r[1] == 1.2345e-300) dst[0] = r[1];
+                } else if (vec && col + 1 < N) {
+                  __stcs(reinterpret_cast<double2 *>(dst), make_double2(r[0], r[1]));
+                } else {
+                  if (col < N) __stcs(dst, r[0]);
+                  if (col + 1 < N) __stcs(dst + 1, r[1]);
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if ((dbg & 128) && blockIdx.x == 0 && threadIdx.x == 0) {   // effective SM clock of this CTA
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    const long long c1 = clock64();
+    printf("k_oz_res: %lld cycles in %llu ns = %.0f MHz\n", c1 - dbg_c0, t1 - dbg_t0,
+           1e3 * (double)(c1 - dbg_c0) / (double)(t1 - dbg_t0));
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
 }  // namespace tc8
 }  // namespace rsb
 
@@ -595,21 +951,23 @@ int64_t rs_oz_workspace_bytes(int64_t M, int64_t N, int64_t K, int slices) {
 int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                     int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
                     int slices, int accumulate, void *work, int64_t work_bytes,
-                    const int32_t *nb, int64_t r3p, int64_t G, void *stream);
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream, int phase);
 
 int rs_oz_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
                int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr, int slices,
                int accumulate, void *work, int64_t work_bytes, void *stream) {
   return rs_oz_gemm_cols(A, lda, B, ldb, C, ldc, M, N, K, ranges, nr, slices, accumulate, work,
-                         work_bytes, nullptr, 0, 0, stream);
+                         work_bytes, nullptr, 0, 0, stream, 3);
 }
 
 /* as rs_oz_gemm; with nb != NULL only the first r3p + (*nb) * G columns of A
- * and B are live (device-side count; the rest is never read). */
+ * and B are live (device-side count; the rest is never read).  phase: 1 = row
+ * exponents and slices only (the operands' preparation), 2 = the GEMM on slices
+ * prepared by an earlier call with the same arguments, 3 = both. */
 int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                     int64_t ldc, int64_t M, int64_t N, int64_t K, const int64_t *ranges, int nr,
                     int slices, int accumulate, void *work, int64_t work_bytes,
-                    const int32_t *nb, int64_t r3p, int64_t G, void *stream) {
+                    const int32_t *nb, int64_t r3p, int64_t G, void *stream, int phase) {
   RS_REQUIRE(M >= 1 && N >= 1 && K >= 1 && lda >= K && ldb >= K && ldc >= N,
              "rs_oz_gemm: bad shape");
   RS_REQUIRE(slices >= 6 && slices <= 8, "rs_oz_gemm: slices must be 6..8");
@@ -628,32 +986,69 @@ int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, 
   int64_t *rin = rg + ceil_div(N, tc8::OZ_BN) * 4 * 2;  // 4 ranges x 2 per tile each
   const int64_t ntn = ceil_div(N, tc8::OZ_BN);
   int st;
-  tc8::k_oz_rowexp<<<(unsigned)ceil_div(M * 32, 256), 256, 0, s>>>(A, M, lda, K, nb, r3p, G, ea);
-  if ((st = check_launch("oz_rowexp A"))) return st;
-  tc8::k_oz_rowexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, s>>>(B, N, ldb, K, nb, r3p, G, eb);
-  if ((st = check_launch("oz_rowexp B"))) return st;
+  if (phase & 1) {
+    tc8::k_oz_rowexp<<<(unsigned)ceil_div(M * 32, 256), 256, 0, s>>>(A, M, lda, K, nb, r3p, G, ea);
+    if ((st = check_launch("oz_rowexp A"))) return st;
+    tc8::k_oz_rowexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, s>>>(B, N, ldb, K, nb, r3p, G, eb);
+    if ((st = check_launch("oz_rowexp B"))) return st;
+  }
+  // dense K <= 160 (the Tucker part): the A-resident warp-specialised kernel
+  // (RSB200_OZ_RES=0: the per-tile kernel below)
+  static const bool res_on = [] {
+    const char *e = getenv("RSB200_OZ_RES");
+    return !(e && e[0] == '0');
+  }();
+  const bool res = res_on && !ranges && !nb && slices <= 7 &&
+                   ceil_div(K, 32) <= tc8::OzRes<7>::MAXSTEPS;
   auto slice = [&](const double *X, int64_t rows, int64_t rows_pad, int TR, int64_t ld,
-                   const int *e, int8_t *out) {
+                   const int *e, int8_t *out, bool interleave) {
     const unsigned g = (unsigned)ceil_div(rows_pad * ksteps * 2, 256);
-    const int64_t ss = rows_pad * ldk;
+    // contiguous slices, or the S slices of every (row tile, K step) block back to back
+    const int64_t ss = interleave ? (int64_t)TR * 32 : rows_pad * ldk;
+    const int64_t ts = interleave ? (int64_t)slices * TR * 32 : (int64_t)TR * 32;
     switch (slices) {
       case 6:
         tc8::k_oz_slice_t<6><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
-                                                ksteps, ss);
+                                                ksteps, ss, ts);
         break;
       case 7:
         tc8::k_oz_slice_t<7><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
-                                                ksteps, ss);
+                                                ksteps, ss, ts);
         break;
       default:
         tc8::k_oz_slice_t<8><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, nb, r3p, G, e, out, TR,
-                                                ksteps, ss);
+                                                ksteps, ss, ts);
         break;
     }
     return check_launch("oz_slice");
   };
-  if ((st = slice(A, M, Mp, 128, lda, ea, SA))) return st;
-  if ((st = slice(B, N, Np, 64, ldb, eb, SB))) return st;
+  if (phase & 1) {
+    if ((st = slice(A, M, Mp, 128, lda, ea, SA, res))) return st;
+    if ((st = slice(B, N, Np, 64, ldb, eb, SB, res))) return st;
+  }
+  if (!(phase & 2)) return RS_OK;
+  if (res) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int nsteps = (int)ceil_div(K, 32);
+    const char *denv = getenv("RSB200_OZ_DBG");
+    const int dbgv = denv ? atoi(denv) : 0;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(M, tc8::BM), sms);
+    auto go = [&](auto kern, int smem, int threads) -> int {
+      cudaError_t e = smem_attr((const void *)kern, smem);
+      if (e != cudaSuccess) return fail(RS_ERR_CUDA, "oz smem: %s", cudaGetErrorString(e));
+      kern<<<grid, threads, smem, s>>>(SA, SB, ksteps, nsteps, ea, eb, C, ldc,
+                                       M, N, (accumulate ? 1 : 0) | (dbgv << 4));
+      return check_launch("oz_res");
+    };
+    ProfScope ps(s, "oz_mma");
+    return slices == 6 ? go(tc8::k_oz_res<6>, tc8::OzRes<6>::SMEM, tc8::OzRes<6>::THREADS_RES)
+                       : go(tc8::k_oz_res<7>, tc8::OzRes<7>::SMEM, tc8::OzRes<7>::THREADS_RES);
+  }
   const int64_t *use = ranges;
   if (!ranges) {  // one full range per tile
     std::vector<int64_t> h(ntn * nr * 2, 0);

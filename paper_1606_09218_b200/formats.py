@@ -583,9 +583,11 @@ def _assemble_fused_l0(long: TuckerTensor, short: CCT, x1_lo: int, x1_hi: int, o
     return out
 
 
-def tucker_plan(n: int, planes: int, rmax: int, workspace_bytes: int = _ASSEMBLE_WORKSPACE):
+def tucker_plan(n: int, planes: int, rmax: int, workspace_bytes: int = _ASSEMBLE_WORKSPACE,
+                flags: Optional[int] = None):
     """(planes per chunk, workspace bytes) of a Tucker-only accumulate."""
-    flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
+    if flags is None:
+        flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
     key = (n, planes, rmax, 0, 0, flags, workspace_bytes)
     plan = _ASM_PLANS.get(key)
     if plan is None:
@@ -608,7 +610,7 @@ def tucker_accumulate(long: TuckerTensor, x1_lo: int, x1_hi: int, out,
     planes = x1_hi - x1_lo
     flags = nat.ASM_LONG | nat.ASM_ACCUMULATE
     L = nat.lib()
-    chunk, wsb = tucker_plan(n, planes, max(r1, r2, r3), workspace_bytes)
+    chunk, wsb = tucker_plan(n, planes, max(r1, r2, r3), workspace_bytes, flags)
     ws = nat.Workspace.get(wsb, workspace_slot)
     core, (v1, v2, v3) = long.core, long.factors
     cp, p1_, p2_, p3_ = core.data_ptr(), v1.data_ptr(), v2.data_ptr(), v3.data_ptr()

@@ -142,7 +142,10 @@ def test_tc8_gemm_s8_exact(nat, cuda, M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K,slices", [(128, 64, 64, 7), (300, 200, 1040, 7), (1000, 256, 712, 8),
-                                          (77, 130, 32, 6), (513, 70, 3000, 7)])
+                                          (77, 130, 32, 6), (513, 70, 3000, 7),
+                                          # K <= 160: the A-resident warp-specialised kernel (k_oz_res)
+                                          (1000, 256, 132, 7), (40000, 192, 160, 7), (300, 201, 100, 6),
+                                          (129, 64, 33, 7)])
 def test_oz_gemm_fp64(nat, cuda, M, N, K, slices):
     """Ozaki-split FP64 GEMM on tcgen05 int8 vs numpy fp64: error within the
     split bound K 2^(-7 S) max|A_i.| max|B_j.| (graded magnitudes per row)."""
@@ -162,6 +165,12 @@ def test_oz_gemm_fp64(nat, cuda, M, N, K, slices):
     scale = np.abs(a).max(1)[:, None] * np.abs(b).max(1)[None, :]
     err = np.abs(C.cpu().numpy() - ref) / scale
     assert err.max() <= 4 * K * 2.0 ** (-7 * slices + 1), err.max()
+    # accumulate: C += A B^T on top of the first result
+    nat.check(L.rs_oz_gemm(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, None, 1,
+                           slices, 1, ws.data_ptr(), ws.numel(), nat.stream_ptr()), "oz")
+    cuda.cuda.synchronize()
+    err = np.abs(C.cpu().numpy() - 2 * ref) / scale
+    assert err.max() <= 8 * K * 2.0 ** (-7 * slices + 1), err.max()
 
 
 @pytest.mark.parametrize("n,b,rank", [(256, 24, 5), (96, 32, 1), (200, 16, 12), (64, 24, 0)])
@@ -185,3 +194,43 @@ def test_topeig_rank_deficient(nat, cuda, n, b, rank):
     if rank:
         proj = np.abs(U[:rank] @ q[:, :rank])
         assert np.allclose(np.diag(proj), 1.0, atol=1e-9)
+
+
+_TUCKER_VARIANT_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1606_09218_b200 import formats
+torch.manual_seed(3)
+dev = "cuda"
+for n, ranks, lo, hi in [(200, (37, 41, 45), 3, 39), (130, (40, 33, 70), 0, 130), (256, (64, 64, 64), 100, 164)]:
+    facs = [torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device=dev))[0].contiguous() for r in ranks]
+    core = torch.randn(ranks, dtype=torch.float64, device=dev)
+    long = formats.TuckerTensor(core, tuple(facs))
+    ref = torch.einsum("abc,ia,jb,kc->ijk", core, facs[0][lo:hi], facs[1], facs[2])
+    scale = float(ref.abs().max())
+    got = formats.assemble_grid(long, None, lo, hi)                      # ACC = false
+    e0 = float((got - ref).abs().max()) / scale
+    base = torch.randn_like(ref)
+    out = base.clone()
+    formats.tucker_accumulate(long, lo, hi, out)                         # ACC = true
+    e1 = float((out - base - ref).abs().max()) / scale
+    print(n, ranks, e0, e1)
+    assert e0 < 1e-13 and e1 < 1e-13, (n, ranks, e0, e1)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("res", ["64", "128", "0"])
+def test_tucker_gemm_variants(cuda, res):
+    """A-resident Tucker GEMM (k_tucker_gemm_res, r3 > 32): 64- and 128-row blocks and the
+    per-tile plane GEMM (RSB200_TUCKER_RES, read when the library loads -> one process
+    each), with and without ACCUMULATE, ragged n, K not a multiple of 16, against einsum
+    (formats.py:173-176)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+    env = dict(os.environ, RSB200_TUCKER_RES=res)
+    r = subprocess.run([sys.executable, "-c", _TUCKER_VARIANT_SCRIPT, root], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
