@@ -260,11 +260,15 @@ def reference_sample_text(name, det, cores):
 def _ncu_traffic(name, kernel="gemm_short"):
     """dram read+write bytes per launch of the dominant kernel from the
     committed ncu --set full summary (profiles/), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
-            return json.load(fh)[name][kernel]["dram_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+    for tag in ("r02", "r01"):   # the latest committed pass that holds this kernel
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_traffic.json")) as fh:
+                v = json.load(fh)[name][kernel]["dram_bytes_per_launch"]
+            if v is not None:
+                return v
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def threads_used():
@@ -526,6 +530,7 @@ def main():
     mma_ms, mma_n = nat.prof_query("short_mma")
     prof = {k: nat.prof_query(k) for k in ("short_mma", "gemm_short", "gemm_tucker", "gemm_plane",
                                           "short_rows", "short_l0", "tucker_f", "topeig", "syrk",
+                                          "oz_mma",
                                           "core", "shift_project")}
     tt = torch.tensor([t_mean], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -651,7 +656,27 @@ def main():
                 "achieved": tb / t_avg / 1e9, "peak": hbm[0], "unit": "GB/s",
                 "frac": tb / t_avg / 1e9 / hbm[0], "peak_source": hbm[1],
                 "algorithmic_bytes_per_launch": tb, "avg_launch_ms": t_avg * 1e3}
-        elif t_n:              # large r3 (C4, C5): the plane GEMM, FP64-bound
+        elif t_n and prof.get("oz_mma", (0.0, 0))[1]:
+            # 96 < r3 <= 160 (C5): Ozaki-split GEMM on the int8 tensor cores (tcgen05, k_oz_res).
+            # Its floor is the slab update itself: 8 B read + 8 B written per grid point.
+            t_avg = t_ms / t_n / 1e3
+            pts = float((x1_hi - x1_lo) * n * n) / (t_n / args.steps)
+            tb, tf = 16.0 * pts, 2.0 * r3 * pts
+            kpad = 32 * -(-r3 // 32)
+            int8_ops = 28 * 2.0 * kpad * pts      # 7 slices: 28 slice products with p + q < 7
+            secondary["tucker"] = {
+                "bound": "hbm", "kernel": "k_oz_res Ozaki-split Tucker GEMM on tcgen05 int8 (7 slices, "
+                                          "TMEM accumulators), accumulated into the slab (gemm_tucker)",
+                "achieved": tb / t_avg / 1e9, "peak": hbm[0], "unit": "GB/s",
+                "frac": tb / t_avg / 1e9 / hbm[0], "peak_source": hbm[1],
+                "algorithmic_bytes_per_launch": tb, "avg_launch_ms": t_avg * 1e3,
+                "fp64_equivalent_tflops": tf / t_avg / 1e12,
+                "fp64_equivalent_vs_dgemm_peak": tf / t_avg / 1e12 / peak,
+                "int8_tops_executed": int8_ops / t_avg / 1e12,
+                "note": "2 r3 flops per grid point in FP64-equivalent terms (above the FP64 DMMA "
+                        "roofline because the products run as exact int8 slice MMAs); the "
+                        "operands' slicing is in tucker_f"}
+        elif t_n:              # large r3 (C4): the plane GEMM, FP64-bound
             t_avg = t_ms / t_n / 1e3
             tf = 2.0 * r3 * (x1_hi - x1_lo) * n * n / (t_n / args.steps)
             secondary["tucker"] = {
@@ -731,7 +756,8 @@ def main():
             "gpu_launches": int(launches),
             "roofline": roof,
             "secondary_rooflines": secondary,
-            "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            # (oz_mma is the tcgen05 kernel inside gemm_tucker: not a stage of its own)
+            "stages_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if k != "oz_mma"},
             "observables": obs,
             "cpu_baseline": cpu,
         }

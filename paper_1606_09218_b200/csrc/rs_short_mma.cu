@@ -57,6 +57,7 @@ constexpr int SM_CAP = 512;    // staged candidate copies per MMA phase
 constexpr int SM_MAXR = 24;    // largest short rank
 constexpr int SM_MAXT3 = 256;  // x3 tiles per grid row (n <= 16384)
 constexpr int SM_ACH = 16;     // columns per staged A chunk (builder variant)
+constexpr int SM_GRP = 4;      // x3 tiles per candidate search (low-overlap systems)
 constexpr int SM_ALD = 132;    // doubles per A column: 8 planes x 16 rows + 4 (= 4 mod 16)
 
 __host__ __device__ inline int sm_pitch(int gamma) {
@@ -66,7 +67,7 @@ __host__ __device__ inline int sm_pitch(int gamma) {
 }
 
 struct SmLayout {
-  int table, rec, cb, kn, seg, grp, kofd, abuf, total;  // byte offsets
+  int table, rec, cb, kn, seg, grp, kofd, abuf, d12, total;  // byte offsets
 };
 
 // one staged candidate copy: charge and the two table offsets of its window
@@ -83,7 +84,8 @@ struct __align__(16) SmSeg {
   int bo;       // B offset Z0 - s + gamma + PAD
 };
 
-__host__ __device__ inline SmLayout sm_layout(int gamma, int Rs, bool build = false) {
+__host__ __device__ inline SmLayout sm_layout(int gamma, int Rs, bool build = false,
+                                              bool grouped = false) {
   SmLayout L;
   int o = 0;
   L.table = o; o += Rs * sm_pitch(gamma) * 8;
@@ -95,6 +97,7 @@ __host__ __device__ inline SmLayout sm_layout(int gamma, int Rs, bool build = fa
   L.kofd = o;  o += (gamma + 2) * 4;
   o = (o + 15) & ~15;
   L.abuf = o;  o += build ? 2 * SM_ACH * SM_ALD * 8 : 0;   // two A chunks (builder variant)
+  L.d12 = o;   o += grouped ? (SM_CAP + 4) * 4 : 0;        // (x1, x2) distance per staged copy
   L.total = (o + 15) & ~15;
   return L;
 }
@@ -170,7 +173,7 @@ __device__ __forceinline__ unsigned sm_live_blocks(int e, int g) {
   return jhi < jlo ? 0u : ((2u << jhi) - 1u) & ~((1u << jlo) - 1u);
 }
 
-template <bool ACC, bool BUILD, bool SKIP>
+template <bool ACC, bool BUILD, bool SKIP, int GRP>
 __global__ void __launch_bounds__(SM_THREADS, 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
                 int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter, int tiles_per_cta,
                 int one, double *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  const SmLayout L = sm_layout(gamma, Rs, BUILD);
+  const SmLayout L = sm_layout(gamma, Rs, BUILD, GRP > 1);
   double *ut = (double *)(sm_raw + L.table);
   SmRec *s_rec = (SmRec *)(sm_raw + L.rec);
   SmSeg *s_seg = (SmSeg *)(sm_raw + L.seg);
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   int *s_off = s_lo + SM_THREADS;
   int *s_b3 = s_off + SM_THREADS;
   int *skofd = (int *)(sm_raw + L.kofd);
+  int *s_d12 = (int *)(sm_raw + L.d12);
   __shared__ int wsum[SM_THREADS / 32];
   __shared__ int s_tile[2];
   __shared__ int s_bands[2 * SM_MAXT3];   // bucket band [lo, hi) of every x3 tile
@@ -203,7 +207,9 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   // depend on where the slab starts (same candidates, same term cuts, same sums)
   const int64_t x1_base = x1_lo - x1_lo % SM_T1;
   const int n3t = (int)((n + SM_T3 - 1) / SM_T3), n2t = (int)((n + SM_T2 - 1) / SM_T2);
-  const int64_t ntiles = (int64_t)n3t * n2t * ((x1_hi - x1_base + SM_T1 - 1) / SM_T1);
+  // work items: groups of GRP consecutive x3 tiles (one candidate search per group)
+  const int n3g = (n3t + GRP - 1) / GRP;
+  const int64_t ntiles = (int64_t)n3g * n2t * ((x1_hi - x1_base + SM_T1 - 1) / SM_T1);
 
   // the factor table, once per CTA: v_k[d] = cbrt(wl_k) ul[d, k] inside the
   // window, zero in the margins
@@ -249,30 +255,34 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     if (tile >= ntiles) break;
     // the next tile's index is requested now: the atomic's latency hides under this tile
     if (tid == 0 && done + 1 < tiles_per_cta) s_tile[(done + 1) & 1] = atomicAdd(counter, 1);
-    const int t3 = (int)(tile % n3t), t2 = (int)((tile / n3t) % n2t);
-    const int64_t t1 = tile / ((int64_t)n3t * n2t);
-    const int X0 = (int)(x1_base + t1 * SM_T1), Y0 = t2 * SM_T2, Z0 = t3 * SM_T3;
+    const int t3g = (int)(tile % n3g), t2 = (int)((tile / n3g) % n2t);
+    const int64_t t1 = tile / ((int64_t)n3g * n2t);
+    const int X0 = (int)(x1_base + t1 * SM_T1), Y0 = t2 * SM_T2;
+    const int t3_lo = t3g * GRP, t3_hi = min(t3_lo + GRP, n3t);
+    int Z0 = t3_lo * SM_T3;   // the x3 tile in work (set per tile below)
 
     double acc[2][8][2];
+    auto zero_acc = [&]() {
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    };
 
-    // one MMA phase over the staged copies [0, len): segments = runs of equal
-    // bucket, column count = max live terms of the run's copies
-    auto flush = [&](int len) {
+    // one MMA phase over the staged copies [base, base + len) (s_cb = their x3 index, s_kn =
+    // their live terms for the tile at Z0): segments = runs of equal bucket, column count =
+    // max live terms of the run's copies
+    auto flush = [&](int base, int len) {
       __syncthreads();
-      if (tid == 0) s_cb[len] = -1;
-      __syncthreads();
+      const int end = base + len;
       int nseg = 0, ncol = 0;
       for (int i0 = 0; i0 < len; i0 += SM_THREADS) {
-        const int i = i0 + tid;
-        const bool start = i < len && (i == 0 || s_cb[i] != s_cb[i - 1]);
+        const int i = base + i0 + tid;
+        const bool start = i < end && (i == base || s_cb[i] != s_cb[i - 1]);
         int K = 0;
         if (start) {   // the run is short (copies of one bucket near the tile)
           const int id = s_cb[i];
-          for (int q = i; s_cb[q] == id; ++q) K = max(K, s_kn[q]);
+          for (int q = i; q < end && s_cb[q] == id; ++q) K = max(K, s_kn[q]);
         }
         int tot;   // one scan for both the segment index (low half) and the column prefix
         const int pre = sm_block_scan(start ? (K << 12) | 1 : 0, wsum, &tot);
@@ -281,7 +291,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
           sg.q_lo = i;
           sg.col = ncol + (pre >> 12);
           sg.K = K;
-          sg.bo = s_cb[i];
+          sg.bo = Z0 - s_cb[i] + gamma + SM_PAD;   // B offset of the bucket for this tile
           s_seg[nseg + (pre & 0xFFF)] = sg;
         }
         nseg += tot & 0xFFF;
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
       }
       if (tid == 0) {
         SmSeg sg;
-        sg.q_lo = len;
+        sg.q_lo = end;
         sg.col = ncol;
         sg.K = 0;
         sg.bo = 0;
@@ -489,98 +499,171 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
       }
     };
 
-    // candidate copies of this tile, bucket group by bucket group
-    const int blo = s_bands[2 * t3], bhi = s_bands[2 * t3 + 1];
     const int c1lo = X0 - gamma, c1hi = X0 + SM_T1 - 1 + gamma;
     const int c2lo = Y0 - gamma, c2hi = Y0 + SM_T2 - 1 + gamma;
-    int len = 0;
-    for (int g = blo; g < bhi; g += SM_THREADS) {
-      const int bi = g + tid;
-      int lo = 0, cnt = 0, b3 = 0;
-      if (bi < bhi) {  // the bucket's copies in the 16-cell x2 blocks the window meets
-        b3 = bc3[bi];
-        const int32_t *yr = y16 + (int64_t)bi * ldy;
-        lo = yr[max(c2lo, 0) >> 4];
-        cnt = yr[min((c2hi >> 4) + 1, ldy - 1)] - lo;
-      }
-      int tot;
-      const int off = sm_block_scan(cnt, wsum, &tot);
-      s_lo[tid] = lo;
-      s_off[tid] = off;
-      s_b3[tid] = b3;
-      const int nbk = min(SM_THREADS, bhi - g);
-      __syncthreads();
-      for (int cs = 0; cs < tot; cs += SM_THREADS) {
-        if (len > SM_CAP - SM_THREADS) {   // uniform
-          flush(len);
-          __syncthreads();
-          len = 0;
-        }
-        const int v = cs + tid;
-        bool cov = false;
-        int kn = 0, bo = 0;
-        SmRec rec;
-        if (v < tot) {   // last bucket with offset <= v (empty buckets share offsets)
-          int l = 0, h = nbk;
-          while (h - l > 1) {
-            const int m = (l + h) >> 1;
-            if (s_off[m] <= v) l = m; else h = m;
-          }
-          const int p = s_lo[l] + (v - s_off[l]);
-          const int a1 = c1[p], a2 = c2[p];
-          const double zp = zq[p];   // with the coordinates: one memory round trip, not two
-          if (a1 >= c1lo && a1 <= c1hi && a2 >= c2lo && a2 <= c2hi) {
-            const int a3 = s_b3[l];
-            const int d1 = max(0, max(X0 - a1, a1 - (X0 + SM_T1 - 1)));
-            const int d2 = max(0, max(Y0 - a2, a2 - (Y0 + SM_T2 - 1)));
-            const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
-            kn = skofd[max(d1, max(d2, d3))];
-            if (kn > 0) {
-              cov = true;
-              rec.z = zp;
-              rec.o1 = 8 * (X0 - a1 + gamma + SM_PAD);   // byte offsets into a table row
-              rec.o2 = 8 * (Y0 - a2 + gamma + SM_PAD);
-              bo = Z0 - a3 + gamma + SM_PAD;   // B offset: identifies the bucket as well
-            }
-          }
-        }
-        int t2;
-        const int pos = sm_block_scan(cov ? 1 : 0, wsum, &t2);
-        if (cov) {
-          s_rec[len + pos] = rec;
-          s_kn[len + pos] = kn;
-          s_cb[len + pos] = bo;
-        }
-        len += t2;
-      }
-      __syncthreads();
-    }
-    if (len > 0) flush(len);
 
-    // epilogue: every grid point of the tile is written once
-    const int64_t x1 = X0 + warp;
-    if (x1 >= x1_lo && x1 < x1_hi) {
+    // epilogue: every grid point of the tile at Z0 is written once
+    auto epilogue = [&]() {
+      const int64_t x1 = X0 + warp;
+      if (x1 >= x1_lo && x1 < x1_hi) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int64_t x2 = Y0 + 8 * i + gid;
-        if (x2 >= n) continue;
-        double *row = out + ((x1 - x1_lo) * n + x2) * n + Z0 + 2 * tig;
+        for (int i = 0; i < 2; ++i) {
+          const int64_t x2 = Y0 + 8 * i + gid;
+          if (x2 >= n) continue;
+          double *row = out + ((x1 - x1_lo) * n + x2) * n + Z0 + 2 * tig;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int64_t x3 = Z0 + 8 * j + 2 * tig;
-          double v0 = acc[i][j][0], v1 = acc[i][j][1];
-          if (x3 + 1 < n) {
-            double2 *p = reinterpret_cast<double2 *>(row + 8 * j);
-            if (ACC) {
-              const double2 o = __ldcs(p);
-              v0 += o.x;
-              v1 += o.y;
+          for (int j = 0; j < 8; ++j) {
+            const int64_t x3 = Z0 + 8 * j + 2 * tig;
+            double v0 = acc[i][j][0], v1 = acc[i][j][1];
+            if (x3 + 1 < n) {
+              double2 *p = reinterpret_cast<double2 *>(row + 8 * j);
+              if (ACC) {
+                const double2 o = __ldcs(p);
+                v0 += o.x;
+                v1 += o.y;
+              }
+              __stcs(p, make_double2(v0, v1));
+            } else if (x3 < n) {
+              if (ACC) v0 += __ldcs(row + 8 * j);
+              __stcs(row + 8 * j, v0);
             }
-            __stcs(p, make_double2(v0, v1));
-          } else if (x3 < n) {
-            if (ACC) v0 += __ldcs(row + 8 * j);
-            __stcs(row + 8 * j, v0);
           }
+        }
+      }
+    };
+
+    // Candidate copies of the x3 tiles [ta, tb) (same x1, x2 window; the union of
+    // their bucket bands), bucket group by bucket group, staged in bucket order.
+    // grouped = false: one tile; the live terms are known at staging and a full
+    // staging area is flushed on the way (returns the copies still staged).
+    // grouped = true: nothing is flushed; returns -1 when the area overflows.
+    auto search = [&](int ta, int tb, bool grouped) -> int {
+      const int blo = s_bands[2 * ta], bhi = s_bands[2 * (tb - 1) + 1];
+      int len = 0;
+      bool over = false;
+      for (int g = blo; g < bhi; g += SM_THREADS) {
+        const int bi = g + tid;
+        int lo = 0, cnt = 0, b3 = 0;
+        if (bi < bhi) {  // the bucket's copies in the 16-cell x2 blocks the window meets
+          b3 = bc3[bi];
+          const int32_t *yr = y16 + (int64_t)bi * ldy;
+          lo = yr[max(c2lo, 0) >> 4];
+          cnt = yr[min((c2hi >> 4) + 1, ldy - 1)] - lo;
+        }
+        int tot;
+        const int off = sm_block_scan(cnt, wsum, &tot);
+        s_lo[tid] = lo;
+        s_off[tid] = off;
+        s_b3[tid] = b3;
+        const int nbk = min(SM_THREADS, bhi - g);
+        __syncthreads();
+        for (int cs = 0; cs < tot; cs += SM_THREADS) {
+          if (len > SM_CAP - SM_THREADS) {   // uniform
+            if (grouped) {
+              over = true;
+              break;
+            }
+            flush(0, len);
+            __syncthreads();
+            len = 0;
+          }
+          const int v = cs + tid;
+          bool cov = false;
+          int kn = 0, a3 = 0, d12 = 0;
+          SmRec rec;
+          if (v < tot) {   // last bucket with offset <= v (empty buckets share offsets)
+            int l = 0, h = nbk;
+            while (h - l > 1) {
+              const int m = (l + h) >> 1;
+              if (s_off[m] <= v) l = m; else h = m;
+            }
+            const int p = s_lo[l] + (v - s_off[l]);
+            const int a1 = c1[p], a2 = c2[p];
+            const double zp = zq[p];   // with the coordinates: one memory round trip, not two
+            if (a1 >= c1lo && a1 <= c1hi && a2 >= c2lo && a2 <= c2hi) {
+              a3 = s_b3[l];
+              const int d1 = max(0, max(X0 - a1, a1 - (X0 + SM_T1 - 1)));
+              const int d2 = max(0, max(Y0 - a2, a2 - (Y0 + SM_T2 - 1)));
+              d12 = max(d1, d2);
+              if (grouped) {
+                kn = skofd[d12];   // an upper bound: the tile's x3 distance cuts it further
+              } else {
+                const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
+                kn = skofd[max(d12, d3)];
+              }
+              if (kn > 0) {
+                cov = true;
+                rec.z = zp;
+                rec.o1 = 8 * (X0 - a1 + gamma + SM_PAD);   // byte offsets into a table row
+                rec.o2 = 8 * (Y0 - a2 + gamma + SM_PAD);
+              }
+            }
+          }
+          int t2;
+          const int pos = sm_block_scan(cov ? 1 : 0, wsum, &t2);
+          if (cov) {
+            s_rec[len + pos] = rec;
+            s_kn[len + pos] = kn;
+            s_cb[len + pos] = a3;   // the bucket's x3 index (ascending along the staging area)
+            if (GRP > 1) s_d12[len + pos] = d12;
+          }
+          len += t2;
+        }
+        __syncthreads();
+        if (over) return -1;
+      }
+      return len;
+    };
+
+    auto tile_alone = [&](int t3) {
+      Z0 = t3 * SM_T3;
+      zero_acc();
+      const int len = search(t3, t3 + 1, false);
+      if (len > 0) flush(0, len);
+      epilogue();
+    };
+
+    if constexpr (GRP == 1) {
+      tile_alone(t3_lo);
+    } else {
+      // one search for the group's tiles (low overlap: a few dozen copies): every tile
+      // then takes the staged copies whose bucket lies within gamma of it -- a
+      // contiguous range, the area is in bucket order -- with the live terms of its
+      // own x3 distance.  An overflowing group falls back to tile-by-tile searches.
+      const int glen = search(t3_lo, t3_hi, true);
+      if (glen < 0) {
+        for (int t3 = t3_lo; t3 < t3_hi; ++t3) {
+          __syncthreads();
+          tile_alone(t3);
+        }
+      } else {
+        for (int t3 = t3_lo; t3 < t3_hi; ++t3) {
+          __syncthreads();   // previous tile's MMA phase done with s_kn / s_seg
+          Z0 = t3 * SM_T3;
+          zero_acc();
+          const int zlo = Z0 - gamma, zhi = Z0 + SM_T3 - 1 + gamma;
+          int qa = 0, qb = glen;   // first staged copy with x3 >= zlo, first with x3 > zhi
+          {
+            int l = 0, h = glen;
+            while (l < h) {
+              const int m = (l + h) >> 1;
+              if (s_cb[m] < zlo) l = m + 1; else h = m;
+            }
+            qa = l;
+            h = glen;
+            while (l < h) {
+              const int m = (l + h) >> 1;
+              if (s_cb[m] <= zhi) l = m + 1; else h = m;
+            }
+            qb = l;
+          }
+          for (int q = qa + tid; q < qb; q += SM_THREADS) {
+            const int a3 = s_cb[q];
+            const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
+            s_kn[q] = skofd[max(s_d12[q], d3)];
+          }
+          if (qb > qa) flush(qa, qb - qa);   // (starts with a barrier: s_kn complete)
+          epilogue();
         }
       }
     }
@@ -645,7 +728,6 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const double ov0 = (double)std::max<int64_t>(count, 1) * (w0 / n) * (w0 / n) * (w0 / n);
   bool build = build_env >= 0 ? build_env != 0 : ov0 >= 64.0;
   if (build && sm_layout((int)gamma, (int)Rs, true).total + 4096 > 227 * 1024) build = false;
-  const SmLayout L = sm_layout((int)gamma, (int)Rs, build);
   const bool acc = flags & RS_ASM_ACCUMULATE;
   // RSB200_MMA_SKIP=1: the MMAs (and B loads) of the 8-wide x3 blocks a step's columns
   // cannot reach are skipped -- 25 % (C5) / 15 % (C4) fewer DMMAs.  Measured no faster
@@ -654,10 +736,18 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   // the candidate search dominate, not the tensor pipe -- so the default issues them all.
   const char *senv = getenv("RSB200_MMA_SKIP");
   const bool skip = senv && senv[0] == '1';
-  auto fn = skip ? (build ? (acc ? k_short_mma<true, true, true> : k_short_mma<false, true, true>)
-                          : (acc ? k_short_mma<true, false, true> : k_short_mma<false, false, true>))
-                 : (build ? (acc ? k_short_mma<true, true, false> : k_short_mma<false, true, false>)
-                          : (acc ? k_short_mma<true, false, false> : k_short_mma<false, false, false>));
+  // low overlap (C5: ~25 candidate copies per tile): one candidate search per group of
+  // SM_GRP consecutive x3 tiles (RSB200_MMA_GROUP=0: per tile)
+  const char *genv = getenv("RSB200_MMA_GROUP");
+  const bool grouped = !build && !skip && ov0 <= 64.0 && !(genv && genv[0] == '0');
+  const SmLayout L = sm_layout((int)gamma, (int)Rs, build, grouped);
+  auto fn = grouped ? (acc ? k_short_mma<true, false, false, SM_GRP>
+                           : k_short_mma<false, false, false, SM_GRP>)
+            : skip ? (build ? (acc ? k_short_mma<true, true, true, 1> : k_short_mma<false, true, true, 1>)
+                            : (acc ? k_short_mma<true, false, true, 1> : k_short_mma<false, false, true, 1>))
+                   : (build ? (acc ? k_short_mma<true, true, false, 1> : k_short_mma<false, true, false, 1>)
+                            : (acc ? k_short_mma<true, false, false, 1>
+                                   : k_short_mma<false, false, false, 1>));
   // RSB200_MMA_PAD_KB: extra dynamic shared memory per CTA (occupancy experiments:
   // one CTA per SM leaves room for another kernel's CTAs)
   const char *penv = getenv("RSB200_MMA_PAD_KB");
@@ -671,7 +761,8 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int per_sm = smem_bytes + 1024 <= 113 * 1024 ? 2 : 1;
-  const int64_t ntiles = ceil_div(n, SM_T3) * ceil_div(n, SM_T2) *
+  // work items: x3 tile groups (of one tile unless grouped)
+  const int64_t ntiles = ceil_div(ceil_div(n, SM_T3), grouped ? SM_GRP : 1) * ceil_div(n, SM_T2) *
                          ceil_div(x1_hi - (x1_lo - x1_lo % SM_T1), SM_T1);
   static const int waves = [] {   // RSB200_MMA_WAVES: CTA generations per SM slot
     const char *e = getenv("RSB200_MMA_WAVES");
@@ -684,7 +775,8 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   // 1/waves of a slot's share, so CTAs keep turning over
   const double w = (double)std::min<int64_t>(2 * gamma + 1, n);
   const double ov = std::max(1.0, (double)std::max<int64_t>(count, 1) * (w / n) * (w / n) * (w / n));
-  const int64_t t_min = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)(100.0 / (0.3 * ov))));
+  const int64_t t_min = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)(100.0 / (0.3 * ov))) /
+                                             (grouped ? SM_GRP : 1));
   const int tiles_per_cta = (int)std::max<int64_t>(
       ceil_div(ntiles, slots * waves), std::min<int64_t>(t_min, ceil_div(ntiles, slots)));
   const unsigned grid = (unsigned)ceil_div(ntiles, tiles_per_cta);

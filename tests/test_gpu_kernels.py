@@ -202,7 +202,9 @@ sys.path.insert(0, sys.argv[1])
 from paper_1606_09218_b200 import formats
 torch.manual_seed(3)
 dev = "cuda"
-for n, ranks, lo, hi in [(200, (37, 41, 45), 3, 39), (130, (40, 33, 70), 0, 130), (256, (64, 64, 64), 100, 164)]:
+# r3 in (96, 160] at n >= 256: the Ozaki-split tcgen05 path (k_oz_res) unless RSB200_TUCKER_OZ=0
+for n, ranks, lo, hi in [(200, (37, 41, 45), 3, 39), (130, (40, 33, 70), 0, 130), (256, (64, 64, 64), 100, 164),
+                         (256, (20, 24, 132), 7, 71), (320, (30, 30, 160), 0, 33), (258, (16, 16, 98), 250, 258)]:
     facs = [torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device=dev))[0].contiguous() for r in ranks]
     core = torch.randn(ranks, dtype=torch.float64, device=dev)
     long = formats.TuckerTensor(core, tuple(facs))
@@ -215,12 +217,13 @@ for n, ranks, lo, hi in [(200, (37, 41, 45), 3, 39), (130, (40, 33, 70), 0, 130)
     formats.tucker_accumulate(long, lo, hi, out)                         # ACC = true
     e1 = float((out - base - ref).abs().max()) / scale
     print(n, ranks, e0, e1)
-    assert e0 < 1e-13 and e1 < 1e-13, (n, ranks, e0, e1)
+    tol = 1e-13 if ranks[2] <= 96 else 2e-12   # 7 slices of 7 bits: K 2^-49 of the row/column scales
+    assert e0 < tol and e1 < tol, (n, ranks, e0, e1)
 print("OK")
 """
 
 
-@pytest.mark.parametrize("res", ["64", "128", "0"])
+@pytest.mark.parametrize("res", ["64", "128", "0", "oz0"])
 def test_tucker_gemm_variants(cuda, res):
     """A-resident Tucker GEMM (k_tucker_gemm_res, r3 > 32): 64- and 128-row blocks and the
     per-tile plane GEMM (RSB200_TUCKER_RES, read when the library loads -> one process
@@ -230,7 +233,11 @@ def test_tucker_gemm_variants(cuda, res):
     import subprocess
     import sys
     root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
-    env = dict(os.environ, RSB200_TUCKER_RES=res)
+    env = dict(os.environ)
+    if res == "oz0":   # large r3 on the FP64 DMMA kernel as well
+        env["RSB200_TUCKER_OZ"] = "0"
+    else:
+        env["RSB200_TUCKER_RES"] = res
     r = subprocess.run([sys.executable, "-c", _TUCKER_VARIANT_SCRIPT, root], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr

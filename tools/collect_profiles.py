@@ -17,7 +17,7 @@ def val(s):
 
 
 def key_of(name):
-    for k, v in (("k_short_mma", "short_mma"), ("k_tucker_gemm_res", "tucker_gemm_res"),
+    for k, v in (("k_short_mma", "short_mma"), ("k_tucker_gemm_res", "tucker_gemm_res"), ("k_oz_res", "oz_res"),
                  ("k_tucker_apply", "tucker_apply"), ("syrk", "syrk"), ("core_h", "core_h")):
         if k in name:
             return v
@@ -54,7 +54,9 @@ with open(f"{P}/{tag}_ncu_summary.md", "w") as fh:
         if os.path.exists(path):
             fh.write(open(path).read().replace(f"{G}/{tag}_full_", f"{tag}_full_"))
 for f in glob.glob(f"{G}/{tag}_bench_*.json") + [f"{G}/{tag}_launch_shares_C5.md",
-                                                  f"{G}/{tag}_launches_C5.csv.gz", f"{G}/{tag}_smi.txt"]:
+                                                  f"{G}/{tag}_launches_C5.csv.gz", f"{G}/{tag}_smi.txt",
+                                                  f"{G}/{tag}_sass_counts.txt",
+                                                  f"{G}/{tag}_pytest_gpu.txt"]:
     if os.path.exists(f):
         shutil.copy(f, f"{P}/" + os.path.basename(f))
 for c in ("C2", "C3", "C4", "C5"):

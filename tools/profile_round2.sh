@@ -7,7 +7,12 @@ TAG=${TAG:-r02}
 O=gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/${TAG}_smi.txt
 nproc >> $O/${TAG}_smi.txt; free -g >> $O/${TAG}_smi.txt
+# SASS evidence of the Blackwell paths (tcgen05 MMA, TMEM loads, bulk copies) and the FP64 tensor path
+cuobjdump -sass paper_1606_09218_b200/librsb200.so > /tmp/rsb200.sass 2>/dev/null
+for m in UTCIMMA LDTM UBLKCP UTMALDG DMMA LDGSTS; do echo "$m $(grep -c "$m" /tmp/rsb200.sass)"; done > $O/${TAG}_sass_counts.txt
+python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu.txt 2>&1
 python bench.py > $O/${TAG}_bench_C5.json 2> $O/${TAG}_bench_C5.err
+RSB200_TUCKER_OZ=0 python bench.py --no-cpu-baseline > $O/${TAG}_bench_C5_dmma_tucker.json 2> $O/${TAG}_bench_C5_dmma_tucker.err
 for c in C4 C3 C2; do
   timeout 600 python bench.py --config $c --no-cpu-baseline > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
 done
@@ -18,7 +23,7 @@ RSB200_SIDE_SMS=0 BENCH_NO_OBSERVABLES=1 timeout 1500 ncu --metrics gpu__time_du
   --log-file $O/${TAG}_launches_C5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/${TAG}_ncu_launch.log 2>&1
 # full captures (one launch of each top kernel, after the warm-up steps)
 RSB200_SIDE_SMS=0 BENCH_NO_OBSERVABLES=1 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_short_mma|k_tucker_gemm_res|k_core_h|k_syrk_part" -s 28 -c 4 -f -o $O/${TAG}_full_C5 \
+  -k regex:"k_short_mma|k_tucker_gemm_res|k_oz_res|k_core_h|k_syrk_part" -s 28 -c 6 -f -o $O/${TAG}_full_C5 \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/${TAG}_ncu_C5.log 2>&1
 summarise() {  # .ncu-rep files are tens of MB (gpurun_out/ is capped at 64 MiB): keep the tables
   python tools/ncu_summary.py $O/${TAG}_full_$1.ncu-rep > $O/${TAG}_ncu_summary_$1.md 2>&1
