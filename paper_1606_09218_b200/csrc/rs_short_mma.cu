@@ -736,10 +736,12 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   // the candidate search dominate, not the tensor pipe -- so the default issues them all.
   const char *senv = getenv("RSB200_MMA_SKIP");
   const bool skip = senv && senv[0] == '1';
-  // low overlap (C5: ~25 candidate copies per tile): one candidate search per group of
-  // SM_GRP consecutive x3 tiles (RSB200_MMA_GROUP=0: per tile)
+  // RSB200_MMA_GROUP=1, low overlap (C5: ~25 candidate copies per tile): one candidate
+  // search per group of SM_GRP consecutive x3 tiles.  Measured no faster (C5 75.8 vs
+  // 76.2 ms: of the 21 ms the kernel takes without its K loop, 11 are the grid store
+  // itself and the per-tile segmentation stays), so the default searches per tile.
   const char *genv = getenv("RSB200_MMA_GROUP");
-  const bool grouped = !build && !skip && ov0 <= 64.0 && !(genv && genv[0] == '0');
+  const bool grouped = !build && !skip && ov0 <= 64.0 && genv && genv[0] == '1';
   const SmLayout L = sm_layout((int)gamma, (int)Rs, build, grouped);
   auto fn = grouped ? (acc ? k_short_mma<true, false, false, SM_GRP>
                            : k_short_mma<false, false, false, SM_GRP>)
