@@ -719,16 +719,24 @@ __global__ void __launch_bounds__(OzRes<S>::THREADS_RES, 1)
     asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
                  : "=r"(leader));
     uint32_t ra = 0, ut = 0;
+    long long w_a = 0, w_e0 = 0, w_e1 = 0, w_f = 0;   // (128) cycles spent waiting, by barrier
+    const bool prof = dbg & 128;
     for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++ra) {
+      long long tw = prof ? clock64() : 0;
       mbar_wait(&a_full, ra & 1u);
+      if (prof) w_a += clock64() - tw;
       for (int64_t ct = 0; ct < ntn; ++ct, ++ut) {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
+          tw = prof ? clock64() : 0;
           if (!(dbg & 8)) mbar_wait(&acc_empty[g], (ut & 1u) ^ 1u);   // (8: free-running MMAs)
+          if (prof) (g ? w_e1 : w_e0) += clock64() - tw;
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           for (int ks = 0; ks < nsteps; ++ks) {
             if (g == 0 && !(dbg & 8)) {   // pass 2 finds the K step in place
+              tw = prof ? clock64() : 0;
               mbar_wait(&full[ks], ut & 1u);
+              if (prof) w_f += clock64() - tw;
               asm volatile("tcgen05.fence::after_thread_sync;\n");
             }
             const uint64_t dak = da0 + (uint64_t)((ks * S * Cfg::A_SLICE) >> 4);
@@ -753,6 +761,16 @@ __global__ void __launch_bounds__(OzRes<S>::THREADS_RES, 1)
       if (leader) umma_commit(&a_empty);
       __syncwarp();
     }
+    // measured at C5 (2.70 M cycles per launch of a 64-plane slab): A 40 K, acc_empty[0]
+    // 423 K, acc_empty[1] 20 K, B full 118 K -- the rest is MMA issue, ~55 cycles per MMA
+    // from one lane, about what the 128 x 64 x 32 MMA takes to execute: the warp is issue
+    // bound and every wait delays the tensor pipe.  An issue form predicated inside the
+    // instruction block (uniform control flow) measured slower (2.96 M cycles); 576
+    // threads cap the kernel at 96 registers (104 already fail to launch), which is what
+    // keeps the old values of C from being requested earlier.
+    if (prof && blockIdx.x == 0 && leader)
+      printf("k_oz_res MMA warp waits (cycles): A %lld, acc_empty0 %lld, acc_empty1 %lld, B full %lld\n",
+             w_a, w_e0, w_e1, w_f);
   } else {             // --------------------------------------------- epilogue
     // 16 warps: warp -> (TMEM lane quarter, 16-column group).  tcgen05.ld 16x256b hands
     // thread T rows T/4 (+8) and column pairs 2 (T%4) (+8) of a 16 x 16 block, so the
