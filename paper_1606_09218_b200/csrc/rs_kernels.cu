@@ -2248,7 +2248,8 @@ int rs_assemble_planes(const double *core, int64_t r1, int64_t r2, int64_t r3, c
       return 0;
     };
     if (with_long && !with_short && g_tucker_res && r3p <= tr::KMAX && n % 2 == 0) {
-      // A-resident Tucker GEMM: one CTA per 128-row block over all column tiles
+      // A-resident Tucker GEMM: one CTA per 64-row block (default; RSB200_TUCKER_RES=128: 128 rows)
+      // over all column tiles
       // Bt chunk width x ring depth: 16 columns x 3 stages, or 32 x 2 for short K
       // (same-job A/B: C5, K = 132: 2.82 vs 2.98 ms per 64 planes; C4, K = 40:
       // 0.381 vs 0.355 ms); RSB200_TUCKER_BK=16|32 forces one
