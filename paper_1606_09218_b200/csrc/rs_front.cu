@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "rs_common.cuh"
+#include "rs_dmma.cuh"
 
 using namespace rsb;
 
@@ -354,6 +355,98 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same H stage on the FP64 tensor cores: for a (bucket q, term k) the (a, b) panel
+// is X^T Y with X = (z w_k TT1[a]) (copies x a) and Y = TT2 (copies x b), K = the
+// bucket's copies (C5: ~86) -- mma.m8n8k4 with a = m, copy = k, b = n.  Block = (bucket,
+// 16 a, 4 terms) as above; warp w owns the 8-wide b blocks w, w + 8, w + 16 for both
+// 8-row a blocks and all 4 terms (48 accumulators per thread); operands are staged per
+// term with the pitch = 4 mod 16 doubles that keeps the fragment gathers conflict free.
+// C5 core_h 6.7 -> see DESIGN (the CUDA-core form ran at 9 % of the FP64 peak).
+constexpr int CHM_NB = 3;      // b blocks per warp: r2 <= 8 * 8 * 3 = 192
+__host__ __device__ inline int chm_pitch(int r) {
+  int p = (r + 7) / 8 * 8;
+  while (p % 16 != 4) ++p;
+  return p;
+}
+__global__ void __launch_bounds__(256)
+    k_core_h_mma(const double *__restrict__ TT1t, const double *__restrict__ TT2t, int r1, int r2,
+                 int64_t n, int R, const double *__restrict__ w, const int32_t *__restrict__ c1,
+                 const int32_t *__restrict__ c2, const double *__restrict__ zq,
+                 const int32_t *__restrict__ bstart, double *__restrict__ H, int64_t ldH) {
+  extern __shared__ double sh[];
+  const int PY = chm_pitch(r2), PX = 20;
+  double *sY = sh;                      // CH_CHUNK x PY
+  double *sX = sh + CH_CHUNK * PY;      // CH_CHUNK x PX (16 a + pad)
+  const int q = blockIdx.y, a0 = blockIdx.x * CH_TA, k0 = blockIdx.z * CH_KG;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
+  const int nbk = (r2 + 7) / 8;
+  double acc[CH_KG][CHM_NB][2][2];
+#pragma unroll
+  for (int k = 0; k < CH_KG; ++k)
+#pragma unroll
+    for (int b = 0; b < CHM_NB; ++b)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) acc[k][b][m][0] = acc[k][b][m][1] = 0.0;
+  const int p_lo = bstart[q], p_hi = bstart[q + 1];
+  for (int i0 = p_lo; i0 < p_hi; i0 += CH_CHUNK) {
+    const int cnt = min(CH_CHUNK, p_hi - i0), cnt4 = (cnt + 3) & ~3;
+#pragma unroll
+    for (int kk = 0; kk < CH_KG; ++kk) {
+      const int k = k0 + kk;
+      if (k < R) {   // uniform
+        for (int e = tid; e < cnt4 * r2; e += 256) {
+          const int j = e / r2, t = e - j * r2;
+          sY[j * PY + t] = j < cnt ? TT2t[((int64_t)(n - c2[i0 + j]) * R + k) * r2 + t] : 0.0;
+        }
+        for (int e = tid; e < cnt4 * CH_TA; e += 256) {
+          const int j = e / CH_TA, u = e - j * CH_TA;
+          const int i = i0 + j;
+          sX[j * PX + u] = (j < cnt && a0 + u < r1)
+                               ? zq[i] * w[k] * TT1t[((int64_t)(n - c1[i]) * R + k) * r1 + a0 + u]
+                               : 0.0;
+        }
+        __syncthreads();
+        for (int j0 = 0; j0 < cnt4; j0 += 4) {
+          const double xa0 = sX[(j0 + tig) * PX + gid], xa1 = sX[(j0 + tig) * PX + 8 + gid];
+#pragma unroll
+          for (int b = 0; b < CHM_NB; ++b) {
+            const int nb = warp + 8 * b;
+            if (nb < nbk) {   // warp-uniform
+              const double yb = sY[(j0 + tig) * PY + 8 * nb + gid];
+              dmma_884(acc[kk][b][0], xa0, yb);
+              dmma_884(acc[kk][b][1], xa1, yb);
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // c[0], c[1]: row a = 8 m + gid, columns b = 8 nb + 2 tig + {0, 1}; per (a, b) one
+  // aligned CH_KG-wide segment of H
+#pragma unroll
+  for (int b = 0; b < CHM_NB; ++b) {
+    const int nb = warp + 8 * b;
+    if (nb >= nbk) continue;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int a = a0 + 8 * m + gid;
+      if (a >= r1) continue;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int bc = 8 * nb + 2 * tig + c;
+        if (bc >= r2) continue;
+        double *dst = H + ((int64_t)a * r2 + bc) * ldH + (int64_t)q * R + k0;
+#pragma unroll
+        for (int kk = 0; kk < CH_KG; ++kk)
+          if (k0 + kk < R) dst[kk] = acc[kk][b][m][c];
+        if (q == (int)gridDim.y - 1 && blockIdx.z == gridDim.z - 1)  // even-K padding column(s)
+          for (int64_t cc = (int64_t)(q + 1) * R; cc < ldH; ++cc) H[((int64_t)a * r2 + bc) * ldH + cc] = 0.0;
+      }
+    }
+  }
+}
+
 // T3[c, q*R + k] = TT3[c, n - bc3[q], k] for occupied buckets, 0 past *nb
 __global__ void k_core_t3(const double *__restrict__ TT3, int r3, int64_t n, int R,
                           const int32_t *__restrict__ bc3, const int32_t *__restrict__ nbp,
@@ -475,13 +568,26 @@ static int back_impl(const double *U, int64_t b, int64_t n, int64_t r1, int64_t 
       TT2, (int)r2, n, (int)R, TT2t);
   if ((st = check_launch("core transpose"))) return st;
   RS_REQUIRE(r2 <= 256, "rs_back: r2 = %lld exceeds the H kernel's block", (long long)r2);
-  const int threads = (int)round_up(r2, 32);
-  const size_t smem = (size_t)CH_CHUNK * (r2 + CH_TA) * 8;
-  cudaError_t e = smem_attr((const void *)k_core_h, (int)smem);
-  if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
-  k_core_h<<<dim3((unsigned)ceil_div(r1, CH_TA), (unsigned)nq, (unsigned)ceil_div(R, CH_KG)),
-             threads, smem, s>>>(
-      TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq, bstart, H, ldH);
+  // RSB200_CORE_H=cuda: the CUDA-core H stage (also beyond the tensor form's r2 <= 192)
+  static const bool h_mma = [] {
+    const char *e = getenv("RSB200_CORE_H");
+    return !(e && e[0] == 'c');
+  }();
+  const dim3 hgrid((unsigned)ceil_div(r1, CH_TA), (unsigned)nq, (unsigned)ceil_div(R, CH_KG));
+  if (h_mma && r2 <= 8 * 8 * CHM_NB) {
+    const size_t smem = (size_t)CH_CHUNK * (chm_pitch((int)r2) + 20) * 8;
+    cudaError_t e = smem_attr((const void *)k_core_h_mma, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
+    k_core_h_mma<<<hgrid, 256, smem, s>>>(TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq,
+                                          bstart, H, ldH);
+  } else {
+    const int threads = (int)round_up(r2, 32);
+    const size_t smem = (size_t)CH_CHUNK * (r2 + CH_TA) * 8;
+    cudaError_t e = smem_attr((const void *)k_core_h, (int)smem);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, "core_h smem: %s", cudaGetErrorString(e));
+    k_core_h<<<hgrid, threads, smem, s>>>(TT1t, TT2t, (int)r1, (int)r2, n, (int)R, w, c1, c2, zq,
+                                          bstart, H, ldH);
+  }
   if ((st = check_launch("core_h"))) return st;
   k_core_t3<<<(unsigned)std::min<int64_t>(ceil_div(r3 * ldH, 256), 4096), 256, 0, s>>>(
       TT3, (int)r3, n, (int)R, bc3, nb, nq, T3, ldH, q_off);
