@@ -351,6 +351,56 @@ __global__ void k_oz_slice_t(const double *__restrict__ X, int64_t rows, int64_t
         make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
 
+// Row exponent and slices in one pass (the A-resident kernel's operands): 16 lanes per
+// row, lane g reads the row's columns [16 g, 16 g + 16) -- a row is one contiguous,
+// coalesced read, seen once -- the half-warp reduces the row's max |x| to the exponent,
+// every lane cuts its 16 values into S digits and writes 16 bytes per slice into the
+// tiled SWIZZLE_32B image (lanes 2 m, 2 m + 1 fill one 32-byte row of K step m).
+// K <= 256 (16 lanes x 16 columns); rows past `rows` (tile padding) are zero.
+template <int S>
+__global__ void __launch_bounds__(256)
+    k_oz_rowslice(const double *__restrict__ X, int64_t rows, int64_t rows_pad, int64_t ld,
+                  int64_t cols, int *__restrict__ e, int8_t *__restrict__ out, int TR,
+                  int64_t ksteps, int64_t sstride, int64_t tstride) {
+  const int g = threadIdx.x & 15;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
+  if (r >= rows_pad) return;   // (whole half-warps leave together)
+  const int64_t kcols = (cols + 31) / 32 * 32;   // K steps in use
+  double x[16];
+  double m = 0.0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t c = g * 16 + j;
+    x[j] = (r < rows && c < cols) ? X[r * ld + c] : 0.0;
+    m = fmax(m, fabs(x[j]));
+  }
+#pragma unroll
+  for (int o = 8; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o, 16));
+  int ex = 0;
+  if (m > 0.0) frexp(m, &ex);
+  if (g == 0 && r < rows) e[r] = ex;
+  if (g * 16 >= kcols) return;
+  uint32_t w[S][4];
+#pragma unroll
+  for (int p = 0; p < S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double a = ldexp(x[j], 6 - ex);  // |a| < 64
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+      const double d = rint(a);
+      a = (a - d) * 128.0;
+      w[p][j >> 2] |= ((uint32_t)((int32_t)d & 0xff)) << (8 * (j & 3));
+    }
+  }
+  const int64_t rt = r / TR, rr = r - rt * TR, ks = g >> 1, c = g & 1;
+  const int64_t off = (rt * ksteps + ks) * tstride + rr * 32 + ((c ^ ((rr >> 2) & 1)) << 4);
+#pragma unroll
+  for (int p = 0; p < S; ++p)
+    *reinterpret_cast<uint4 *>(out + p * sstride + off) =
+        make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
 // fp64-column ranges (nr per column tile) -> int8-slice ranges rounded out to
 // multiples of 32 (the UMMA K step) and merged when they touch; columns added
 // by the rounding hold zero operands for this tile (outside its band).
@@ -1004,12 +1054,6 @@ int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, 
   int64_t *rin = rg + ceil_div(N, tc8::OZ_BN) * 4 * 2;  // 4 ranges x 2 per tile each
   const int64_t ntn = ceil_div(N, tc8::OZ_BN);
   int st;
-  if (phase & 1) {
-    tc8::k_oz_rowexp<<<(unsigned)ceil_div(M * 32, 256), 256, 0, s>>>(A, M, lda, K, nb, r3p, G, ea);
-    if ((st = check_launch("oz_rowexp A"))) return st;
-    tc8::k_oz_rowexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, s>>>(B, N, ldb, K, nb, r3p, G, eb);
-    if ((st = check_launch("oz_rowexp B"))) return st;
-  }
   // dense K <= 160 (the Tucker part): the A-resident warp-specialised kernel
   // (RSB200_OZ_RES=0: the per-tile kernel below)
   static const bool res_on = [] {
@@ -1018,6 +1062,12 @@ int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, 
   }();
   const bool res = res_on && !ranges && !nb && slices <= 7 &&
                    ceil_div(K, 32) <= tc8::OzRes<7>::MAXSTEPS;
+  if ((phase & 1) && !res) {
+    tc8::k_oz_rowexp<<<(unsigned)ceil_div(M * 32, 256), 256, 0, s>>>(A, M, lda, K, nb, r3p, G, ea);
+    if ((st = check_launch("oz_rowexp A"))) return st;
+    tc8::k_oz_rowexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, s>>>(B, N, ldb, K, nb, r3p, G, eb);
+    if ((st = check_launch("oz_rowexp B"))) return st;
+  }
   auto slice = [&](const double *X, int64_t rows, int64_t rows_pad, int TR, int64_t ld,
                    const int *e, int8_t *out, bool interleave) {
     const unsigned g = (unsigned)ceil_div(rows_pad * ksteps * 2, 256);
@@ -1040,7 +1090,21 @@ int rs_oz_gemm_cols(const double *A, int64_t lda, const double *B, int64_t ldb, 
     }
     return check_launch("oz_slice");
   };
-  if (phase & 1) {
+  // exponent + slices of a dense operand in one pass, S slices of a block interleaved
+  auto rowslice = [&](const double *X, int64_t rows, int64_t rows_pad, int TR, int64_t ld, int *e,
+                      int8_t *out) {
+    const unsigned g = (unsigned)ceil_div(rows_pad * 16, 256);
+    const int64_t ss = (int64_t)TR * 32, ts = (int64_t)slices * TR * 32;
+    if (slices == 6)
+      tc8::k_oz_rowslice<6><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, e, out, TR, ksteps, ss, ts);
+    else
+      tc8::k_oz_rowslice<7><<<g, 256, 0, s>>>(X, rows, rows_pad, ld, K, e, out, TR, ksteps, ss, ts);
+    return check_launch("oz_rowslice");
+  };
+  if ((phase & 1) && res) {
+    if ((st = rowslice(A, M, Mp, 128, lda, ea, SA))) return st;
+    if ((st = rowslice(B, N, Np, 64, ldb, eb, SB))) return st;
+  } else if (phase & 1) {
     if ((st = slice(A, M, Mp, 128, lda, ea, SA, res))) return st;
     if ((st = slice(B, N, Np, 64, ldb, eb, SB, res))) return st;
   }
