@@ -241,3 +241,35 @@ def test_tucker_gemm_variants(cuda, res):
     r = subprocess.run([sys.executable, "-c", _TUCKER_VARIANT_SCRIPT, root], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
+
+
+def test_tucker_oz_workspace_fallback(nat, cuda):
+    """rs_assemble_planes picks the Ozaki-split Tucker GEMM for 96 < r3 <= 160 only when the
+    caller's workspace has room for the slices; a workspace sized for the FP64 path alone
+    must still give the Tucker planes (DMMA kernel), not an error (formats.py:173-176)."""
+    torch = cuda
+    from paper_1606_09218_b200 import formats
+    torch.manual_seed(11)
+    n, ranks, lo, hi = 256, (16, 16, 100), 10, 18
+    facs = [torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device="cuda"))[0].contiguous()
+            for r in ranks]
+    core = torch.randn(ranks, dtype=torch.float64, device="cuda")
+    ref = torch.einsum("abc,ia,jb,kc->ijk", core, facs[0][lo:hi], facs[1], facs[2])
+    L = nat.lib()
+    flags = nat.ASM_LONG
+    planes, rmax = hi - lo, max(ranks)
+    full = L.rs_assemble_workspace_bytes(n, planes, rmax, 0, 0, flags)
+    oz = L.rs_oz_workspace_bytes(planes * n, n, 100, 7)
+    small = full - (oz + 255) // 256 * 256
+    assert 0 < small < full
+    for size in (small, full):
+        ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+        out = torch.empty((planes, n, n), dtype=torch.float64, device="cuda")
+        nat.check(L.rs_assemble_planes(core.data_ptr(), *ranks, facs[0].data_ptr(),
+                                       facs[1].data_ptr(), facs[2].data_ptr(), n, None, None, 0,
+                                       0, None, None, None, None, None, None, 0, lo, hi, flags,
+                                       out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       nat.stream_ptr()), "rs_assemble_planes")
+        torch.cuda.synchronize()
+        err = float((out - ref).abs().max() / ref.abs().max())
+        assert err < 2e-12, (size, err)
