@@ -173,8 +173,8 @@ __device__ __forceinline__ unsigned sm_live_blocks(int e, int g) {
   return jhi < jlo ? 0u : ((2u << jhi) - 1u) & ~((1u << jlo) - 1u);
 }
 
-template <bool ACC, bool BUILD, bool SKIP, int GRP>
-__global__ void __launch_bounds__(SM_THREADS, 2)
+template <bool ACC, bool BUILD, bool SKIP, int GRP, int NJ>
+__global__ void __launch_bounds__(SM_THREADS, NJ == 4 ? 3 : 2)
     k_short_mma(const double *__restrict__ ul, const double *__restrict__ wl, int Rs, int gamma,
                 int64_t n, const int32_t *__restrict__ c1, const int32_t *__restrict__ c2,
                 const double *__restrict__ zq, const int32_t *__restrict__ bstart,
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 const int *__restrict__ kofd_g, const int32_t *__restrict__ y16, int ldy,
                 int64_t x1_lo, int64_t x1_hi, int *__restrict__ counter, int tiles_per_cta,
                 int one, double *__restrict__ out) {
+  constexpr int T3 = 8 * NJ;   // x3 columns per tile: NJ MMA column blocks
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const SmLayout L = sm_layout(gamma, Rs, BUILD, GRP > 1);
   double *ut = (double *)(sm_raw + L.table);
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   // x1 tiles sit on absolute multiples of SM_T1, so a slab's values do not
   // depend on where the slab starts (same candidates, same term cuts, same sums)
   const int64_t x1_base = x1_lo - x1_lo % SM_T1;
-  const int n3t = (int)((n + SM_T3 - 1) / SM_T3), n2t = (int)((n + SM_T2 - 1) / SM_T2);
+  const int n3t = (int)((n + T3 - 1) / T3), n2t = (int)((n + SM_T2 - 1) / SM_T2);
   // work items: groups of GRP consecutive x3 tiles (one candidate search per group)
   const int n3g = (n3t + GRP - 1) / GRP;
   const int64_t ntiles = (int64_t)n3g * n2t * ((x1_hi - x1_base + SM_T1 - 1) / SM_T1);
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
   // tiles in parallel (per tile this was ~18 dependent global loads by one
   // thread with the CTA waiting at a barrier)
   for (int t3 = tid; t3 < n3t; t3 += SM_THREADS) {
-    const int lo_x = t3 * SM_T3 - gamma, hi_x = t3 * SM_T3 + SM_T3 - 1 + gamma;
+    const int lo_x = t3 * T3 - gamma, hi_x = t3 * T3 + T3 - 1 + gamma;
     int l = 0, h = nb;
     while (l < h) {
       const int m = (l + h) >> 1;
@@ -259,14 +260,14 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     const int64_t t1 = tile / ((int64_t)n3g * n2t);
     const int X0 = (int)(x1_base + t1 * SM_T1), Y0 = t2 * SM_T2;
     const int t3_lo = t3g * GRP, t3_hi = min(t3_lo + GRP, n3t);
-    int Z0 = t3_lo * SM_T3;   // the x3 tile in work (set per tile below)
+    int Z0 = t3_lo * T3;   // the x3 tile in work (set per tile below)
 
-    double acc[2][8][2];
+    double acc[2][NJ][2];
     auto zero_acc = [&]() {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     };
 
     // one MMA phase over the staged copies [base, base + len) (s_cb = their x3 index, s_kn =
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
         const int LDb = LD * 8;
         for (int st = 0; st < steps; ++st) {
           const int c = 4 * st + tig;
-          double a0 = 0.0, a1 = 0.0, b[8];
+          double a0 = 0.0, a1 = 0.0, b[NJ];
           unsigned own = 0;   // x3 blocks of the tile this lane's column reaches
           uint32_t ub = ut2_s;
           if (c < ncol) {
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
               bob = 8 * bo;
               e3 = bo - gamma - SM_PAD;
             }
-            own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : 0xFFu;
+            own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : (1u << NJ) - 1u;
             const uint32_t koff = (uint32_t)((c - col0) * LDb);
             const uint32_t u1 = ut1_s + koff, u2 = ut2_s + koff;
   #pragma unroll 2
@@ -352,17 +353,11 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
           }
           // the step's 4 columns (mostly consecutive terms of one bucket) reach only
           // some of the tile's 8 x3 blocks: the others' MMAs and B loads are skipped
-          const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : 0xFFu;
-          b[0] = (own & 1u) ? sm_lds(ub) : 0.0;
-          b[1] = (own & 2u) ? sm_lds_at<64>(ub) : 0.0;
-          b[2] = (own & 4u) ? sm_lds_at<128>(ub) : 0.0;
-          b[3] = (own & 8u) ? sm_lds_at<192>(ub) : 0.0;
-          b[4] = (own & 16u) ? sm_lds_at<256>(ub) : 0.0;
-          b[5] = (own & 32u) ? sm_lds_at<320>(ub) : 0.0;
-          b[6] = (own & 64u) ? sm_lds_at<384>(ub) : 0.0;
-          b[7] = (own & 128u) ? sm_lds_at<448>(ub) : 0.0;
+          const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : (1u << NJ) - 1u;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) b[j] = (own & (1u << j)) ? sm_lds(ub + 64 * j) : 0.0;
   #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < NJ; ++j) {
             if (SKIP) {
               // a predicated-off DMMA costs the pipe as much as a live one
               // (tools/probe_dmma_pred.cu), and ptxas if-converts any plain `if` around
@@ -450,7 +445,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
             if (4 * ks + ch * SM_ACH >= ncol) break;   // uniform: no live column in this step
             const uint32_t ap = buf + (uint32_t)((4 * ks + tig) * SM_ALD * 8);
             const double a0 = sm_lds(ap), a1 = sm_lds_at<64>(ap);
-            double b[8];
+            double b[NJ];
             unsigned own = 0;
             uint32_t ub = ut2_s;
             if (c < ncol) {
@@ -466,20 +461,14 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
                 bob = 8 * bo;
                 e3 = bo - gamma - SM_PAD;
               }
-              own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : 0xFFu;
+              own = SKIP ? sm_live_blocks(e3, s_gk[c - col0]) : (1u << NJ) - 1u;
               ub = ut2_s + (uint32_t)((c - col0) * LDb) + bob;
             }
-            const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : 0xFFu;
-            b[0] = (own & 1u) ? sm_lds(ub) : 0.0;
-            b[1] = (own & 2u) ? sm_lds_at<64>(ub) : 0.0;
-            b[2] = (own & 4u) ? sm_lds_at<128>(ub) : 0.0;
-            b[3] = (own & 8u) ? sm_lds_at<192>(ub) : 0.0;
-            b[4] = (own & 16u) ? sm_lds_at<256>(ub) : 0.0;
-            b[5] = (own & 32u) ? sm_lds_at<320>(ub) : 0.0;
-            b[6] = (own & 64u) ? sm_lds_at<384>(ub) : 0.0;
-            b[7] = (own & 128u) ? sm_lds_at<448>(ub) : 0.0;
+            const unsigned live = SKIP ? __reduce_or_sync(0xffffffffu, own) : (1u << NJ) - 1u;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < NJ; ++j) b[j] = (own & (1u << j)) ? sm_lds(ub + 64 * j) : 0.0;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
               if (SKIP) {
                 if (live & (1u << j)) {
 #pragma unroll 1
@@ -512,7 +501,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
           if (x2 >= n) continue;
           double *row = out + ((x1 - x1_lo) * n + x2) * n + Z0 + 2 * tig;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < NJ; ++j) {
             const int64_t x3 = Z0 + 8 * j + 2 * tig;
             double v0 = acc[i][j][0], v1 = acc[i][j][1];
             if (x3 + 1 < n) {
@@ -588,7 +577,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
               if (grouped) {
                 kn = skofd[d12];   // an upper bound: the tile's x3 distance cuts it further
               } else {
-                const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
+                const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + T3 - 1)));
                 kn = skofd[max(d12, d3)];
               }
               if (kn > 0) {
@@ -616,7 +605,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
     };
 
     auto tile_alone = [&](int t3) {
-      Z0 = t3 * SM_T3;
+      Z0 = t3 * T3;
       zero_acc();
       const int len = search(t3, t3 + 1, false);
       if (len > 0) flush(0, len);
@@ -639,9 +628,9 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
       } else {
         for (int t3 = t3_lo; t3 < t3_hi; ++t3) {
           __syncthreads();   // previous tile's MMA phase done with s_kn / s_seg
-          Z0 = t3 * SM_T3;
+          Z0 = t3 * T3;
           zero_acc();
-          const int zlo = Z0 - gamma, zhi = Z0 + SM_T3 - 1 + gamma;
+          const int zlo = Z0 - gamma, zhi = Z0 + T3 - 1 + gamma;
           int qa = 0, qb = glen;   // first staged copy with x3 >= zlo, first with x3 > zhi
           {
             int l = 0, h = glen;
@@ -659,7 +648,7 @@ __global__ void __launch_bounds__(SM_THREADS, 2)
           }
           for (int q = qa + tid; q < qb; q += SM_THREADS) {
             const int a3 = s_cb[q];
-            const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + SM_T3 - 1)));
+            const int d3 = max(0, max(Z0 - a3, a3 - (Z0 + T3 - 1)));
             s_kn[q] = skofd[max(s_d12[q], d3)];
           }
           if (qb > qa) flush(qa, qb - qa);   // (starts with a barrier: s_kn complete)
@@ -743,13 +732,20 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
   const char *genv = getenv("RSB200_MMA_GROUP");
   const bool grouped = !build && !skip && ov0 <= 64.0 && genv && genv[0] == '1';
   const SmLayout L = sm_layout((int)gamma, (int)Rs, build, grouped);
-  auto fn = grouped ? (acc ? k_short_mma<true, false, false, SM_GRP>
-                           : k_short_mma<false, false, false, SM_GRP>)
-            : skip ? (build ? (acc ? k_short_mma<true, true, true, 1> : k_short_mma<false, true, true, 1>)
-                            : (acc ? k_short_mma<true, false, true, 1> : k_short_mma<false, false, true, 1>))
-                   : (build ? (acc ? k_short_mma<true, true, false, 1> : k_short_mma<false, true, false, 1>)
-                            : (acc ? k_short_mma<true, false, false, 1>
-                                   : k_short_mma<false, false, false, 1>));
+  // RSB200_MMA_T3=32: 32-wide x3 tiles (half the accumulators: three CTAs per SM)
+  const char *tenv = getenv("RSB200_MMA_T3");
+  const bool narrow = tenv && atoi(tenv) == 32 && !grouped && !skip && ceil_div(n, 32) <= SM_MAXT3;
+  const int t3w = narrow ? 32 : SM_T3;
+  auto fn = narrow ? (build ? (acc ? k_short_mma<true, true, false, 1, 4> : k_short_mma<false, true, false, 1, 4>)
+                            : (acc ? k_short_mma<true, false, false, 1, 4>
+                                   : k_short_mma<false, false, false, 1, 4>))
+            : grouped ? (acc ? k_short_mma<true, false, false, SM_GRP, 8>
+                             : k_short_mma<false, false, false, SM_GRP, 8>)
+            : skip ? (build ? (acc ? k_short_mma<true, true, true, 1, 8> : k_short_mma<false, true, true, 1, 8>)
+                            : (acc ? k_short_mma<true, false, true, 1, 8> : k_short_mma<false, false, true, 1, 8>))
+                   : (build ? (acc ? k_short_mma<true, true, false, 1, 8> : k_short_mma<false, true, false, 1, 8>)
+                            : (acc ? k_short_mma<true, false, false, 1, 8>
+                                   : k_short_mma<false, false, false, 1, 8>));
   // RSB200_MMA_PAD_KB: extra dynamic shared memory per CTA (occupancy experiments:
   // one CTA per SM leaves room for another kernel's CTAs)
   const char *penv = getenv("RSB200_MMA_PAD_KB");
@@ -762,9 +758,9 @@ int rs_assemble_short_mma(const double *ul, const double *wl, int64_t Rs, int64_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int per_sm = smem_bytes + 1024 <= 113 * 1024 ? 2 : 1;
+  const int per_sm = (narrow && smem_bytes + 1024 <= 75 * 1024) ? 3 : smem_bytes + 1024 <= 113 * 1024 ? 2 : 1;
   // work items: x3 tile groups (of one tile unless grouped)
-  const int64_t ntiles = ceil_div(ceil_div(n, SM_T3), grouped ? SM_GRP : 1) * ceil_div(n, SM_T2) *
+  const int64_t ntiles = ceil_div(ceil_div(n, t3w), grouped ? SM_GRP : 1) * ceil_div(n, SM_T2) *
                          ceil_div(x1_hi - (x1_lo - x1_lo % SM_T1), SM_T1);
   static const int waves = [] {   // RSB200_MMA_WAVES: CTA generations per SM slot
     const char *e = getenv("RSB200_MMA_WAVES");

@@ -29,6 +29,12 @@ def test_workspace_queries_without_gpu():
     assert lib.rs_core_workspace_bytes(12, 12, 12, 1000, 14) >= 12 ** 3 * 8
     assert lib.rs_assemble_workspace_bytes(256, 4, 12, 50, 14, 3) >= 4 * 256 * (12 + 50 * 14) * 8
     assert lib.rs_sum_workspace_bytes(1000) >= 16
+    # Tucker-only planes: 96 < r3 <= 160 reserves the slices of the Ozaki-split tcgen05 GEMM
+    if os.environ.get("RSB200_TUCKER_OZ", "7") in ("6", "7"):
+        base = 4 * 256 * 132 * 8
+        with_oz = lib.rs_assemble_workspace_bytes(256, 4, 132, 0, 0, 1)
+        assert with_oz >= base + lib.rs_oz_workspace_bytes(4 * 256, 256, 132, 7)
+        assert lib.rs_assemble_workspace_bytes(256, 4, 96, 0, 0, 1) < with_oz
 
 
 def test_domain_errors_without_gpu():

@@ -23,7 +23,7 @@ RSB200_SIDE_SMS=0 BENCH_NO_OBSERVABLES=1 timeout 1500 ncu --metrics gpu__time_du
   --log-file $O/${TAG}_launches_C5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/${TAG}_ncu_launch.log 2>&1
 # full captures (one launch of each top kernel, after the warm-up steps)
 RSB200_SIDE_SMS=0 BENCH_NO_OBSERVABLES=1 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_short_mma|k_tucker_gemm_res|k_oz_res|k_core_h|k_syrk_part" -s 28 -c 6 -f -o $O/${TAG}_full_C5 \
+  -k regex:"k_short_mma|k_tucker_gemm_res|k_oz_res|k_oz_rowslice|k_core_h|k_syrk_part" -s 36 -c 10 -f -o $O/${TAG}_full_C5 \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/${TAG}_ncu_C5.log 2>&1
 summarise() {  # .ncu-rep files are tens of MB (gpurun_out/ is capped at 64 MiB): keep the tables
   python tools/ncu_summary.py $O/${TAG}_full_$1.ncu-rep > $O/${TAG}_ncu_summary_$1.md 2>&1
